@@ -1,0 +1,89 @@
+/*
+ * cce_b200.h — C ABI of libcce_b200.so, the B200 (sm_100a) Cut Cross-Entropy hot path.
+ *
+ * The reference (arxiv 2411.09009, /root/reference/pkg/src/cce) is a pure-Python package whose
+ * hot path is three functions composed by cce_loss.  Each entry point below replaces one of
+ * them; the Python layer (paper_2411_09009_b200/api.py) binds this header with ctypes exactly
+ * as a reference-side maintainer would.
+ *
+ * Conventions
+ *  - Every function returns 0 on success, nonzero on failure; cce_last_error() then describes it.
+ *    No C++ exception crosses the ABI.  No host synchronisation is performed.
+ *  - Pointers are device pointers unless stated; `stream` is a cudaStream_t (void*).
+ *  - E is bf16 [n, d] row-major, C is bf16 [v, d] row-major (reference core.py:5-8 layout:
+ *    token-major embeddings, vocab-major classifier).  d must be a multiple of 8.
+ *  - Outputs and workspaces are caller-allocated (so torch's allocator accounts every byte,
+ *    mirroring instrument.py's scratch/output split).
+ */
+#ifndef CCE_B200_H
+#define CCE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Message of the last failing call on this thread. */
+const char* cce_last_error(void);
+int cce_abi_version(void);
+
+/* ---- forward: indexed_matmul (kernels.py:204-251) + lse_forward (kernels.py:254-319) ----
+ * One fused persistent tcgen05 kernel: per token row, the log-sum-exp over this shard's
+ * vocabulary rows [vocab_start, vocab_start + v) (lse_local) and the target logit when the
+ * target falls in the shard (correct, else 0).  softcap > 0 applies cap*tanh(z/cap) to every
+ * logit.  Logits never reach HBM; ws holds splits*n float2 partials. */
+size_t cce_fwd_workspace_bytes(int64_t n, int64_t d, int64_t v);
+int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int64_t d, int64_t v,
+            int64_t ignore_index, int64_t vocab_start, float softcap, void* ws, size_t ws_bytes,
+            float* lse_local, float* correct, void* stream);
+
+/* ---- combine shards (log_add_exp merge, kernels.py:121-137; scatter kernels.py:539-547) ----
+ * lse_parts / correct_parts are [num_shards][n]; lse_out = log-add-exp over shards (0 at
+ * ignored rows), loss_out = lse - sum(correct) (0 at ignored rows). */
+int cce_merge_shards(int num_shards, const float* lse_parts, const float* correct_parts,
+                     const int64_t* targets, int64_t ignore_index, int64_t n, float* lse_out,
+                     float* loss_out, void* stream);
+
+/* ---- vocabulary order (compute_vocab_order, kernels.py:145-160) ----
+ * cce_ebar: column sums of the rows of E whose target != ignore_index (targets may be NULL =
+ * all rows).  cce_vocab_order: key = C . ebar_sum / n_valid (the reference's mean_logits),
+ * perm = stable descending argsort of key (ties by ascending index). */
+int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_t n, int64_t d,
+             float* ebar_sum, void* stream);
+size_t cce_sort_workspace_bytes(int64_t v);
+int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64_t v, int64_t d,
+                    int32_t* perm, float* key_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- backward (lse_backward, kernels.py:327-486) ----
+ * cce_bwd_prep: perm padded to a multiple of 256 and its inverse, label positions in tile
+ * order (-1 = ignored or owned by another shard), and the zero-upstream token-tile flags
+ * (kernels.py:434-438).  perm may be NULL (natural order).
+ * cce_bwd: recompute every 128x256 logit tile on the tensor cores, S = exp(z - lse), skip the
+ * tile when it holds no label and every S < eps (block_skip_decision, kernels.py:140-142;
+ * eps = 0 disables filtering), else S-hat = up * (S - onehot) and dE += S-hat C, dC += S-hat^T E.
+ * de_acc is fp32 [e_rows, d], dc is bf16 [v, d]; both must be zeroed by the caller.
+ * counters[3] = {kept tiles, eps-skipped tiles, zero-upstream-skipped tiles}
+ * (BackwardStats, kernels.py:66-76). */
+int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t ignore_index,
+                 int64_t vocab_start, const float* upstream, int64_t n, int32_t* perm_padded,
+                 int32_t* inv_perm, int32_t* pos, uint8_t* block_zero, void* stream);
+int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_padded,
+            const int32_t* row_map, const int32_t* pos, const float* lse, const float* upstream,
+            const uint8_t* block_zero, int64_t n_rows, int64_t d, int64_t v, float softcap,
+            float eps, float* de_acc, void* dc, unsigned long long* counters, void* stream);
+
+/* fp32 -> bf16 cast of the dE accumulator (count % 4 == 0). */
+int cce_f32_to_bf16(const float* x, void* y, int64_t count, void* stream);
+
+/* indexed_matmul alone (kernels.py:204-251): out[i] = C[x_i - vocab_start] . E[i], 0 when the
+ * target is ignored or outside the shard; softcap applied when > 0. */
+int cce_indexed_dot(const void* E, const void* C, const int64_t* targets, int64_t n, int64_t d,
+                    int64_t v, int64_t ignore_index, int64_t vocab_start, float softcap, float* out,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCE_B200_H */

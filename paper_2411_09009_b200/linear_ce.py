@@ -1,0 +1,130 @@
+"""`linear_cross_entropy`: the drop-in loss (north_star API) as a torch.autograd.Function.
+
+Semantics follow the reference cce_loss (kernels.py:513-580) through the adapter of SURVEY §8(b):
+
+  ignore_index   targets == ignore_index play the reference's IGNORE_INDEX = -1 (core.py:23)
+  reduction      "mean" = "mean-over-valid" (core.py:194-197; an all-ignored batch gives 0 loss
+                 and zero grads, never NaN), "sum", "none" (per-token, 0 at ignored rows)
+  filter_eps     "auto" -> 2**-12 (EPSILON_DEFAULT, core.py:27); None / 0 -> filtering off
+  softcap        z' = softcap * tanh(z / softcap) applied to every logit (absent from the
+                 reference; restated in oracle/cce_oracle.py and pinned by finite differences)
+
+Deviation (documented): for reduction="none" the reference raises on a nonzero upstream at an
+ignored row (kernels.py:371-372); here the upstream is masked to 0 there instead.
+
+Vocab-parallel: pass `process_group` and the classifier shard `c` holding global rows
+[vocab_start, vocab_start + c.shape[0]).  E and targets are replicated; each rank returns the
+full loss, dE is all-reduced, dC stays local (see vocab_parallel.py).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .ops import EPSILON_DEFAULT
+
+
+def _resolve_eps(filter_eps):
+    if filter_eps is None or filter_eps is False:
+        return 0.0
+    if isinstance(filter_eps, str):
+        if filter_eps != "auto":
+            raise ValueError(f"filter_eps must be 'auto', a float in (0,1) or None, got {filter_eps!r}")
+        return EPSILON_DEFAULT
+    eps = float(filter_eps)
+    if eps == 0.0:
+        return 0.0
+    if not (0.0 < eps < 1.0):
+        raise ValueError(f"epsilon must be in (0, 1), got {eps}")  # core.py:151-152
+    return eps
+
+
+class _LinearCrossEntropy(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
+                vocab_start):
+        if group is None:
+            lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
+            lse, loss = ops.merge_shards(lse_local[None], correct[None], targets, ignore_index)
+        else:
+            from .vocab_parallel import gather_and_merge
+
+            lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
+            lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group)
+        valid = targets != ignore_index
+        ctx.save_for_backward(e, c, targets, lse)
+        ctx.cfg = (ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start)
+        if reduction == "none":
+            return loss
+        total = loss.sum()
+        if reduction == "sum":
+            return total
+        n_valid = valid.sum()
+        return torch.where(n_valid > 0, total / n_valid.clamp_min(1), torch.zeros_like(total))
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        e, c, targets, lse = ctx.saved_tensors
+        ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start = ctx.cfg
+        valid = targets != ignore_index
+        g = grad_out.to(torch.float32)
+        if reduction == "none":
+            up = torch.where(valid, g, torch.zeros_like(g))
+        elif reduction == "sum":
+            up = valid.to(torch.float32) * g
+        else:  # mean over valid tokens (default_upstream, core.py:181-200)
+            n_valid = valid.sum().clamp_min(1).to(torch.float32)
+            up = valid.to(torch.float32) * (g / n_valid)
+        up = up.contiguous()
+        if group is None:
+            de, dc, _, _ = ops.backward(e, c, targets, lse, up, ignore_index=ignore_index,
+                                        vocab_start=vocab_start, softcap=softcap, eps=eps,
+                                        vocab_sorting=vocab_sorting)
+        else:
+            from .vocab_parallel import sharded_backward
+
+            de, dc = sharded_backward(e, c, targets, lse, up, ignore_index=ignore_index,
+                                      vocab_start=vocab_start, softcap=softcap, eps=eps,
+                                      vocab_sorting=vocab_sorting, group=group)
+        return de, dc, None, None, None, None, None, None, None, None
+
+
+def linear_cross_entropy(
+    e: torch.Tensor,
+    c: torch.Tensor,
+    targets: torch.Tensor,
+    ignore_index: int = -100,
+    softcap: float | None = None,
+    reduction: str = "mean",
+    filter_eps: float | str | None = "auto",
+    vocab_sorting: bool = True,
+    process_group=None,
+    vocab_start: int = 0,
+) -> torch.Tensor:
+    """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
+
+    e: [..., D] bf16 CUDA embeddings; c: [V, D] bf16 classifier (nn.Linear weight layout);
+    targets: [...] int64.  Returns a scalar for "mean"/"sum", else per-token losses of shape
+    e.shape[:-1].
+    """
+    if reduction not in ("mean", "sum", "none"):
+        raise ValueError(f"unknown reduction {reduction!r}")
+    lead = e.shape[:-1]
+    e2 = e.reshape(-1, e.shape[-1])
+    t2 = targets.reshape(-1)
+    if t2.shape[0] != e2.shape[0]:
+        raise ValueError(f"label count {t2.shape[0]} != token count {e2.shape[0]}")
+    if not e2.is_contiguous():
+        e2 = e2.contiguous()
+    ops.check_operands(e2, c, t2.to(torch.int64) if t2.dtype != torch.int64 else t2)
+    t2 = t2.to(torch.int64).contiguous()
+    cap = float(softcap) if softcap else 0.0
+    if cap < 0:
+        raise ValueError("softcap must be positive")
+    eps = _resolve_eps(filter_eps)
+    out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
+                                    bool(vocab_sorting), process_group, int(vocab_start))
+    if reduction == "none":
+        return out.reshape(lead)
+    return out
