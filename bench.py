@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: Cut Cross-Entropy fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gemma2-2b] [--impl ours|reference]
+
+One "step" = linear_cross_entropy forward + backward (reduction "mean", filter_eps 2**-12, vocab
+sorting on) over one synthetic batch of the named head.  N=1 runs the Gemma-2-2B head
+(BASELINE.json configs[1]).  N>1 (torchrun, one rank per GPU, NCCL) runs vocab-parallel: rank p
+holds classifier rows of its shard, E/targets replicated, total work fixed ("strong").
+`--mode token` instead gives every rank its own full batch (token-sharded DP, "weak").
+
+`--impl reference` times the reference algorithm's CPU restatement (oracle/, numpy + BLAS on all
+host cores; the reference is pure Python and cannot travel to the GPU box) on a bounded sample of
+the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# name: (N tokens, D, V, softcap, ignore-padding fraction per sequence, logit sigma)
+CONFIGS = {
+    "gpt2": (4096, 768, 50257, 0.0, 0.0, 1.0),
+    "gemma2-2b": (8192, 2304, 256000, 0.0, 0.0, 1.0),
+    "llama3-8b": (16384, 4096, 128256, 0.0, 0.25, 1.0),
+    "gemma2-9b": (32768, 3584, 256000, 30.0, 0.0, 1.0),
+    "nemo-12b": (65536, 5120, 131072, 0.0, 0.0, 1.0),
+}
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return FALLBACK_PEAKS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU side: the reference algorithm (oracle port) on a bounded sample
+# ------------------------------------------------------------------------------------------
+def cpu_sample(cfg_name: str, tokens: int = 128, seed: int = 0):
+    import numpy as np
+
+    from oracle import cce_oracle as O
+
+    n, d, v, cap, _, sigma = CONFIGS[cfg_name]
+    import torch
+
+    g = torch.Generator().manual_seed(seed)
+    e = torch.randn(tokens, d, generator=g).bfloat16().float().numpy()
+    c = (torch.randn(v, d, generator=g) * (sigma / math.sqrt(d))).bfloat16().float().numpy()
+    x = torch.randint(0, v, (tokens,), generator=g).numpy()
+
+    def step():
+        O.cce_loss(e, c, x, softcap=cap, eps=O.EPSILON_DEFAULT, vocab_sorting=True)
+
+    return step
+
+
+def run_cpu(cfg_name: str, steps: int, warmup: int, tokens: int = 128):
+    step = cpu_sample(cfg_name, tokens)
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    return tokens / dt, dt
+
+
+def cpu_desc(tokens: int) -> dict:
+    try:
+        model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")), "?")
+    except OSError:
+        model = "?"
+    return {"cores": os.cpu_count(), "cpu": model}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    tokens = args.cpu_tokens
+    val, dt = run_cpu(args.config, args.steps, max(0, min(args.warmup, 1)), tokens)
+    desc = cpu_desc(tokens)
+    sample = (f"{tokens} of {cfg[0]} tokens (full D={cfg[1]}, V={cfg[2]}), numpy/BLAS oracle port of "
+              f"cce_loss fwd+bwd (sort+filter), f32, {desc['cpu']}")
+    line = {
+        "impl": "reference", "metric": "fwd+bwd tokens/s", "value": val, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} head N={cfg[0]} D={cfg[1]} V={cfg[2]}", "sample_tokens": tokens},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": desc["cores"], "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="gemma2-2b", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="vocab", choices=["vocab", "token"])
+    ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
+    ap.add_argument("--no-sort", action="store_true")
+    ap.add_argument("--no-filter", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_09009_b200 import linear_cross_entropy, ops
+    from paper_2411_09009_b200.vocab_parallel import shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    n, d, v, cap, pad_frac, sigma = CONFIGS[args.config]
+    if args.sigma is not None:
+        sigma = args.sigma
+    eps = None if args.no_filter else "auto"
+    sort = not args.no_sort
+    token_mode = world > 1 and args.mode == "token"
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0 + (rank if token_mode else 0))
+    e = torch.randn(n, d, device=dev, generator=gen).to(torch.bfloat16)
+    gen.manual_seed(1)
+    if world > 1 and not token_mode:
+        v0, v1 = shard_range(v, rank, world)
+        c_full_rows = v1 - v0
+        # deterministic shard of the same global classifier: generate only this shard's rows
+        gen.manual_seed(1000 + v0)
+        c = (torch.randn(c_full_rows, d, device=dev, generator=gen) * (sigma / math.sqrt(d))).to(torch.bfloat16)
+    else:
+        v0 = 0
+        c = (torch.randn(v, d, device=dev, generator=gen) * (sigma / math.sqrt(d))).to(torch.bfloat16)
+    gen.manual_seed(2 + (rank if token_mode else 0))
+    t = torch.randint(0, v, (n,), device=dev, generator=gen)
+    if pad_frac:
+        seq = 4096
+        pos = torch.arange(n, device=dev) % seq
+        t[pos >= int(seq * (1 - pad_frac))] = -100
+    e.requires_grad_(True)
+    c.requires_grad_(True)
+
+    kw = dict(reduction="mean", filter_eps=eps, vocab_sorting=sort, softcap=cap or None)
+    if world > 1 and not token_mode:
+        kw.update(process_group=group, vocab_start=v0)
+
+    def step(ei, ci, ti):
+        ei.grad = None
+        ci.grad = None
+        loss = linear_cross_entropy(ei, ci, ti, **kw)
+        loss.backward()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- memory: forward-only and backward transient (instrument.py:3-10 definition)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    with torch.no_grad():
+        ops.forward_local(e.detach(), c.detach(), t, -100, v0, cap)
+    torch.cuda.synchronize()
+    fwd_transient = torch.cuda.max_memory_allocated(dev) - base  # outputs lse/correct (8N B) included
+
+    for _ in range(args.warmup):
+        step(e, c, t)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    step(e, c, t)
+    torch.cuda.synchronize()
+    grad_bytes = e.numel() * 2 + c.numel() * 2
+    bwd_transient = torch.cuda.max_memory_allocated(dev) - base - grad_bytes
+
+    # ---- timed region: device time with CUDA events, max over ranks
+    ops.KERNEL_EVENTS = {}
+    launches0 = ops.LAUNCHES["count"]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            step(e, c, t)
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    launches = (ops.LAUNCHES["count"] - launches0) // args.steps
+    kev = {k: sum(a.elapsed_time(b) for a, b in evs) / len(evs) for k, evs in ops.KERNEL_EVENTS.items()}
+    ops.KERNEL_EVENTS = None
+    counters = ops.LAST_COUNTERS["counters"].tolist()
+    if world > 1:
+        mt = torch.tensor([ms], device=dev)
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms = float(mt.item())
+    total_tokens = n * (world if token_mode else 1)
+    value = total_tokens / (ms / 1e3)
+
+    # ---- end to end through the public API with host (pinned) inputs
+    e2e = None
+    if not args.no_e2e:
+        eh = e.detach().cpu().pin_memory()
+        ch = c.detach().cpu().pin_memory()
+        th = t.cpu().pin_memory()
+        lh = torch.empty((), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            ei = eh.to(dev, non_blocking=True).requires_grad_(True)
+            ci = ch.to(dev, non_blocking=True).requires_grad_(True)
+            ti = th.to(dev, non_blocking=True)
+            loss = step(ei, ci, ti)
+            lh.copy_(loss.detach(), non_blocking=True)
+            return ei, ci
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / args.steps
+        if world > 1:
+            mt = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(mt.item())
+        e2e = {"value": total_tokens / (e2e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": eh.numel() * 2 + ch.numel() * 2 + th.numel() * 8,
+               "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms}
+
+    # ---- roofline of the dominant kernel (executed flops / event-timed launch duration)
+    peaks, peak_src = load_peaks()
+    n_valid = int((t != -100).sum().item())
+    v_loc = c.shape[0]
+    kept = counters[0]
+    flops_fwd = 2.0 * n * v_loc * d
+    flops_bwd = 2.0 * n_valid * v_loc * d + 4.0 * d * kept * 128 * 256
+    dom = "bwd" if kev.get("bwd", 0) >= kev.get("fwd", 0) else "fwd"
+    dom_flops = flops_bwd if dom == "bwd" else flops_fwd
+    dom_ms = kev[dom]
+    achieved = dom_flops / (dom_ms / 1e3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(args.config, {}).get(f"{dom}_dram_bytes")
+        except (ValueError, AttributeError):
+            traffic = None
+    total_tiles = -(-n_valid // 128) * -(-v_loc // 256)
+    step_flops = flops_fwd + flops_bwd
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cval, _ = run_cpu(args.config, 2, 0, args.cpu_tokens)
+        desc = cpu_desc(args.cpu_tokens)
+        cpu = {"value": cval, "unit": "tokens/s", "cores": desc["cores"], "kind": "port",
+               "sample": f"{args.cpu_tokens} of {n} tokens, full D/V, numpy+BLAS oracle port of cce_loss "
+                         f"fwd+bwd on {desc['cpu']}, mean of 2 runs"}
+
+    if rank == 0:
+        line = {
+            "metric": "fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if (world == 1 or token_mode) else "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random E ~ N(0,1), C ~ N(0, sigma^2/D), uniform targets)",
+            "config": {
+                "workload": f"{args.config} head N={n} D={d} V={v}", "sigma": sigma, "softcap": cap,
+                "ignore_pad_frac": pad_frac, "filter_eps": None if args.no_filter else 2 ** -12,
+                "vocab_sorting": sort, "reduction": "mean",
+                "parallelism": (f"vocab{world}" if world > 1 and not token_mode else f"token{world}"),
+                "l2": "inputs larger than L2 (C alone is %.2f GB)" % (v_loc * d * 2 / 1e9),
+            },
+            "gpu_launches": launches,
+            "kernel_ms": kev,
+            "skip": {"kept_tiles": kept, "eps_skipped": counters[1], "zero_up_skipped": counters[2],
+                     "total_tiles": total_tiles, "skip_rate": 1 - kept / max(1, total_tiles)},
+            "step_tflops": step_flops / (ms / 1e3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": f"cce_main_kernel<{dom.upper()}>",
+                         "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["bf16_tflops"],
+                         "frac_sustained": achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                         "peak_source": peak_src + " bf16 burst", "traffic": traffic,
+                         "flops_per_launch": dom_flops},
+            "memory": {"fwd_transient_bytes": int(fwd_transient), "bwd_transient_bytes": int(bwd_transient)},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

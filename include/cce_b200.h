@@ -60,19 +60,36 @@ int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64
  * cce_bwd_prep: perm padded to a multiple of 256 and its inverse, label positions in tile
  * order (-1 = ignored or owned by another shard), and the zero-upstream token-tile flags
  * (kernels.py:434-438).  perm may be NULL (natural order).
- * cce_bwd: recompute every 128x256 logit tile on the tensor cores, S = exp(z - lse), skip the
- * tile when it holds no label and every S < eps (block_skip_decision, kernels.py:140-142;
- * eps = 0 disables filtering), else S-hat = up * (S - onehot) and dE += S-hat C, dC += S-hat^T E.
- * de_acc is fp32 [e_rows, d], dc is bf16 [v, d]; both must be zeroed by the caller.
- * counters[3] = {kept tiles, eps-skipped tiles, zero-upstream-skipped tiles}
- * (BackwardStats, kernels.py:66-76). */
+ *
+ * cce_bwd: token tiles are processed in groups of `group_tiles`; kept tiles of a group take
+ * compact 64 KiB bf16 S-hat slots, `capacity_tiles` of them (workspace: cce_bwd_workspace_bytes).
+ * If a group keeps more tiles than the capacity, *overflow is set to 1 and the outputs are
+ * invalid: rerun with capacity_tiles >= group_tiles * ceil(v/256) (never overflows).
+ * Per group: (B1) recompute every 128x256 logit tile on the tensor cores, keep it iff it holds
+ * a label or some S = exp(z - lse) >= eps (block_skip_decision, kernels.py:140-142, label tiles
+ * exempt as in kernels.py:447-455; eps = 0 disables filtering) and store S-hat = up * (S - onehot)
+ * of kept tiles; (B2) dE[n] = sum_m S-hat[n,m] C[m] and (B3) dC[m] (+)= sum_n S-hat[n,m]^T E[n],
+ * both output-stationary in TMEM, no atomics.  de_out: [e_rows, d] bf16 (or fp32 if de_fp32),
+ * written for every compact row; other rows must be zeroed by the caller.  dc: [v, d] bf16,
+ * fully written.  counters[3] = {kept, eps-skipped, zero-upstream-skipped} tiles
+ * (BackwardStats, kernels.py:66-76), accumulated (caller zeroes). */
 int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t ignore_index,
                  int64_t vocab_start, const float* upstream, int64_t n, int32_t* perm_padded,
                  int32_t* inv_perm, int32_t* pos, uint8_t* block_zero, void* stream);
+size_t cce_bwd_workspace_bytes(int64_t n_rows, int64_t d, int64_t v, int64_t group_tiles,
+                               int64_t capacity_tiles);
 int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_padded,
             const int32_t* row_map, const int32_t* pos, const float* lse, const float* upstream,
-            const uint8_t* block_zero, int64_t n_rows, int64_t d, int64_t v, float softcap,
-            float eps, float* de_acc, void* dc, unsigned long long* counters, void* stream);
+            const uint8_t* block_zero, int64_t n_rows, int64_t d, int64_t v, float softcap, float eps,
+            int64_t group_tiles, int64_t capacity_tiles, int c_sorted, void* ws, size_t ws_bytes,
+            void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
+            void* stream);
+
+/* dst[i] = src[index[i]] for bf16 rows of `cols` elements.  With c_sorted != 0, cce_bwd takes C
+ * already permuted this way (C[perm], the vocabulary-sorted classifier) and loads plain tiles;
+ * perm_padded then only maps sorted rows back to dC rows. */
+int cce_gather_rows(const void* src, const int32_t* index, int64_t rows, int64_t cols, void* dst,
+                    void* stream);
 
 /* fp32 -> bf16 cast of the dE accumulator (count % 4 == 0). */
 int cce_f32_to_bf16(const float* x, void* y, int64_t count, void* stream);

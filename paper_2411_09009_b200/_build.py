@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libcce_b200.so"
 SOURCES = [CSRC / "cce_kernels.cu"]
-HEADERS = [CSRC / "cce_ptx.cuh", PKG.parent / "include" / "cce_b200.h"]
+HEADERS = sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "cce_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

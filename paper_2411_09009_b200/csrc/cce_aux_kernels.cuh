@@ -1,0 +1,192 @@
+// Small helper kernels of the CCE path: split/shard LSE merges, the vocabulary sort key, the
+// backward prep (inverse permutation, label positions, zero-upstream tiles) and casts.
+#pragma once
+#include "cce_common.cuh"
+
+namespace cce {
+
+// ---------------------------------------------------------------------------------------
+// Small kernels
+// ---------------------------------------------------------------------------------------
+
+// Merge the per-split (max2, sum2) partials of each row into this shard's natural-log LSE.
+__global__ void combine_splits_kernel(const float2* __restrict__ part, int splits, int n,
+                                      float* __restrict__ lse_local) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = -INFINITY;
+  for (int s = 0; s < splits; ++s) m = fmaxf(m, part[(size_t)s * n + i].x);
+  float acc = 0.f;
+  if (m != -INFINITY)
+    for (int s = 0; s < splits; ++s) {
+      const float2 v = part[(size_t)s * n + i];
+      acc += v.y * exp2f(v.x - m);
+    }
+  lse_local[i] = (m == -INFINITY) ? -INFINITY : (m + log2f(acc)) * 0.6931471805599453f;
+}
+
+// Vocab-parallel / single-shard finish: lse = logaddexp over shards, correct = sum over shards.
+// Mirrors cce_loss's scatter (kernels.py:539-547): loss and lse are 0 at ignored rows.
+__global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
+                                    const float* __restrict__ correct_parts,
+                                    const int64_t* __restrict__ targets, int64_t ignore_index,
+                                    int n, float* __restrict__ lse_out, float* __restrict__ loss_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = -INFINITY;
+  for (int q = 0; q < P; ++q) m = fmaxf(m, lse_parts[(size_t)q * n + i]);
+  float acc = 0.f, corr = 0.f;
+  for (int q = 0; q < P; ++q) {
+    const float l = lse_parts[(size_t)q * n + i];
+    if (m != -INFINITY) acc += expf(l - m);
+    corr += correct_parts[(size_t)q * n + i];
+  }
+  const float lse = (m == -INFINITY) ? -INFINITY : m + logf(acc);
+  const bool valid = targets[i] != ignore_index;
+  lse_out[i] = valid ? lse : 0.f;
+  loss_out[i] = valid ? lse - corr : 0.f;
+}
+
+// zero a float buffer (used for `correct` so rows whose label lives in another shard read 0)
+__global__ void fill_kernel(float* __restrict__ x, float v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+// Column mean of E over valid rows, fp32: ebar[d] = sum_i valid_i * E[i, d] / n_valid.
+__global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* __restrict__ targets,
+                            int64_t ignore_index, int n, int d, float* __restrict__ ebar_acc,
+                            int rows_per_block) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(n, r0 + rows_per_block);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r)
+    if (targets == nullptr || targets[r] != ignore_index) acc += __bfloat162float(E[(size_t)r * d + col]);
+  atomicAdd(&ebar_acc[col], acc);
+}
+
+// key[v] = C[v] . ebar  (fp32); one warp per vocab row.  Equals lse_forward's mean_logits
+// (kernels.py:305-308, :317-318), which is a mean of logits over the valid tokens.
+__global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float* __restrict__ ebar_sum,
+                                float inv_n, int v, int d, float* __restrict__ key) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= v) return;
+  const __nv_bfloat16* c = C + (size_t)row * d;
+  float acc = 0.f;
+  for (int j = lane * 8; j < d; j += 256) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(c + j);
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += __bfloat162float(h[q]) * ebar_sum[j + q];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) key[row] = acc * inv_n;
+}
+
+// out[i] = C[x_i] . E[i] (indexed_matmul, kernels.py:204-251); one warp per token row.
+__global__ void indexed_dot_kernel(const __nv_bfloat16* __restrict__ E, const __nv_bfloat16* __restrict__ C,
+                                   const int64_t* __restrict__ targets, int64_t ignore_index,
+                                   int64_t vocab_start, int n, int d, int v, float softcap,
+                                   float* __restrict__ out) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const int64_t tg = targets[row];
+  const int64_t l = tg - vocab_start;
+  if (tg == ignore_index || l < 0 || l >= v) {
+    if (lane == 0) out[row] = 0.f;
+    return;
+  }
+  const __nv_bfloat16* e = E + (size_t)row * d;
+  const __nv_bfloat16* c = C + (size_t)l * d;
+  float acc = 0.f;
+  for (int j = lane * 8; j < d; j += 256) {
+    const uint4 re = *reinterpret_cast<const uint4*>(e + j);
+    const uint4 rc = *reinterpret_cast<const uint4*>(c + j);
+    const __nv_bfloat16* he = reinterpret_cast<const __nv_bfloat16*>(&re);
+    const __nv_bfloat16* hc = reinterpret_cast<const __nv_bfloat16*>(&rc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += __bfloat162float(he[q]) * __bfloat162float(hc[q]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = softcap > 0.f ? softcap * tanhf(acc / softcap) : acc;
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ x, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+
+// inv[perm[j]] = j for j < v ; padding positions of perm (>= v) point at row 0.
+__global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int v, int vpad,
+                                   int32_t* __restrict__ perm_padded, int32_t* __restrict__ inv) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= vpad) return;
+  if (j < v) {
+    const int32_t r = perm[j];
+    perm_padded[j] = r;
+    inv[r] = j;
+  } else {
+    perm_padded[j] = 0;
+  }
+}
+
+// pos[i] = tile-order position of row i's label (or -1: ignored / label owned by another shard)
+__global__ void label_pos_kernel(const int64_t* __restrict__ targets, int64_t ignore_index,
+                                 int64_t vocab_start, int v, const int32_t* __restrict__ inv,
+                                 int n, int32_t* __restrict__ pos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t tg = targets[i];
+  int32_t r = -1;
+  if (tg != ignore_index) {
+    const int64_t l = tg - vocab_start;
+    if (l >= 0 && l < v) r = inv ? inv[l] : (int32_t)l;
+  }
+  pos[i] = r;
+}
+
+// block_zero[b] = all upstream of token tile b are exactly zero (kernels.py:434-438)
+__global__ void block_zero_kernel(const float* __restrict__ up, int n, uint8_t* __restrict__ bz) {
+  const int b = blockIdx.x;
+  const int i = b * BM + threadIdx.x;
+  const bool nz = (i < n) && (up[i] != 0.f);
+  const int any = __syncthreads_or(nz);
+  if (threadIdx.x == 0) bz[b] = any ? 0 : 1;
+}
+
+// dst[i, :] = src[index[i], :] for bf16 rows of `cols` elements (cols % 8 == 0); one warp per row.
+// Materialises the vocabulary-sorted classifier C[perm] for the backward so every tile load is a
+// plain TMA box instead of 64 tile::gather4 transfers.
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const int32_t* __restrict__ index,
+                                   int64_t rows, int cols, __nv_bfloat16* __restrict__ dst) {
+  const int warps = blockDim.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)index[r] * cols);
+  uint4* d = reinterpret_cast<uint4*>(dst + (size_t)r * cols);
+  const int n16 = cols / 8;
+#pragma unroll 4
+  for (int j = lane; j < n16; j += 32) d[j] = __ldg(s + j);
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                   int64_t n4) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 v = reinterpret_cast<const float4*>(x)[i];
+  uint2 o;
+  o.x = pack_bf16x2(v.x, v.y);
+  o.y = pack_bf16x2(v.z, v.w);
+  reinterpret_cast<uint2*>(y)[i] = o;
+}
+
+}  // namespace cce

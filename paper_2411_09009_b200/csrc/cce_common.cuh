@@ -1,0 +1,137 @@
+// Shared constants, parameter blocks and TMA issue helpers of the CCE kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "cce_ptx.cuh"
+
+namespace cce {
+
+constexpr int BM = 128;                   // tokens per logit tile (TMEM lanes, MMA M)
+constexpr int BN = 256;                   // vocab rows per logit tile (MMA N)
+constexpr int BK = 64;                    // D elements per K-block: one 128 B swizzle atom
+constexpr int A_BYTES = BM * BK * 2;      // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;      // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;          // warp0 TMA, warp1 MMA, warps 2..5 epilogue
+constexpr int LSE_STAGES = 4;
+constexpr int TMEM_COLS = 512;
+constexpr int DCH = 256;                  // D columns per gradient chunk (MMA N of dE / dC)
+constexpr int SHAT_TILE_BYTES = BM * BN * 2;  // one stored S-hat tile, bf16 row-major [128][256]
+
+enum Mode { FWD = 0, BWD = 1 };
+
+// Forward (FWD) and backward filter pass (BWD, "B1") of the fused logit-tile kernel.
+struct Params {
+  int n_rows;        // token rows handled (N, or N_valid after compaction in the backward)
+  int d;             // hidden size
+  int v;             // vocab rows of C (this shard)
+  int nt;            // token tiles covered by this launch (a group in the backward)
+  int n_base;        // first token tile of this launch
+  int mt;            // vocab tiles
+  int splits;        // vocab splits per token tile (units = nt * splits)
+  int num_kb;        // ceil(d / BK)
+  float softcap;     // 0 => off
+  // forward
+  const int64_t* targets;
+  int64_t ignore_index;
+  int64_t vocab_start;
+  float2* part;      // [splits][n_rows]  (running max, running sum) in log2 units
+  float* correct;    // [n_rows] target logit (written by the tile that owns the label)
+  // backward filter pass
+  const float* lse;        // [n_rows] global log-sum-exp (natural log)
+  const float* upstream;   // [n_rows] dLoss/dloss_i, 0 at ignored rows
+  const int32_t* pos;      // [n_rows] label position in tile order, -1 if none
+  const int32_t* perm;     // [mt*BN] tile-order position -> C row (nullptr = identity)
+  const int32_t* row_map;  // [nt*BM] compact row -> E row / dE row (nullptr = identity)
+  const uint8_t* block_zero;  // [all token tiles] 1 if every upstream in the tile is zero
+  float eps;               // filter threshold (0 = filtering off)
+  __nv_bfloat16* shat;     // [capacity][BM][BN] S-hat of kept tiles, compact slots
+  int32_t* slot_of;        // [nt*mt] slot of tile (local n, m), -1 if not stored (host: -1)
+  int* slot_ctr;           // next free slot (host: 0)
+  int capacity;            // slots available
+  int* overflow;           // set to 1 if a kept tile found no slot (host: 0)
+  int* cnt_n;              // [nt] kept tiles per token tile
+  int* cnt_m;              // [mt] kept tiles per vocab tile
+  unsigned long long* counters;  // [3] kept, eps-skipped, zero-upstream-skipped
+};
+
+// dE pass ("B2") and dC pass ("B3").
+struct GradParams {
+  int n_rows, d, v, mt, ndc;
+  int n_base, g;           // token tiles [n_base, n_base + g) of this group
+  const int32_t* slot_of;  // [g*mt]
+  const int* cnt_n;
+  const int* cnt_m;
+  const int32_t* perm;     // C-row gather index for tile loads (padded), or nullptr
+  const int32_t* perm_store;  // tile-order position -> dC row (padded), or nullptr
+  const int32_t* row_map;  // padded, or nullptr
+  __nv_bfloat16* de_bf16;  // [N_orig][d]   (one of de_bf16 / de_f32)
+  float* de_f32;
+  __nv_bfloat16* dc;       // [v][d]
+  int accumulate;          // dC: add to the existing values (groups after the first)
+};
+
+__device__ __forceinline__ void advance_stage(int& stage, uint32_t& phase, int stages) {
+  if (++stage == stages) {
+    stage = 0;
+    phase ^= 1;
+  }
+}
+
+// A box of `rows` (<= 256) logical rows x 64 columns of a row-major bf16 matrix lands in a
+// 128B-swizzled smem box either as one TMA tile load (no index; lane 0 issues it) or as a row
+// gather through `index` (logical row -> physical row) split across the producer warp: lane l
+// issues the tile::gather4 transfers of its own 4-row groups, whose indices it loaded into
+// registers once per tile (so no index load sits between two gathers).
+struct RowGather {
+  // up to two 4-row groups per lane: rows 4*(lane + 32*j) .. +3 of the box
+  int4 idx[2];
+  int groups;  // 4-row groups per lane (0, 1 or 2)
+  __device__ __forceinline__ void load(const int32_t* index, int row0, int rows) {
+    const int lane = threadIdx.x & 31;
+    groups = 0;
+    if (index == nullptr) return;
+    const int4* ix = reinterpret_cast<const int4*>(index + row0);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int gi = lane + 32 * j;
+      if (gi * 4 < rows) {
+        idx[j] = __ldg(ix + gi);
+        groups = j + 1;
+      }
+    }
+  }
+  __device__ __forceinline__ void issue(const CUtensorMap* tm_gather, uint64_t* bar, uint8_t* dst,
+                                        int c0) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (j < groups)
+        tma_gather4(tm_gather, bar, dst + (lane + 32 * j) * 512, c0, idx[j].x, idx[j].y, idx[j].z,
+                    idx[j].w);
+  }
+};
+
+template <int ROWS>
+__device__ __forceinline__ void load_rows_warp(const CUtensorMap* tm_tile, const CUtensorMap* tm_gather,
+                                               const RowGather& rg, bool gather, uint64_t* bar,
+                                               uint8_t* dst, int c0, int row0) {
+  if (!gather) {
+    if ((threadIdx.x & 31) == 0) tma_load_2d(tm_tile, bar, dst, c0, row0);
+  } else {
+    rg.issue(tm_gather, bar, dst, c0);
+  }
+}
+
+// softcap: z' = cap * tanh(z / cap), tanh(x) = 1 - 2 / (exp(2x) + 1) (exact limits at +-inf)
+__device__ __forceinline__ float softcap_tanh(float z, float inv_cap) {
+  const float e = ex2_approx(z * inv_cap * 2.8853900817779268f);  // 2*log2(e)
+  return 1.0f - __fdividef(2.0f, e + 1.0f);
+}
+
+constexpr float LOG2E = 1.4426950408889634f;
+
+}  // namespace cce

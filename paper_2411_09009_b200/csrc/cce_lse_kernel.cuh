@@ -1,0 +1,306 @@
+// Fused logit-tile kernel: forward LSE (FWD) and backward filter pass (BWD).
+//
+//   FWD = indexed_matmul (kernels.py:204-251) + lse_forward (kernels.py:254-319): per token row,
+//         an online (max, sum-exp) over this CTA's vocabulary split plus the target logit.
+//   BWD = the recompute / S / filter half of lse_backward (kernels.py:425-459): per 128x256
+//         tile, keep it iff it holds a label or any S = exp(z - lse) >= eps (block_skip_decision,
+//         kernels.py:140-142); kept tiles store S-hat = up * (S - onehot) [* (1 - tanh^2)] as bf16
+//         for the dE / dC passes (cce_grad_kernels.cuh).
+//
+// Persistent, one CTA per SM, 192 threads:
+//   warp 0      TMA producer (one thread): E rows [n*128, +128) and C rows of tile m, 64 D-columns
+//               per stage, 4-stage ring
+//   warp 1      TMEM allocator + MMA issuer: 36 K-blocks x 4 tcgen05.mma (M=128, N=256, K=16)
+//               into one of two 256-column fp32 accumulators (double buffered)
+//   warps 2..5  epilogue: thread (warp%4)*32+lane owns token row of the tile, reads its 256
+//               accumulator columns with tcgen05.ld
+#pragma once
+#include "cce_common.cuh"
+
+namespace cce {
+
+struct TileIter {
+  // Static persistent schedule: unit u = s * nt + n (token tile fastest), so the CTAs running
+  // concurrently share the same vocab tiles of C while E stays L2-resident.
+  int unit, units, m, m_end, n, s;
+  const Params* p;
+  __device__ void begin_unit() {
+    n = p->n_base + unit % p->nt;
+    s = unit / p->nt;
+    m = (int)(((long long)s * p->mt) / p->splits);
+    m_end = (int)(((long long)(s + 1) * p->mt) / p->splits);
+  }
+  __device__ bool valid() const { return unit < units; }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cce_lse_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
+                   const Params p) {
+  constexpr int STAGES = LSE_STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: logits ready
+  uint64_t* acc_free = acc_full + 2;    // [2] epilogue -> MMA: accumulator reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+  uint32_t* s_vote = tmem_slot + 1;     // [2][4]
+  int* s_slot = reinterpret_cast<int*>(s_vote + 8);  // [2]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmE);
+    tma_prefetch_desc(&tmC);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_free[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  TileIter it;
+  it.p = &p;
+  it.units = p.nt * p.splits;
+
+  if (warp == 0) {
+    // ================================ TMA producer (whole warp) ===========================
+    int stage = 0;
+    uint32_t phase = 0;
+    const bool gather_e = p.row_map != nullptr;
+    const bool gather_c = p.perm != nullptr;
+    RowGather rge, rgc;
+    for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
+      it.begin_unit();
+      if (MODE == BWD && p.block_zero[it.n]) continue;
+      rge.load(p.row_map, it.n * BM, BM);
+      for (; it.m < it.m_end; ++it.m) {
+        rgc.load(p.perm, it.m * BN, BN);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          }
+          __syncwarp();
+          load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, it.n * BM);
+          load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, it.m * BN);
+          advance_stage(stage, phase, STAGES);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================== MMA issuer ====================================
+    if (lane == 0) {
+      constexpr uint32_t IDESC = make_idesc_bf16(BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int t = 0;
+      for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
+        it.begin_unit();
+        if (MODE == BWD && p.block_zero[it.n]) continue;
+        for (; it.m < it.m_end; ++it.m, ++t) {
+          const int buf = t & 1;
+          mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + buf * BN;
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024), make_sdesc(b0 + 32 * k, 0, 1024),
+                          IDESC, (kb | k) != 0);
+            mma_commit(&empty[stage]);
+            advance_stage(stage, phase, STAGES);
+          }
+          mma_commit(&acc_full[buf]);
+        }
+      }
+    }
+  } else {
+    // ===================================== epilogue ======================================
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool use_softcap = p.softcap > 0.f;
+    const float inv_cap = use_softcap ? 1.0f / p.softcap : 0.f;
+    const int epi_tid = threadIdx.x - 64;  // 0..127
+    int t = 0;
+
+    for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
+      it.begin_unit();
+      const int grow = it.n * BM + row;
+      const bool valid = grow < p.n_rows;
+      if (MODE == FWD) {
+        int64_t tpos = -1;
+        if (valid) {
+          const int64_t tg = p.targets[grow];
+          if (tg != p.ignore_index) tpos = tg - p.vocab_start;
+        }
+        float run_m = -INFINITY, run_s = 0.f, corr = 0.f;
+        bool have_corr = false;
+        for (; it.m < it.m_end; ++it.m, ++t) {
+          const int buf = t & 1;
+          mbar_wait(&acc_full[buf], (t >> 1) & 1);
+          tc_fence_after();
+          const int col0 = it.m * BN;
+          const bool tile_has_t = tpos >= col0 && tpos < col0 + BN;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tmem_base + lane_off + buf * BN + c * 32, r);
+            tmem_ld_wait();
+            float y[32];
+            float cm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float z = __uint_as_float(r[j]);
+              if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
+              const int col = col0 + c * 32 + j;
+              if (tile_has_t && col == tpos) {
+                corr = z;
+                have_corr = true;
+              }
+              y[j] = col < p.v ? z * LOG2E : -INFINITY;
+              cm = fmaxf(cm, y[j]);
+            }
+            const float nm = fmaxf(run_m, cm);
+            if (nm != -INFINITY) {
+              float acc = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc += ex2_approx(y[j] - nm);
+              run_s = run_s * ex2_approx(run_m - nm) + acc;
+              run_m = nm;
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&acc_free[buf]);
+        }
+        if (valid) {
+          p.part[(size_t)it.s * p.n_rows + grow] = make_float2(run_m, run_s);
+          if (have_corr) p.correct[grow] = corr;
+        }
+      } else {
+        // ------------------------------- backward filter pass ------------------------------
+        if (p.block_zero[it.n]) {
+          if (epi_tid == 0) atomicAdd(&p.counters[2], (unsigned long long)(it.m_end - it.m));
+          continue;
+        }
+        const float lse2 = valid ? p.lse[grow] * LOG2E : INFINITY;
+        const float up_r = valid ? p.upstream[grow] : 0.f;
+        const int pos_r = valid ? p.pos[grow] : -1;
+        const int ln = it.n - p.n_base;
+        for (; it.m < it.m_end; ++it.m, ++t) {
+          const int buf = t & 1;
+          mbar_wait(&acc_full[buf], (t >> 1) & 1);
+          tc_fence_after();
+          const int col0 = it.m * BN;
+          const uint32_t tacc = tmem_base + lane_off + buf * BN;
+          // pass 1: row max of the raw logits.  S = exp(z' - lse) is monotone in z, so
+          // "all S < eps" (block_skip_decision) holds iff S(row max) < eps for every row.
+          float zmax = -INFINITY;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + c * 32 + j < p.v) zmax = fmaxf(zmax, __uint_as_float(r[j]));
+          }
+          bool big = false;
+          if (valid && zmax != -INFINITY) {
+            const float zc = use_softcap ? p.softcap * softcap_tanh(zmax, inv_cap) : zmax;
+            big = ex2_approx(zc * LOG2E - lse2) >= p.eps;
+          }
+          const bool in_tile = pos_r >= col0 && pos_r < col0 + BN;
+          const uint32_t wvote = __any_sync(0xffffffffu, big || in_tile);
+          if (lane == 0) s_vote[(t & 1) * 4 + quarter] = wvote;
+          named_bar_sync(1, 128);
+          const uint32_t* vv = s_vote + (t & 1) * 4;
+          const bool kept = (vv[0] | vv[1] | vv[2] | vv[3]) != 0;
+          if (kept) {
+            // one slot per kept tile, handed out in completion order; results do not depend on
+            // slot numbers (the gradient passes visit tiles in index order)
+            if (epi_tid == 0) {
+              int slot = atomicAdd(p.slot_ctr, 1);
+              if (slot >= p.capacity) {
+                slot = -1;
+                atomicExch(p.overflow, 1);
+              } else {
+                p.slot_of[(size_t)ln * p.mt + it.m] = slot;
+                atomicAdd(&p.cnt_n[ln], 1);
+                atomicAdd(&p.cnt_m[it.m], 1);
+              }
+              s_slot[t & 1] = slot;
+              atomicAdd(&p.counters[0], 1ull);
+            }
+            named_bar_sync(1, 128);
+            const int slot = s_slot[t & 1];
+            if (slot >= 0) {
+              // pass 2: S-hat row -> bf16 -> global, row-major [slot][128][256]
+              uint4* dst = reinterpret_cast<uint4*>(p.shat + ((size_t)slot * BM + row) * BN);
+#pragma unroll 1
+              for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tacc + c * 32, r);
+                tmem_ld_wait();
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                  float g2[2];
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    float z = __uint_as_float(r[j + h]);
+                    float dcap = 1.f;
+                    if (use_softcap) {
+                      const float th = softcap_tanh(z, inv_cap);
+                      z = p.softcap * th;
+                      dcap = 1.f - th * th;
+                    }
+                    const int col = col0 + c * 32 + j + h;
+                    const float s = (col < p.v) ? ex2_approx(z * LOG2E - lse2) : 0.f;
+                    g2[h] = ((col == pos_r) ? s - 1.f : s) * up_r * dcap;
+                  }
+                  pk[j >> 1] = pack_bf16x2(g2[0], g2[1]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              }
+            }
+          } else if (epi_tid == 0) {
+            atomicAdd(&p.counters[1], 1ull);
+          }
+          tc_fence_before();
+          mbar_arrive(&acc_free[buf]);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace cce

@@ -9,6 +9,7 @@ anything on the host; if libcce_b200.so is missing, the first call raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -18,6 +19,30 @@ from . import _lib
 BLOCK_TOKENS = 128      # GPU tile rows  (reference BlockSpec.n_b)
 BLOCK_VOCAB = 256       # GPU tile cols  (reference BlockSpec.m_b)
 EPSILON_DEFAULT = 2.0 ** -12   # core.py:27
+
+
+# Optional CUDA-event timing of the two tcgen05 kernels (bench.py's roofline leg).  When
+# enabled, an event pair is recorded on the launching stream around each cce_fwd / cce_bwd call.
+KERNEL_EVENTS: dict[str, list] | None = None
+LAST_COUNTERS: dict = {}
+LAST_OVERFLOW = {"count": 0}  # backward reruns caused by S-hat slot overflow
+LAUNCHES = {"count": 0}   # kernels launched from libcce_b200.so (bench.py's gpu_launches)
+
+
+def _ev_begin(name: str):
+    if KERNEL_EVENTS is None:
+        return None
+    a = torch.cuda.Event(enable_timing=True)
+    a.record()
+    return a
+
+
+def _ev_end(name: str, a) -> None:
+    if a is None:
+        return
+    b = torch.cuda.Event(enable_timing=True)
+    b.record()
+    KERNEL_EVENTS.setdefault(name, []).append((a, b))
 
 
 def _p(t: torch.Tensor | None):
@@ -68,9 +93,12 @@ def forward_local(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
         return lse_local, correct
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    ev = _ev_begin("fwd")
     _lib.check(lib.cce_fwd(_p(e), _p(c), _p(targets), n, d, v, int(ignore_index), int(vocab_start),
                            float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
                            _stream(dev)), "cce_fwd")
+    _ev_end("fwd", ev)
+    LAUNCHES["count"] += 3
     return lse_local, correct
 
 
@@ -84,6 +112,7 @@ def merge_shards(lse_parts, correct_parts, targets, ignore_index: int):
         _lib.check(lib.cce_merge_shards(p, _p(lse_parts.contiguous()), _p(correct_parts.contiguous()),
                                         _p(targets), int(ignore_index), n, _p(lse), _p(loss),
                                         _stream(lse_parts.device)), "cce_merge_shards")
+        LAUNCHES["count"] += 1
     return lse, loss
 
 
@@ -113,6 +142,7 @@ def vocab_order(e, c, targets, ignore_index: int, n_valid: int):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.check(lib.cce_vocab_order(_p(c), _p(ebar), int(n_valid), v, d, _p(perm), _p(key), _p(ws),
                                    ws_bytes, _stream(dev)), "cce_vocab_order")
+    LAUNCHES["count"] += 3 + 5  # ebar, sort key, iota + CUB onesweep radix sort passes
     return perm, key
 
 
@@ -181,18 +211,59 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(tg_c), int(ignore_index), int(vocab_start), _p(up_c),
                                 n_valid, _p(perm_padded), _p(inv_perm), _p(pos), _p(block_zero),
                                 stream), "cce_bwd_prep")
-    de_acc = torch.zeros(n, d, dtype=torch.float32, device=dev)
-    dc = torch.zeros(v, d, dtype=torch.bfloat16, device=dev)
+    LAUNCHES["count"] += 3 if perm is not None else 2
+    compacted = row_map is not None
+    de_dtype = torch.float32 if fp32_de else torch.bfloat16
+    de = (torch.zeros if compacted or n_valid == 0 else torch.empty)(n, d, dtype=de_dtype, device=dev)
+    dc = (torch.zeros if n_valid == 0 else torch.empty)(v, d, dtype=torch.bfloat16, device=dev)
     counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    if n_valid == 0:
+        return de, dc, counters, perm
     filt_eps = 0.0 if (eps is None or eps == 0) else float(eps)
-    _lib.check(lib.cce_bwd(_p(e), n, _p(c), _p(perm_padded), _p(row_map), _p(pos), _p(lse_c), _p(up_c),
-                           _p(block_zero), n_valid, d, v, float(softcap or 0.0), filt_eps, _p(de_acc),
-                           _p(dc), _p(counters), stream), "cce_bwd")
-    if fp32_de:
-        return de_acc, dc, counters, perm
-    de = torch.empty(n, d, dtype=torch.bfloat16, device=dev)
-    _lib.check(lib.cce_f32_to_bf16(_p(de_acc), _p(de), n * d, stream), "cce_f32_to_bf16")
+    mt = -(-v // BLOCK_VOCAB)
+    budget = shat_budget_tiles()
+    # first try: every token tile in one group, compact S-hat slots up to the budget
+    plans = [(nt, min(budget, nt * mt))]
+    if plans[0][1] < nt * mt:
+        g = max(1, budget // mt)          # fallback: groups whose worst case fits the budget
+        plans.append((g, g * mt))
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    # Vocabulary order: materialise C[perm] once (1 HBM read + write of C) so every tile load in
+    # the backward is a plain TMA box; CCE_SORT_GATHER=1 instead gathers rows with TMA gather4
+    # inside the kernels (no copy, but gather-bound).
+    c_src, c_sorted = c, 0
+    if perm is not None and os.environ.get("CCE_SORT_GATHER", "0") != "1":
+        c_src = torch.empty_like(c)
+        _lib.check(lib.cce_gather_rows(_p(c), _p(perm), v, d, _p(c_src), stream), "cce_gather_rows")
+        LAUNCHES["count"] += 1
+        c_sorted = 1
+    for i, (g, cap) in enumerate(plans):
+        ws_bytes = lib.cce_bwd_workspace_bytes(n_valid, d, v, g, cap)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        if i:
+            counters.zero_()
+        ev = _ev_begin("bwd")
+        _lib.check(lib.cce_bwd(_p(e), n, _p(c_src), _p(perm_padded), _p(row_map), _p(pos), _p(lse_c),
+                               _p(up_c), _p(block_zero), n_valid, d, v, float(softcap or 0.0), filt_eps,
+                               g, cap, c_sorted, _p(ws), ws_bytes, _p(de), int(fp32_de), _p(dc),
+                               _p(counters), _p(overflow), stream), "cce_bwd")
+        _ev_end("bwd", ev)
+        LAUNCHES["count"] += 3 * (-(-nt // g))
+        del ws
+        # the single-group plan can only overflow when the budget is below the worst case;
+        # checking needs one host read, paid only in that situation
+        if i + 1 == len(plans) or int(overflow.item()) == 0:
+            break
+        overflow.zero_()
+        LAST_OVERFLOW["count"] += 1
+    LAST_COUNTERS["counters"] = counters
     return de, dc, counters, perm
+
+
+def shat_budget_tiles() -> int:
+    """S-hat slots (64 KiB each) the backward may hold: CCE_SHAT_BUDGET_MB (default 2048)."""
+    budget = int(os.environ.get("CCE_SHAT_BUDGET_MB", "2048")) << 20
+    return max(1, budget // (BLOCK_TOKENS * BLOCK_VOCAB * 2))
 
 
 def f32_to_bf16(x: torch.Tensor) -> torch.Tensor:

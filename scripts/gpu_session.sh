@@ -1,0 +1,23 @@
+#!/bin/bash
+# usage: bash scripts/gpu_session.sh <tag> <steps...>   (each step is a named block below)
+tag=$1; shift
+out=gpurun_out/$tag; mkdir -p $out
+python -m paper_2411_09009_b200._build > $out/build.log 2>&1
+for s in "$@"; do
+  case $s in
+    tests) timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $out/pytest_gpu.log 2>&1; echo "exit $?" >> $out/pytest_gpu.log ;;
+    testsall) timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/pytest_gpu.log 2>&1; echo "exit $?" >> $out/pytest_gpu.log ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "exit $?" >> $out/smoke.log ;;
+    check) timeout 300 python scripts/gpu_check.py all > $out/check.log 2>&1; echo "exit $?" >> $out/check.log ;;
+    bench) timeout 600 python bench.py --steps 5 --warmup 3 > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
+    benchfast) timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
+    benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
+        timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
+    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+        python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $out/launches.log 2>&1; echo "exit $?" >> $out/launches.log ;;
+    ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_(lse|de|dc)_kernel" -s 1 -c 4 -o $out/prof \
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $out/ncu.log 2>&1; echo "exit $?" >> $out/ncu.log ;;
+    refarm) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/ref.log 2>&1; echo "exit $?" >> $out/ref.log ;;
+  esac
+done
+tail -n 4 $out/*.log

@@ -222,3 +222,38 @@ def test_all_ignored_mean_is_zero_not_nan(cuda_device):
     out.backward()
     assert out.item() == 0.0
     assert torch.all(e.grad == 0) and torch.all(c.grad == 0)
+
+
+def test_shat_budget_overflow_falls_back_to_groups(cuda_device, monkeypatch):
+    """A budget below the kept-tile count forces the grouped rerun; results are unchanged."""
+    rng = np.random.default_rng(21)
+    n, d, v = 700, 64, 3000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    base = _run(e, c, x)
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.setenv("CCE_SHAT_BUDGET_MB", "1")  # 16 slots: 6x12 tiles cannot fit
+    before = ops.LAST_OVERFLOW["count"]
+    small = _run(e, c, x)
+    assert ops.LAST_OVERFLOW["count"] == before + 1
+    for a, b in zip(base[:4], small[:4]):
+        assert O.rel_err(a, b) < 1e-2
+    assert np.array_equal(base[4], small[4])
+
+
+def test_sort_gather4_path_matches_sorted_copy(cuda_device, monkeypatch):
+    """CCE_SORT_GATHER=1 loads C rows through TMA gather4 instead of the materialised C[perm]."""
+    rng = np.random.default_rng(8)
+    n, d, v = 333, 128, 2500
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 1.5 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::5] = -1
+    a = _run(e, c, x)
+    monkeypatch.setenv("CCE_SORT_GATHER", "1")
+    b = _run(e, c, x)
+    assert np.array_equal(a[4], b[4])
+    for u, w in zip(a[:4], b[:4]):
+        assert np.array_equal(u, w)
