@@ -49,45 +49,53 @@ int cce_merge_shards(int num_shards, const float* lse_parts, const float* correc
 /* ---- vocabulary order (compute_vocab_order, kernels.py:145-160) ----
  * cce_ebar: column sums of the rows of E whose target != ignore_index (targets may be NULL =
  * all rows).  cce_vocab_order: key = C . ebar_sum / n_valid (the reference's mean_logits),
- * perm = stable descending argsort of key (ties by ascending index). */
+ * perm = stable descending argsort of key (ties by ascending index); n_valid is a device int. */
 int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_t n, int64_t d,
              float* ebar_sum, void* stream);
 size_t cce_sort_workspace_bytes(int64_t v);
-int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64_t v, int64_t d,
+int cce_vocab_order(const void* C, const float* ebar_sum, const int* n_valid, int64_t v, int64_t d,
                     int32_t* perm, float* key_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- backward (lse_backward, kernels.py:327-486) ----
- * cce_bwd_prep: perm padded to a multiple of 256 and its inverse, label positions in tile
- * order (-1 = ignored or owned by another shard), and the zero-upstream token-tile flags
- * (kernels.py:434-438).  perm may be NULL (natural order).
+ * cce_compact_rows: filter_ignored (kernels.py:494-510) on the device: row_map[k] = k-th row
+ * whose target != ignore_index (row_map sized ceil(n/128)*128, tail zero), *n_valid = count.
+ * Nothing is read back to the host.
+ * cce_bwd_prep: perm padded to a multiple of 256 and its inverse, and per ORIGINAL row the label
+ * position in tile order (-1 = ignored or owned by another shard).  perm may be NULL.
  *
- * cce_bwd: token tiles are processed in groups of `group_tiles`; kept tiles of a group take
- * compact 64 KiB bf16 S-hat slots, `capacity_tiles` of them (workspace: cce_bwd_workspace_bytes).
- * If a group keeps more tiles than the capacity, *overflow is set to 1 and the outputs are
- * invalid: rerun with capacity_tiles >= group_tiles * ceil(v/256) (never overflows).
- * Per group: (B1) recompute every 128x256 logit tile on the tensor cores, keep it iff it holds
- * a label or some S = exp(z - lse) >= eps (block_skip_decision, kernels.py:140-142, label tiles
- * exempt as in kernels.py:447-455; eps = 0 disables filtering) and store S-hat = up * (S - onehot)
- * of kept tiles; (B2) dE[n] = sum_m S-hat[n,m] C[m] and (B3) dC[m] (+)= sum_n S-hat[n,m]^T E[n],
- * both output-stationary in TMEM, no atomics.  de_out: [e_rows, d] bf16 (or fp32 if de_fp32),
- * written for every compact row; other rows must be zeroed by the caller.  dc: [v, d] bf16,
- * fully written.  counters[3] = {kept, eps-skipped, zero-upstream-skipped} tiles
- * (BackwardStats, kernels.py:66-76), accumulated (caller zeroes). */
+ * cce_bwd: rows are the compacted rows (row_map, *n_valid); E is compacted into the workspace
+ * (or, with e_gather, read through row_map by TMA gather4).  C is either the classifier in
+ * natural order (perm_padded NULL), sorted rows gathered on the fly (perm_padded, c_sorted = 0)
+ * or the pre-sorted C[perm] (c_sorted = 1, see cce_gather_rows).  Token tiles are processed in
+ * groups of `group_tiles`; kept tiles take compact 64 KiB bf16 S-hat slots, `capacity_tiles` of
+ * them.  Per group: (B1) recompute every 128x256 logit tile on the tensor cores and keep it iff
+ * it holds a label or some S = exp(z - lse) >= eps (block_skip_decision, kernels.py:140-142;
+ * label tiles exempt as in kernels.py:447-455; eps = 0 disables filtering; token tiles whose
+ * upstream is all zero are skipped, kernels.py:434-438), storing S-hat = up * (S - onehot);
+ * (B2) dE[n] = sum_m S-hat[n,m] C[m] and (B3) dC[m] (+)= sum_n S-hat[n,m]^T E[n], both
+ * output-stationary in TMEM, no atomics.  lse / upstream / pos are indexed by original row.
+ * de_out: [n, d] bf16 (or fp32 if de_fp32), written for every compact row; the caller zeroes it.
+ * dc: [v, d] bf16, fully written.  counters[3] += {kept, eps-skipped, zero-upstream-skipped}
+ * (BackwardStats, kernels.py:66-76).  If a group keeps more tiles than the capacity, *overflow
+ * is set and the outputs are invalid; a second call with run_if = overflow and
+ * capacity_tiles >= group_tiles * ceil(v/256) then recomputes them (every kernel of a call with
+ * *run_if == 0 exits immediately, so the fallback needs no host synchronisation). */
+int cce_compact_rows(const int64_t* targets, int64_t ignore_index, int64_t n, int32_t* row_map,
+                     int* n_valid, void* stream);
 int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t ignore_index,
-                 int64_t vocab_start, const float* upstream, int64_t n, int32_t* perm_padded,
-                 int32_t* inv_perm, int32_t* pos, uint8_t* block_zero, void* stream);
-size_t cce_bwd_workspace_bytes(int64_t n_rows, int64_t d, int64_t v, int64_t group_tiles,
+                 int64_t vocab_start, int64_t n, int32_t* perm_padded, int32_t* inv_perm, int32_t* pos,
+                 void* stream);
+size_t cce_bwd_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t group_tiles,
                                int64_t capacity_tiles);
-int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_padded,
-            const int32_t* row_map, const int32_t* pos, const float* lse, const float* upstream,
-            const uint8_t* block_zero, int64_t n_rows, int64_t d, int64_t v, float softcap, float eps,
-            int64_t group_tiles, int64_t capacity_tiles, int c_sorted, void* ws, size_t ws_bytes,
-            void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
-            void* stream);
+int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sorted,
+            const int32_t* row_map, const int* n_valid, const int32_t* pos, const float* lse,
+            const float* upstream, int64_t n, int64_t d, int64_t v, float softcap, float eps,
+            int64_t group_tiles, int64_t capacity_tiles, const int* run_if, int e_gather, void* ws,
+            size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+            int* overflow, void* stream);
 
-/* dst[i] = src[index[i]] for bf16 rows of `cols` elements.  With c_sorted != 0, cce_bwd takes C
- * already permuted this way (C[perm], the vocabulary-sorted classifier) and loads plain tiles;
- * perm_padded then only maps sorted rows back to dC rows. */
+/* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
+ * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */
 int cce_gather_rows(const void* src, const int32_t* index, int64_t rows, int64_t cols, void* dst,
                     void* stream);
 

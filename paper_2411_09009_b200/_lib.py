@@ -29,15 +29,16 @@ SIGNATURES = {
                                  c_void_p, c_void_p]),
     "cce_ebar": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p]),
     "cce_sort_workspace_bytes": (c_size, [c_i64]),
-    "cce_vocab_order": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p,
+    "cce_vocab_order": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p,
                                 c_void_p, c_size, c_void_p]),
-    "cce_bwd_prep": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p,
-                             c_void_p, c_void_p, c_void_p, c_void_p]),
+    "cce_compact_rows": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_void_p, c_void_p]),
+    "cce_bwd_prep": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p,
+                             c_void_p, c_void_p]),
     "cce_bwd_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64, c_i64]),
-    "cce_bwd": (c_int, [c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+    "cce_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                         c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_i64, c_i64,
-                        c_int, c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
-                        c_void_p]),
+                        c_void_p, c_int, c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p,
+                        c_void_p, c_void_p]),
     "cce_gather_rows": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "cce_f32_to_bf16": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "cce_indexed_dot": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_i64, c_i64,

@@ -67,25 +67,82 @@ __global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* 
   atomicAdd(&ebar_acc[col], acc);
 }
 
-// key[v] = C[v] . ebar  (fp32); one warp per vocab row.  Equals lse_forward's mean_logits
-// (kernels.py:305-308, :317-318), which is a mean of logits over the valid tokens.
+// key[v] = C[v] . ebar_sum / n_valid (fp32): the reference's mean_logits (kernels.py:305-308,
+// :317-318), a mean of logits over the valid tokens.  HBM-bound GEMV: ebar in smem, one warp per
+// row, 4 independent 16-byte loads in flight per lane.
 __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float* __restrict__ ebar_sum,
-                                float inv_n, int v, int d, float* __restrict__ key) {
+                                const int* __restrict__ n_valid, int v, int d, float* __restrict__ key) {
+  extern __shared__ float s_ebar[];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) s_ebar[j] = ebar_sum[j];
+  __syncthreads();
+  const float inv_n = *n_valid > 0 ? 1.0f / (float)*n_valid : 0.f;
   const int warps = blockDim.x >> 5;
-  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= v) return;
-  const __nv_bfloat16* c = C + (size_t)row * d;
-  float acc = 0.f;
-  for (int j = lane * 8; j < d; j += 256) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(c + j);
-    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+  const int n16 = d / 8;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < v; row += gridDim.x * warps) {
+    const uint4* c = reinterpret_cast<const uint4*>(C + (size_t)row * d);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int j = lane;
+    for (; j + 96 < n16; j += 128) {
+      uint4 raw[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc += __bfloat162float(h[q]) * ebar_sum[j + q];
+      for (int u = 0; u < 4; ++u) raw[u] = __ldg(c + j + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[u]);
+        const float* eb = s_ebar + (j + 32 * u) * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u] += __bfloat162float(h[q]) * eb[q];
+      }
+    }
+    for (; j < n16; j += 32) {
+      const uint4 raw = __ldg(c + j);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[0] += __bfloat162float(h[q]) * s_ebar[j * 8 + q];
+    }
+    float a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) key[row] = a * inv_n;
   }
+}
+
+// Stable compaction of the valid rows (filter_ignored, kernels.py:494-510), one block:
+// row_map[k] = k-th row with targets != ignore_index, *n_valid = their count.  row_map must be
+// pre-filled (entries past the count stay as they are, e.g. 0, so padded gathers stay in bounds).
+__global__ void compact_rows_kernel(const int64_t* __restrict__ targets, int64_t ignore_index, int n,
+                                    int32_t* __restrict__ row_map, int* __restrict__ n_valid) {
+  constexpr int T = 1024;
+  __shared__ int s_warp[T / 32];
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += T) {
+    const int i = c0 + threadIdx.x;
+    const bool ok = i < n && targets[i] != ignore_index;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+    const int before = __popc(bal & ((1u << lane) - 1));
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      int x = s_warp[lane];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) key[row] = acc * inv_n;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      s_warp[lane] = x;  // inclusive
+    }
+    __syncthreads();
+    const int base = s_base + (wid ? s_warp[wid - 1] : 0);
+    if (ok) row_map[base + before] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += s_warp[T / 32 - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_valid = s_base;
 }
 
 // out[i] = C[x_i] . E[i] (indexed_matmul, kernels.py:204-251); one warp per token row.
@@ -153,11 +210,12 @@ __global__ void label_pos_kernel(const int64_t* __restrict__ targets, int64_t ig
   pos[i] = r;
 }
 
-// block_zero[b] = all upstream of token tile b are exactly zero (kernels.py:434-438)
-__global__ void block_zero_kernel(const float* __restrict__ up, int n, uint8_t* __restrict__ bz) {
+// block_zero[b] = every upstream of compact token tile b is exactly zero (kernels.py:434-438)
+__global__ void block_zero_kernel(const float* __restrict__ up, const int32_t* __restrict__ row_map,
+                                  const int* __restrict__ n_valid, uint8_t* __restrict__ bz) {
   const int b = blockIdx.x;
   const int i = b * BM + threadIdx.x;
-  const bool nz = (i < n) && (up[i] != 0.f);
+  const bool nz = (i < *n_valid) && (up[row_map[i]] != 0.f);
   const int any = __syncthreads_or(nz);
   if (threadIdx.x == 0) bz[b] = any ? 0 : 1;
 }

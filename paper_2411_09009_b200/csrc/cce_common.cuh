@@ -24,11 +24,17 @@ constexpr int SHAT_TILE_BYTES = BM * BN * 2;  // one stored S-hat tile, bf16 row
 enum Mode { FWD = 0, BWD = 1 };
 
 // Forward (FWD) and backward filter pass (BWD, "B1") of the fused logit-tile kernel.
+//
+// Token rows: the forward runs on all n_total rows of E.  The backward runs on the compacted
+// valid rows (filter_ignored, kernels.py:494-510), whose count *n_valid lives on the device; when
+// it equals n_total the compaction is the identity and E is read directly.
 struct Params {
-  int n_rows;        // token rows handled (N, or N_valid after compaction in the backward)
+  int n_total;       // rows of E
+  const int* n_valid;  // device count of compacted rows (backward), nullptr = n_total
+  const int* run_if;   // device flag: kernel does nothing unless *run_if != 0 (nullptr = always)
   int d;             // hidden size
   int v;             // vocab rows of C (this shard)
-  int nt;            // token tiles covered by this launch (a group in the backward)
+  int nt;            // token tiles per launch (a group in the backward); clamped on the device
   int n_base;        // first token tile of this launch
   int mt;            // vocab tiles
   int splits;        // vocab splits per token tile (units = nt * splits)
@@ -38,15 +44,16 @@ struct Params {
   const int64_t* targets;
   int64_t ignore_index;
   int64_t vocab_start;
-  float2* part;      // [splits][n_rows]  (running max, running sum) in log2 units
-  float* correct;    // [n_rows] target logit (written by the tile that owns the label)
-  // backward filter pass
-  const float* lse;        // [n_rows] global log-sum-exp (natural log)
-  const float* upstream;   // [n_rows] dLoss/dloss_i, 0 at ignored rows
-  const int32_t* pos;      // [n_rows] label position in tile order, -1 if none
-  const int32_t* perm;     // [mt*BN] tile-order position -> C row (nullptr = identity)
-  const int32_t* row_map;  // [nt*BM] compact row -> E row / dE row (nullptr = identity)
-  const uint8_t* block_zero;  // [all token tiles] 1 if every upstream in the tile is zero
+  float2* part;      // [splits][n_total]  (running max, running sum) in log2 units
+  float* correct;    // [n_total] target logit (written by the tile that owns the label)
+  // backward filter pass (lse / upstream / pos are indexed by ORIGINAL row)
+  const float* lse;        // global log-sum-exp (natural log)
+  const float* upstream;   // dLoss/dloss_i, 0 at ignored rows
+  const int32_t* pos;      // label position in tile order, -1 if none
+  const int32_t* perm;     // [mt*BN] tile-order position -> C row for gathers (nullptr = plain)
+  const int32_t* row_map;  // compact row -> original row (padded); identity when no compaction
+  int e_gather;            // 1: load E rows through row_map with gather4 (else E is compacted)
+  const uint8_t* block_zero;  // [token tiles] 1 if every upstream in the compact tile is zero
   float eps;               // filter threshold (0 = filtering off)
   __nv_bfloat16* shat;     // [capacity][BM][BN] S-hat of kept tiles, compact slots
   int32_t* slot_of;        // [nt*mt] slot of tile (local n, m), -1 if not stored (host: -1)
@@ -60,19 +67,40 @@ struct Params {
 
 // dE pass ("B2") and dC pass ("B3").
 struct GradParams {
-  int n_rows, d, v, mt, ndc;
-  int n_base, g;           // token tiles [n_base, n_base + g) of this group
+  int n_total, d, v, mt, ndc;
+  const int* n_valid;
+  const int* run_if;
+  int n_base, g;           // token tiles [n_base, n_base + g) of this group (clamped on device)
   const int32_t* slot_of;  // [g*mt]
   const int* cnt_n;
   const int* cnt_m;
   const int32_t* perm;     // C-row gather index for tile loads (padded), or nullptr
   const int32_t* perm_store;  // tile-order position -> dC row (padded), or nullptr
-  const int32_t* row_map;  // padded, or nullptr
-  __nv_bfloat16* de_bf16;  // [N_orig][d]   (one of de_bf16 / de_f32)
+  const int32_t* row_map;  // compact row -> original row (padded)
+  int e_gather;            // 1: gather E rows through row_map (else E is compacted)
+  int atoms3d;             // 1: d % 64 == 0, operand tiles load as one 3-D TMA box (all atoms)
+  __nv_bfloat16* de_bf16;  // [n_total][d]   (one of de_bf16 / de_f32)
   float* de_f32;
   __nv_bfloat16* dc;       // [v][d]
   int accumulate;          // dC: add to the existing values (groups after the first)
 };
+
+// Device-side view of the compaction: valid row count, token tiles of this launch.
+struct Rows {
+  int n;        // rows handled (compacted count)
+  bool ident;   // compaction is the identity
+  int g;        // token tiles of this launch after clamping
+  __device__ __forceinline__ Rows(const int* n_valid, int n_total, int n_base, int nt) {
+    n = n_valid ? *n_valid : n_total;
+    ident = (n == n_total);
+    const int nt_dev = (n + BM - 1) / BM;
+    g = max(0, min(nt, nt_dev - n_base));
+  }
+};
+
+__device__ __forceinline__ bool skip_launch(const int* run_if) {
+  return run_if != nullptr && *run_if == 0;
+}
 
 __device__ __forceinline__ void advance_stage(int& stage, uint32_t& phase, int stages) {
   if (++stage == stages) {

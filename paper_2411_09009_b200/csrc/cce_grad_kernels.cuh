@@ -8,9 +8,9 @@
 //   B2 cce_de_kernel : unit = (token tile n, 256 D-columns).  TMEM accumulates
 //                      dE[n, dchunk] = sum over kept m of S-hat[n,m] (128x256, K-major A) x
 //                      C[m, dchunk] (256x256, MN-major B), two K-steps of 128 vocab per tile.
-//   B3 cce_dc_kernel : unit = (vocab tile m, 256 D-columns).  TMEM accumulates both 128-row
-//                      halves of dC[m, dchunk] = sum over kept n of S-hat^T (MN-major A) x
-//                      E[n, dchunk] (MN-major B), two K-steps of 64 tokens per tile.
+//   B3 cce_dc_kernel : unit = (vocab tile m, 256 D-columns, 128-row vocab half).  TMEM
+//                      accumulates dC[m half, dchunk] = sum over kept n of S-hat^T (MN-major A)
+//                      x E[n, dchunk] (MN-major B), two K-steps of 64 tokens per tile.
 //
 // Both: persistent, 192 threads (warp 0 TMA producer scanning the kept-tile map with the whole
 // warp, warp 1 MMA issuer, warps 2..5 epilogue writing bf16 / fp32 rows straight to HBM).
@@ -23,8 +23,8 @@ constexpr int DE_STAGES = 2;
 constexpr int DE_A_BYTES = BM * 128 * 2;        // S-hat [128 tok][128 voc]  = 32 KiB (2 atoms)
 constexpr int DE_B_BYTES = 128 * DCH * 2;       // C [128 voc][256 d]       = 64 KiB (4 atoms)
 constexpr int DE_STAGE_BYTES = DE_A_BYTES + DE_B_BYTES;
-constexpr int DC_STAGES = 3;
-constexpr int DC_A_BYTES = 64 * BN * 2;         // S-hat [64 tok][256 voc]  = 32 KiB (4 atoms)
+constexpr int DC_STAGES = 4;
+constexpr int DC_A_BYTES = 64 * 128 * 2;        // S-hat [64 tok][128 voc]  = 16 KiB (2 atoms)
 constexpr int DC_B_BYTES = 64 * DCH * 2;        // E [64 tok][256 d]        = 32 KiB (4 atoms)
 constexpr int DC_STAGE_BYTES = DC_A_BYTES + DC_B_BYTES;
 
@@ -67,7 +67,9 @@ __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_b
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_de_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmC,
-                  const __grid_constant__ CUtensorMap tmCg, const GradParams p) {
+                  const __grid_constant__ CUtensorMap tmC3, const __grid_constant__ CUtensorMap tmCg,
+                  const GradParams p) {
+  if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -96,13 +98,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int units = p.g * p.ndc;  // dchunk-major: concurrent CTAs share C[:, dchunk]
+  const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
+  const int G = rows.g;
+  const int units = G * p.ndc;  // dchunk-major: concurrent CTAs share C[:, dchunk]
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int dc = u / p.g, ln = u % p.g;
+      const int dc = u / G, ln = u % G;
       for_each_kept(p.slot_of + (size_t)ln * p.mt, p.mt, 1, [&](int m, int slot) {
         for (int h = 0; h < 2; ++h) {
           RowGather rgc;
@@ -112,14 +116,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], DE_STAGE_BYTES);
-            tma_load_2d(&tmS, &full[stage], sa, 128 * h, slot * BM);
-            tma_load_2d(&tmS, &full[stage], sa + BM * 128, 128 * h + 64, slot * BM);
+            // S-hat [128 tok][128 voc] as 2 swizzle atoms in one box
+            tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, 2 * h);
+            if (p.atoms3d && p.perm == nullptr)  // C [128 voc][256 d] as 4 atoms in one box
+              tma_load_3d(&tmC3, &full[stage], sb, 0, m * BN + 128 * h, dc * (DCH / 64));
           }
           __syncwarp();
+          if (!(p.atoms3d && p.perm == nullptr)) {
 #pragma unroll 1
-          for (int a = 0; a < DCH / 64; ++a)
-            load_rows_warp<128>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage], sb + a * (128 * 128),
-                                dc * DCH + 64 * a, m * BN + 128 * h);
+            for (int a = 0; a < DCH / 64; ++a)
+              load_rows_warp<128>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage], sb + a * (128 * 128),
+                                  dc * DCH + 64 * a, m * BN + 128 * h);
+          }
           advance_stage(stage, phase, DE_STAGES);
         }
       });
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int t = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-        const int ln = u % p.g;
+        const int ln = u % G;
         const int buf = t & 1;
         const int ksteps = 2 * p.cnt_n[ln];
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
@@ -160,14 +168,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     int t = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-      const int dc = u / p.g, ln = u % p.g;
+      const int dc = u / G, ln = u % G;
       const int buf = t & 1;
       mbar_wait(&acc_full[buf], (t >> 1) & 1);
       tc_fence_after();
       const bool has = p.cnt_n[ln] > 0;
       const int grow = (p.n_base + ln) * BM + row;
-      const bool valid = grow < p.n_rows;
-      const int drow = valid ? (p.row_map ? p.row_map[grow] : grow) : 0;
+      const bool valid = grow < rows.n;
+      const int drow = valid ? p.row_map[grow] : 0;
 #pragma unroll 1
       for (int c = 0; c < DCH / 32; ++c) {
         const int col = dc * DCH + c * 32;
@@ -205,15 +213,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_dc_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmE,
-                  const __grid_constant__ CUtensorMap tmEg, const GradParams p) {
+                  const __grid_constant__ CUtensorMap tmE3, const __grid_constant__ CUtensorMap tmEg,
+                  const GradParams p) {
+  if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DC_STAGES * DC_STAGE_BYTES);
   uint64_t* empty = full + DC_STAGES;
   uint64_t* acc_full = empty + DC_STAGES;
-  uint64_t* acc_free = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
+  uint64_t* acc_free = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -223,8 +233,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(&acc_full[0], 1);
-    mbar_init(&acc_free[0], 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_free[i], 128);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -232,32 +244,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int units = p.mt * p.ndc;  // vocab-tile-major: concurrent CTAs share the m's S-hat tiles
+  const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
+  const int G = rows.g;
+  // unit u = ((m * ndc) + dc) * 2 + vh: the two vocab halves of one (m, dchunk) run side by side
+  // and share their E / S-hat loads through L2
+  const int units = p.mt * p.ndc * 2;
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int m = u / p.ndc, dc = u % p.ndc;
-      for_each_kept(p.slot_of + m, p.g, p.mt, [&](int ln, int slot) {
+      const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
+      for_each_kept(p.slot_of + m, G, p.mt, [&](int ln, int slot) {
         const int n = p.n_base + ln;
         for (int h = 0; h < 2; ++h) {
           RowGather rge;
-          rge.load(p.row_map, n * BM + 64 * h, 64);
+          rge.load(p.e_gather ? p.row_map : nullptr, n * BM + 64 * h, 64);
           uint8_t* sa = smem + stage * DC_STAGE_BYTES;
           uint8_t* sb = sa + DC_A_BYTES;
+          const bool e3 = p.atoms3d && !p.e_gather;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], DC_STAGE_BYTES);
-#pragma unroll 1
-            for (int a = 0; a < BN / 64; ++a)
-              tma_load_2d(&tmS, &full[stage], sa + a * (64 * 128), 64 * a, slot * BM + 64 * h);
+            // S-hat^T half: tokens [64h, +64) x vocab atoms 2vh, 2vh+1 in one box
+            tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM + 64 * h, 2 * vh);
+            if (e3)  // E [64 tok][256 d] as 4 atoms in one box
+              tma_load_3d(&tmE3, &full[stage], sb, 0, n * BM + 64 * h, dc * (DCH / 64));
           }
           __syncwarp();
+          if (!e3) {
 #pragma unroll 1
-          for (int a = 0; a < DCH / 64; ++a)
-            load_rows_warp<64>(&tmE, &tmEg, rge, p.row_map != nullptr, &full[stage], sb + a * (64 * 128),
-                               dc * DCH + 64 * a, n * BM + 64 * h);
+            for (int a = 0; a < DCH / 64; ++a)
+              load_rows_warp<64>(&tmE, &tmEg, rge, p.e_gather != 0, &full[stage], sb + a * (64 * 128),
+                                 dc * DCH + 64 * a, n * BM + 64 * h);
+          }
           advance_stage(stage, phase, DC_STAGES);
         }
       });
@@ -269,26 +289,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int t = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-        const int m = u / p.ndc;
+        const int m = (u >> 1) / p.ndc;
+        const int buf = t & 1;
         const int ksteps = 2 * p.cnt_m[m];
-        mbar_wait(&acc_free[0], (t & 1) ^ 1);
+        mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * DCH;
         for (int s = 0; s < ksteps; ++s) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * DC_STAGE_BYTES);
           const uint32_t b0 = a0 + DC_A_BYTES;
 #pragma unroll
-          for (int vh = 0; vh < 2; ++vh)
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              mma_bf16_ss(tmem_base + vh * DCH,
-                          make_sdesc(a0 + 2 * vh * (64 * 128) + ks * 2048, 64 * 128, 1024),
-                          make_sdesc(b0 + ks * 2048, 64 * 128, 1024), IDESC, (s | ks) != 0);
+          for (int ks = 0; ks < 4; ++ks)
+            mma_bf16_ss(d_tmem, make_sdesc(a0 + ks * 2048, 64 * 128, 1024),
+                        make_sdesc(b0 + ks * 2048, 64 * 128, 1024), IDESC, (s | ks) != 0);
           mma_commit(&empty[stage]);
           advance_stage(stage, phase, DC_STAGES);
         }
-        mma_commit(&acc_full[0]);
+        mma_commit(&acc_full[buf]);
       }
     }
   } else {
@@ -297,50 +316,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     int t = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-      const int m = u / p.ndc, dc = u % p.ndc;
-      mbar_wait(&acc_full[0], t & 1);
+      const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
+      const int buf = t & 1;
+      mbar_wait(&acc_full[buf], (t >> 1) & 1);
       tc_fence_after();
       const bool has = p.cnt_m[m] > 0;
+      const int vpos = m * BN + vh * 128 + row;
+      const bool vok = vpos < p.v;
       if (has || !p.accumulate) {
+        const int vrow = vok ? (p.perm_store ? p.perm_store[vpos] : vpos) : 0;
 #pragma unroll 1
-        for (int vh = 0; vh < 2; ++vh) {
-          const int vpos = m * BN + vh * 128 + row;
-          const bool vok = vpos < p.v;
-          const int vrow = vok ? (p.perm_store ? p.perm_store[vpos] : vpos) : 0;
-#pragma unroll 1
-          for (int c = 0; c < DCH / 32; ++c) {
-            const int col = dc * DCH + c * 32;
-            float x[32];
-            if (has) {
-              uint32_t r[32];
-              tmem_ld32(tmem_base + lane_off + vh * DCH + c * 32, r);
-              tmem_ld_wait();
+        for (int c = 0; c < DCH / 32; ++c) {
+          const int col = dc * DCH + c * 32;
+          float x[32];
+          if (has) {
+            uint32_t r[32];
+            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 32, r);
+            tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
-            } else {
+            for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+          } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) x[j] = 0.f;
+            for (int j = 0; j < 32; ++j) x[j] = 0.f;
+          }
+          if (vok && col < p.d) {
+            __nv_bfloat16* dst = p.dc + (size_t)vrow * p.d + col;
+            const int lim = p.d - col;
+            if (p.accumulate) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8)
+                if (j < lim) {
+                  const uint4 old = *reinterpret_cast<const uint4*>(dst + j);
+                  const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&old);
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) x[j + q] += __bfloat162float(ob[q]);
+                }
             }
-            if (vok && col < p.d) {
-              __nv_bfloat16* dst = p.dc + (size_t)vrow * p.d + col;
-              const int lim = p.d - col;
-              if (p.accumulate) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 8)
-                  if (j < lim) {
-                    const uint4 old = *reinterpret_cast<const uint4*>(dst + j);
-                    const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&old);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) x[j + q] += __bfloat162float(ob[q]);
-                  }
-              }
-              store_row32(nullptr, dst, x, lim);
-            }
+            store_row32(nullptr, dst, x, lim);
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_free[0]);
+      mbar_arrive(&acc_free[buf]);
     }
   }
   tc_fence_before();

@@ -73,6 +73,23 @@ bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int
   return r == CUDA_SUCCESS;
 }
 
+// 3-D view of a row-major bf16 [rows, cols] matrix as {64 (within atom), rows, cols/64 atoms};
+// a box {64, box_rows, box_atoms} lands as box_atoms consecutive 128B-swizzled [box_rows][64]
+// atoms, i.e. one request for a whole MN-major / multi-atom K-major operand tile.
+bool make_tmap3d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows,
+                 int box_atoms) {
+  auto enc = get_encode_fn();
+  if (!enc || cols % 64 != 0) return false;
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols * 2), 128};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_atoms)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int gather_box_rows() {
   static int rows = [] {
     const char* e = getenv("CCE_GATHER4_BOX_ROWS");
@@ -124,36 +141,44 @@ int choose_splits(int nt, int mt, int grid, bool prefer_fine) {
   return best;
 }
 
-// Backward workspace: compact S-hat slots + per-group maps.
+// Backward workspace: compact S-hat slots + compacted E + per-group maps.
 struct BwdWs {
   __nv_bfloat16* shat;
-  int32_t* slot_of;  // [group_tiles * mt], -1 = not stored
-  int* slot_ctr;     // [1]
-  int* cnt_n;        // [group_tiles]
-  int* cnt_m;        // [mt]
-  size_t map_bytes;  // slot_of
-  size_t zero_bytes; // slot_ctr + counts
+  __nv_bfloat16* e_compact;  // [n][d] compacted rows of E
+  uint8_t* block_zero;       // [token tiles]
+  int32_t* slot_of;          // [group_tiles * mt], -1 = not stored
+  int* slot_ctr;             // [1]
+  int* cnt_n;                // [group_tiles]
+  int* cnt_m;                // [mt]
+  size_t map_bytes;          // slot_of
+  size_t zero_bytes;         // slot_ctr + counts
   size_t total;
 };
 
-BwdWs bwd_layout(void* base, int64_t v, int64_t group_tiles, int64_t capacity) {
+BwdWs bwd_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t group_tiles, int64_t capacity) {
   const int64_t mt = (v + cce::BN - 1) / cce::BN;
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t shat = (size_t)capacity * cce::SHAT_TILE_BYTES;
+  const int64_t nt = (n + cce::BM - 1) / cce::BM;
+  auto up = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  const size_t shat = up((size_t)capacity * cce::SHAT_TILE_BYTES);
+  const size_t ec = up((size_t)n * d * 2);
+  const size_t bz = up((size_t)nt);
   const size_t map = up((size_t)group_tiles * mt * 4);
   const size_t ctr = 256;
   const size_t cn = up((size_t)group_tiles * 4);
   const size_t cm = up((size_t)mt * 4);
   uint8_t* b = static_cast<uint8_t*>(base);
   BwdWs w;
-  w.shat = reinterpret_cast<__nv_bfloat16*>(b);
-  w.slot_of = reinterpret_cast<int32_t*>(b + shat);
-  w.slot_ctr = reinterpret_cast<int*>(b + shat + map);
-  w.cnt_n = reinterpret_cast<int*>(b + shat + map + ctr);
-  w.cnt_m = reinterpret_cast<int*>(b + shat + map + ctr + cn);
+  size_t o = 0;
+  w.shat = reinterpret_cast<__nv_bfloat16*>(b + o); o += shat;
+  w.e_compact = reinterpret_cast<__nv_bfloat16*>(b + o); o += ec;
+  w.block_zero = b + o; o += bz;
+  w.slot_of = reinterpret_cast<int32_t*>(b + o); o += map;
+  w.slot_ctr = reinterpret_cast<int*>(b + o); o += ctr;
+  w.cnt_n = reinterpret_cast<int*>(b + o); o += cn;
+  w.cnt_m = reinterpret_cast<int*>(b + o); o += cm;
   w.map_bytes = map;
   w.zero_bytes = ctr + cn + cm;
-  w.total = shat + map + ctr + cn + cm;
+  w.total = o;
   return w;
 }
 
@@ -190,7 +215,7 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   if (!make_tmap(&tmE, E, n, d, cce::BM) || !make_tmap(&tmC, C, v, d, cce::BN))
     return fail("cce_fwd: cuTensorMapEncodeTiled failed");
   cce::Params p{};
-  p.n_rows = (int)n;
+  p.n_total = (int)n;
   p.d = (int)d;
   p.v = (int)v;
   p.nt = nt;
@@ -250,7 +275,7 @@ int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_
   return 0;
 }
 
-int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64_t v, int64_t d,
+int cce_vocab_order(const void* C, const float* ebar_sum, const int* n_valid, int64_t v, int64_t d,
                     int32_t* perm, float* key_out, void* ws, size_t ws_bytes, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_vocab_order: D must be a multiple of 8");
@@ -262,9 +287,10 @@ int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64
   int32_t* idx = reinterpret_cast<int32_t*>(key_sorted + v);
   void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(idx + v) + 255) & ~uintptr_t(255));
   size_t tmp_bytes = need - 3 * (size_t)v * 4 - 1024;
-  const float inv_n = n_valid > 0 ? 1.0f / (float)n_valid : 0.f;
-  cce::sort_key_kernel<<<(unsigned)((v + 7) / 8), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(C), ebar_sum, inv_n, (int)v, (int)d, key);
+  CCE_CUDA(cudaFuncSetAttribute(cce::sort_key_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(d * sizeof(float))));
+  cce::sort_key_kernel<<<(unsigned)std::min<int64_t>((v + 7) / 8, 4 * num_sms()), 256, d * sizeof(float), stream>>>(
+      static_cast<const __nv_bfloat16*>(C), ebar_sum, n_valid, (int)v, (int)d, key);
   CCE_CUDA(cudaGetLastError());
   cce::iota_kernel<<<(unsigned)((v + 255) / 256), 256, 0, stream>>>(idx, (int)v);
   CCE_CUDA(cudaGetLastError());
@@ -275,9 +301,19 @@ int cce_vocab_order(const void* C, const float* ebar_sum, int64_t n_valid, int64
 }
 
 // Backward prep: padded perm / inverse perm, label positions, zero-upstream tile flags.
+int cce_compact_rows(const int64_t* targets, int64_t ignore_index, int64_t n, int32_t* row_map,
+                     int* n_valid, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  const int64_t npad = ((n + cce::BM - 1) / cce::BM) * cce::BM;
+  CCE_CUDA(cudaMemsetAsync(row_map, 0, std::max<int64_t>(npad, 1) * sizeof(int32_t), stream));
+  cce::compact_rows_kernel<<<1, 1024, 0, stream>>>(targets, ignore_index, (int)n, row_map, n_valid);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t ignore_index,
-                 int64_t vocab_start, const float* upstream, int64_t n, int32_t* perm_padded,
-                 int32_t* inv_perm, int32_t* pos, uint8_t* block_zero, void* stream_ptr) {
+                 int64_t vocab_start, int64_t n, int32_t* perm_padded, int32_t* inv_perm, int32_t* pos,
+                 void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   const int64_t vpad = ((v + cce::BN - 1) / cce::BN) * cce::BN;
   if (perm) {
@@ -289,60 +325,69 @@ int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t
     cce::label_pos_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
         targets, ignore_index, vocab_start, (int)v, perm ? inv_perm : nullptr, (int)n, pos);
     CCE_CUDA(cudaGetLastError());
-    const int nt = (int)((n + cce::BM - 1) / cce::BM);
-    cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, (int)n, block_zero);
-    CCE_CUDA(cudaGetLastError());
   }
   return 0;
 }
 
-size_t cce_bwd_workspace_bytes(int64_t n_rows, int64_t d, int64_t v, int64_t group_tiles,
+size_t cce_bwd_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t group_tiles,
                                int64_t capacity_tiles) {
-  (void)n_rows;
-  (void)d;
-  return bwd_layout(nullptr, v, group_tiles, capacity_tiles).total;
+  return bwd_layout(nullptr, n, d, v, group_tiles, capacity_tiles).total;
 }
 
-// Filtered backward (lse_backward).  Rows are the (possibly compacted) token rows; row_map maps
-// them to E / dE rows (nullptr = identity, else padded to a multiple of 128 entries).  Token tiles
-// are processed in groups of `group_tiles`: filter pass (B1) -> dE pass (B2) -> dC pass (B3,
-// accumulating into dc after the first group).  de_out is written for every compact row (bf16,
-// or fp32 when de_fp32 != 0); rows outside the compaction must be zeroed by the caller.
-int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_padded,
-            const int32_t* row_map, const int32_t* pos, const float* lse, const float* upstream,
-            const uint8_t* block_zero, int64_t n_rows, int64_t d, int64_t v, float softcap, float eps,
-            int64_t group_tiles, int64_t capacity_tiles, int c_sorted, void* ws, size_t ws_bytes,
-            void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
-            void* stream_ptr) {
+// Filtered backward (lse_backward).  See include/cce_b200.h.
+int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sorted,
+            const int32_t* row_map, const int* n_valid, const int32_t* pos, const float* lse,
+            const float* upstream, int64_t n, int64_t d, int64_t v, float softcap, float eps,
+            int64_t group_tiles, int64_t capacity_tiles, const int* run_if, int e_gather, void* ws,
+            size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+            int* overflow, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd: D must be a multiple of 8");
-  if (n_rows == 0) return 0;
-  if (group_tiles < 1) return fail("cce_bwd: group_tiles must be >= 1");
-  if (capacity_tiles < 1) return fail("cce_bwd: capacity_tiles must be >= 1");
-  const BwdWs w = bwd_layout(ws, v, group_tiles, capacity_tiles);
+  if (n <= 0) return 0;
+  if (group_tiles < 1 || capacity_tiles < 1) return fail("cce_bwd: group_tiles / capacity_tiles must be >= 1");
+  const BwdWs w = bwd_layout(ws, n, d, v, group_tiles, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd: workspace too small");
   if (int e = ensure_attr(cce::cce_lse_kernel<cce::BWD>, kLseSmem)) return e;
   if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
   if (int e = ensure_attr(cce::cce_dc_kernel, kDcSmem)) return e;
-  const int nt = (int)((n_rows + cce::BM - 1) / cce::BM);
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
   const int grid = num_sms();
   const int gbox = gather_box_rows();
-  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64;
+  // compact E (filter_ignored) unless rows are gathered on the fly; zero-upstream tile flags
+  const void* e_src = E;
+  if (!e_gather) {
+    cce::gather_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_compact);
+    CCE_CUDA(cudaGetLastError());
+    e_src = w.e_compact;
+  }
+  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  CCE_CUDA(cudaGetLastError());
+  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3;
   const int64_t shat_rows = capacity_tiles * cce::BM;
-  bool ok = make_tmap(&tmE, E, e_rows, d, cce::BM) && make_tmap(&tmEg, E, e_rows, d, gbox) &&
+  const bool atoms3d = d % 64 == 0;
+  bool ok = make_tmap(&tmE, e_src, n, d, cce::BM) && make_tmap(&tmEg, E, n, d, gbox) &&
             make_tmap(&tmC, C, v, d, cce::BN) && make_tmap(&tmCg, C, v, d, gbox) &&
-            make_tmap(&tmC128, C, v, d, 128) && make_tmap(&tmE64, E, e_rows, d, 64) &&
-            make_tmap(&tmS128, w.shat, shat_rows, cce::BN, 128) &&
-            make_tmap(&tmS64, w.shat, shat_rows, cce::BN, 64);
+            make_tmap(&tmC128, C, v, d, 128) && make_tmap(&tmE64, e_src, n, d, 64) &&
+            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 2) &&
+            make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
+  if (ok && atoms3d)
+    ok = make_tmap3d(&tmC3, C, v, d, 128, cce::DCH / 64) && make_tmap3d(&tmE3, e_src, n, d, 64, cce::DCH / 64);
+  else {
+    tmC3 = tmC128;
+    tmE3 = tmE64;
+  }
   if (!ok) return fail("cce_bwd: cuTensorMapEncodeTiled failed");
   for (int g0 = 0; g0 < nt; g0 += (int)group_tiles) {
     const int g = std::min((int)group_tiles, nt - g0);
     CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, w.map_bytes, stream));
     CCE_CUDA(cudaMemsetAsync(w.slot_ctr, 0, w.zero_bytes, stream));
     cce::Params p{};
-    p.n_rows = (int)n_rows;
+    p.n_total = (int)n;
+    p.n_valid = n_valid;
+    p.run_if = run_if;
     p.d = (int)d;
     p.v = (int)v;
     p.nt = g;
@@ -356,7 +401,8 @@ int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_pa
     p.pos = pos;
     p.perm = c_sorted ? nullptr : perm_padded;
     p.row_map = row_map;
-    p.block_zero = block_zero;
+    p.e_gather = e_gather;
+    p.block_zero = w.block_zero;
     p.eps = eps;
     p.shat = w.shat;
     p.slot_of = w.slot_of;
@@ -370,7 +416,9 @@ int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_pa
         tmE, tmEg, tmC, tmCg, p);
     CCE_CUDA(cudaGetLastError());
     cce::GradParams q{};
-    q.n_rows = (int)n_rows;
+    q.n_total = (int)n;
+    q.n_valid = n_valid;
+    q.run_if = run_if;
     q.d = (int)d;
     q.v = (int)v;
     q.mt = mt;
@@ -383,13 +431,15 @@ int cce_bwd(const void* E, int64_t e_rows, const void* C, const int32_t* perm_pa
     q.perm = c_sorted ? nullptr : perm_padded;
     q.perm_store = perm_padded;
     q.row_map = row_map;
+    q.e_gather = e_gather;
+    q.atoms3d = atoms3d ? 1 : 0;
     q.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
-    cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmCg, q);
+    cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmC3, tmCg, q);
     CCE_CUDA(cudaGetLastError());
-    cce::cce_dc_kernel<<<std::min(grid, mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmEg, q);
+    cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmEg, q);
     CCE_CUDA(cudaGetLastError());
   }
   return 0;

@@ -20,13 +20,13 @@
 namespace cce {
 
 struct TileIter {
-  // Static persistent schedule: unit u = s * nt + n (token tile fastest), so the CTAs running
+  // Static persistent schedule: unit u = s * g + n (token tile fastest), so the CTAs running
   // concurrently share the same vocab tiles of C while E stays L2-resident.
-  int unit, units, m, m_end, n, s;
+  int unit, units, m, m_end, n, s, g;
   const Params* p;
   __device__ void begin_unit() {
-    n = p->n_base + unit % p->nt;
-    s = unit / p->nt;
+    n = p->n_base + unit % g;
+    s = unit / g;
     m = (int)(((long long)s * p->mt) / p->splits);
     m_end = (int)(((long long)(s + 1) * p->mt) / p->splits);
   }
@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
                    const Params p) {
   constexpr int STAGES = LSE_STAGES;
+  if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -72,21 +73,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  const Rows rows(p.n_valid, p.n_total, p.n_base, p.nt);
   TileIter it;
   it.p = &p;
-  it.units = p.nt * p.splits;
+  it.g = rows.g;
+  it.units = rows.g * p.splits;
 
   if (warp == 0) {
     // ================================ TMA producer (whole warp) ===========================
     int stage = 0;
     uint32_t phase = 0;
-    const bool gather_e = p.row_map != nullptr;
+    const bool gather_e = p.e_gather != 0;
     const bool gather_c = p.perm != nullptr;
     RowGather rge, rgc;
     for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
       it.begin_unit();
       if (MODE == BWD && p.block_zero[it.n]) continue;
-      rge.load(p.row_map, it.n * BM, BM);
+      rge.load(p.e_gather ? p.row_map : nullptr, it.n * BM, BM);
       for (; it.m < it.m_end; ++it.m) {
         rgc.load(p.perm, it.m * BN, BN);
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
       it.begin_unit();
       const int grow = it.n * BM + row;
-      const bool valid = grow < p.n_rows;
+      const bool valid = grow < rows.n;
       if (MODE == FWD) {
         int64_t tpos = -1;
         if (valid) {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive(&acc_free[buf]);
         }
         if (valid) {
-          p.part[(size_t)it.s * p.n_rows + grow] = make_float2(run_m, run_s);
+          p.part[(size_t)it.s * p.n_total + grow] = make_float2(run_m, run_s);
           if (have_corr) p.correct[grow] = corr;
         }
       } else {
@@ -202,9 +205,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (epi_tid == 0) atomicAdd(&p.counters[2], (unsigned long long)(it.m_end - it.m));
           continue;
         }
-        const float lse2 = valid ? p.lse[grow] * LOG2E : INFINITY;
-        const float up_r = valid ? p.upstream[grow] : 0.f;
-        const int pos_r = valid ? p.pos[grow] : -1;
+        const int orow = valid ? p.row_map[grow] : 0;
+        const float lse2 = valid ? p.lse[orow] * LOG2E : INFINITY;
+        const float up_r = valid ? p.upstream[orow] : 0.f;
+        const int pos_r = valid ? p.pos[orow] : -1;
         const int ln = it.n - p.n_base;
         for (; it.m < it.m_end; ++it.m, ++t) {
           const int buf = t & 1;
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               int slot = atomicAdd(p.slot_ctr, 1);
               if (slot >= p.capacity) {
                 slot = -1;
-                atomicExch(p.overflow, 1);
+                if (p.overflow) atomicExch(p.overflow, 1);
               } else {
                 p.slot_of[(size_t)ln * p.mt + it.m] = slot;
                 atomicAdd(&p.cnt_n[ln], 1);

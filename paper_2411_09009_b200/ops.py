@@ -25,7 +25,7 @@ EPSILON_DEFAULT = 2.0 ** -12   # core.py:27
 # enabled, an event pair is recorded on the launching stream around each cce_fwd / cce_bwd call.
 KERNEL_EVENTS: dict[str, list] | None = None
 LAST_COUNTERS: dict = {}
-LAST_OVERFLOW = {"count": 0}  # backward reruns caused by S-hat slot overflow
+LAST_OVERFLOW: dict = {}  # device flag of the last backward: 1 if the fallback pass ran
 LAUNCHES = {"count": 0}   # kernels launched from libcce_b200.so (bench.py's gpu_launches)
 
 
@@ -128,19 +128,23 @@ def indexed_dot(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap:
     return out
 
 
-def vocab_order(e, c, targets, ignore_index: int, n_valid: int):
-    """(perm, mean_logits): stable descending sort of C . mean(E[valid]) (kernels.py:145-160)."""
+def vocab_order(e, c, targets, ignore_index: int, n_valid):
+    """(perm, mean_logits): stable descending sort of C . mean(E[valid]) (kernels.py:145-160).
+
+    `n_valid` is the device int32 count of valid rows (or a host int)."""
     lib = _lib.load()
     n, d = e.shape
     v = c.shape[0]
     dev = e.device
+    if not torch.is_tensor(n_valid):
+        n_valid = torch.tensor([int(n_valid)], dtype=torch.int32, device=dev)
     ebar = torch.empty(d, dtype=torch.float32, device=dev)
     _lib.check(lib.cce_ebar(_p(e), _p(targets), int(ignore_index), n, d, _p(ebar), _stream(dev)), "cce_ebar")
     perm = torch.empty(v, dtype=torch.int32, device=dev)
     key = torch.empty(v, dtype=torch.float32, device=dev)
     ws_bytes = lib.cce_sort_workspace_bytes(v)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    _lib.check(lib.cce_vocab_order(_p(c), _p(ebar), int(n_valid), v, d, _p(perm), _p(key), _p(ws),
+    _lib.check(lib.cce_vocab_order(_p(c), _p(ebar), _p(n_valid), v, d, _p(perm), _p(key), _p(ws),
                                    ws_bytes, _stream(dev)), "cce_vocab_order")
     LAUNCHES["count"] += 3 + 5  # ebar, sort key, iota + CUB onesweep radix sort passes
     return perm, key
@@ -173,90 +177,91 @@ def _pad_to(x: torch.Tensor, mult: int, value: int = 0) -> torch.Tensor:
     return out
 
 
+def compact_rows(targets, ignore_index: int):
+    """Device-side filter_ignored (kernels.py:494-510): (row_map padded to a multiple of 128,
+    n_valid as a device int32[1]).  No host synchronisation."""
+    lib = _lib.load()
+    n = targets.shape[0]
+    dev = targets.device
+    row_map = torch.empty(max(1, -(-n // BLOCK_TOKENS) * BLOCK_TOKENS), dtype=torch.int32, device=dev)
+    n_valid = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_compact_rows(_p(targets), int(ignore_index), n, _p(row_map), _p(n_valid),
+                                    _stream(dev)), "cce_compact_rows")
+    LAUNCHES["count"] += 1
+    return row_map, n_valid
+
+
 def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
              softcap: float = 0.0, eps: float | None = EPSILON_DEFAULT, vocab_sorting: bool = True,
              perm: torch.Tensor | None = None, fp32_de: bool = False):
     """Filtered, vocab-sorted CCE backward (lse_backward, kernels.py:327-486).
 
-    Ignored rows are compacted first (filter_ignored, kernels.py:494-510) so token tiles hold
-    valid rows only, exactly as cce_loss does before calling lse_backward.  `upstream` must be
-    0 at ignored rows.  Returns (dE, dC, counters[3] tensor, perm).  With fp32_de the fp32 dE
-    accumulator is returned instead of its bf16 cast (vocab-parallel all-reduces it first).
+    Ignored rows are compacted on the device first (filter_ignored, kernels.py:494-510), so
+    token tiles hold valid rows only, exactly as cce_loss does before calling lse_backward.
+    `lse` / `upstream` are per original row; `upstream` must be 0 at ignored rows.  Returns
+    (dE, dC, counters[3] tensor, perm); with fp32_de, dE stays fp32 (vocab-parallel all-reduces
+    it before the cast).  The whole call is asynchronous: no value is read back to the host.
     """
     lib = _lib.load()
     n, d = e.shape
     v = c.shape[0]
     dev = e.device
     stream = _stream(dev)
-    valid = targets != ignore_index
-    idx = torch.nonzero(valid).squeeze(1)
-    n_valid = int(idx.numel())
-    if n_valid == n:
-        row_map = None
-        lse_c, up_c, tg_c = lse, upstream, targets
-    else:
-        row_map = _pad_to(idx.to(torch.int32), BLOCK_TOKENS)
-        lse_c, up_c, tg_c = lse[idx].contiguous(), upstream[idx].contiguous(), targets[idx].contiguous()
-    lse_c = lse_c.to(torch.float32).contiguous()
-    up_c = up_c.to(torch.float32).contiguous()
-
-    if vocab_sorting and perm is None and n_valid > 0:
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    row_map, n_valid = compact_rows(targets, ignore_index)
+    if vocab_sorting and perm is None:
         perm, _ = vocab_order(e, c, targets, ignore_index, n_valid)
     vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
-    nt = max(1, -(-n_valid // BLOCK_TOKENS))
+    nt = max(1, -(-n // BLOCK_TOKENS))
+    mt = -(-v // BLOCK_VOCAB)
     perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev) if perm is not None else None
     inv_perm = torch.empty(v, dtype=torch.int32, device=dev) if perm is not None else None
-    pos = torch.empty(max(n_valid, 1), dtype=torch.int32, device=dev)
-    block_zero = torch.empty(nt, dtype=torch.uint8, device=dev)
-    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(tg_c), int(ignore_index), int(vocab_start), _p(up_c),
-                                n_valid, _p(perm_padded), _p(inv_perm), _p(pos), _p(block_zero),
-                                stream), "cce_bwd_prep")
-    LAUNCHES["count"] += 3 if perm is not None else 2
-    compacted = row_map is not None
-    de_dtype = torch.float32 if fp32_de else torch.bfloat16
-    de = (torch.zeros if compacted or n_valid == 0 else torch.empty)(n, d, dtype=de_dtype, device=dev)
-    dc = (torch.zeros if n_valid == 0 else torch.empty)(v, d, dtype=torch.bfloat16, device=dev)
-    counters = torch.zeros(3, dtype=torch.int64, device=dev)
-    if n_valid == 0:
-        return de, dc, counters, perm
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
+                                _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
+    LAUNCHES["count"] += 2 if perm is not None else 1
+    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev)
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    if n == 0:
+        return de, dc.zero_(), torch.zeros(3, dtype=torch.int64, device=dev), perm
     filt_eps = 0.0 if (eps is None or eps == 0) else float(eps)
-    mt = -(-v // BLOCK_VOCAB)
-    budget = shat_budget_tiles()
-    # first try: every token tile in one group, compact S-hat slots up to the budget
-    plans = [(nt, min(budget, nt * mt))]
-    if plans[0][1] < nt * mt:
-        g = max(1, budget // mt)          # fallback: groups whose worst case fits the budget
-        plans.append((g, g * mt))
-    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
-    # Vocabulary order: materialise C[perm] once (1 HBM read + write of C) so every tile load in
-    # the backward is a plain TMA box; CCE_SORT_GATHER=1 instead gathers rows with TMA gather4
-    # inside the kernels (no copy, but gather-bound).
+    gather = os.environ.get("CCE_SORT_GATHER", "0") == "1"
+    # Vocabulary order: materialise C[perm] once (one HBM read + write of C) so every tile load of
+    # the backward is a plain TMA box; CCE_SORT_GATHER=1 instead gathers rows (C through perm, E
+    # through row_map) with TMA gather4 inside the kernels: no copies, but gather-bound.
     c_src, c_sorted = c, 0
-    if perm is not None and os.environ.get("CCE_SORT_GATHER", "0") != "1":
+    if perm is not None and not gather:
         c_src = torch.empty_like(c)
         _lib.check(lib.cce_gather_rows(_p(c), _p(perm), v, d, _p(c_src), stream), "cce_gather_rows")
         LAUNCHES["count"] += 1
         c_sorted = 1
-    for i, (g, cap) in enumerate(plans):
-        ws_bytes = lib.cce_bwd_workspace_bytes(n_valid, d, v, g, cap)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        if i:
-            counters.zero_()
+    # S-hat slots: every token tile in one group with compact slots up to the budget; if more
+    # tiles are kept than that, a fallback pass over budget-sized groups (worst case fits) runs,
+    # gated on the device overflow flag -- no host read either way.
+    budget = shat_budget_tiles()
+    plans = [(nt, min(budget, nt * mt), None)]
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    if plans[0][1] < nt * mt:
+        g = max(1, budget // mt)
+        plans.append((g, g * mt, overflow))
+    all_counters = []
+    ws_bytes = max(lib.cce_bwd_workspace_bytes(n, d, v, g, cap) for g, cap, _ in plans)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    for g, cap, run_if in plans:
+        counters = torch.zeros(3, dtype=torch.int64, device=dev)
         ev = _ev_begin("bwd")
-        _lib.check(lib.cce_bwd(_p(e), n, _p(c_src), _p(perm_padded), _p(row_map), _p(pos), _p(lse_c),
-                               _p(up_c), _p(block_zero), n_valid, d, v, float(softcap or 0.0), filt_eps,
-                               g, cap, c_sorted, _p(ws), ws_bytes, _p(de), int(fp32_de), _p(dc),
-                               _p(counters), _p(overflow), stream), "cce_bwd")
+        _lib.check(lib.cce_bwd(_p(e), _p(c_src), _p(perm_padded), c_sorted, _p(row_map), _p(n_valid),
+                               _p(pos), _p(lse), _p(upstream), n, d, v, float(softcap or 0.0), filt_eps,
+                               g, cap, _p(run_if), int(gather), _p(ws), ws_bytes, _p(de), int(fp32_de),
+                               _p(dc), _p(counters), _p(overflow if run_if is None else None), stream),
+                   "cce_bwd")
         _ev_end("bwd", ev)
-        LAUNCHES["count"] += 3 * (-(-nt // g))
-        del ws
-        # the single-group plan can only overflow when the budget is below the worst case;
-        # checking needs one host read, paid only in that situation
-        if i + 1 == len(plans) or int(overflow.item()) == 0:
-            break
-        overflow.zero_()
-        LAST_OVERFLOW["count"] += 1
+        LAUNCHES["count"] += 2 + 3 * (-(-nt // g))
+        all_counters.append(counters)
+    counters = all_counters[0] if len(plans) == 1 else torch.where(overflow.bool(), all_counters[1], all_counters[0])
     LAST_COUNTERS["counters"] = counters
+    LAST_OVERFLOW["flag"] = overflow
     return de, dc, counters, perm
 
 

@@ -17,6 +17,9 @@ for s in "$@"; do
         python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $out/launches.log 2>&1; echo "exit $?" >> $out/launches.log ;;
     ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_(lse|de|dc)_kernel" -s 1 -c 4 -o $out/prof \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $out/ncu.log 2>&1; echo "exit $?" >> $out/ncu.log ;;
+    trace) timeout 600 python scripts/trace_step.py > $out/trace.log 2>&1; echo "exit $?" >> $out/trace.log ;;
+    ncugrad) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_d[ec]_kernel" -c 2 -o $out/profgrad \
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $out/ncugrad.log 2>&1; echo "exit $?" >> $out/ncugrad.log ;;
     refarm) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/ref.log 2>&1; echo "exit $?" >> $out/ref.log ;;
   esac
 done

@@ -53,3 +53,35 @@ def test_product_rejects_cpu_tensors():
     t = torch.zeros(4, dtype=torch.int64)
     with pytest.raises(ValueError, match="CUDA"):
         linear_cross_entropy(e, c, t)
+
+
+_C2CTYPES = {
+    "int64_t": "c_int64", "size_t": "c_size_t", "float": "c_float", "int": "c_int",
+}
+
+
+def _header_signatures():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    sigs = {}
+    for m in re.finditer(r"\b(?:int|size_t|const char\*)\s+(cce_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
+        args = [a.strip() for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        kinds = []
+        for a in args:
+            a = re.sub(r"\s+\w+$", "", a)  # drop the parameter name
+            kinds.append("c_void_p" if "*" in a else _C2CTYPES[a.replace("const ", "").strip()])
+        sigs[m.group(1)] = kinds
+    return sigs
+
+
+def test_ctypes_table_matches_header_argument_types():
+    """Every ctypes argtypes entry agrees with the C prototype (count and kind)."""
+    import ctypes as ct
+
+    from paper_2411_09009_b200 import _lib
+
+    for name, kinds in _header_signatures().items():
+        _, argtypes = _lib.SIGNATURES[name]
+        got = [t.__name__ for t in argtypes]
+        # c_size_t is an alias of c_ulong on LP64
+        want = [ct.c_size_t.__name__ if k == "c_size_t" else getattr(ct, k).__name__ for k in kinds]
+        assert got == want, (name, got, want)
