@@ -21,7 +21,7 @@ constexpr int TMEM_COLS = 512;
 constexpr int DCH = 256;                  // D columns per gradient chunk (MMA N of dE / dC)
 constexpr int SHAT_TILE_BYTES = BM * BN * 2;  // one stored S-hat tile, bf16 row-major [128][256]
 
-enum Mode { FWD = 0, BWD = 1 };
+enum Mode { FWD = 0, BWD = 1, KEPT = 2 };
 
 // Forward (FWD) and backward filter pass (BWD, "B1") of the fused logit-tile kernel.
 //
@@ -46,10 +46,11 @@ struct Params {
   int64_t vocab_start;
   float2* part;      // [splits][n_total]  (running max, running sum) in log2 units
   float* correct;    // [n_total] target logit (written by the tile that owns the label)
+  float* tile_max;   // [nt][mt][BM] max raw logit of each row in each tile, or nullptr
   // backward filter pass (lse / upstream / pos are indexed by ORIGINAL row)
   const float* lse;        // global log-sum-exp (natural log)
   const float* upstream;   // dLoss/dloss_i, 0 at ignored rows
-  const int32_t* pos;      // label position in tile order, -1 if none
+  const int32_t* pos;      // label position in tile order, -1 if none (FWD: nullptr = targets)
   const int32_t* perm;     // [mt*BN] tile-order position -> C row for gathers (nullptr = plain)
   const int32_t* row_map;  // compact row -> original row (padded); identity when no compaction
   int e_gather;            // 1: load E rows through row_map with gather4 (else E is compacted)
@@ -63,6 +64,9 @@ struct Params {
   int* cnt_n;              // [nt] kept tiles per token tile
   int* cnt_m;              // [mt] kept tiles per vocab tile
   unsigned long long* counters;  // [3] kept, eps-skipped, zero-upstream-skipped
+  // KEPT
+  const int2* list;        // [capacity] (token tile, vocab tile) of each slot
+  const int* list_count;   // kept tiles (slots used = min(count, capacity))
 };
 
 // dE pass ("B2") and dC pass ("B3").
@@ -161,5 +165,16 @@ __device__ __forceinline__ float softcap_tanh(float z, float inv_cap) {
 }
 
 constexpr float LOG2E = 1.4426950408889634f;
+
+// The filter test of one row of one tile: S = exp(softcap(z) - lse) is monotone in z, so the
+// row has an entry >= eps iff its max raw logit does (block_skip_decision, kernels.py:140-142,
+// strict "<" to skip).  Shared by the in-kernel filter and the decision from forward maxima, so
+// both take bit-identical decisions.
+__device__ __forceinline__ bool tile_row_big(float zmax, float lse2, float softcap, float inv_cap,
+                                             float eps) {
+  if (zmax == -INFINITY) return false;
+  const float zc = softcap > 0.f ? softcap * softcap_tanh(zmax, inv_cap) : zmax;
+  return ex2_approx(zc * LOG2E - lse2) >= eps;
+}
 
 }  // namespace cce

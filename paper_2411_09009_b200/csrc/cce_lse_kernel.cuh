@@ -1,37 +1,64 @@
-// Fused logit-tile kernel: forward LSE (FWD) and backward filter pass (BWD).
+// Fused logit-tile kernel: forward LSE (FWD), backward filter pass (BWD) and backward recompute
+// of already-selected tiles (KEPT).
 //
-//   FWD = indexed_matmul (kernels.py:204-251) + lse_forward (kernels.py:254-319): per token row,
-//         an online (max, sum-exp) over this CTA's vocabulary split plus the target logit.
-//   BWD = the recompute / S / filter half of lse_backward (kernels.py:425-459): per 128x256
-//         tile, keep it iff it holds a label or any S = exp(z - lse) >= eps (block_skip_decision,
-//         kernels.py:140-142); kept tiles store S-hat = up * (S - onehot) [* (1 - tanh^2)] as bf16
-//         for the dE / dC passes (cce_grad_kernels.cuh).
+//   FWD  = indexed_matmul (kernels.py:204-251) + lse_forward (kernels.py:254-319): per token row,
+//          an online (max, sum-exp) over this CTA's vocabulary split plus the target logit.
+//          Optionally records each row's max raw logit per 128x256 tile (`tile_max`) so the
+//          backward can take the filter decision without recomputing skipped tiles.
+//   BWD  = recompute / S / filter half of lse_backward (kernels.py:425-459) over every tile:
+//          keep a tile iff it holds a label or any S = exp(z - lse) >= eps (block_skip_decision,
+//          kernels.py:140-142); kept tiles store S-hat = up * (S - onehot) [* (1 - tanh^2)] as
+//          bf16 for the dE / dC passes (cce_grad_kernels.cuh).
+//   KEPT = S-hat of the tiles in a precomputed kept list (the decision having been taken from the
+//          forward's tile maxima, cce_aux_kernels.cuh: decide_tiles_kernel).
 //
 // Persistent, one CTA per SM, 192 threads:
-//   warp 0      TMA producer (one thread): E rows [n*128, +128) and C rows of tile m, 64 D-columns
-//               per stage, 4-stage ring
-//   warp 1      TMEM allocator + MMA issuer: 36 K-blocks x 4 tcgen05.mma (M=128, N=256, K=16)
+//   warp 0      TMA producer (whole warp; gathers split over lanes): E rows [n*128, +128) and C
+//               rows of tile m, 64 D-columns per stage, 4-stage ring
+//   warp 1      TMEM allocator + MMA issuer: K-blocks x 4 tcgen05.mma (M=128, N=256, K=16)
 //               into one of two 256-column fp32 accumulators (double buffered)
-//   warps 2..5  epilogue: thread (warp%4)*32+lane owns token row of the tile, reads its 256
-//               accumulator columns with tcgen05.ld
+//   warps 2..5  epilogue: thread (warp%4)*32+lane owns one token row of the tile and reads its
+//               256 accumulator columns with tcgen05.ld
 #pragma once
 #include "cce_common.cuh"
 
 namespace cce {
 
-struct TileIter {
-  // Static persistent schedule: unit u = s * g + n (token tile fastest), so the CTAs running
-  // concurrently share the same vocab tiles of C while E stays L2-resident.
-  int unit, units, m, m_end, n, s, g;
-  const Params* p;
-  __device__ void begin_unit() {
-    n = p->n_base + unit % g;
-    s = unit / g;
-    m = (int)(((long long)s * p->mt) / p->splits);
-    m_end = (int)(((long long)(s + 1) * p->mt) / p->splits);
-  }
-  __device__ bool valid() const { return unit < units; }
+struct TileRef {
+  int n, m;     // token tile, vocab tile (tile order)
+  int s;        // vocabulary split of the unit (FWD / BWD) or slot (KEPT)
+  bool first;   // first tile of its unit
+  bool last;    // last tile of its unit
 };
+
+// Visit this CTA's tiles in schedule order.  FWD / BWD: static persistent schedule over units
+// u = s * g + n (token tile fastest), so concurrently running CTAs share the vocab tiles of C
+// while E stays L2-resident; each unit is a contiguous range of vocab tiles of one token tile.
+// KEPT: grid-stride over the kept list (vocab-tile-major, so concurrent CTAs share C tiles).
+// `skip(n, count)` is called for BWD units whose upstream is all zero (kernels.py:434-438).
+template <int MODE, typename F, typename S>
+__device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, F&& f, S&& skip) {
+  if (MODE == KEPT) {
+    const int total = min(*p.list_count, p.capacity);
+    for (int i = blockIdx.x; i < total; i += gridDim.x) {
+      const int2 t = p.list[i];
+      f(TileRef{t.x, t.y, i, true, true});
+    }
+    return;
+  }
+  const int units = rows.g * p.splits;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int n = p.n_base + u % rows.g;
+    const int s = u / rows.g;
+    const int m0 = (int)(((long long)s * p.mt) / p.splits);
+    const int m1 = (int)(((long long)(s + 1) * p.mt) / p.splits);
+    if (MODE == BWD && p.block_zero[n]) {
+      skip(n, m1 - m0);
+      continue;
+    }
+    for (int m = m0; m < m1; ++m) f(TileRef{n, m, s, m == m0, m == m1 - 1});
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -72,12 +99,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
   const Rows rows(p.n_valid, p.n_total, p.n_base, p.nt);
-  TileIter it;
-  it.p = &p;
-  it.g = rows.g;
-  it.units = rows.g * p.splits;
+  auto no_skip = [](int, int) {};
 
   if (warp == 0) {
     // ================================ TMA producer (whole warp) ===========================
@@ -86,25 +109,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool gather_e = p.e_gather != 0;
     const bool gather_c = p.perm != nullptr;
     RowGather rge, rgc;
-    for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
-      it.begin_unit();
-      if (MODE == BWD && p.block_zero[it.n]) continue;
-      rge.load(p.e_gather ? p.row_map : nullptr, it.n * BM, BM);
-      for (; it.m < it.m_end; ++it.m) {
-        rgc.load(p.perm, it.m * BN, BN);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          if (lane == 0) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          }
-          __syncwarp();
-          load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, it.n * BM);
-          load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, it.m * BN);
-          advance_stage(stage, phase, STAGES);
-        }
+    int cur_n = -1;
+    for_each_tile<MODE>(p, rows, [&](const TileRef& t) {
+      if (t.n != cur_n) {
+        rge.load(gather_e ? p.row_map : nullptr, t.n * BM, BM);
+        cur_n = t.n;
       }
-    }
+      rgc.load(p.perm, t.m * BN, BN);
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+        }
+        __syncwarp();
+        load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, t.n * BM);
+        load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);
+        advance_stage(stage, phase, STAGES);
+      }
+    }, no_skip);
   } else if (warp == 1) {
     // ===================================== MMA issuer ====================================
     if (lane == 0) {
@@ -112,29 +135,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
-        it.begin_unit();
-        if (MODE == BWD && p.block_zero[it.n]) continue;
-        for (; it.m < it.m_end; ++it.m, ++t) {
-          const int buf = t & 1;
-          mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
+      for_each_tile<MODE>(p, rows, [&](const TileRef&) {
+        const int buf = t & 1;
+        mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + buf * BN;
-          for (int kb = 0; kb < p.num_kb; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
-            const uint32_t b0 = a0 + A_BYTES;
+          const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b0 = a0 + A_BYTES;
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024), make_sdesc(b0 + 32 * k, 0, 1024),
-                          IDESC, (kb | k) != 0);
-            mma_commit(&empty[stage]);
-            advance_stage(stage, phase, STAGES);
-          }
-          mma_commit(&acc_full[buf]);
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024), make_sdesc(b0 + 32 * k, 0, 1024),
+                        IDESC, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          advance_stage(stage, phase, STAGES);
         }
-      }
+        mma_commit(&acc_full[buf]);
+        ++t;
+      }, no_skip);
     }
   } else {
     // ===================================== epilogue ======================================
@@ -145,158 +165,181 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float inv_cap = use_softcap ? 1.0f / p.softcap : 0.f;
     const int epi_tid = threadIdx.x - 64;  // 0..127
     int t = 0;
+    // per-row state, refreshed whenever the token tile changes
+    int cur_n = -1;
+    bool valid = false;
+    int grow = 0;
+    int64_t tpos = -1;             // FWD: target position in C's row order
+    float lse2 = 0.f, up_r = 0.f;  // BWD / KEPT
+    int pos_r = -1;
+    float run_m = -INFINITY, run_s = 0.f, corr = 0.f;
+    bool have_corr = false;
 
-    for (it.unit = blockIdx.x; it.valid(); it.unit += gridDim.x) {
-      it.begin_unit();
-      const int grow = it.n * BM + row;
-      const bool valid = grow < rows.n;
+    auto load_row = [&](int n) {
+      grow = n * BM + row;
+      valid = grow < rows.n;
+      const int orow = valid ? (p.row_map ? p.row_map[grow] : grow) : 0;
       if (MODE == FWD) {
-        int64_t tpos = -1;
+        tpos = -1;
         if (valid) {
-          const int64_t tg = p.targets[grow];
-          if (tg != p.ignore_index) tpos = tg - p.vocab_start;
-        }
-        float run_m = -INFINITY, run_s = 0.f, corr = 0.f;
-        bool have_corr = false;
-        for (; it.m < it.m_end; ++it.m, ++t) {
-          const int buf = t & 1;
-          mbar_wait(&acc_full[buf], (t >> 1) & 1);
-          tc_fence_after();
-          const int col0 = it.m * BN;
-          const bool tile_has_t = tpos >= col0 && tpos < col0 + BN;
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tmem_base + lane_off + buf * BN + c * 32, r);
-            tmem_ld_wait();
-            float y[32];
-            float cm = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float z = __uint_as_float(r[j]);
-              if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
-              const int col = col0 + c * 32 + j;
-              if (tile_has_t && col == tpos) {
-                corr = z;
-                have_corr = true;
-              }
-              y[j] = col < p.v ? z * LOG2E : -INFINITY;
-              cm = fmaxf(cm, y[j]);
-            }
-            const float nm = fmaxf(run_m, cm);
-            if (nm != -INFINITY) {
-              float acc = 0.f;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) acc += ex2_approx(y[j] - nm);
-              run_s = run_s * ex2_approx(run_m - nm) + acc;
-              run_m = nm;
-            }
+          if (p.pos) {
+            tpos = p.pos[orow];
+          } else {
+            const int64_t tg = p.targets[orow];
+            if (tg != p.ignore_index) tpos = tg - p.vocab_start;
           }
-          tc_fence_before();
-          mbar_arrive(&acc_free[buf]);
-        }
-        if (valid) {
-          p.part[(size_t)it.s * p.n_total + grow] = make_float2(run_m, run_s);
-          if (have_corr) p.correct[grow] = corr;
         }
       } else {
-        // ------------------------------- backward filter pass ------------------------------
-        if (p.block_zero[it.n]) {
-          if (epi_tid == 0) atomicAdd(&p.counters[2], (unsigned long long)(it.m_end - it.m));
-          continue;
-        }
-        const int orow = valid ? p.row_map[grow] : 0;
-        const float lse2 = valid ? p.lse[orow] * LOG2E : INFINITY;
-        const float up_r = valid ? p.upstream[orow] : 0.f;
-        const int pos_r = valid ? p.pos[orow] : -1;
-        const int ln = it.n - p.n_base;
-        for (; it.m < it.m_end; ++it.m, ++t) {
-          const int buf = t & 1;
-          mbar_wait(&acc_full[buf], (t >> 1) & 1);
-          tc_fence_after();
-          const int col0 = it.m * BN;
-          const uint32_t tacc = tmem_base + lane_off + buf * BN;
-          // pass 1: row max of the raw logits.  S = exp(z' - lse) is monotone in z, so
-          // "all S < eps" (block_skip_decision) holds iff S(row max) < eps for every row.
-          float zmax = -INFINITY;
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + c * 32 + j < p.v) zmax = fmaxf(zmax, __uint_as_float(r[j]));
-          }
-          bool big = false;
-          if (valid && zmax != -INFINITY) {
-            const float zc = use_softcap ? p.softcap * softcap_tanh(zmax, inv_cap) : zmax;
-            big = ex2_approx(zc * LOG2E - lse2) >= p.eps;
-          }
-          const bool in_tile = pos_r >= col0 && pos_r < col0 + BN;
-          const uint32_t wvote = __any_sync(0xffffffffu, big || in_tile);
-          if (lane == 0) s_vote[(t & 1) * 4 + quarter] = wvote;
-          named_bar_sync(1, 128);
-          const uint32_t* vv = s_vote + (t & 1) * 4;
-          const bool kept = (vv[0] | vv[1] | vv[2] | vv[3]) != 0;
-          if (kept) {
-            // one slot per kept tile, handed out in completion order; results do not depend on
-            // slot numbers (the gradient passes visit tiles in index order)
-            if (epi_tid == 0) {
-              int slot = atomicAdd(p.slot_ctr, 1);
-              if (slot >= p.capacity) {
-                slot = -1;
-                if (p.overflow) atomicExch(p.overflow, 1);
-              } else {
-                p.slot_of[(size_t)ln * p.mt + it.m] = slot;
-                atomicAdd(&p.cnt_n[ln], 1);
-                atomicAdd(&p.cnt_m[it.m], 1);
-              }
-              s_slot[t & 1] = slot;
-              atomicAdd(&p.counters[0], 1ull);
-            }
-            named_bar_sync(1, 128);
-            const int slot = s_slot[t & 1];
-            if (slot >= 0) {
-              // pass 2: S-hat row -> bf16 -> global, row-major [slot][128][256]
-              uint4* dst = reinterpret_cast<uint4*>(p.shat + ((size_t)slot * BM + row) * BN);
-#pragma unroll 1
-              for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tacc + c * 32, r);
-                tmem_ld_wait();
-                uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                  float g2[2];
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    float z = __uint_as_float(r[j + h]);
-                    float dcap = 1.f;
-                    if (use_softcap) {
-                      const float th = softcap_tanh(z, inv_cap);
-                      z = p.softcap * th;
-                      dcap = 1.f - th * th;
-                    }
-                    const int col = col0 + c * 32 + j + h;
-                    const float s = (col < p.v) ? ex2_approx(z * LOG2E - lse2) : 0.f;
-                    g2[h] = ((col == pos_r) ? s - 1.f : s) * up_r * dcap;
-                  }
-                  pk[j >> 1] = pack_bf16x2(g2[0], g2[1]);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-              }
-            }
-          } else if (epi_tid == 0) {
-            atomicAdd(&p.counters[1], 1ull);
-          }
-          tc_fence_before();
-          mbar_arrive(&acc_free[buf]);
-        }
+        lse2 = valid ? p.lse[orow] * LOG2E : INFINITY;
+        up_r = valid ? p.upstream[orow] : 0.f;
+        pos_r = valid ? p.pos[orow] : -1;
       }
-    }
+    };
+
+    // this thread's S-hat row of the tile in accumulator `tacc` -> bf16 -> slot, row-major
+    // [slot][128][256]
+    auto store_shat = [&](uint32_t tacc, int col0, int slot) {
+      uint4* dst = reinterpret_cast<uint4*>(p.shat + ((size_t)slot * BM + row) * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tacc + c * 32, r);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float g2[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float z = __uint_as_float(r[j + h]);
+            float dcap = 1.f;
+            if (use_softcap) {
+              const float th = softcap_tanh(z, inv_cap);
+              z = p.softcap * th;
+              dcap = 1.f - th * th;
+            }
+            const int col = col0 + c * 32 + j + h;
+            const float s = (col < p.v) ? ex2_approx(z * LOG2E - lse2) : 0.f;
+            g2[h] = ((col == pos_r) ? s - 1.f : s) * up_r * dcap;
+          }
+          pk[j >> 1] = pack_bf16x2(g2[0], g2[1]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+    };
+
+    for_each_tile<MODE>(p, rows, [&](const TileRef& tr) {
+      if (tr.n != cur_n) {
+        load_row(tr.n);
+        cur_n = tr.n;
+      }
+      const int buf = t & 1;
+      mbar_wait(&acc_full[buf], (t >> 1) & 1);
+      tc_fence_after();
+      const int col0 = tr.m * BN;
+      const uint32_t tacc = tmem_base + lane_off + buf * BN;
+      if (MODE == FWD) {
+        if (tr.first) {
+          run_m = -INFINITY;
+          run_s = 0.f;
+          have_corr = false;
+        }
+        const bool tile_has_t = tpos >= col0 && tpos < col0 + BN;
+        float zmax = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_ld_wait();
+          float y[32];
+          float cm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float z = __uint_as_float(r[j]);
+            const int col = col0 + c * 32 + j;
+            const bool in_v = col < p.v;
+            if (in_v) zmax = fmaxf(zmax, z);
+            if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
+            if (tile_has_t && col == tpos) {
+              corr = z;
+              have_corr = true;
+            }
+            y[j] = in_v ? z * LOG2E : -INFINITY;
+            cm = fmaxf(cm, y[j]);
+          }
+          const float nm = fmaxf(run_m, cm);
+          if (nm != -INFINITY) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += ex2_approx(y[j] - nm);
+            run_s = run_s * ex2_approx(run_m - nm) + acc;
+            run_m = nm;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_free[buf]);
+        if (p.tile_max) p.tile_max[((size_t)tr.n * p.mt + tr.m) * BM + row] = zmax;
+        if (tr.last && valid) {
+          p.part[(size_t)tr.s * p.n_total + grow] = make_float2(run_m, run_s);
+          if (have_corr) p.correct[grow] = corr;
+        }
+      } else if (MODE == KEPT) {
+        store_shat(tacc, col0, tr.s);
+        tc_fence_before();
+        mbar_arrive(&acc_free[buf]);
+      } else {
+        // ------------------------------- backward filter pass ------------------------------
+        // pass 1: row max of the raw logits.  S = exp(z' - lse) is monotone in z, so
+        // "all S < eps" (block_skip_decision) holds iff S(row max) < eps for every row.
+        float zmax = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + c * 32 + j < p.v) zmax = fmaxf(zmax, __uint_as_float(r[j]));
+        }
+        const bool big = valid && tile_row_big(zmax, lse2, p.softcap, inv_cap, p.eps);
+        const bool in_tile = pos_r >= col0 && pos_r < col0 + BN;
+        const uint32_t wvote = __any_sync(0xffffffffu, big || in_tile);
+        if (lane == 0) s_vote[(t & 1) * 4 + quarter] = wvote;
+        named_bar_sync(1, 128);
+        const uint32_t* vv = s_vote + (t & 1) * 4;
+        const bool kept = (vv[0] | vv[1] | vv[2] | vv[3]) != 0;
+        const int ln = tr.n - p.n_base;
+        if (kept) {
+          // one slot per kept tile, handed out in completion order; results do not depend on
+          // slot numbers (the gradient passes visit tiles in index order)
+          if (epi_tid == 0) {
+            int slot = atomicAdd(p.slot_ctr, 1);
+            if (slot >= p.capacity) {
+              slot = -1;
+              if (p.overflow) atomicExch(p.overflow, 1);
+            } else {
+              p.slot_of[(size_t)ln * p.mt + tr.m] = slot;
+              atomicAdd(&p.cnt_n[ln], 1);
+              atomicAdd(&p.cnt_m[tr.m], 1);
+            }
+            s_slot[t & 1] = slot;
+            atomicAdd(&p.counters[0], 1ull);
+          }
+          named_bar_sync(1, 128);
+          const int slot = s_slot[t & 1];
+          if (slot >= 0) store_shat(tacc, col0, slot);
+        } else if (epi_tid == 0) {
+          atomicAdd(&p.counters[1], 1ull);
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_free[buf]);
+      }
+      ++t;
+    }, [&](int, int count) {
+      if (MODE == BWD && epi_tid == 0) atomicAdd(&p.counters[2], (unsigned long long)count);
+    });
   }
 
   tc_fence_before();

@@ -266,8 +266,8 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
 
 
 def shat_budget_tiles() -> int:
-    """S-hat slots (64 KiB each) the backward may hold: CCE_SHAT_BUDGET_MB (default 2048)."""
-    budget = int(os.environ.get("CCE_SHAT_BUDGET_MB", "2048")) << 20
+    """S-hat slots (64 KiB each) the backward may hold: CCE_SHAT_BUDGET_MB (default 1024)."""
+    budget = int(os.environ.get("CCE_SHAT_BUDGET_MB", "1024")) << 20
     return max(1, budget // (BLOCK_TOKENS * BLOCK_VOCAB * 2))
 
 
