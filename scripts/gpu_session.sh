@@ -9,7 +9,7 @@ for s in "$@"; do
     testsall) timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/pytest_gpu.log 2>&1; echo "exit $?" >> $out/pytest_gpu.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "exit $?" >> $out/smoke.log ;;
     check) timeout 300 python scripts/gpu_check.py all > $out/check.log 2>&1; echo "exit $?" >> $out/check.log ;;
-    bench) timeout 600 python bench.py --steps 5 --warmup 3 > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
+    bench) timeout 900 python bench.py > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
     benchfast) timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
     benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
@@ -20,6 +20,8 @@ for s in "$@"; do
     trace) timeout 600 python scripts/trace_step.py > $out/trace.log 2>&1; echo "exit $?" >> $out/trace.log ;;
     ncugrad) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_d[ec]_kernel" -c 2 -o $out/profgrad \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $out/ncugrad.log 2>&1; echo "exit $?" >> $out/ncugrad.log ;;
+    configs) for cfg in gpt2 llama3-8b gemma2-9b nemo-12b; do
+        timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> $out/configs.log 2>&1; echo "exit $cfg $?" >> $out/configs.log; done ;;
     refarm) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/ref.log 2>&1; echo "exit $?" >> $out/ref.log ;;
   esac
 done

@@ -1,0 +1,70 @@
+"""Host-side behaviour of the reference-mirroring API (no GPU): option validation, reductions,
+vocabulary order, helpers - the same cases the reference's test_core.py / test_kernels.py pin."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2411_09009_b200 import api
+
+
+def test_constants_match_reference():  # core.py:23, :27
+    assert api.IGNORE_INDEX == -1
+    assert api.EPSILON_DEFAULT == 2.0 ** -12
+
+
+@pytest.mark.parametrize("kw", [dict(epsilon=0.0), dict(epsilon=1.0), dict(reduction="avg"),
+                                dict(thread_count=0)])
+def test_options_validation(kw):  # core.py:150-156
+    with pytest.raises(ValueError):
+        api.CceOptions(**kw)
+
+
+def test_blockspec_validation():
+    assert api.BlockSpec() == api.BlockSpec(128, 256, 64)
+    with pytest.raises(ValueError):
+        api.BlockSpec(n_b=0)
+    with pytest.raises(ValueError, match="tile"):
+        api.BlockSpec(n_b=128, m_b=128)
+
+
+def test_default_upstream_reductions():  # core.py:181-200
+    x = torch.tensor([3, -1, 0, 2])
+    assert torch.allclose(api.default_upstream(x, "sum"), torch.tensor([1.0, 0, 1, 1]))
+    assert torch.allclose(api.default_upstream(x, "mean-over-valid"), torch.tensor([1 / 3, 0, 1 / 3, 1 / 3]))
+    assert torch.all(api.default_upstream(torch.tensor([-1, -1]), "mean-over-valid") == 0)
+    with pytest.raises(ValueError):
+        api.default_upstream(x, "none")
+
+
+def test_vocab_order_descending_stable():  # test_kernels.py:206-225
+    order = api.compute_vocab_order(torch.tensor([0.5, 2.0, 0.5, 2.0, -1.0]))
+    assert order.perm.tolist() == [1, 3, 0, 2, 4]
+    with pytest.raises(ValueError):
+        api.compute_vocab_order(torch.zeros(2, 2))
+
+
+def test_log_add_exp_and_skip_decision():  # test_kernels.py:87-99, kernels.py:140-142
+    assert float(api.log_add_exp(1.0, 2.0)) == pytest.approx(2.3132616875182228, rel=1e-14)
+    assert float(api.log_add_exp(-math.inf, -2.5)) == -2.5
+    eps = 2.0 ** -12
+    assert api.block_skip_decision(torch.full((2, 2), eps / 2), eps)
+    assert not api.block_skip_decision(torch.full((2, 2), eps), eps)
+
+
+def test_filter_ignored_compaction():  # kernels.py:494-510
+    e = torch.arange(12.0).reshape(4, 3)
+    x = torch.tensor([5, -1, 2, -1])
+    ce, cx, idx = api.filter_ignored(e, x)
+    assert idx.tolist() == [0, 2] and cx.tolist() == [5, 2] and torch.equal(ce, e[[0, 2]])
+    ce, cx, idx = api.filter_ignored(e, torch.tensor([1, 1, 1, 1]))
+    assert ce is e and idx.tolist() == [0, 1, 2, 3]
+
+
+def test_no_cpu_fallback():
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(RuntimeError, match="CUDA"):
+        api.cce_loss(np.zeros((2, 8), np.float32), np.zeros((3, 8), np.float32), np.array([0, 1]))

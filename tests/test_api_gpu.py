@@ -1,0 +1,132 @@
+"""The reference's own kernel tests (pkg/tests/test_kernels.py) replayed against the mirrored API
+on the GPU, plus the reference-run fixtures through cce_loss."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, golden_cases
+from oracle import cce_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_2411_09009_b200 import api
+
+    return api
+
+
+def _make(d, n, v, seed, sigma=1.0):
+    rng = np.random.default_rng(seed)
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * sigma / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    return e, c, x
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_cce_loss_reference_fixture(cuda_device, name):
+    api = _api()
+    g = np.load(GOLDEN / f"{name}.npz")
+    opts = api.CceOptions(filtering=bool(g["filtering"]), vocab_sorting=bool(g["sorting"]))
+    out, back = api.cce_loss(g["e"], g["c"], g["x"], options=opts)
+    valid = g["x"] != -1
+    tol = 1e-3 * max(1.0, float(np.abs(g["loss"]).max()))
+    assert np.max(np.abs(out.per_token_loss.cpu().numpy() - g["loss"])) < tol
+    assert np.max(np.abs(out.lse.cpu().numpy()[valid] - g["lse"][valid])) < tol
+    if bool(g["sorting"]) and valid.any():
+        assert O.rel_err(out.mean_logits.cpu().numpy(), g["mean_logits"]) < 1e-4
+    if not valid.any():
+        return
+    stats = api.BackwardStats()
+    if bool(g["sorting"]):
+        # filtered parity needs the GPU's own order in the reference run
+        perm = torch.sort(out.mean_logits, descending=True, stable=True).indices.cpu().numpy()
+        ce, cl, idx = O.filter_ignored(g["e"], g["x"])
+        rde_c, rdc = O.lse_backward_blocked(ce, g["c"], cl, g["lse"][idx], g["upstream"][idx],
+                                            perm=perm, eps=O.EPSILON_DEFAULT if bool(g["filtering"]) else None)
+        rde = np.zeros_like(g["e"])
+        rde[idx] = rde_c
+    else:
+        rde, rdc = g["d_e"], g["d_c"]
+    gr = back(stats=stats)
+    assert O.rel_err(gr.d_e.cpu().numpy(), rde) < 1e-2
+    assert O.rel_err(gr.d_c.cpu().numpy(), rdc) < 1e-2
+    assert stats.total_tiles == int(g["stats"][0])
+
+
+def test_zero_upstream_gives_zero_grads(cuda_device):  # test_kernels.py:240-246
+    api = _api()
+    e, c, x = _make(16, 300, 700, 1)
+    out, back = api.cce_loss(e, c, x)
+    stats = api.BackwardStats()
+    g = back(np.zeros(300, np.float32), stats=stats)
+    assert torch.all(g.d_e == 0) and torch.all(g.d_c == 0)
+    assert stats.skipped_zero_upstream == stats.total_tiles
+
+
+def test_vocab_one_zero_loss(cuda_device):  # test_kernels.py:139-143, :249-255
+    api = _api()
+    e, c, x = _make(16, 40, 1, 2)
+    out, back = api.cce_loss(e, c, np.zeros(40, np.int64))
+    assert torch.allclose(out.per_token_loss, torch.zeros_like(out.per_token_loss), atol=1e-6)
+    g = back()
+    assert float(g.d_e.abs().max()) < 1e-6 and float(g.d_c.abs().max()) < 1e-6
+
+
+def test_upstream_at_ignored_rejected(cuda_device):  # kernels.py:553-558
+    api = _api()
+    e, c, x = _make(16, 10, 50, 3)
+    x[2] = -1
+    _, back = api.cce_loss(e, c, x)
+    up = np.ones(10, np.float32)
+    with pytest.raises(ValueError, match="ignored"):
+        back(up)
+
+
+def test_errors_match_reference(cuda_device):  # core.py:98-114, kernels.py:168-170
+    api = _api()
+    e, c, x = _make(16, 10, 50, 4)
+    with pytest.raises(ValueError, match="out of range"):
+        api.cce_loss(e, c, np.full(10, 50))
+    with pytest.raises(ValueError, match="feature dims"):
+        api.cce_loss(e, c[:, :8], x)
+    with pytest.raises(ValueError, match="label count"):
+        api.cce_loss(e, c, x[:5])
+    with pytest.raises(ValueError, match="non-negative"):
+        api.cce_loss(e, c, np.full(10, -2))
+
+
+def test_sorting_and_order_invariance(cuda_device):  # test_kernels.py:496-517
+    api = _api()
+    e, c, x = _make(64, 500, 3000, 5, sigma=2.0)
+    out_s, back_s = api.cce_loss(e, c, x, options=api.CceOptions(filtering=False, vocab_sorting=True))
+    out_n, back_n = api.cce_loss(e, c, x, options=api.CceOptions(filtering=False, vocab_sorting=False))
+    assert torch.allclose(out_s.per_token_loss, out_n.per_token_loss, atol=1e-5)
+    gs, gn = back_s(), back_n()
+    assert O.rel_err(gs.d_e.cpu().numpy(), gn.d_e.cpu().numpy()) < 1e-2
+    assert O.rel_err(gs.d_c.cpu().numpy(), gn.d_c.cpu().numpy()) < 1e-2
+
+
+def test_deterministic_bitwise(cuda_device):  # test_kernels.py:520-531
+    api = _api()
+    e, c, x = _make(64, 700, 5000, 6)
+    x[::3] = -1
+    outs = [api.cce_loss(e, c, x) for _ in range(2)]
+    grads = [b() for _, b in outs]
+    assert torch.equal(outs[0][0].per_token_loss, outs[1][0].per_token_loss)
+    assert torch.equal(grads[0].d_e, grads[1].d_e) and torch.equal(grads[0].d_c, grads[1].d_c)
+
+
+def test_lse_forward_and_indexed_matmul(cuda_device):  # test_kernels.py:26-39, :146-152
+    api = _api()
+    e, c, x = _make(32, 200, 900, 7)
+    lse, mean = api.lse_forward(e, c)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    assert np.max(np.abs(lse.cpu().numpy() - nlse)) < 1e-3
+    assert O.rel_err(mean.cpu().numpy(), c.astype(np.float64) @ e.astype(np.float64).mean(0)) < 1e-4
+    ones = api.indexed_matmul(np.ones((5, 8), np.float32), np.ones((3, 8), np.float32), np.array([0, 1, 2, 0, -1]))
+    assert ones.tolist() == [8, 8, 8, 8, 0]

@@ -257,3 +257,42 @@ def test_sort_gather4_path_matches_sorted_copy(cuda_device, monkeypatch):
     assert np.array_equal(a[4], b[4])
     for u, w in zip(a[:4], b[:4]):
         assert np.array_equal(u, w)
+
+
+@pytest.mark.parametrize("shards,filt", [(3, False), (4, True)])
+def test_fake_vocab_parallel_on_one_gpu(cuda_device, shards, filt):
+    """Vocab-parallel math without NCCL: each shard runs the local kernels with its
+    vocab_start, the 2N-float partials are merged with the log-add-exp kernel, every shard
+    filters against the global LSE, the -1 label term lands on the owner shard only, and the fp32
+    dE partials sum to the full gradient."""
+    from paper_2411_09009_b200 import ops
+    from paper_2411_09009_b200.vocab_parallel import shard_range
+
+    rng = np.random.default_rng(30 + shards)
+    n, d, v = 640, 128, 3001
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::6] = -100
+    ed, cd, td = _dev(e, torch.bfloat16), _dev(c, torch.bfloat16), _dev(x)
+    parts = [shard_range(v, r, shards) for r in range(shards)]
+    lses, corrs = zip(*[ops.forward_local(ed, cd[a:b].contiguous(), td, -100, a) for a, b in parts])
+    lse, loss = ops.merge_shards(torch.stack(lses), torch.stack(corrs), td, -100)
+    xo = np.where(x == -100, -1, x)
+    nl, nlse, _ = O.naive_forward(e, c, xo)
+    valid = xo != -1
+    assert _loss_err(loss.cpu().numpy(), nl) < LOSS_TOL
+    assert _loss_err(lse.cpu().numpy()[valid], nlse[valid]) < LOSS_TOL
+    up = _dev(O.default_upstream(xo, "mean-over-valid").astype(np.float32))
+    de = torch.zeros(n, d, device="cuda")
+    dcs = []
+    for a, b in parts:
+        de_p, dc_p, _, _ = ops.backward(ed, cd[a:b].contiguous(), td, lse, up, ignore_index=-100,
+                                        vocab_start=a, eps=O.EPSILON_DEFAULT if filt else 0.0,
+                                        fp32_de=True)
+        de += de_p
+        dcs.append(dc_p.float())
+    fde, fdc = O.naive_backward(e, c, xo, O.default_upstream(xo, "mean-over-valid"))
+    tol = 2e-2 if filt else GRAD_TOL
+    assert O.rel_err(de.cpu().numpy(), fde) < tol
+    assert O.rel_err(torch.cat(dcs).cpu().numpy(), fdc) < tol
