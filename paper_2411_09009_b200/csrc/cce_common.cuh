@@ -38,6 +38,7 @@ struct Params {
   int n_base;        // first token tile of this launch
   int mt;            // vocab tiles
   int splits;        // vocab splits per token tile (units = nt * splits)
+  int band;          // token tiles per raster band (bounds the E working set of concurrent CTAs)
   int num_kb;        // ceil(d / BK)
   float softcap;     // 0 => off
   // forward

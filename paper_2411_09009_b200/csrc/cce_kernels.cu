@@ -123,6 +123,20 @@ int ensure_attr(K kernel, size_t bytes) {
   return 0;
 }
 
+// Token tiles per raster band: concurrent CTAs then read at most this many E tiles, which must
+// stay L2-resident (~40 MB of the 126 MB L2; C tiles stream through the rest).
+int choose_band(int64_t d) {
+  const int64_t e_tile = (int64_t)cce::BM * d * 2;
+  return (int)std::max<int64_t>(1, (40ll << 20) / e_tile);
+}
+
+// Splits must give every band enough units to fill the grid.
+int clamp_splits(int splits, int nt, int mt, int band, int grid) {
+  const int nb = std::max(1, std::min(band, nt));
+  const int need = (grid + nb - 1) / nb;
+  return std::min(mt, std::max(splits, need));
+}
+
 // Choose the vocab split count so units = nt*splits balance over the persistent grid.
 int choose_splits(int nt, int mt, int grid, bool prefer_fine) {
   int best = 1;
@@ -193,8 +207,7 @@ int cce_abi_version(void) { return 1; }
 size_t cce_fwd_workspace_bytes(int64_t n, int64_t d, int64_t v) {
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
-  const int s = choose_splits(nt, mt, num_sms(), false);
-  (void)d;
+  const int s = clamp_splits(choose_splits(nt, mt, num_sms(), false), nt, mt, choose_band(d), num_sms());
   return (size_t)s * (size_t)n * sizeof(float2);
 }
 
@@ -208,7 +221,8 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int grid = num_sms();
-  const int splits = choose_splits(nt, mt, grid, false);
+  const int band = choose_band(d);
+  const int splits = clamp_splits(choose_splits(nt, mt, grid, false), nt, mt, band, grid);
   if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd: workspace too small");
   if (int e = ensure_attr(cce::cce_lse_kernel<cce::FWD>, kLseSmem)) return e;
   CUtensorMap tmE, tmC;
@@ -222,6 +236,7 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   p.n_base = 0;
   p.mt = mt;
   p.splits = splits;
+  p.band = band;
   p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
   p.softcap = softcap;
   p.targets = targets;
@@ -393,7 +408,8 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     p.nt = g;
     p.n_base = g0;
     p.mt = mt;
-    p.splits = choose_splits(g, mt, grid, true);
+    p.band = choose_band(d);
+    p.splits = clamp_splits(choose_splits(g, mt, grid, true), g, mt, p.band, grid);
     p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
     p.softcap = softcap;
     p.lse = lse;

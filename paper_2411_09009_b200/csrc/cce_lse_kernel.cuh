@@ -32,8 +32,10 @@ struct TileRef {
 };
 
 // Visit this CTA's tiles in schedule order.  FWD / BWD: static persistent schedule over units
-// u = s * g + n (token tile fastest), so concurrently running CTAs share the vocab tiles of C
-// while E stays L2-resident; each unit is a contiguous range of vocab tiles of one token tile.
+// (token tile n, vocab split s), each a contiguous range of vocab tiles of one token tile.  Units
+// are rastered in bands of `band` token tiles (token tile fastest inside a band, then split, then
+// band), so the CTAs running at any moment touch at most `band` E tiles (kept L2-resident by the
+// host's choice of band) and a handful of C tiles, each shared by many CTAs.
 // KEPT: grid-stride over the kept list (vocab-tile-major, so concurrent CTAs share C tiles).
 // `skip(n, count)` is called for BWD units whose upstream is all zero (kernels.py:434-438).
 template <int MODE, typename F, typename S>
@@ -47,9 +49,13 @@ __device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows,
     return;
   }
   const int units = rows.g * p.splits;
+  const int band = max(1, min(p.band, rows.g));
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const int n = p.n_base + u % rows.g;
-    const int s = u / rows.g;
+    const int b = u / (band * p.splits);
+    const int r = u - b * band * p.splits;
+    const int nb = min(band, rows.g - b * band);
+    const int n = p.n_base + b * band + r % nb;
+    const int s = r / nb;
     const int m0 = (int)(((long long)s * p.mt) / p.splits);
     const int m1 = (int)(((long long)(s + 1) * p.mt) / p.splits);
     if (MODE == BWD && p.block_zero[n]) {
