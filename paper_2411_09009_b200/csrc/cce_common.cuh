@@ -88,6 +88,7 @@ struct GradParams {
   float* de_f32;
   __nv_bfloat16* dc;       // [v][d]
   int accumulate;          // dC: add to the existing values (groups after the first)
+  int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
 };
 
 // Device-side view of the compaction: valid row count, token tiles of this launch.

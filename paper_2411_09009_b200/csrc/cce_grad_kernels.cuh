@@ -27,6 +27,8 @@ constexpr int DC_STAGES = 4;
 constexpr int DC_A_BYTES = 64 * 128 * 2;        // S-hat [64 tok][128 voc]  = 16 KiB (2 atoms)
 constexpr int DC_B_BYTES = 64 * DCH * 2;        // E [64 tok][256 d]        = 32 KiB (4 atoms)
 constexpr int DC_STAGE_BYTES = DC_A_BYTES + DC_B_BYTES;
+constexpr int DC_STG_PITCH = 144;                 // bytes per staged row (128 B + 16 B pad)
+constexpr int DC_STG_BYTES = 4 * 32 * DC_STG_PITCH;  // epilogue row-transpose staging, 4 warps
 
 // Visit, in index order, the stored tiles slot_of[i * stride] >= 0 for i < count; the warp reads
 // 32 entries per step and every lane calls f(i, slot) for each stored tile.
@@ -115,10 +117,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sb = sa + DE_A_BYTES;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], DE_STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DE_A_BYTES) + ((p.debug & 2) ? 0 : DE_B_BYTES));
             // S-hat [128 tok][128 voc] as 2 swizzle atoms in one box
-            tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, 2 * h);
-            if (p.atoms3d && p.perm == nullptr)  // C [128 voc][256 d] as 4 atoms in one box
+            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, 2 * h);
+            if (p.atoms3d && p.perm == nullptr && !(p.debug & 2))  // C [128 voc][256 d] as 4 atoms
               tma_load_3d(&tmC3, &full[stage], sb, 0, m * BN + 128 * h, dc * (DCH / 64));
           }
           __syncwarp();
@@ -219,7 +221,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DC_STAGES * DC_STAGE_BYTES);
+  uint8_t* stg = smem + DC_STAGES * DC_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + DC_STG_BYTES);
   uint64_t* empty = full + DC_STAGES;
   uint64_t* acc_full = empty + DC_STAGES;
   uint64_t* acc_free = acc_full + 2;
@@ -265,10 +268,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool e3 = p.atoms3d && !p.e_gather;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], DC_STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DC_A_BYTES) + ((p.debug & 2) ? 0 : DC_B_BYTES));
             // S-hat^T half: tokens [64h, +64) x vocab atoms 2vh, 2vh+1 in one box
-            tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM + 64 * h, 2 * vh);
-            if (e3)  // E [64 tok][256 d] as 4 atoms in one box
+            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM + 64 * h, 2 * vh);
+            if (e3 && !(p.debug & 2))  // E [64 tok][256 d] as 4 atoms in one box
               tma_load_3d(&tmE3, &full[stage], sb, 0, n * BM + 64 * h, dc * (DCH / 64));
           }
           __syncwarp();
@@ -311,9 +314,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
+    // Each thread owns one vocabulary row of the accumulator (its TMEM lane).  Rows are written
+    // through a per-warp shared-memory transpose so every global store instruction covers four
+    // full 128-byte row segments instead of 32 scattered 16-byte pieces.
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    uint8_t* wstg = stg + quarter * 32 * DC_STG_PITCH;
     int t = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
       const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
@@ -322,38 +329,56 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const bool has = p.cnt_m[m] > 0;
       const int vpos = m * BN + vh * 128 + row;
-      const bool vok = vpos < p.v;
+      const int my_vrow = vpos < p.v ? (p.perm_store ? p.perm_store[vpos] : vpos) : -1;
       if (has || !p.accumulate) {
-        const int vrow = vok ? (p.perm_store ? p.perm_store[vpos] : vpos) : 0;
 #pragma unroll 1
-        for (int c = 0; c < DCH / 32; ++c) {
-          const int col = dc * DCH + c * 32;
-          float x[32];
+        for (int c = 0; c < DCH / 64; ++c) {
+          // 1) this thread's 64 columns -> bf16 -> staging row `lane`
+          uint32_t pk[32];
           if (has) {
-            uint32_t r[32];
-            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 32, r);
+            uint32_t r0[32], r1[32];
+            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64, r0);
+            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64 + 32, r1);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) {
+              pk[j] = pack_bf16x2(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+              pk[16 + j] = pack_bf16x2(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+            }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) x[j] = 0.f;
+            for (int j = 0; j < 32; ++j) pk[j] = 0u;
           }
-          if (vok && col < p.d) {
-            __nv_bfloat16* dst = p.dc + (size_t)vrow * p.d + col;
-            const int lim = p.d - col;
-            if (p.accumulate) {
+          uint4* srow = reinterpret_cast<uint4*>(wstg + lane * DC_STG_PITCH);
 #pragma unroll
-              for (int j = 0; j < 32; j += 8)
-                if (j < lim) {
-                  const uint4 old = *reinterpret_cast<const uint4*>(dst + j);
-                  const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&old);
+          for (int q = 0; q < 8; ++q) srow[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          __syncwarp();
+          // 2) warp-cooperative stores: lanes 8k..8k+7 write row (4*it + k), 16 B each
+          const int col = dc * DCH + c * 64 + (lane & 7) * 8;
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) x[j + q] += __bfloat162float(ob[q]);
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (lane >> 3);
+            const int vrow = __shfl_sync(0xffffffffu, my_vrow, rr);
+            uint4 val = *reinterpret_cast<const uint4*>(wstg + rr * DC_STG_PITCH + (lane & 7) * 16);
+            if (vrow >= 0 && col < p.d) {
+              __nv_bfloat16* dst = p.dc + (size_t)vrow * p.d + col;
+              if (p.accumulate) {
+                const uint4 old = *reinterpret_cast<const uint4*>(dst);
+                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
+                const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 fa = __bfloat1622float2(a2[q]);
+                  const float2 fo = __bfloat1622float2(o2[q]);
+                  w[q] = pack_bf16x2(fa.x + fo.x, fa.y + fo.y);
                 }
+                val = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+              *reinterpret_cast<uint4*>(dst) = val;
             }
-            store_row32(nullptr, dst, x, lim);
           }
+          __syncwarp();
         }
       }
       tc_fence_before();

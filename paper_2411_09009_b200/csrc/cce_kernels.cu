@@ -113,7 +113,7 @@ int num_sms() {
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
 constexpr size_t kDeSmem = 1024 + (size_t)cce::DE_STAGES * cce::DE_STAGE_BYTES + kCtrlBytes;
-constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + kCtrlBytes;
+constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
 
 template <typename K>
 int ensure_attr(K kernel, size_t bytes) {
@@ -453,6 +453,10 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
+    {
+      const char* dbg = getenv("CCE_DEBUG_GRAD");
+      q.debug = dbg ? atoi(dbg) : 0;
+    }
     cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmC3, tmCg, q);
     CCE_CUDA(cudaGetLastError());
     cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmEg, q);
