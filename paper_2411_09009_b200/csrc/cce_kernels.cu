@@ -112,6 +112,7 @@ int num_sms() {
 
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
+constexpr size_t kLsePairSmem = 1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes;
 constexpr size_t kDeSmem = 1024 + (size_t)cce::DE_STAGES * cce::DE_STAGE_BYTES + kCtrlBytes;
 constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
 
@@ -196,6 +197,56 @@ BwdWs bwd_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t group_tile
   return w;
 }
 
+// CTA pairs (cta_group::2) for the logit-tile kernel unless CCE_PAIR=0; only for plain tile loads.
+bool use_pairs() {
+  static int v = [] {
+    const char* e = getenv("CCE_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0 && num_sms() >= 2;
+}
+
+// Vocabulary splits of the logit-tile kernel for `nt` token tiles (pairs: nt/2 token-tile pairs
+// on grid/2 CTA pairs).
+int lse_splits(int nt, int mt, int64_t d, bool pair, bool prefer_fine) {
+  const int grid = pair ? num_sms() / 2 : num_sms();
+  const int units_n = pair ? (nt + 1) / 2 : nt;
+  const int band = pair ? (choose_band(d) + 1) / 2 : choose_band(d);
+  return clamp_splits(choose_splits(units_n, mt, grid, prefer_fine), units_n, mt, band, grid);
+}
+
+// Launch cce_lse_kernel<MODE> on single CTAs or on CTA pairs (cluster of 2).
+template <int MODE>
+int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CUtensorMap& tmEg,
+               const CUtensorMap& tmC256, const CUtensorMap& tmCg, const CUtensorMap& tmC128,
+               cudaStream_t stream) {
+  if (!pair) {
+    if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 1>, kLseSmem)) return e;
+    const int units = p.nt * p.splits;
+    cce::cce_lse_kernel<MODE, 1><<<std::max(1, std::min(num_sms(), units)), cce::NUM_THREADS, kLseSmem,
+                                   stream>>>(tmE, tmEg, tmC256, tmCg, p);
+    CCE_CUDA(cudaGetLastError());
+    return 0;
+  }
+  if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 2>, kLsePairSmem)) return e;
+  const int pair_units = ((p.nt + 1) / 2) * p.splits;
+  const int grid = 2 * std::max(1, std::min(num_sms() / 2, pair_units));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(cce::NUM_THREADS);
+  cfg.dynamicSmemBytes = kLsePairSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CCE_CUDA(cudaLaunchKernelEx(&cfg, cce::cce_lse_kernel<MODE, 2>, tmE, tmEg, tmC128, tmCg, p));
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -207,7 +258,7 @@ int cce_abi_version(void) { return 1; }
 size_t cce_fwd_workspace_bytes(int64_t n, int64_t d, int64_t v) {
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
-  const int s = clamp_splits(choose_splits(nt, mt, num_sms(), false), nt, mt, choose_band(d), num_sms());
+  const int s = lse_splits(nt, mt, d, use_pairs(), false);
   return (size_t)s * (size_t)n * sizeof(float2);
 }
 
@@ -221,13 +272,15 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int grid = num_sms();
+  const bool pair = use_pairs();
   const int band = choose_band(d);
-  const int splits = clamp_splits(choose_splits(nt, mt, grid, false), nt, mt, band, grid);
+  const int splits = lse_splits(nt, mt, d, pair, false);
   if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd: workspace too small");
-  if (int e = ensure_attr(cce::cce_lse_kernel<cce::FWD>, kLseSmem)) return e;
-  CUtensorMap tmE, tmC;
-  if (!make_tmap(&tmE, E, n, d, cce::BM) || !make_tmap(&tmC, C, v, d, cce::BN))
+  CUtensorMap tmE, tmC, tmC128;
+  if (!make_tmap(&tmE, E, n, d, cce::BM) || !make_tmap(&tmC, C, v, d, cce::BN) ||
+      !make_tmap(&tmC128, C, v, d, cce::BN / 2))
     return fail("cce_fwd: cuTensorMapEncodeTiled failed");
+  (void)grid;
   cce::Params p{};
   p.n_total = (int)n;
   p.d = (int)d;
@@ -246,9 +299,8 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   p.correct = correct;
   const int units = nt * splits;
   cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
-  cce::cce_lse_kernel<cce::FWD><<<std::min(grid, units), cce::NUM_THREADS, kLseSmem, stream>>>(
-      tmE, tmE, tmC, tmC, p);
-  CCE_CUDA(cudaGetLastError());
+  (void)units;
+  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
   cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
       static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());
@@ -362,7 +414,6 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   if (group_tiles < 1 || capacity_tiles < 1) return fail("cce_bwd: group_tiles / capacity_tiles must be >= 1");
   const BwdWs w = bwd_layout(ws, n, d, v, group_tiles, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd: workspace too small");
-  if (int e = ensure_attr(cce::cce_lse_kernel<cce::BWD>, kLseSmem)) return e;
   if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
   if (int e = ensure_attr(cce::cce_dc_kernel, kDcSmem)) return e;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
@@ -380,12 +431,13 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   }
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
-  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3;
+  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmC128h;
   const int64_t shat_rows = capacity_tiles * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, e_src, n, d, cce::BM) && make_tmap(&tmEg, E, n, d, gbox) &&
             make_tmap(&tmC, C, v, d, cce::BN) && make_tmap(&tmCg, C, v, d, gbox) &&
             make_tmap(&tmC128, C, v, d, 128) && make_tmap(&tmE64, e_src, n, d, 64) &&
+            make_tmap(&tmC128h, C, v, d, cce::BN / 2) &&
             make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 2) &&
             make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
@@ -408,8 +460,9 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     p.nt = g;
     p.n_base = g0;
     p.mt = mt;
+    const bool pair = use_pairs() && !e_gather && (c_sorted || perm_padded == nullptr);
     p.band = choose_band(d);
-    p.splits = clamp_splits(choose_splits(g, mt, grid, true), g, mt, p.band, grid);
+    p.splits = lse_splits(g, mt, d, pair, true);
     p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
     p.softcap = softcap;
     p.lse = lse;
@@ -428,9 +481,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     p.cnt_n = w.cnt_n;
     p.cnt_m = w.cnt_m;
     p.counters = counters;
-    cce::cce_lse_kernel<cce::BWD><<<std::min(grid, g * p.splits), cce::NUM_THREADS, kLseSmem, stream>>>(
-        tmE, tmEg, tmC, tmCg, p);
-    CCE_CUDA(cudaGetLastError());
+    if (int e = launch_lse<cce::BWD>(p, pair, tmE, tmEg, tmC, tmCg, tmC128h, stream)) return e;
     cce::GradParams q{};
     q.n_total = (int)n;
     q.n_valid = n_valid;

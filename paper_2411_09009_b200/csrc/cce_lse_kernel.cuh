@@ -12,6 +12,12 @@
 //   KEPT = S-hat of the tiles in a precomputed kept list (the decision having been taken from the
 //          forward's tile maxima, cce_aux_kernels.cuh: decide_tiles_kernel).
 //
+// CG = 2 runs the same kernel on CTA pairs (cta_group::2): the pair computes a 256-token x
+// 256-vocab tile with one M=256 tcgen05.mma issued by the leader; each CTA loads its own 128 E
+// rows and half of the 256 C rows (so per-SM operand traffic per flop drops by a third) and owns
+// its 128 token rows in its own TMEM, so the epilogues are unchanged.  Filter decisions stay per
+// 128x256 tile (per CTA), as in the 1-CTA kernel.
+//
 // Persistent, one CTA per SM, 192 threads:
 //   warp 0      TMA producer (whole warp; gathers split over lanes): E rows [n*128, +128) and C
 //               rows of tile m, 64 D-columns per stage, 4-stage ring
@@ -29,54 +35,74 @@ struct TileRef {
   int s;        // vocabulary split of the unit (FWD / BWD) or slot (KEPT)
   bool first;   // first tile of its unit
   bool last;    // last tile of its unit
+  bool ok;      // this CTA's token tile exists (pairs: the second tile of an odd count does not)
+  bool zero;    // BWD, pairs: this CTA's token tile has zero upstream but the peer's does not
 };
 
 // Visit this CTA's tiles in schedule order.  FWD / BWD: static persistent schedule over units
-// (token tile n, vocab split s), each a contiguous range of vocab tiles of one token tile.  Units
-// are rastered in bands of `band` token tiles (token tile fastest inside a band, then split, then
-// band), so the CTAs running at any moment touch at most `band` E tiles (kept L2-resident by the
-// host's choice of band) and a handful of C tiles, each shared by many CTAs.
+// (token tile n, vocab split s), each a contiguous range of vocab tiles of one token tile (CG = 2:
+// of one token-tile pair, CTA rank r taking tile 2*pair + r).  Units are rastered in bands of
+// `band` token tiles (token tile fastest inside a band, then split, then band), so the CTAs
+// running at any moment touch at most `band` E tiles (kept L2-resident by the host's choice of
+// band) and a handful of C tiles, each shared by many CTAs.
 // KEPT: grid-stride over the kept list (vocab-tile-major, so concurrent CTAs share C tiles).
 // `skip(n, count)` is called for BWD units whose upstream is all zero (kernels.py:434-438).
-template <int MODE, typename F, typename S>
-__device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, F&& f, S&& skip) {
+template <int MODE, int CG, typename F, typename S>
+__device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, int rank, F&& f,
+                                              S&& skip) {
   if (MODE == KEPT) {
     const int total = min(*p.list_count, p.capacity);
     for (int i = blockIdx.x; i < total; i += gridDim.x) {
       const int2 t = p.list[i];
-      f(TileRef{t.x, t.y, i, true, true});
+      f(TileRef{t.x, t.y, i, true, true, true, false});
     }
     return;
   }
-  const int units = rows.g * p.splits;
-  const int band = max(1, min(p.band, rows.g));
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+  const int gp = (rows.g + CG - 1) / CG;  // token tiles (CG = 2: token-tile pairs) of this launch
+  const int units = gp * p.splits;
+  const int band = max(1, min((p.band + CG - 1) / CG, gp));
+  const int start = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  for (int u = start; u < units; u += stride) {
     const int b = u / (band * p.splits);
     const int r = u - b * band * p.splits;
-    const int nb = min(band, rows.g - b * band);
-    const int n = p.n_base + b * band + r % nb;
+    const int nb = min(band, gp - b * band);
+    const int local = (b * band + r % nb) * CG + rank;  // this CTA's token tile within the launch
+    const int n = p.n_base + local;
     const int s = r / nb;
     const int m0 = (int)(((long long)s * p.mt) / p.splits);
     const int m1 = (int)(((long long)(s + 1) * p.mt) / p.splits);
-    if (MODE == BWD && p.block_zero[n]) {
-      skip(n, m1 - m0);
-      continue;
+    const bool ok = local < rows.g;
+    bool zero = false;
+    if (MODE == BWD) {
+      zero = !ok || p.block_zero[n];
+      bool skip_unit = zero;
+      if (CG == 2) {
+        const int peer_local = local ^ 1;
+        const bool peer_zero = peer_local >= rows.g || p.block_zero[p.n_base + peer_local];
+        skip_unit = zero && peer_zero;  // the pair skips together or computes together
+      }
+      if (skip_unit) {
+        if (ok) skip(n, m1 - m0);
+        continue;
+      }
     }
-    for (int m = m0; m < m1; ++m) f(TileRef{n, m, s, m == m0, m == m1 - 1});
+    for (int m = m0; m < m1; ++m) f(TileRef{n, m, s, m == m0, m == m1 - 1, ok, zero});
   }
 }
 
-template <int MODE>
+template <int MODE, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_lse_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
                    const Params p) {
-  constexpr int STAGES = LSE_STAGES;
+  constexpr int STAGES = CG == 2 ? LSE_STAGES_PAIR : LSE_STAGES;
+  constexpr int SBYTES = CG == 2 ? PAIR_STAGE_BYTES : STAGE_BYTES;  // per-CTA bytes per stage
   if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SBYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: logits ready
   uint64_t* acc_free = acc_full + 2;    // [2] epilogue -> MMA: accumulator reusable
@@ -86,23 +112,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmE);
     tma_prefetch_desc(&tmC);
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], CG);  // pairs: both producers arrive on the leader's barrier
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_free[i], 128);
+      mbar_init(&acc_free[i], CG == 2 ? 2 : 128);  // pairs: one arrival per CTA epilogue
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2)
+      tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const Rows rows(p.n_valid, p.n_total, p.n_base, p.nt);
@@ -116,32 +149,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool gather_c = p.perm != nullptr;
     RowGather rge, rgc;
     int cur_n = -1;
-    for_each_tile<MODE>(p, rows, [&](const TileRef& t) {
-      if (t.n != cur_n) {
-        rge.load(gather_e ? p.row_map : nullptr, t.n * BM, BM);
-        cur_n = t.n;
+    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& t) {
+      if (CG == 1) {
+        if (t.n != cur_n) {
+          rge.load(gather_e ? p.row_map : nullptr, t.n * BM, BM);
+          cur_n = t.n;
+        }
+        rgc.load(p.perm, t.m * BN, BN);
       }
-      rgc.load(p.perm, t.m * BN, BN);
       for (int kb = 0; kb < p.num_kb; ++kb) {
-        uint8_t* sa = smem + stage * STAGE_BYTES;
+        uint8_t* sa = smem + stage * SBYTES;
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          if (CG == 2) {
+            // both CTAs' bytes complete on the leader's barrier; the follower only arrives
+            if (rank == 0)
+              mbar_arrive_expect_tx(&full[stage], 2 * SBYTES);
+            else
+              mbar_arrive_cluster(&full[stage], 0);
+            const uint32_t lb = leader_addr(&full[stage]);
+            tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
+            tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          }
         }
         __syncwarp();
-        load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, t.n * BM);
-        load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);
+        if (CG == 1) {
+          load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, t.n * BM);
+          load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);
+        }
         advance_stage(stage, phase, STAGES);
       }
     }, no_skip);
   } else if (warp == 1) {
     // ===================================== MMA issuer ====================================
-    if (lane == 0) {
-      constexpr uint32_t IDESC = make_idesc_bf16(BM, BN, 0, 0);
+    if (lane == 0 && rank == 0) {  // pairs: the leader issues for both CTAs
+      constexpr uint32_t IDESC = make_idesc_bf16(BM * CG, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for_each_tile<MODE>(p, rows, [&](const TileRef&) {
+      for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef&) {
         const int buf = t & 1;
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -149,16 +197,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t a0 = smem_u32(smem + stage * SBYTES);
           const uint32_t b0 = a0 + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024), make_sdesc(b0 + 32 * k, 0, 1024),
-                        IDESC, (kb | k) != 0);
-          mma_commit(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k) {
+            if (CG == 2)
+              mma_bf16_ss_pair(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024),
+                               make_sdesc(b0 + 32 * k, 0, 1024), IDESC, (kb | k) != 0);
+            else
+              mma_bf16_ss(d_tmem, make_sdesc(a0 + 32 * k, 0, 1024), make_sdesc(b0 + 32 * k, 0, 1024),
+                          IDESC, (kb | k) != 0);
+          }
+          if (CG == 2)
+            mma_commit_pair(&empty[stage]);
+          else
+            mma_commit(&empty[stage]);
           advance_stage(stage, phase, STAGES);
         }
-        mma_commit(&acc_full[buf]);
+        if (CG == 2)
+          mma_commit_pair(&acc_full[buf]);
+        else
+          mma_commit(&acc_full[buf]);
         ++t;
       }, no_skip);
     }
@@ -181,9 +240,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float run_m = -INFINITY, run_s = 0.f, corr = 0.f;
     bool have_corr = false;
 
-    auto load_row = [&](int n) {
+    auto load_row = [&](int n, bool ok) {
       grow = n * BM + row;
-      valid = grow < rows.n;
+      valid = ok && grow < rows.n;
       const int orow = valid ? (p.row_map ? p.row_map[grow] : grow) : 0;
       if (MODE == FWD) {
         tpos = -1;
@@ -236,9 +295,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     };
 
-    for_each_tile<MODE>(p, rows, [&](const TileRef& tr) {
+    // hand the accumulator back to the MMA issuer (pairs: one arrival per CTA on the leader)
+    auto release_acc = [&](int buf) {
+      tc_fence_before();
+      if (CG == 2) {
+        named_bar_sync(2, 128);
+        if (epi_tid == 0) {
+          if (rank == 0)
+            mbar_arrive(&acc_free[buf]);
+          else
+            mbar_arrive_cluster(&acc_free[buf], 0);
+        }
+      } else {
+        mbar_arrive(&acc_free[buf]);
+      }
+    };
+
+    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& tr) {
       if (tr.n != cur_n) {
-        load_row(tr.n);
+        load_row(tr.n, tr.ok);
         cur_n = tr.n;
       }
       const int buf = t & 1;
@@ -284,17 +359,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             run_m = nm;
           }
         }
-        tc_fence_before();
-        mbar_arrive(&acc_free[buf]);
-        if (p.tile_max) p.tile_max[((size_t)tr.n * p.mt + tr.m) * BM + row] = zmax;
+        release_acc(buf);
+        if (p.tile_max && tr.ok) p.tile_max[((size_t)tr.n * p.mt + tr.m) * BM + row] = zmax;
         if (tr.last && valid) {
           p.part[(size_t)tr.s * p.n_total + grow] = make_float2(run_m, run_s);
           if (have_corr) p.correct[grow] = corr;
         }
       } else if (MODE == KEPT) {
         store_shat(tacc, col0, tr.s);
-        tc_fence_before();
-        mbar_arrive(&acc_free[buf]);
+        release_acc(buf);
+      } else if (!tr.ok || tr.zero) {
+        // pairs only: this CTA's tile is missing or has zero upstream while the peer's is live
+        if (tr.ok && epi_tid == 0) atomicAdd(&p.counters[2], 1ull);
+        release_acc(buf);
       } else {
         // ------------------------------- backward filter pass ------------------------------
         // pass 1: row max of the raw logits.  S = exp(z' - lse) is monotone in z, so
@@ -339,8 +416,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else if (epi_tid == 0) {
           atomicAdd(&p.counters[1], 1ull);
         }
-        tc_fence_before();
-        mbar_arrive(&acc_free[buf]);
+        release_acc(buf);
       }
       ++t;
     }, [&](int, int count) {
@@ -350,9 +426,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
