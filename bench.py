@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--no-filter", action="store_true")
+    ap.add_argument("--low-memory", action="store_true",
+                    help="low_memory=True: O(N) forward state, filter pass recomputes every tile")
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -234,7 +236,8 @@ def main():
     e.requires_grad_(True)
     c.requires_grad_(True)
 
-    kw = dict(reduction="mean", filter_eps=eps, vocab_sorting=sort, softcap=cap or None)
+    kw = dict(reduction="mean", filter_eps=eps, vocab_sorting=sort, softcap=cap or None,
+              low_memory=args.low_memory)
     if world > 1 and not token_mode:
         kw.update(process_group=group, vocab_start=v0)
 
@@ -249,24 +252,37 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # ---- memory: forward-only and backward transient (instrument.py:3-10 definition)
+    # ---- memory (instrument.py:3-10 definition: transients only; inputs E, C, targets and the
+    # outputs dE, dC, loss are not counted).  Measured on one training step, then on the
+    # low-memory forward (inference / low_memory=True: only O(N) state).
+    def mem_step():
+        e.grad = None
+        c.grad = None
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        loss = linear_cross_entropy(e, c, t, **kw)
+        torch.cuda.synchronize()
+        fwd_peak = torch.cuda.max_memory_allocated(dev) - base
+        held = torch.cuda.memory_allocated(dev) - base
+        loss.backward()
+        torch.cuda.synchronize()
+        grad_bytes = e.grad.numel() * e.grad.element_size() + c.grad.numel() * c.grad.element_size()
+        step_peak = torch.cuda.max_memory_allocated(dev) - base - grad_bytes
+        return fwd_peak, held, step_peak
+
+    for _ in range(args.warmup):
+        step(e, c, t)
+    fwd_peak, fwd_held, step_peak = mem_step()
+    e.grad = None
+    c.grad = None
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
     with torch.no_grad():
         ops.forward_local(e.detach(), c.detach(), t, -100, v0, cap)
     torch.cuda.synchronize()
-    fwd_transient = torch.cuda.max_memory_allocated(dev) - base  # outputs lse/correct (8N B) included
-
-    for _ in range(args.warmup):
-        step(e, c, t)
-    torch.cuda.synchronize()
-    base = torch.cuda.memory_allocated(dev)
-    torch.cuda.reset_peak_memory_stats(dev)
-    step(e, c, t)
-    torch.cuda.synchronize()
-    grad_bytes = e.numel() * 2 + c.numel() * 2
-    bwd_transient = torch.cuda.max_memory_allocated(dev) - base - grad_bytes
+    fwd_lean = torch.cuda.max_memory_allocated(dev) - base  # outputs lse/correct (8N B) included
 
     # ---- timed region: device time with CUDA events, max over ranks
     ops.KERNEL_EVENTS = {}
@@ -358,8 +374,13 @@ def main():
     n_valid = int((t != -100).sum().item())
     v_loc = c.shape[0]
     kept = counters[0]
-    flops_fwd = 2.0 * n * v_loc * d
-    flops_bwd = 2.0 * n_valid * v_loc * d + 4.0 * d * kept * 128 * 256
+    tile_area = 128 * 256
+    tiles_path = not (args.low_memory or args.no_filter)  # forward on compacted rows
+    flops_fwd = 2.0 * (n_valid if tiles_path else n) * v_loc * d
+    # backward recompute: every tile (low_memory filter pass) or the kept tiles only (decision
+    # taken from the forward's tile maxima); then dE and dC over the kept tiles
+    flops_recompute = 2.0 * d * kept * tile_area if tiles_path else 2.0 * n_valid * v_loc * d
+    flops_bwd = flops_recompute + 4.0 * d * kept * tile_area
     # dominant single kernel: the forward logit-tile kernel (cce_fwd is one tcgen05 launch plus two
     # tiny ones); the backward entry is three kernels (B1 filter, B2 dE, B3 dC) and is reported
     # as a group in `kernel_ms` / `step_tflops`.
@@ -394,7 +415,7 @@ def main():
             "config": {
                 "workload": f"{args.config} head N={n} D={d} V={v}", "sigma": sigma, "softcap": cap,
                 "ignore_pad_frac": pad_frac, "filter_eps": None if args.no_filter else 2 ** -12,
-                "vocab_sorting": sort, "reduction": "mean",
+                "vocab_sorting": sort, "reduction": "mean", "low_memory": args.low_memory,
                 "parallelism": (f"vocab{world}" if world > 1 and not token_mode else f"token{world}"),
                 "l2": "inputs larger than L2 (C alone is %.2f GB)" % (v_loc * d * 2 / 1e9),
             },
@@ -411,7 +432,9 @@ def main():
                          "frac_sustained": achieved / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
                          "peak_source": peak_src + " bf16 burst", "traffic": traffic,
                          "flops_per_launch": dom_flops},
-            "memory": {"fwd_transient_bytes": int(fwd_transient), "bwd_transient_bytes": int(bwd_transient)},
+            "memory": {"step_peak_transient_bytes": int(step_peak), "fwd_peak_transient_bytes": int(fwd_peak),
+                       "fwd_to_bwd_state_bytes": int(fwd_held), "lean_fwd_transient_bytes": int(fwd_lean),
+                       "mode": "low_memory" if args.low_memory else "filter_from_forward"},
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

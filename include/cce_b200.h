@@ -94,6 +94,35 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
             size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
             int* overflow, void* stream);
 
+/* ---- filter decision taken from the forward (the default training path) ----
+ * The reference decides per (token block, vocab block) tile whether lse_backward recomputes it
+ * (kernels.py:434-455).  Here the forward already visits every tile, so it records each row's
+ * max raw logit per tile and the backward recomputes only the kept tiles.
+ *
+ * cce_fwd_tiles: forward over the COMPACTED rows E_c (row k = E[row_map[k]], k < *n_valid; see
+ * cce_compact_rows / cce_gather_rows) against the classifier in tile order C_t (C[perm] with
+ * vocab sorting, else C).  pos[i] (per ORIGINAL row, cce_bwd_prep) is the label position in tile
+ * order or -1.  lse_local / correct are per ORIGINAL row (undefined / 0 at ignored rows).
+ * tile_max: [ceil(n/128)][ceil(v/256)][128] fp32 (cce_tile_max_bytes), the max raw logit of
+ * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).
+ *
+ * cce_bwd_kept: the backward from tile_max.  Keeps tile (n, m) iff its upstream is not all zero
+ * and it holds a label or some S >= eps (the same strict test as cce_bwd, eps > 0 required);
+ * recomputes S-hat for the kept tiles only, then the dE / dC passes of cce_bwd.  dC rows land
+ * through perm_padded (NULL = tile order is C's order).  If more than capacity_tiles tiles are
+ * kept, *overflow = 1 and nothing past the decision runs: the caller then runs cce_bwd with
+ * run_if = overflow (device-gated, no host synchronisation).  counters as cce_bwd. */
+size_t cce_tile_max_bytes(int64_t n, int64_t v);
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream);
+size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles);
+int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+                 const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                 const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
+                 int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
+                 unsigned long long* counters, int* overflow, void* stream);
+
 /* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
  * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */
 int cce_gather_rows(const void* src, const int32_t* index, int64_t rows, int64_t cols, void* dst,

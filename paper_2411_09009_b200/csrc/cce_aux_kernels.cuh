@@ -236,6 +236,150 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
   for (int j = lane; j < n16; j += 32) d[j] = __ldg(s + j);
 }
 
+// ---------------------------------------------------------------------------------------
+// Filter decision from the forward's tile maxima (lse_backward's skip test, kernels.py:434-455,
+// taken without recomputing any logit tile)
+// ---------------------------------------------------------------------------------------
+
+// keep[m * nt + n] = 1 iff compact token tile n must be recomputed against vocab tile m: its
+// upstream is not all zero (kernels.py:434-438) and it holds a label (kernels.py:447-455) or some
+// row's largest S = exp(z' - lse) is >= eps (block_skip_decision, kernels.py:140-142, strict <).
+// tile_max[(n * mt + m) * 128 + r] is the forward's max raw logit of row r in tile (n, m);
+// tile_row_big is the same test the in-kernel filter (cce_lse_kernel<BWD>) applies.
+// Grid (ceil(mt / 64), nt), 256 threads: warp w takes vocab tiles blockIdx.x * 64 + w + 8j, lane l
+// rows 4l .. 4l + 3.  counters[1] += eps-skipped, counters[2] += zero-upstream-skipped tiles.
+__global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const float* __restrict__ lse,
+                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ row_map,
+                                    const int* __restrict__ n_valid, const uint8_t* __restrict__ block_zero,
+                                    int nt, int mt, float softcap, float eps, uint8_t* __restrict__ keep,
+                                    unsigned long long* __restrict__ counters) {
+  __shared__ unsigned s_cnt[2];
+  const int n = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = *n_valid;
+  const int nt_dev = (nv + BM - 1) / BM;
+  const int m_lo = blockIdx.x * 64;
+  const int m_hi = min(mt, m_lo + 64);
+  if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if (n >= nt_dev) {  // token tile past the compacted rows: not a tile of this backward
+    for (int m = m_lo + threadIdx.x; m < m_hi; m += blockDim.x) keep[(size_t)m * nt + n] = 0;
+    return;
+  }
+  if (block_zero[n]) {
+    for (int m = m_lo + threadIdx.x; m < m_hi; m += blockDim.x) keep[(size_t)m * nt + n] = 0;
+    if (threadIdx.x == 0) atomicAdd(&counters[2], (unsigned long long)(m_hi - m_lo));
+    return;
+  }
+  const bool use_softcap = softcap > 0.f;
+  const float inv_cap = use_softcap ? 1.0f / softcap : 0.f;
+  float lse2[4];
+  int pr[4];
+  bool ok[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int grow = n * BM + 4 * lane + k;
+    ok[k] = grow < nv;
+    const int orow = ok[k] ? row_map[grow] : 0;
+    lse2[k] = ok[k] ? lse[orow] * LOG2E : INFINITY;
+    pr[k] = ok[k] ? pos[orow] : -1;
+  }
+  unsigned skipped = 0;
+  for (int m = m_lo + warp; m < m_hi; m += 8) {
+    const float4 z = reinterpret_cast<const float4*>(tile_max + ((size_t)n * mt + m) * BM)[lane];
+    const float zz[4] = {z.x, z.y, z.z, z.w};
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      any |= ok[k] && tile_row_big(zz[k], lse2[k], softcap, inv_cap, eps);
+      any |= pr[k] >= m * BN && pr[k] < (m + 1) * BN;
+    }
+    const bool kept = __any_sync(0xffffffffu, any);
+    if (lane == 0) {
+      keep[(size_t)m * nt + n] = kept ? 1 : 0;
+      skipped += kept ? 0 : 1;
+    }
+  }
+  if (lane == 0 && skipped) atomicAdd(&s_cnt[0], skipped);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt[0]) atomicAdd(&counters[1], (unsigned long long)s_cnt[0]);
+}
+
+// One block of 1024 threads: the kept flags in vocab-tile-major order become the kept-tile list
+// (slot = list position, so concurrently running CTAs of the KEPT pass share C tiles), slot_of
+// (pre-filled with -1), per-tile counts, counters[0] += kept, and the capacity flags: *ok = 1 and
+// *overflow = 0 when every kept tile got a slot, else *ok = 0 and *overflow = 1.  `keep` is padded
+// with zeros to a multiple of 16 bytes.
+__global__ void __launch_bounds__(1024) build_list_kernel(
+    const uint8_t* __restrict__ keep, int nt, int mt, int capacity, int2* __restrict__ list,
+    int32_t* __restrict__ slot_of, int* __restrict__ cnt_n, int* __restrict__ cnt_m,
+    int* __restrict__ list_count, int* __restrict__ ok, int* __restrict__ overflow,
+    unsigned long long* __restrict__ counters) {
+  constexpr int T = 1024;
+  __shared__ int s_warp[T / 32];
+  const int total = nt * mt;
+  const int total16 = (total + 15) / 16;
+  const int per16 = (total16 + T - 1) / T;  // uint4 words per thread
+  const int w0 = threadIdx.x * per16, w1 = min(total16, w0 + per16);
+  const uint4* kw = reinterpret_cast<const uint4*>(keep);
+  auto bytes_of = [](uint4 x, int j) {
+    const uint32_t w = j < 4 ? x.x : j < 8 ? x.y : j < 12 ? x.z : x.w;
+    return (w >> (8 * (j & 3))) & 0xFFu;
+  };
+  int c = 0;
+  for (int w = w0; w < w1; ++w) {
+    const uint4 x = kw[w];
+    c += __popc(x.x & 0x01010101u) + __popc(x.y & 0x01010101u) + __popc(x.z & 0x01010101u) +
+         __popc(x.w & 0x01010101u);
+  }
+  // block exclusive scan of c
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int x = s_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_warp[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  int slot = (wid ? s_warp[wid - 1] : 0) + incl - c;
+  const int kept_total = s_warp[T / 32 - 1];
+  for (int w = w0; w < w1; ++w) {
+    const uint4 x = kw[w];
+    if ((x.x | x.y | x.z | x.w) == 0u) continue;
+#pragma unroll 1
+    for (int j = 0; j < 16; ++j) {
+      if (!bytes_of(x, j)) continue;
+      const int i = w * 16 + j;
+      const int m = i / nt, n = i - m * nt;
+      if (slot < capacity) {
+        list[slot] = make_int2(n, m);
+        slot_of[(size_t)n * mt + m] = slot;
+        atomicAdd(&cnt_n[n], 1);
+        atomicAdd(&cnt_m[m], 1);
+      }
+      ++slot;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *list_count = kept_total;
+    const bool fits = kept_total <= capacity;
+    *ok = fits ? 1 : 0;
+    *overflow = fits ? 0 : 1;
+    atomicAdd(&counters[0], (unsigned long long)kept_total);
+  }
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                    int64_t n4) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

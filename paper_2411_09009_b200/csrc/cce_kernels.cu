@@ -247,6 +247,44 @@ int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CU
   return 0;
 }
 
+struct KeptWs {
+  __nv_bfloat16* shat;
+  uint8_t* keep;
+  int2* list;
+  int32_t* slot_of;
+  uint8_t* block_zero;
+  int* list_count;
+  int* ok;
+  int* cnt_n;
+  int* cnt_m;
+  size_t keep_bytes, slot_bytes, cnt_bytes;
+  size_t total;
+};
+
+KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
+  const int64_t mt = (v + cce::BN - 1) / cce::BN;
+  const int64_t nt = (n + cce::BM - 1) / cce::BM;
+  auto up = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  uint8_t* b = static_cast<uint8_t*>(base);
+  KeptWs w;
+  size_t o = 0;
+  w.shat = reinterpret_cast<__nv_bfloat16*>(b + o); o += up((size_t)capacity * cce::SHAT_TILE_BYTES);
+  w.keep_bytes = up((size_t)nt * mt);
+  w.keep = b + o; o += w.keep_bytes;
+  w.list = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
+  w.slot_bytes = up((size_t)nt * mt * 4);
+  w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
+  w.block_zero = b + o; o += up((size_t)nt);
+  // zeroed together: list_count, ok, cnt_n[nt], cnt_m[mt]
+  w.cnt_bytes = up(256 + (size_t)(nt + mt) * 4);
+  w.list_count = reinterpret_cast<int*>(b + o);
+  w.ok = w.list_count + 1;
+  w.cnt_n = reinterpret_cast<int*>(b + o + 256);
+  w.cnt_m = w.cnt_n + nt;
+  o += w.cnt_bytes;
+  w.total = o;
+  return w;
+}
 }  // namespace
 
 extern "C" {
@@ -513,6 +551,163 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmEg, q);
     CCE_CUDA(cudaGetLastError());
   }
+  return 0;
+}
+
+// ---- filter from the forward: forward in tile order with tile maxima, backward on kept tiles ----
+
+size_t cce_tile_max_bytes(int64_t n, int64_t v) {
+  const int64_t nt = (n + cce::BM - 1) / cce::BM;
+  const int64_t mt = (v + cce::BN - 1) / cce::BN;
+  return (size_t)(nt * mt * cce::BM) * sizeof(float);
+}
+
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (n < 0 || d <= 0 || v <= 0) return fail("cce_fwd_tiles: bad sizes");
+  if (d % 8 != 0) return fail("cce_fwd_tiles: D must be a multiple of 8 (16-byte TMA row pitch)");
+  if (!row_map || !n_valid || !pos || !tile_max) return fail("cce_fwd_tiles: row_map, n_valid, pos, tile_max required");
+  if (n == 0) return 0;
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
+  const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  const bool pair = use_pairs();
+  const int splits = lse_splits(nt, mt, d, pair, false);
+  if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd_tiles: workspace too small");
+  CUtensorMap tmE, tmC, tmC128;
+  if (!make_tmap(&tmE, E_c, n, d, cce::BM) || !make_tmap(&tmC, C_t, v, d, cce::BN) ||
+      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2))
+    return fail("cce_fwd_tiles: cuTensorMapEncodeTiled failed");
+  cce::Params p{};
+  p.n_total = (int)n;
+  p.n_valid = n_valid;
+  p.d = (int)d;
+  p.v = (int)v;
+  p.nt = nt;
+  p.n_base = 0;
+  p.mt = mt;
+  p.splits = splits;
+  p.band = choose_band(d);
+  p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
+  p.softcap = softcap;
+  p.pos = pos;
+  p.row_map = row_map;
+  p.part = static_cast<float2*>(ws);
+  p.correct = correct;
+  p.tile_max = tile_max;
+  cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
+  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
+  cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+      static_cast<const float2*>(ws), splits, (int)n, lse_local);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+
+size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles) {
+  (void)d;
+  return kept_layout(nullptr, n, v, capacity_tiles).total;
+}
+
+int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+                 const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                 const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
+                 int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
+                 unsigned long long* counters, int* overflow, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
+  if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
+  if (!overflow) return fail("cce_bwd_kept: overflow flag required");
+  if (capacity_tiles < 1) return fail("cce_bwd_kept: capacity_tiles must be >= 1");
+  if (n <= 0) return 0;
+  const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
+  if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
+  if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
+  if (int e = ensure_attr(cce::cce_dc_kernel, kDcSmem)) return e;
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
+  const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
+  const int grid = num_sms();
+  CCE_CUDA(cudaMemsetAsync(w.keep, 0, w.keep_bytes, stream));
+  CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, w.slot_bytes, stream));
+  CCE_CUDA(cudaMemsetAsync(w.list_count, 0, w.cnt_bytes, stream));
+  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  CCE_CUDA(cudaGetLastError());
+  cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
+      tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, w.keep, counters);
+  CCE_CUDA(cudaGetLastError());
+  cce::build_list_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, (int)capacity_tiles, w.list, w.slot_of,
+                                                 w.cnt_n, w.cnt_m, w.list_count, w.ok, overflow, counters);
+  CCE_CUDA(cudaGetLastError());
+
+  CUtensorMap tmE, tmC, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3;
+  const int64_t shat_rows = capacity_tiles * cce::BM;
+  const bool atoms3d = d % 64 == 0;
+  bool ok = make_tmap(&tmE, E_c, n, d, cce::BM) && make_tmap(&tmC, C_t, v, d, cce::BN) &&
+            make_tmap(&tmC128, C_t, v, d, 128) && make_tmap(&tmE64, E_c, n, d, 64) &&
+            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 2) &&
+            make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
+  if (ok && atoms3d)
+    ok = make_tmap3d(&tmC3, C_t, v, d, 128, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64);
+  else {
+    tmC3 = tmC128;
+    tmE3 = tmE64;
+  }
+  if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
+
+  // S-hat of the kept tiles only (cce_lse_kernel<KEPT>, grid-stride over the list)
+  cce::Params p{};
+  p.n_total = (int)n;
+  p.n_valid = n_valid;
+  p.run_if = w.ok;
+  p.d = (int)d;
+  p.v = (int)v;
+  p.nt = nt;
+  p.n_base = 0;
+  p.mt = mt;
+  p.splits = std::max(1, (grid + nt - 1) / nt);  // grid sizing only
+  p.band = choose_band(d);
+  p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
+  p.softcap = softcap;
+  p.lse = lse;
+  p.upstream = upstream;
+  p.pos = pos;
+  p.row_map = row_map;
+  p.eps = eps;
+  p.shat = w.shat;
+  p.capacity = (int)capacity_tiles;
+  p.counters = counters;
+  p.list = w.list;
+  p.list_count = w.list_count;
+  if (int e = launch_lse<cce::KEPT>(p, false, tmE, tmE, tmC, tmC, tmC, stream)) return e;
+
+  cce::GradParams q{};
+  q.n_total = (int)n;
+  q.n_valid = n_valid;
+  q.run_if = w.ok;
+  q.d = (int)d;
+  q.v = (int)v;
+  q.mt = mt;
+  q.ndc = ndc;
+  q.n_base = 0;
+  q.g = nt;
+  q.slot_of = w.slot_of;
+  q.cnt_n = w.cnt_n;
+  q.cnt_m = w.cnt_m;
+  q.perm = nullptr;
+  q.perm_store = perm_padded;
+  q.row_map = row_map;
+  q.e_gather = 0;
+  q.atoms3d = atoms3d ? 1 : 0;
+  q.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
+  q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
+  q.dc = static_cast<__nv_bfloat16*>(dc);
+  q.accumulate = 0;
+  cce::cce_de_kernel<<<std::min(grid, nt * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmC3, tmC128, q);
+  CCE_CUDA(cudaGetLastError());
+  cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmE64, q);
+  CCE_CUDA(cudaGetLastError());
   return 0;
 }
 

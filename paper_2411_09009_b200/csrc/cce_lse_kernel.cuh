@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int cur_n = -1;
     bool valid = false;
     int grow = 0;
+    int orow = 0;                  // original row of E (row_map; identity without compaction)
     int64_t tpos = -1;             // FWD: target position in C's row order
     float lse2 = 0.f, up_r = 0.f;  // BWD / KEPT
     int pos_r = -1;
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto load_row = [&](int n, bool ok) {
       grow = n * BM + row;
       valid = ok && grow < rows.n;
-      const int orow = valid ? (p.row_map ? p.row_map[grow] : grow) : 0;
+      orow = valid ? (p.row_map ? p.row_map[grow] : grow) : 0;
       if (MODE == FWD) {
         tpos = -1;
         if (valid) {
@@ -361,9 +362,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         release_acc(buf);
         if (p.tile_max && tr.ok) p.tile_max[((size_t)tr.n * p.mt + tr.m) * BM + row] = zmax;
-        if (tr.last && valid) {
-          p.part[(size_t)tr.s * p.n_total + grow] = make_float2(run_m, run_s);
-          if (have_corr) p.correct[grow] = corr;
+        if (tr.last && valid) {  // per ORIGINAL row (rows may be compacted, filter_ignored)
+          p.part[(size_t)tr.s * p.n_total + orow] = make_float2(run_m, run_s);
+          if (have_corr) p.correct[orow] = corr;
         }
       } else if (MODE == KEPT) {
         store_shat(tacc, col0, tr.s);

@@ -43,14 +43,21 @@ def _resolve_eps(filter_eps):
 class _LinearCrossEntropy(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
-                vocab_start):
-        if group is None:
+                vocab_start, low_memory):
+        # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
+        # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
+        # low_memory / inference: plain forward, only O(N) transients survive to the backward.
+        ctx.state = None
+        if eps > 0 and not low_memory and (ctx.needs_input_grad[0] or ctx.needs_input_grad[1]):
+            lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
+                                                              softcap, vocab_sorting)
+        else:
             lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
+        if group is None:
             lse, loss = ops.merge_shards(lse_local[None], correct[None], targets, ignore_index)
         else:
             from .vocab_parallel import gather_and_merge
 
-            lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
             lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group)
         valid = targets != ignore_index
         ctx.save_for_backward(e, c, targets, lse)
@@ -77,7 +84,16 @@ class _LinearCrossEntropy(torch.autograd.Function):
             n_valid = valid.sum().clamp_min(1).to(torch.float32)
             up = valid.to(torch.float32) * (g / n_valid)
         up = up.contiguous()
-        if group is None:
+        state, ctx.state = ctx.state, None
+        if state is not None:
+            de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                                           fp32_de=group is not None)
+            del state
+            if group is not None:
+                from .vocab_parallel import all_reduce_de
+
+                de = all_reduce_de(de, group)
+        elif group is None:
             de, dc, _, _ = ops.backward(e, c, targets, lse, up, ignore_index=ignore_index,
                                         vocab_start=vocab_start, softcap=softcap, eps=eps,
                                         vocab_sorting=vocab_sorting)
@@ -87,7 +103,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
             de, dc = sharded_backward(e, c, targets, lse, up, ignore_index=ignore_index,
                                       vocab_start=vocab_start, softcap=softcap, eps=eps,
                                       vocab_sorting=vocab_sorting, group=group)
-        return de, dc, None, None, None, None, None, None, None, None
+        return de, dc, None, None, None, None, None, None, None, None, None
 
 
 def linear_cross_entropy(
@@ -101,12 +117,15 @@ def linear_cross_entropy(
     vocab_sorting: bool = True,
     process_group=None,
     vocab_start: int = 0,
+    low_memory: bool = False,
 ) -> torch.Tensor:
     """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
 
     e: [..., D] bf16 CUDA embeddings; c: [V, D] bf16 classifier (nn.Linear weight layout);
     targets: [...] int64.  Returns a scalar for "mean"/"sum", else per-token losses of shape
-    e.shape[:-1].
+    e.shape[:-1].  low_memory=True keeps only O(N) state between forward and backward (the
+    backward then recomputes every tile to take the filter decision) instead of the sorted
+    classifier copy and the per-tile row maxima.
     """
     if reduction not in ("mean", "sum", "none"):
         raise ValueError(f"unknown reduction {reduction!r}")
@@ -124,7 +143,8 @@ def linear_cross_entropy(
         raise ValueError("softcap must be positive")
     eps = _resolve_eps(filter_eps)
     out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
-                                    bool(vocab_sorting), process_group, int(vocab_start))
+                                    bool(vocab_sorting), process_group, int(vocab_start),
+                                    bool(low_memory))
     if reduction == "none":
         return out.reshape(lead)
     return out

@@ -265,6 +265,149 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     return de, dc, counters, perm
 
 
+@dataclass
+class TileState:
+    """What the filter-from-forward path hands from the forward to the backward.
+
+    e_c      compacted rows of E (filter_ignored, kernels.py:494-510) [n, d] bf16
+    c_t      classifier in tile order: C[perm] (vocab sorting) or C itself
+    row_map / n_valid   compaction (device), perm / perm_padded (None without sorting)
+    pos      label position in tile order per original row (-1 ignored / other shard)
+    tile_max [nt, mt, 128] fp32 max raw logit per compact row per tile
+    """
+
+    e: torch.Tensor
+    e_c: torch.Tensor
+    c_t: torch.Tensor
+    row_map: torch.Tensor
+    n_valid: torch.Tensor
+    perm: torch.Tensor | None
+    perm_padded: torch.Tensor | None
+    pos: torch.Tensor
+    tile_max: torch.Tensor
+    vocab_start: int
+    softcap: float
+
+    def nbytes(self) -> int:
+        own = [self.e_c, self.row_map, self.n_valid, self.pos, self.tile_max]
+        if self.perm is not None:
+            own += [self.c_t, self.perm, self.perm_padded]
+        return sum(t.numel() * t.element_size() for t in own)
+
+
+def gather_rows(src: torch.Tensor, index: torch.Tensor, rows: int) -> torch.Tensor:
+    """dst[i] = src[index[i]] for i < rows (bf16 rows)."""
+    lib = _lib.load()
+    dst = torch.empty(rows, src.shape[1], dtype=src.dtype, device=src.device)
+    if rows:
+        _lib.check(lib.cce_gather_rows(_p(src), _p(index), rows, src.shape[1], _p(dst),
+                                       _stream(src.device)), "cce_gather_rows")
+        LAUNCHES["count"] += 1
+    return dst
+
+
+def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
+                  vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+    """Forward of the filter-from-forward path: (lse_local, correct, TileState).
+
+    Same results as forward_local (indexed_matmul + lse_forward, kernels.py:204-319), computed
+    the way cce_loss orders the work: ignored rows are compacted first (kernels.py:494-510, 531)
+    and, with vocab sorting, the vocabulary order (compute_vocab_order, kernels.py:145-160; the
+    mean logit C.ebar is a GEMV of the valid rows' mean) is fixed before the tile sweep so the
+    forward visits exactly the backward's tiles and records each row's max logit per tile.
+    """
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    row_map, n_valid = compact_rows(targets, ignore_index)
+    e_c = gather_rows(e, row_map, n)
+    if vocab_sorting and perm is None:
+        perm, _ = vocab_order(e, c, targets, ignore_index, n_valid)
+    vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
+    perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev) if perm is not None else None
+    inv_perm = torch.empty(v, dtype=torch.int32, device=dev) if perm is not None else None
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
+                                _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
+    LAUNCHES["count"] += 2 if perm is not None else 1
+    c_t = gather_rows(c, perm, v) if perm is not None else c
+    tile_max = torch.empty(lib.cce_tile_max_bytes(n, v) // 4, dtype=torch.float32, device=dev)
+    lse_local = torch.empty(n, dtype=torch.float32, device=dev)
+    correct = torch.empty(n, dtype=torch.float32, device=dev)
+    state = TileState(e, e_c, c_t, row_map, n_valid, perm, perm_padded, pos, tile_max,
+                      int(vocab_start), float(softcap or 0.0))
+    if n == 0:
+        return lse_local, correct, state
+    ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    ev = _ev_begin("fwd")
+    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), n, d, v,
+                                 float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
+                                 _p(tile_max), stream), "cce_fwd_tiles")
+    _ev_end("fwd", ev)
+    LAUNCHES["count"] += 3
+    return lse_local, correct, state
+
+
+def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
+                   eps: float = EPSILON_DEFAULT, fp32_de: bool = False):
+    """Backward of the filter-from-forward path (lse_backward, kernels.py:327-486).
+
+    The skip decision of every tile comes from the forward's tile maxima (the same strict test
+    as the in-kernel filter), so only kept tiles are recomputed.  If the kept tiles exceed the
+    S-hat budget, the full filter pass (`backward`'s grouped path) runs instead, gated on a
+    device flag.  Returns (dE, dC, counters[3]).
+    """
+    lib = _lib.load()
+    e, c_t = state.e, state.c_t
+    n, d = e.shape
+    v = c_t.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev)
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    if n == 0:
+        return de, dc.zero_(), counters
+    if not eps:
+        raise ValueError("backward_tiles needs filtering (eps > 0)")
+    nt = -(-n // BLOCK_TOKENS)
+    mt = -(-v // BLOCK_VOCAB)
+    budget = shat_budget_tiles()
+    cap = min(budget, nt * mt)
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws_bytes = lib.cce_bwd_kept_workspace_bytes(n, d, v, cap)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ev = _ev_begin("bwd")
+    _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.perm_padded), _p(state.row_map),
+                                _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
+                                n, d, v, state.softcap, float(eps), cap, _p(ws), ws_bytes, _p(de),
+                                int(fp32_de), _p(dc), _p(counters), _p(overflow), stream), "cce_bwd_kept")
+    LAUNCHES["count"] += 6
+    del ws
+    # overflow fallback: the grouped filter pass over budget-sized token groups (worst case fits)
+    if cap < nt * mt:
+        g = max(1, budget // mt)
+        counters2 = torch.zeros(3, dtype=torch.int64, device=dev)
+        ws_bytes = lib.cce_bwd_workspace_bytes(n, d, v, g, g * mt)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        _lib.check(lib.cce_bwd(_p(e), _p(c_t), _p(state.perm_padded), 1 if state.perm is not None else 0,
+                               _p(state.row_map), _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream),
+                               n, d, v, state.softcap, float(eps), g, g * mt, _p(overflow), 0, _p(ws),
+                               ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters2), _p(None), stream),
+                   "cce_bwd")
+        LAUNCHES["count"] += 2 + 3 * (-(-nt // g))
+        counters = torch.where(overflow.bool(), counters2, counters)
+    _ev_end("bwd", ev)
+    LAST_COUNTERS["counters"] = counters
+    LAST_OVERFLOW["flag"] = overflow
+    return de, dc, counters
+
+
 def shat_budget_tiles() -> int:
     """S-hat slots (64 KiB each) the backward may hold: CCE_SHAT_BUDGET_MB (default 1024)."""
     budget = int(os.environ.get("CCE_SHAT_BUDGET_MB", "1024")) << 20

@@ -38,13 +38,18 @@ def gather_and_merge(lse_local, correct, targets, ignore_index, group):
     return ops.merge_shards(allp[:, 0].contiguous(), allp[:, 1].contiguous(), targets, ignore_index)
 
 
+def all_reduce_de(de_acc, group):
+    """Sum the fp32 dE partials of all vocab shards, then cast to bf16."""
+    dist.all_reduce(de_acc, op=dist.ReduceOp.SUM, group=group)
+    return ops.f32_to_bf16(de_acc)
+
+
 def sharded_backward(e, c, targets, lse, upstream, *, ignore_index, vocab_start, softcap, eps,
                      vocab_sorting, group):
     de_acc, dc, _, _ = ops.backward(e, c, targets, lse, upstream, ignore_index=ignore_index,
                                     vocab_start=vocab_start, softcap=softcap, eps=eps,
                                     vocab_sorting=vocab_sorting, fp32_de=True)
-    dist.all_reduce(de_acc, op=dist.ReduceOp.SUM, group=group)
-    return ops.f32_to_bf16(de_acc), dc
+    return all_reduce_de(de_acc, group), dc
 
 
 def vocab_parallel_cross_entropy(e, c_shard, targets, *, vocab_start: int, group=None, **kw):

@@ -11,6 +11,7 @@ for s in "$@"; do
     check) timeout 300 python scripts/gpu_check.py all > $out/check.log 2>&1; echo "exit $?" >> $out/check.log ;;
     bench) timeout 900 python bench.py > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
     benchfast) timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
+    benchlow) timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --low-memory > $out/benchlow.log 2>&1; echo "exit $?" >> $out/benchlow.log ;;
     benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \

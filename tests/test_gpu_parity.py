@@ -28,22 +28,34 @@ def _dev(x, dtype=None):
     return t.to(dtype) if dtype is not None else t
 
 
+PATHS = ["filter", "tiles"]  # backward filter pass (low_memory) / decision from the forward
+
+
 def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sorting=True,
-         upstream=None, perm=None):
+         upstream=None, perm=None, path="filter"):
     from paper_2411_09009_b200 import ops
 
     ed = _dev(e, torch.bfloat16)
     cd = _dev(c, torch.bfloat16)
     td = _dev(x.astype(np.int64))
-    lse_l, corr = ops.forward_local(ed, cd, td, ignore_index, 0, softcap)
+    pd = None if perm is None else _dev(perm.astype(np.int32))
+    tiles = path == "tiles" and bool(eps)
+    if tiles:
+        lse_l, corr, st = ops.forward_tiles(ed, cd, td, ignore_index, 0, softcap, vocab_sorting=sorting,
+                                            perm=pd)
+    else:
+        lse_l, corr = ops.forward_local(ed, cd, td, ignore_index, 0, softcap)
     lse, loss = ops.merge_shards(lse_l[None], corr[None], td, ignore_index)
     if upstream is None:
         xx = np.where(x == ignore_index, -1, x)
         upstream = O.default_upstream(xx, "mean-over-valid")
     up = _dev(upstream.astype(np.float32))
-    de, dc, cnt, perm_out = ops.backward(ed, cd, td, lse, up, ignore_index=ignore_index,
-                                        softcap=softcap, eps=eps, vocab_sorting=sorting,
-                                        perm=None if perm is None else _dev(perm.astype(np.int32)))
+    if tiles:
+        de, dc, cnt = ops.backward_tiles(st, td, lse, up, ignore_index=ignore_index, eps=eps)
+        perm_out = st.perm
+    else:
+        de, dc, cnt, perm_out = ops.backward(ed, cd, td, lse, up, ignore_index=ignore_index,
+                                            softcap=softcap, eps=eps, vocab_sorting=sorting, perm=pd)
     torch.cuda.synchronize()
     return (loss.cpu().numpy(), lse.cpu().numpy(), de.float().cpu().numpy(), dc.float().cpu().numpy(),
             cnt.cpu().numpy(), None if perm_out is None else perm_out.cpu().numpy())
@@ -53,14 +65,15 @@ def _loss_err(a, b):
     return float(np.max(np.abs(a - b))) / max(1.0, float(np.max(np.abs(b))))
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", golden_cases())
-def test_matches_reference_fixture(cuda_device, name):
+def test_matches_reference_fixture(cuda_device, name, path):
     """Reference-run fixtures: same bf16 inputs, same tile geometry, same vocab order."""
     g = np.load(GOLDEN / f"{name}.npz")
     e, c, x = g["e"], g["c"], g["x"]
     filt, srt = bool(g["filtering"]), bool(g["sorting"])
     loss, lse, de, dc, cnt, _ = _run(e, c, x, eps=O.EPSILON_DEFAULT if filt else 0.0, sorting=srt,
-                                     perm=g["perm"] if srt else None)
+                                     perm=g["perm"] if srt else None, path=path)
     valid = x != -1
     assert _loss_err(loss, g["loss"]) < LOSS_TOL
     assert _loss_err(lse[valid], g["lse"][valid]) < LOSS_TOL
@@ -80,14 +93,15 @@ def test_matches_reference_fixture(cuda_device, name):
     (129, 64, 257, 1.0, 0.0, 30.0, False),
     (1024, 768, 50257, 1.0, 0.0, 0.0, True),
 ])
-def test_random_against_oracle(cuda_device, n, d, v, sigma, ign, cap, sort):
+@pytest.mark.parametrize("path", PATHS)
+def test_random_against_oracle(cuda_device, n, d, v, sigma, ign, cap, sort, path):
     rng = np.random.default_rng(n + d + v)
     e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
     c = O.round_to_bf16((rng.standard_normal((v, d)) * sigma / math.sqrt(d)).astype(np.float32))
     x = rng.integers(0, v, n)
     if ign:
         x[rng.random(n) < ign] = -1
-    loss, lse, de, dc, cnt, perm = _run(e, c, x, softcap=cap, sorting=sort)
+    loss, lse, de, dc, cnt, perm = _run(e, c, x, softcap=cap, sorting=sort, path=path)
     nl, nlse, _ = O.naive_forward(e, c, x, softcap=cap)
     valid = x != -1
     assert _loss_err(loss, nl) < LOSS_TOL
@@ -101,6 +115,7 @@ def test_random_against_oracle(cuda_device, n, d, v, sigma, ign, cap, sort):
     assert O.rel_err(de, rde) < GRAD_TOL
     assert O.rel_err(dc, rdc) < GRAD_TOL
     assert int(cnt[1]) == st["skipped_epsilon"]
+    assert int(cnt.sum()) == st["total_tiles"]
 
 
 @pytest.mark.parametrize("cap", [0.0, 5.0])
@@ -136,16 +151,17 @@ def test_uniform_classifier_and_margin(cuda_device):  # test_kernels.py:132-136,
     assert loss[0] == pytest.approx(math.log(1.0 + (v - 1) * math.exp(-10.0)), abs=1e-4)
 
 
-def test_zero_upstream_and_all_ignored(cuda_device):  # test_kernels.py:240-246, :408-415
+@pytest.mark.parametrize("path", PATHS)
+def test_zero_upstream_and_all_ignored(cuda_device, path):  # test_kernels.py:240-246, :408-415
     rng = np.random.default_rng(5)
     e = O.round_to_bf16(rng.standard_normal((300, 32)).astype(np.float32))
     c = O.round_to_bf16(rng.standard_normal((700, 32)).astype(np.float32) * 0.2)
     x = rng.integers(0, 700, 300)
-    loss, lse, de, dc, cnt, _ = _run(e, c, x, upstream=np.zeros(300, np.float32))
+    loss, lse, de, dc, cnt, _ = _run(e, c, x, upstream=np.zeros(300, np.float32), path=path)
     assert np.all(de == 0) and np.all(dc == 0)
     assert int(cnt[2]) == 3 * 3 and int(cnt[0]) == 0
     xi = np.full(300, -1)
-    loss, lse, de, dc, cnt, _ = _run(e, c, xi)
+    loss, lse, de, dc, cnt, _ = _run(e, c, xi, path=path)
     assert np.all(loss == 0) and np.all(lse == 0) and np.all(de == 0) and np.all(dc == 0)
 
 
@@ -224,19 +240,20 @@ def test_all_ignored_mean_is_zero_not_nan(cuda_device):
     assert torch.all(e.grad == 0) and torch.all(c.grad == 0)
 
 
-def test_shat_budget_overflow_falls_back_to_groups(cuda_device, monkeypatch):
+@pytest.mark.parametrize("path", PATHS)
+def test_shat_budget_overflow_falls_back_to_groups(cuda_device, monkeypatch, path):
     """A budget below the kept-tile count forces the grouped rerun; results are unchanged."""
     rng = np.random.default_rng(21)
     n, d, v = 700, 64, 3000
     e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
     c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
     x = rng.integers(0, v, n)
-    base = _run(e, c, x)
+    base = _run(e, c, x, path=path)
     from paper_2411_09009_b200 import ops
 
     assert int(ops.LAST_OVERFLOW["flag"].item()) == 0
     monkeypatch.setenv("CCE_SHAT_BUDGET_MB", "1")  # 16 slots: 6x12 tiles cannot fit
-    small = _run(e, c, x)
+    small = _run(e, c, x, path=path)
     assert int(ops.LAST_OVERFLOW["flag"].item()) == 1
     for a, b in zip(base[:4], small[:4]):
         assert O.rel_err(a, b) < 1e-2
@@ -296,3 +313,31 @@ def test_fake_vocab_parallel_on_one_gpu(cuda_device, shards, filt):
     tol = 2e-2 if filt else GRAD_TOL
     assert O.rel_err(de.cpu().numpy(), fde) < tol
     assert O.rel_err(torch.cat(dcs).cpu().numpy(), fdc) < tol
+
+
+@pytest.mark.parametrize("cap,ign", [(0.0, 0.2), (20.0, 0.0)])
+def test_linear_cross_entropy_tile_path_matches_low_memory(cuda_device, cap, ign):
+    """Training default (decision from the forward's tile maxima) vs low_memory=True (in-kernel
+    filter pass): same loss, same kept/skipped tiles, gradients within bf16 tolerance."""
+    from paper_2411_09009_b200 import linear_cross_entropy, ops
+
+    rng = np.random.default_rng(77)
+    n, d, v = 1000, 256, 20000  # logit std 0.4 at V=20000: a mix of kept and eps-skipped tiles
+    e0 = torch.from_numpy(O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))).cuda().bfloat16()
+    c0 = torch.from_numpy(O.round_to_bf16((rng.standard_normal((v, d)) * 0.4 / math.sqrt(d)).astype(np.float32))).cuda().bfloat16()
+    t = torch.from_numpy(rng.integers(0, v, n)).cuda()
+    if ign:
+        t[torch.from_numpy(rng.random(n) < ign).cuda()] = -100
+    out = {}
+    for low in (False, True):
+        e = e0.clone().requires_grad_(True)
+        c = c0.clone().requires_grad_(True)
+        loss = linear_cross_entropy(e, c, t, softcap=cap or None, low_memory=low)
+        loss.backward()
+        out[low] = (loss.item(), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy(),
+                    ops.LAST_COUNTERS["counters"].cpu().tolist())
+    assert out[False][0] == pytest.approx(out[True][0], rel=1e-6)
+    assert out[False][3] == out[True][3]
+    assert out[False][3][1] > 0 and out[False][3][0] > 0  # some tiles skipped, some kept
+    assert O.rel_err(out[False][1], out[True][1]) < 1e-2
+    assert O.rel_err(out[False][2], out[True][2]) < 1e-2
