@@ -380,6 +380,54 @@ __global__ void __launch_bounds__(1024) build_list_kernel(
   }
 }
 
+// One block: CTA-pair work list of the KEPT pass.  The kept tiles of vocab tile m hold the
+// consecutive slots [off_m, off_m + cnt_m) (build_list_kernel); pair j of m takes slots
+// off_m + 2j and, if it exists, off_m + 2j + 1.  pairs[k] = (first slot, tiles in the pair).
+__global__ void __launch_bounds__(1024) build_pairs_kernel(const int* __restrict__ cnt_m, int mt,
+                                                           int2* __restrict__ pairs,
+                                                           int* __restrict__ pair_count) {
+  constexpr int T = 1024;
+  __shared__ int s_a[T / 32], s_b[T / 32];
+  const int per = (mt + T - 1) / T;
+  const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
+  int slots = 0, np = 0;
+  for (int m = m0; m < m1; ++m) {
+    slots += cnt_m[m];
+    np += (cnt_m[m] + 1) / 2;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int ia = slots, ib = np;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ya = __shfl_up_sync(0xffffffffu, ia, o);
+    const int yb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += ya; ib += yb; }
+  }
+  if (lane == 31) { s_a[wid] = ia; s_b[wid] = ib; }
+  __syncthreads();
+  if (wid == 0) {
+    int xa = s_a[lane], xb = s_b[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(0xffffffffu, xa, o);
+      const int yb = __shfl_up_sync(0xffffffffu, xb, o);
+      if (lane >= o) { xa += ya; xb += yb; }
+    }
+    s_a[lane] = xa;
+    s_b[lane] = xb;
+  }
+  __syncthreads();
+  int off = (wid ? s_a[wid - 1] : 0) + ia - slots;
+  int poff = (wid ? s_b[wid - 1] : 0) + ib - np;
+  for (int m = m0; m < m1; ++m) {
+    const int c = cnt_m[m];
+    for (int j = 0; 2 * j < c; ++j) pairs[poff + j] = make_int2(off + 2 * j, min(2, c - 2 * j));
+    off += c;
+    poff += (c + 1) / 2;
+  }
+  if (threadIdx.x == T - 1) *pair_count = poff;
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                    int64_t n4) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

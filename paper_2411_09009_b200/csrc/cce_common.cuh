@@ -70,6 +70,8 @@ struct Params {
   // KEPT
   const int2* list;        // [capacity] (token tile, vocab tile) of each slot
   const int* list_count;   // kept tiles (slots used = min(count, capacity))
+  const int2* pairs;       // CTA pairs: (first slot, 1 or 2 tiles) of one vocab tile
+  const int* pair_count;
 };
 
 // dE pass ("B2") and dC pass ("B3").

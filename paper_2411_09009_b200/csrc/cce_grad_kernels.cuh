@@ -7,7 +7,8 @@
 //
 //   B2 cce_de_kernel : unit = (token tile n, 256 D-columns).  TMEM accumulates
 //                      dE[n, dchunk] = sum over kept m of S-hat[n,m] (128x256, K-major A) x
-//                      C[m, dchunk] (256x256, MN-major B), two K-steps of 128 vocab per tile.
+//                      C[m, dchunk] (256x256, MN-major B), four 4-deep pipeline stages of 64
+//                      vocab rows per tile.
 //   B3 cce_dc_kernel : unit = (vocab tile m, 256 D-columns, 128-row vocab half).  TMEM
 //                      accumulates dC[m half, dchunk] = sum over kept n of S-hat^T (MN-major A)
 //                      x E[n, dchunk] (MN-major B), two K-steps of 64 tokens per tile.
@@ -19,9 +20,10 @@
 
 namespace cce {
 
-constexpr int DE_STAGES = 2;
-constexpr int DE_A_BYTES = BM * 128 * 2;        // S-hat [128 tok][128 voc]  = 32 KiB (2 atoms)
-constexpr int DE_B_BYTES = 128 * DCH * 2;       // C [128 voc][256 d]       = 64 KiB (4 atoms)
+constexpr int DE_KV = 64;                       // vocab rows (MMA K) per dE stage
+constexpr int DE_STAGES = 4;
+constexpr int DE_A_BYTES = BM * DE_KV * 2;      // S-hat [128 tok][64 voc]   = 16 KiB (1 atom)
+constexpr int DE_B_BYTES = DE_KV * DCH * 2;     // C [64 voc][256 d]         = 32 KiB (4 atoms)
 constexpr int DE_STAGE_BYTES = DE_A_BYTES + DE_B_BYTES;
 constexpr int DC_STAGES = 4;
 constexpr int DC_A_BYTES = 64 * 128 * 2;        // S-hat [64 tok][128 voc]  = 16 KiB (2 atoms)
@@ -110,25 +112,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int dc = u / G, ln = u % G;
       for_each_kept(p.slot_of + (size_t)ln * p.mt, p.mt, 1, [&](int m, int slot) {
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < BN / DE_KV; ++h) {
           RowGather rgc;
-          rgc.load(p.perm, m * BN + 128 * h, 128);
+          rgc.load(p.perm, m * BN + DE_KV * h, DE_KV);
           uint8_t* sa = smem + stage * DE_STAGE_BYTES;
           uint8_t* sb = sa + DE_A_BYTES;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DE_A_BYTES) + ((p.debug & 2) ? 0 : DE_B_BYTES));
-            // S-hat [128 tok][128 voc] as 2 swizzle atoms in one box
-            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, 2 * h);
-            if (p.atoms3d && p.perm == nullptr && !(p.debug & 2))  // C [128 voc][256 d] as 4 atoms
-              tma_load_3d(&tmC3, &full[stage], sb, 0, m * BN + 128 * h, dc * (DCH / 64));
+            // S-hat [128 tok][64 voc]: swizzle atom h of the stored tile
+            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
+            if (p.atoms3d && p.perm == nullptr && !(p.debug & 2))  // C [64 voc][256 d] as 4 atoms
+              tma_load_3d(&tmC3, &full[stage], sb, 0, m * BN + DE_KV * h, dc * (DCH / 64));
           }
           __syncwarp();
           if (!(p.atoms3d && p.perm == nullptr)) {
 #pragma unroll 1
             for (int a = 0; a < DCH / 64; ++a)
-              load_rows_warp<128>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage], sb + a * (128 * 128),
-                                  dc * DCH + 64 * a, m * BN + 128 * h);
+              load_rows_warp<DE_KV>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage], sb + a * (DE_KV * 128),
+                                    dc * DCH + 64 * a, m * BN + DE_KV * h);
           }
           advance_stage(stage, phase, DE_STAGES);
         }
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
         const int ln = u % G;
         const int buf = t & 1;
-        const int ksteps = 2 * p.cnt_n[ln];
+        const int ksteps = (BN / DE_KV) * p.cnt_n[ln];
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * DCH;
@@ -153,11 +155,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t a0 = smem_u32(smem + stage * DE_STAGE_BYTES);
           const uint32_t b0 = a0 + DE_A_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
-            const uint32_t a = a0 + (ks >> 2) * (BM * 128) + (ks & 3) * 32;
-            mma_bf16_ss(d_tmem, make_sdesc(a, 0, 1024), make_sdesc(b0 + ks * 2048, 128 * 128, 1024),
-                        IDESC, (s | ks) != 0);
-          }
+          for (int ks = 0; ks < DE_KV / 16; ++ks)  // A: K-major atom; B: 4 MN-major atoms, 16 K-rows each
+            mma_bf16_ss(d_tmem, make_sdesc(a0 + ks * 32, 0, 1024),
+                        make_sdesc(b0 + ks * 2048, DE_KV * 128, 1024), IDESC, (s | ks) != 0);
           mma_commit(&empty[stage]);
           advance_stage(stage, phase, DE_STAGES);
         }

@@ -251,6 +251,8 @@ struct KeptWs {
   __nv_bfloat16* shat;
   uint8_t* keep;
   int2* list;
+  int2* pairs;
+  int* pair_count;
   int32_t* slot_of;
   uint8_t* block_zero;
   int* list_count;
@@ -272,6 +274,7 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.keep_bytes = up((size_t)nt * mt);
   w.keep = b + o; o += w.keep_bytes;
   w.list = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
+  w.pairs = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
   w.slot_bytes = up((size_t)nt * mt * 4);
   w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
   w.block_zero = b + o; o += up((size_t)nt);
@@ -279,6 +282,7 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.cnt_bytes = up(256 + (size_t)(nt + mt) * 4);
   w.list_count = reinterpret_cast<int*>(b + o);
   w.ok = w.list_count + 1;
+  w.pair_count = w.list_count + 2;
   w.cnt_n = reinterpret_cast<int*>(b + o + 256);
   w.cnt_m = w.cnt_n + nt;
   o += w.cnt_bytes;
@@ -469,19 +473,19 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   }
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
-  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmC128h;
+  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmC128h, tmC64;
   const int64_t shat_rows = capacity_tiles * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, e_src, n, d, cce::BM) && make_tmap(&tmEg, E, n, d, gbox) &&
             make_tmap(&tmC, C, v, d, cce::BN) && make_tmap(&tmCg, C, v, d, gbox) &&
             make_tmap(&tmC128, C, v, d, 128) && make_tmap(&tmE64, e_src, n, d, 64) &&
-            make_tmap(&tmC128h, C, v, d, cce::BN / 2) &&
-            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 2) &&
+            make_tmap(&tmC128h, C, v, d, cce::BN / 2) && make_tmap(&tmC64, C, v, d, cce::DE_KV) &&
+            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 1) &&
             make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
-    ok = make_tmap3d(&tmC3, C, v, d, 128, cce::DCH / 64) && make_tmap3d(&tmE3, e_src, n, d, 64, cce::DCH / 64);
+    ok = make_tmap3d(&tmC3, C, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, e_src, n, d, 64, cce::DCH / 64);
   else {
-    tmC3 = tmC128;
+    tmC3 = tmC64;
     tmE3 = tmE64;
   }
   if (!ok) return fail("cce_bwd: cuTensorMapEncodeTiled failed");
@@ -546,7 +550,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
       const char* dbg = getenv("CCE_DEBUG_GRAD");
       q.debug = dbg ? atoi(dbg) : 0;
     }
-    cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmC3, tmCg, q);
+    cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmCg, q);
     CCE_CUDA(cudaGetLastError());
     cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmEg, q);
     CCE_CUDA(cudaGetLastError());
@@ -640,18 +644,24 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   cce::build_list_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, (int)capacity_tiles, w.list, w.slot_of,
                                                  w.cnt_n, w.cnt_m, w.list_count, w.ok, overflow, counters);
   CCE_CUDA(cudaGetLastError());
+  const bool pair = use_pairs();
+  if (pair) {
+    cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, w.pairs, w.pair_count);
+    CCE_CUDA(cudaGetLastError());
+  }
 
-  CUtensorMap tmE, tmC, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3;
+  CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3;
   const int64_t shat_rows = capacity_tiles * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, E_c, n, d, cce::BM) && make_tmap(&tmC, C_t, v, d, cce::BN) &&
-            make_tmap(&tmC128, C_t, v, d, 128) && make_tmap(&tmE64, E_c, n, d, 64) &&
-            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 2) &&
+            make_tmap(&tmC64, C_t, v, d, cce::DE_KV) && make_tmap(&tmE64, E_c, n, d, 64) &&
+            make_tmap(&tmC128h, C_t, v, d, cce::BN / 2) &&
+            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 1) &&
             make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
-    ok = make_tmap3d(&tmC3, C_t, v, d, 128, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64);
+    ok = make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64);
   else {
-    tmC3 = tmC128;
+    tmC3 = tmC64;
     tmE3 = tmE64;
   }
   if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
@@ -666,7 +676,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   p.nt = nt;
   p.n_base = 0;
   p.mt = mt;
-  p.splits = std::max(1, (grid + nt - 1) / nt);  // grid sizing only
+  p.splits = std::max(1, (2 * grid + nt - 1) / nt);  // grid sizing only
   p.band = choose_band(d);
   p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
   p.softcap = softcap;
@@ -680,7 +690,9 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   p.counters = counters;
   p.list = w.list;
   p.list_count = w.list_count;
-  if (int e = launch_lse<cce::KEPT>(p, false, tmE, tmE, tmC, tmC, tmC, stream)) return e;
+  p.pairs = w.pairs;
+  p.pair_count = w.pair_count;
+  if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
 
   cce::GradParams q{};
   q.n_total = (int)n;
@@ -704,7 +716,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
   q.dc = static_cast<__nv_bfloat16*>(dc);
   q.accumulate = 0;
-  cce::cce_de_kernel<<<std::min(grid, nt * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC128, tmC3, tmC128, q);
+  cce::cce_de_kernel<<<std::min(grid, nt * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmC64, q);
   CCE_CUDA(cudaGetLastError());
   cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmE64, q);
   CCE_CUDA(cudaGetLastError());

@@ -51,6 +51,19 @@ template <int MODE, int CG, typename F, typename S>
 __device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, int rank, F&& f,
                                               S&& skip) {
   if (MODE == KEPT) {
+    if (CG == 2) {
+      // pair entry = up to two kept tiles of one vocab tile (consecutive slots); a lone tile's
+      // partner CTA recomputes the same rows and discards them
+      const int total = *p.pair_count;
+      for (int i = blockIdx.x >> 1; i < total; i += gridDim.x >> 1) {
+        const int2 pe = p.pairs[i];
+        const bool ok = rank < pe.y;
+        const int slot = pe.x + (ok ? rank : 0);
+        const int2 t = p.list[slot];
+        f(TileRef{t.x, t.y, slot, true, true, ok, false});
+      }
+      return;
+    }
     const int total = min(*p.list_count, p.capacity);
     for (int i = blockIdx.x; i < total; i += gridDim.x) {
       const int2 t = p.list[i];
@@ -232,6 +245,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int t = 0;
     // per-row state, refreshed whenever the token tile changes
     int cur_n = -1;
+    bool cur_ok = false;
     bool valid = false;
     int grow = 0;
     int orow = 0;                  // original row of E (row_map; identity without compaction)
@@ -313,9 +327,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
 
     for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& tr) {
-      if (tr.n != cur_n) {
+      if (tr.n != cur_n || tr.ok != cur_ok) {  // KEPT pairs: a lone tile's partner visits it with ok = false
         load_row(tr.n, tr.ok);
         cur_n = tr.n;
+        cur_ok = tr.ok;
       }
       const int buf = t & 1;
       mbar_wait(&acc_full[buf], (t >> 1) & 1);
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (have_corr) p.correct[orow] = corr;
         }
       } else if (MODE == KEPT) {
-        store_shat(tacc, col0, tr.s);
+        if (tr.ok) store_shat(tacc, col0, tr.s);
         release_acc(buf);
       } else if (!tr.ok || tr.zero) {
         // pairs only: this CTA's tile is missing or has zero upstream while the peer's is live
