@@ -213,10 +213,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 // B3: dC
 // ------------------------------------------------------------------------------------------
+// CG = 2: the two vocabulary halves of one (vocab tile, 256 D-columns) unit run as a CTA pair
+// with one M = 256 tcgen05.mma per K-step issued by the leader: each CTA loads its own S-hat^T
+// half (A) and half of the shared E[64 tok][256 d] operand (B, 128 d-columns), so per-SM operand
+// traffic per flop drops by a third; each CTA's TMEM holds its 128 vocab rows.
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_dc_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmE,
                   const __grid_constant__ CUtensorMap tmE3, const __grid_constant__ CUtensorMap tmEg,
                   const GradParams p) {
+  constexpr int B_BYTES = DC_B_BYTES / CG;  // this CTA's part of E[64 tok][256 d]
+  constexpr int SBYTES = DC_A_BYTES + B_BYTES;
   if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -229,34 +236,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmS);
     tma_prefetch_desc(&tmE);
     for (int i = 0; i < DC_STAGES; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], CG);  // pairs: both producers arrive on the leader's barrier
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_free[i], 128);
+      mbar_init(&acc_free[i], CG == 2 ? 2 : 128);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2)
+      tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
   const int G = rows.g;
   // unit u = ((m * ndc) + dc) * 2 + vh: the two vocab halves of one (m, dchunk) run side by side
-  // and share their E / S-hat loads through L2
+  // (CG = 1: adjacent units sharing their E / S-hat loads through L2; CG = 2: one CTA pair)
   const int units = p.mt * p.ndc * 2;
+  const int start = CG == 2 ? (int)(blockIdx.x & ~1u) + rank : (int)blockIdx.x;
+  const int stride = (int)gridDim.x;
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = start; u < units; u += stride) {
       const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
       for_each_kept(p.slot_of + m, G, p.mt, [&](int ln, int slot) {
         const int n = p.n_base + ln;
@@ -268,14 +284,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool e3 = p.atoms3d && !p.e_gather;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DC_A_BYTES) + ((p.debug & 2) ? 0 : DC_B_BYTES));
-            // S-hat^T half: tokens [64h, +64) x vocab atoms 2vh, 2vh+1 in one box
-            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM + 64 * h, 2 * vh);
-            if (e3 && !(p.debug & 2))  // E [64 tok][256 d] as 4 atoms in one box
-              tma_load_3d(&tmE3, &full[stage], sb, 0, n * BM + 64 * h, dc * (DCH / 64));
+            if (CG == 2) {
+              if (rank == 0)
+                mbar_arrive_expect_tx(&full[stage], 2 * SBYTES);
+              else
+                mbar_arrive_cluster(&full[stage], 0);
+              const uint32_t lb = leader_addr(&full[stage]);
+              // S-hat^T half vh: tokens [64h, +64) x vocab atoms 2vh, 2vh+1; E: this CTA's 2 atoms
+              tma_load_3d_pair(&tmS, lb, sa, 0, slot * BM + 64 * h, 2 * vh);
+              tma_load_3d_pair(&tmE3, lb, sb, 0, n * BM + 64 * h, dc * (DCH / 64) + 2 * rank);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DC_A_BYTES) + ((p.debug & 2) ? 0 : DC_B_BYTES));
+              // S-hat^T half: tokens [64h, +64) x vocab atoms 2vh, 2vh+1 in one box
+              if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM + 64 * h, 2 * vh);
+              if (e3 && !(p.debug & 2))  // E [64 tok][256 d] as 4 atoms in one box
+                tma_load_3d(&tmE3, &full[stage], sb, 0, n * BM + 64 * h, dc * (DCH / 64));
+            }
           }
           __syncwarp();
-          if (!e3) {
+          if (CG == 1 && !e3) {
 #pragma unroll 1
             for (int a = 0; a < DCH / 64; ++a)
               load_rows_warp<64>(&tmE, &tmEg, rge, p.e_gather != 0, &full[stage], sb + a * (64 * 128),
@@ -286,12 +313,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       });
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = make_idesc_bf16(BM, DCH, 1, 1);  // A, B both MN-major
+    if (lane == 0 && rank == 0) {  // pairs: the leader issues for both CTAs
+      constexpr uint32_t IDESC = make_idesc_bf16(BM * CG, DCH, 1, 1);  // A, B both MN-major
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      for (int u = start; u < units; u += stride, ++t) {
         const int m = (u >> 1) / p.ndc;
         const int buf = t & 1;
         const int ksteps = 2 * p.cnt_m[m];
@@ -304,13 +331,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t a0 = smem_u32(smem + stage * DC_STAGE_BYTES);
           const uint32_t b0 = a0 + DC_A_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            mma_bf16_ss(d_tmem, make_sdesc(a0 + ks * 2048, 64 * 128, 1024),
-                        make_sdesc(b0 + ks * 2048, 64 * 128, 1024), IDESC, (s | ks) != 0);
-          mma_commit(&empty[stage]);
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ad = make_sdesc(a0 + ks * 2048, 64 * 128, 1024);
+            const uint64_t bd = make_sdesc(b0 + ks * 2048, 64 * 128, 1024);
+            if (CG == 2)
+              mma_bf16_ss_pair(d_tmem, ad, bd, IDESC, (s | ks) != 0);
+            else
+              mma_bf16_ss(d_tmem, ad, bd, IDESC, (s | ks) != 0);
+          }
+          if (CG == 2)
+            mma_commit_pair(&empty[stage]);
+          else
+            mma_commit(&empty[stage]);
           advance_stage(stage, phase, DC_STAGES);
         }
-        mma_commit(&acc_full[buf]);
+        if (CG == 2)
+          mma_commit_pair(&acc_full[buf]);
+        else
+          mma_commit(&acc_full[buf]);
       }
     }
   } else {
@@ -319,10 +357,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // full 128-byte row segments instead of 32 scattered 16-byte pieces.
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
+    const int epi_tid = threadIdx.x - 64;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     uint8_t* wstg = stg + quarter * 32 * DC_STG_PITCH;
     int t = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+    for (int u = start; u < units; u += stride, ++t) {
       const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
       const int buf = t & 1;
       mbar_wait(&acc_full[buf], (t >> 1) & 1);
@@ -382,14 +421,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_free[buf]);
+      if (CG == 2) {
+        named_bar_sync(2, 128);
+        if (epi_tid == 0) {
+          if (rank == 0)
+            mbar_arrive(&acc_free[buf]);
+          else
+            mbar_arrive_cluster(&acc_free[buf], 0);
+        }
+      } else {
+        mbar_arrive(&acc_free[buf]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 

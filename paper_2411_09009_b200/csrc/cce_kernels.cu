@@ -289,6 +289,35 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.total = o;
   return w;
 }
+// dC pass (B3) on single CTAs or CTA pairs (the pair needs the 3-D E map with 2-atom boxes).
+int launch_dc(const cce::GradParams& q, bool pair, const CUtensorMap& tmS64, const CUtensorMap& tmE64,
+              const CUtensorMap& tmE3, const CUtensorMap& tmE3h, const CUtensorMap& tmEg,
+              cudaStream_t stream) {
+  const int units = q.mt * q.ndc * 2;
+  if (!pair) {
+    if (int e = ensure_attr(cce::cce_dc_kernel<1>, kDcSmem)) return e;
+    cce::cce_dc_kernel<1><<<std::min(num_sms(), units), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3,
+                                                                                              tmEg, q);
+    CCE_CUDA(cudaGetLastError());
+    return 0;
+  }
+  if (int e = ensure_attr(cce::cce_dc_kernel<2>, kDcSmem)) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * std::max(1, std::min(num_sms() / 2, units / 2)));
+  cfg.blockDim = dim3(cce::NUM_THREADS);
+  cfg.dynamicSmemBytes = kDcSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CCE_CUDA(cudaLaunchKernelEx(&cfg, cce::cce_dc_kernel<2>, tmS64, tmE64, tmE3h, tmE64, q));
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -457,7 +486,6 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   const BwdWs w = bwd_layout(ws, n, d, v, group_tiles, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd: workspace too small");
   if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
-  if (int e = ensure_attr(cce::cce_dc_kernel, kDcSmem)) return e;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
@@ -473,7 +501,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   }
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
-  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmC128h, tmC64;
+  CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h, tmC128h, tmC64;
   const int64_t shat_rows = capacity_tiles * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, e_src, n, d, cce::BM) && make_tmap(&tmEg, E, n, d, gbox) &&
@@ -483,12 +511,15 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
             make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 1) &&
             make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
-    ok = make_tmap3d(&tmC3, C, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, e_src, n, d, 64, cce::DCH / 64);
+    ok = make_tmap3d(&tmC3, C, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, e_src, n, d, 64, cce::DCH / 64) &&
+         make_tmap3d(&tmE3h, e_src, n, d, 64, cce::DCH / 128);
   else {
     tmC3 = tmC64;
     tmE3 = tmE64;
+    tmE3h = tmE64;
   }
   if (!ok) return fail("cce_bwd: cuTensorMapEncodeTiled failed");
+  const bool dc_pair = use_pairs() && atoms3d && !e_gather;
   for (int g0 = 0; g0 < nt; g0 += (int)group_tiles) {
     const int g = std::min((int)group_tiles, nt - g0);
     CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, w.map_bytes, stream));
@@ -552,8 +583,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     }
     cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmCg, q);
     CCE_CUDA(cudaGetLastError());
-    cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmEg, q);
-    CCE_CUDA(cudaGetLastError());
+    if (int e = launch_dc(q, dc_pair, tmS64, tmE64, tmE3, tmE3h, tmEg, stream)) return e;
   }
   return 0;
 }
@@ -628,7 +658,6 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
-  if (int e = ensure_attr(cce::cce_dc_kernel, kDcSmem)) return e;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
@@ -650,7 +679,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     CCE_CUDA(cudaGetLastError());
   }
 
-  CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3;
+  CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h;
   const int64_t shat_rows = capacity_tiles * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, E_c, n, d, cce::BM) && make_tmap(&tmC, C_t, v, d, cce::BN) &&
@@ -659,10 +688,12 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
             make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 1) &&
             make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
-    ok = make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64);
+    ok = make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64) &&
+         make_tmap3d(&tmE3h, E_c, n, d, 64, cce::DCH / 128);
   else {
     tmC3 = tmC64;
     tmE3 = tmE64;
+    tmE3h = tmE64;
   }
   if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
 
@@ -718,9 +749,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   q.accumulate = 0;
   cce::cce_de_kernel<<<std::min(grid, nt * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmC64, q);
   CCE_CUDA(cudaGetLastError());
-  cce::cce_dc_kernel<<<std::min(grid, 2 * mt * ndc), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3, tmE64, q);
-  CCE_CUDA(cudaGetLastError());
-  return 0;
+  return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
 }
 
 int cce_indexed_dot(const void* E, const void* C, const int64_t* targets, int64_t n, int64_t d,

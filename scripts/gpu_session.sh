@@ -6,12 +6,17 @@ python -m paper_2411_09009_b200._build > $out/build.log 2>&1
 for s in "$@"; do
   case $s in
     tests) timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $out/pytest_gpu.log 2>&1; echo "exit $?" >> $out/pytest_gpu.log ;;
+    testsnopair) CCE_PAIR=0 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/pytest_gpu_nopair.log 2>&1; echo "exit $?" >> $out/pytest_gpu_nopair.log ;;
     testsall) timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/pytest_gpu.log 2>&1; echo "exit $?" >> $out/pytest_gpu.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "exit $?" >> $out/smoke.log ;;
     check) timeout 300 python scripts/gpu_check.py all > $out/check.log 2>&1; echo "exit $?" >> $out/check.log ;;
     bench) timeout 900 python bench.py > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
     benchfast) timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $out/bench.log 2>&1; echo "exit $?" >> $out/bench.log ;;
     benchlow) timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --low-memory > $out/benchlow.log 2>&1; echo "exit $?" >> $out/benchlow.log ;;
+    multirank) for mode in vocab token; do
+        CCE_BENCH_BACKEND=gloo CCE_BENCH_SAME_DEVICE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+          --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline --mode $mode \
+          >> $out/multirank.log 2>&1; echo "exit $mode $?" >> $out/multirank.log; done ;;
     benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
