@@ -92,6 +92,8 @@ struct GradParams {
   float* de_f32;
   __nv_bfloat16* dc;       // [v][d]
   int accumulate;          // dC: add to the existing values (groups after the first)
+  int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
+  int de_order;            // dE: 0 chunk-major units, 1 token-tile-major
   int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
 };
 

@@ -21,10 +21,19 @@
 namespace cce {
 
 constexpr int DE_KV = 64;                       // vocab rows (MMA K) per dE stage
-constexpr int DE_STAGES = 4;
-constexpr int DE_A_BYTES = BM * DE_KV * 2;      // S-hat [128 tok][64 voc]   = 16 KiB (1 atom)
-constexpr int DE_B_BYTES = DE_KV * DCH * 2;     // C [64 voc][256 d]         = 32 KiB (4 atoms)
-constexpr int DE_STAGE_BYTES = DE_A_BYTES + DE_B_BYTES;
+constexpr int DE_A_BYTES = BM * DE_KV * 2;      // S-hat [128 tok][64 voc] = 16 KiB (1 atom)
+constexpr int DE_CHUNK_BYTES = DE_KV * DCH * 2;  // C [64 voc][256 d]      = 32 KiB (4 atoms)
+constexpr int DE_SMEM_BUDGET = 200 * 1024;
+// CH = 256-column D chunks per unit: CH = 1 double-buffers two 256-column accumulators in TMEM,
+// CH = 2 fills TMEM with one 512-column accumulator (S-hat stage shared by both chunks).
+template <int CH>
+struct DeCfg {
+  static constexpr int STAGE_BYTES = DE_A_BYTES + CH * DE_CHUNK_BYTES;
+  static constexpr int STAGES = DE_SMEM_BUDGET / STAGE_BYTES;
+  static constexpr int ACC = CH == 1 ? 2 : 1;  // accumulator buffers
+  static constexpr int SMEM = STAGES * STAGE_BYTES;
+};
+constexpr int DE_QUEUE = 4;                     // scheduled units in flight
 constexpr int DC_STAGES = 4;
 constexpr int DC_A_BYTES = 64 * 128 * 2;        // S-hat [64 tok][128 voc]  = 16 KiB (2 atoms)
 constexpr int DC_B_BYTES = 64 * DCH * 2;        // E [64 tok][256 d]        = 32 KiB (4 atoms)
@@ -69,31 +78,48 @@ __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_b
 // ------------------------------------------------------------------------------------------
 // B2: dE
 // ------------------------------------------------------------------------------------------
+// Unit = (token tile n, pair j of 256-column D chunks): both chunks accumulate in TMEM (512
+// columns, single-buffered) from the same S-hat stage, so S-hat is streamed once per chunk pair.
+// Units are ordered pair-major (the CTAs running at once share C[:, pair]) and handed out by an
+// atomic counter (p.sched): units differ in length (kept tiles per token tile, a lone last chunk).
+template <int CH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_de_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ CUtensorMap tmC3, const __grid_constant__ CUtensorMap tmCg,
                   const GradParams p) {
+  using Cfg = DeCfg<CH>;
+  constexpr int DE_STAGES = Cfg::STAGES;
+  constexpr int DE_STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int DE_CH = CH;
+  constexpr int ACC = Cfg::ACC;
   if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DE_STAGES * DE_STAGE_BYTES);
   uint64_t* empty = full + DE_STAGES;
-  uint64_t* acc_full = empty + DE_STAGES;
-  uint64_t* acc_free = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+  uint64_t* acc_full = empty + DE_STAGES;  // [ACC]
+  uint64_t* acc_free = acc_full + ACC;     // [ACC]
+  uint64_t* unit_full = acc_free + ACC;    // [DE_QUEUE] producer -> MMA / epilogue
+  uint64_t* unit_empty = unit_full + DE_QUEUE;
+  int* s_unit = reinterpret_cast<int*>(unit_empty + DE_QUEUE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_unit + DE_QUEUE);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmS);
-    tma_prefetch_desc(&tmC);
+    tma_prefetch_desc(&tmC3);
     for (int i = 0; i < DE_STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < ACC; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_free[i], 128);
+    }
+    for (int i = 0; i < DE_QUEUE; ++i) {
+      mbar_init(&unit_full[i], 1);
+      mbar_init(&unit_empty[i], 1 + 4);  // MMA thread + one lane per epilogue warp
     }
     fence_barrier_init();
   }
@@ -104,13 +130,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
   const int G = rows.g;
-  const int units = G * p.ndc;  // dchunk-major: concurrent CTAs share C[:, dchunk]
+  const int npair = (p.ndc + DE_CH - 1) / DE_CH;
+  const int units = G * npair;
+  const bool plain = p.atoms3d && p.perm == nullptr;
+  // unit u -> (chunk group j, token tile ln): chunk-major (concurrent CTAs share C[:, j]) or
+  // token-tile-major (concurrent CTAs share S-hat[n])
+  auto decode = [&](int u, int& j, int& ln) {
+    if (p.de_order == 0) {
+      j = u / G;
+      ln = u % G;
+    } else {
+      ln = u / npair;
+      j = u % npair;
+    }
+  };
+
+  // unit queue: the producer claims units and publishes them; -1 ends the stream
+  auto next_unit = [&](int k, uint32_t ph) {
+    mbar_wait(&unit_full[k], ph);
+    return *reinterpret_cast<volatile int*>(&s_unit[k]);
+  };
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int dc = u / G, ln = u % G;
+    for (int q = 0;; ++q) {
+      const int k = q % DE_QUEUE;
+      const uint32_t ph = (q / DE_QUEUE) & 1;
+      int u = 0;
+      if (lane == 0) {
+        mbar_wait(&unit_empty[k], ph ^ 1);
+        u = p.sched ? atomicAdd(p.sched, 1) : (int)blockIdx.x + q * (int)gridDim.x;
+        if (u >= units) u = -1;
+        s_unit[k] = u;
+        mbar_arrive(&unit_full[k]);
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
+      int j, ln;
+      decode(u, j, ln);
+      const int nch = min(DE_CH, p.ndc - DE_CH * j);
+      const uint32_t bytes = DE_A_BYTES + nch * DE_CHUNK_BYTES;
       for_each_kept(p.slot_of + (size_t)ln * p.mt, p.mt, 1, [&](int m, int slot) {
         for (int h = 0; h < BN / DE_KV; ++h) {
           RowGather rgc;
@@ -119,18 +179,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sb = sa + DE_A_BYTES;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DE_A_BYTES) + ((p.debug & 2) ? 0 : DE_B_BYTES));
+            mbar_arrive_expect_tx(&full[stage], bytes);
             // S-hat [128 tok][64 voc]: swizzle atom h of the stored tile
-            if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
-            if (p.atoms3d && p.perm == nullptr && !(p.debug & 2))  // C [64 voc][256 d] as 4 atoms
-              tma_load_3d(&tmC3, &full[stage], sb, 0, m * BN + DE_KV * h, dc * (DCH / 64));
+            tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
+            if (plain)  // C [64 voc][256 d] per chunk as 4 atoms
+              for (int c = 0; c < nch; ++c)
+                tma_load_3d(&tmC3, &full[stage], sb + c * DE_CHUNK_BYTES, 0, m * BN + DE_KV * h,
+                            (DE_CH * j + c) * (DCH / 64));
           }
           __syncwarp();
-          if (!(p.atoms3d && p.perm == nullptr)) {
+          if (!plain) {
 #pragma unroll 1
-            for (int a = 0; a < DCH / 64; ++a)
-              load_rows_warp<DE_KV>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage], sb + a * (DE_KV * 128),
-                                    dc * DCH + 64 * a, m * BN + DE_KV * h);
+            for (int c = 0; c < nch; ++c)
+#pragma unroll 1
+              for (int a = 0; a < DCH / 64; ++a)
+                load_rows_warp<DE_KV>(&tmC, &tmCg, rgc, p.perm != nullptr, &full[stage],
+                                      sb + c * DE_CHUNK_BYTES + a * (DE_KV * 128),
+                                      (DE_CH * j + c) * DCH + 64 * a, m * BN + DE_KV * h);
           }
           advance_stage(stage, phase, DE_STAGES);
         }
@@ -141,14 +206,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t IDESC = make_idesc_bf16(BM, DCH, 0, 1);  // A K-major, B MN-major
       int stage = 0;
       uint32_t phase = 0;
-      int t = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-        const int ln = u % G;
-        const int buf = t & 1;
+      for (int q = 0;; ++q) {
+        const int k = q % DE_QUEUE;
+        const int u = next_unit(k, (q / DE_QUEUE) & 1);
+        mbar_arrive(&unit_empty[k]);
+        if (u < 0) break;
+        int j, ln;
+        decode(u, j, ln);
+        const int nch = min(DE_CH, p.ndc - DE_CH * j);
         const int ksteps = (BN / DE_KV) * p.cnt_n[ln];
-        mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
+        const int buf = q % ACC;
+        mbar_wait(&acc_free[buf], ((q / ACC) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * DCH;
+        const uint32_t d_tmem = tmem_base + buf * (DE_CH * DCH);
         for (int s = 0; s < ksteps; ++s) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -156,8 +226,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t b0 = a0 + DE_A_BYTES;
 #pragma unroll
           for (int ks = 0; ks < DE_KV / 16; ++ks)  // A: K-major atom; B: 4 MN-major atoms, 16 K-rows each
-            mma_bf16_ss(d_tmem, make_sdesc(a0 + ks * 32, 0, 1024),
-                        make_sdesc(b0 + ks * 2048, DE_KV * 128, 1024), IDESC, (s | ks) != 0);
+            for (int c = 0; c < nch; ++c)
+              mma_bf16_ss(d_tmem + c * DCH, make_sdesc(a0 + ks * 32, 0, 1024),
+                          make_sdesc(b0 + c * DE_CHUNK_BYTES + ks * 2048, DE_KV * 128, 1024), IDESC,
+                          (s | ks) != 0);
           mma_commit(&empty[stage]);
           advance_stage(stage, phase, DE_STAGES);
         }
@@ -168,29 +240,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    int t = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++t) {
-      const int dc = u / G, ln = u % G;
-      const int buf = t & 1;
-      mbar_wait(&acc_full[buf], (t >> 1) & 1);
+    for (int q = 0;; ++q) {
+      const int k = q % DE_QUEUE;
+      const int u = next_unit(k, (q / DE_QUEUE) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&unit_empty[k]);
+      if (u < 0) break;
+      int j, ln;
+      decode(u, j, ln);
+      const int nch = min(DE_CH, p.ndc - DE_CH * j);
+      const int buf = q % ACC;
+      mbar_wait(&acc_full[buf], (q / ACC) & 1);
       tc_fence_after();
       const bool has = p.cnt_n[ln] > 0;
       const int grow = (p.n_base + ln) * BM + row;
       const bool valid = grow < rows.n;
       const int drow = valid ? p.row_map[grow] : 0;
 #pragma unroll 1
-      for (int c = 0; c < DCH / 32; ++c) {
-        const int col = dc * DCH + c * 32;
+      for (int c = 0; c < nch * (DCH / 32); ++c) {
+        const int col = DE_CH * j * DCH + c * 32;
         float x[32];
         if (has) {
           uint32_t r[32];
-          tmem_ld32(tmem_base + lane_off + buf * DCH + c * 32, r);
+          tmem_ld32(tmem_base + lane_off + buf * (DE_CH * DCH) + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+          for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) x[j] = 0.f;
+          for (int i = 0; i < 32; ++i) x[i] = 0.f;
         }
         if (valid && col < p.d) {
           const size_t off = (size_t)drow * p.d + col;

@@ -113,7 +113,8 @@ int num_sms() {
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
 constexpr size_t kLsePairSmem = 1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes;
-constexpr size_t kDeSmem = 1024 + (size_t)cce::DE_STAGES * cce::DE_STAGE_BYTES + kCtrlBytes;
+template <int CH>
+constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH>::SMEM + kCtrlBytes; }
 constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
 
 template <typename K>
@@ -289,6 +290,31 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.total = o;
   return w;
 }
+// dE pass (B2).  Variant knobs (CCE_DE="<chunks per unit>,<order>,<dynamic>"): default 1,0,0 =
+// two double-buffered 256-column accumulators, chunk-major units, static round-robin.
+int launch_de(cce::GradParams q, int* sched_ctr, const CUtensorMap& tmS, const CUtensorMap& tmC,
+              const CUtensorMap& tmC3, const CUtensorMap& tmCg, cudaStream_t stream) {
+  static int cfg[3] = {-1, 0, 0};
+  if (cfg[0] < 0) {
+    cfg[0] = 1;
+    if (const char* e = getenv("CCE_DE")) sscanf(e, "%d,%d,%d", &cfg[0], &cfg[1], &cfg[2]);
+  }
+  const int ch = cfg[0] == 2 ? 2 : 1;
+  q.de_order = cfg[1];
+  q.sched = cfg[2] ? sched_ctr : nullptr;
+  const int units = q.g * ((q.ndc + ch - 1) / ch);
+  const int grid = std::max(1, std::min(num_sms(), units));
+  if (ch == 2) {
+    if (int e = ensure_attr(cce::cce_de_kernel<2>, de_smem<2>())) return e;
+    cce::cce_de_kernel<2><<<grid, cce::NUM_THREADS, de_smem<2>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
+  } else {
+    if (int e = ensure_attr(cce::cce_de_kernel<1>, de_smem<1>())) return e;
+    cce::cce_de_kernel<1><<<grid, cce::NUM_THREADS, de_smem<1>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
+  }
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
 // dC pass (B3) on single CTAs or CTA pairs (the pair needs the 3-D E map with 2-atom boxes).
 int launch_dc(const cce::GradParams& q, bool pair, const CUtensorMap& tmS64, const CUtensorMap& tmE64,
               const CUtensorMap& tmE3, const CUtensorMap& tmE3h, const CUtensorMap& tmEg,
@@ -485,7 +511,6 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   if (group_tiles < 1 || capacity_tiles < 1) return fail("cce_bwd: group_tiles / capacity_tiles must be >= 1");
   const BwdWs w = bwd_layout(ws, n, d, v, group_tiles, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd: workspace too small");
-  if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
@@ -581,8 +606,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
       const char* dbg = getenv("CCE_DEBUG_GRAD");
       q.debug = dbg ? atoi(dbg) : 0;
     }
-    cce::cce_de_kernel<<<std::min(grid, g * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmCg, q);
-    CCE_CUDA(cudaGetLastError());
+    if (int e = launch_de(q, w.slot_ctr + 1, tmS128, tmC64, tmC3, tmCg, stream)) return e;  // counter zeroed per group
     if (int e = launch_dc(q, dc_pair, tmS64, tmE64, tmE3, tmE3h, tmEg, stream)) return e;
   }
   return 0;
@@ -657,7 +681,6 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   if (n <= 0) return 0;
   const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
-  if (int e = ensure_attr(cce::cce_de_kernel, kDeSmem)) return e;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
@@ -747,8 +770,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
   q.dc = static_cast<__nv_bfloat16*>(dc);
   q.accumulate = 0;
-  cce::cce_de_kernel<<<std::min(grid, nt * ndc), cce::NUM_THREADS, kDeSmem, stream>>>(tmS128, tmC64, tmC3, tmC64, q);
-  CCE_CUDA(cudaGetLastError());
+  if (int e = launch_de(q, w.list_count + 3, tmS128, tmC64, tmC3, tmC64, stream)) return e;
   return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
 }
 

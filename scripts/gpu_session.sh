@@ -21,7 +21,7 @@ for s in "$@"; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
         python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $out/launches.log 2>&1; echo "exit $?" >> $out/launches.log ;;
-    ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_(lse|de|dc)_kernel" -s 1 -c 4 -o $out/prof \
+    ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_(lse|de|dc)_kernel" -c 4 -o $out/prof \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $out/ncu.log 2>&1; echo "exit $?" >> $out/ncu.log ;;
     trace) timeout 600 python scripts/trace_step.py > $out/trace.log 2>&1; echo "exit $?" >> $out/trace.log ;;
     ncugrad) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cce_d[ec]_kernel" -c 2 -o $out/profgrad \
