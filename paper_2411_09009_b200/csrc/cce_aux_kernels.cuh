@@ -305,32 +305,35 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
   if (threadIdx.x == 0 && s_cnt[0]) atomicAdd(&counters[1], (unsigned long long)s_cnt[0]);
 }
 
-// One block of 1024 threads: the kept flags in vocab-tile-major order become the kept-tile list
-// (slot = list position, so concurrently running CTAs of the KEPT pass share C tiles), slot_of
-// (pre-filled with -1), per-tile counts, counters[0] += kept, and the capacity flags: *ok = 1 and
-// *overflow = 0 when every kept tile got a slot, else *ok = 0 and *overflow = 1.  `keep` is padded
-// with zeros to a multiple of 16 bytes.
+// One block of 1024 threads: the kept flags of token tiles [n_lo, n_lo + g), in vocab-tile-major
+// order, become the kept-tile list (slot = list position, so concurrently running CTAs of the
+// KEPT pass share C tiles) and slot_of / cnt_n / cnt_m of that group (local token-tile index
+// n - n_lo; slot_of pre-filled with -1, counts zeroed).  primary: also counters[0] += kept and
+// the capacity flags (*ok = 1, *overflow = 0 when every kept tile got a slot, else *ok = 0 and
+// *overflow = 1).  Runs only if run_if is null or *run_if != 0.
 __global__ void __launch_bounds__(1024) build_list_kernel(
-    const uint8_t* __restrict__ keep, int nt, int mt, int capacity, int2* __restrict__ list,
-    int32_t* __restrict__ slot_of, int* __restrict__ cnt_n, int* __restrict__ cnt_m,
-    int* __restrict__ list_count, int* __restrict__ ok, int* __restrict__ overflow,
+    const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g, int capacity, const int* run_if,
+    int primary, int2* __restrict__ list, int32_t* __restrict__ slot_of, int* __restrict__ cnt_n,
+    int* __restrict__ cnt_m, int* __restrict__ list_count, int* __restrict__ ok, int* __restrict__ overflow,
     unsigned long long* __restrict__ counters) {
-  constexpr int T = 1024;
+  if (run_if != nullptr && *run_if == 0) return;
+  constexpr int T = 1024, U = 8;
   __shared__ int s_warp[T / 32];
-  const int total = nt * mt;
-  const int total16 = (total + 15) / 16;
-  const int per16 = (total16 + T - 1) / T;  // uint4 words per thread
-  const int w0 = threadIdx.x * per16, w1 = min(total16, w0 + per16);
-  const uint4* kw = reinterpret_cast<const uint4*>(keep);
-  auto bytes_of = [](uint4 x, int j) {
-    const uint32_t w = j < 4 ? x.x : j < 8 ? x.y : j < 12 ? x.z : x.w;
-    return (w >> (8 * (j & 3))) & 0xFFu;
+  const long long total = (long long)g * mt;
+  const long long per = ((total + T - 1) / T + U - 1) / U * U;
+  const long long i0 = (long long)threadIdx.x * per;
+  const long long i1 = min(total, i0 + per);
+  auto flag = [&](long long i) -> int {
+    const int m = (int)(i / g), n = n_lo + (int)(i - (long long)m * g);
+    return keep[(size_t)m * nt + n];
   };
   int c = 0;
-  for (int w = w0; w < w1; ++w) {
-    const uint4 x = kw[w];
-    c += __popc(x.x & 0x01010101u) + __popc(x.y & 0x01010101u) + __popc(x.z & 0x01010101u) +
-         __popc(x.w & 0x01010101u);
+  for (long long i = i0; i < i1; i += U) {
+    int f[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) f[k] = (i + k < i1) ? flag(i + k) : 0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) c += f[k];
   }
   // block exclusive scan of c
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -354,29 +357,26 @@ __global__ void __launch_bounds__(1024) build_list_kernel(
   __syncthreads();
   int slot = (wid ? s_warp[wid - 1] : 0) + incl - c;
   const int kept_total = s_warp[T / 32 - 1];
-  for (int w = w0; w < w1; ++w) {
-    const uint4 x = kw[w];
-    if ((x.x | x.y | x.z | x.w) == 0u) continue;
-#pragma unroll 1
-    for (int j = 0; j < 16; ++j) {
-      if (!bytes_of(x, j)) continue;
-      const int i = w * 16 + j;
-      const int m = i / nt, n = i - m * nt;
+  if (c)
+    for (long long i = i0; i < i1; ++i) {
+      if (!flag(i)) continue;
+      const int m = (int)(i / g), ln = (int)(i - (long long)m * g);
       if (slot < capacity) {
-        list[slot] = make_int2(n, m);
-        slot_of[(size_t)n * mt + m] = slot;
-        atomicAdd(&cnt_n[n], 1);
+        list[slot] = make_int2(n_lo + ln, m);
+        slot_of[(size_t)ln * mt + m] = slot;
+        atomicAdd(&cnt_n[ln], 1);
         atomicAdd(&cnt_m[m], 1);
       }
       ++slot;
     }
-  }
   if (threadIdx.x == 0) {
     *list_count = kept_total;
-    const bool fits = kept_total <= capacity;
-    *ok = fits ? 1 : 0;
-    *overflow = fits ? 0 : 1;
-    atomicAdd(&counters[0], (unsigned long long)kept_total);
+    if (primary) {
+      const bool fits = kept_total <= capacity;
+      *ok = fits ? 1 : 0;
+      *overflow = fits ? 0 : 1;
+      atomicAdd(&counters[0], (unsigned long long)kept_total);
+    }
   }
 }
 
@@ -384,8 +384,9 @@ __global__ void __launch_bounds__(1024) build_list_kernel(
 // consecutive slots [off_m, off_m + cnt_m) (build_list_kernel); pair j of m takes slots
 // off_m + 2j and, if it exists, off_m + 2j + 1.  pairs[k] = (first slot, tiles in the pair).
 __global__ void __launch_bounds__(1024) build_pairs_kernel(const int* __restrict__ cnt_m, int mt,
-                                                           int2* __restrict__ pairs,
+                                                           const int* run_if, int2* __restrict__ pairs,
                                                            int* __restrict__ pair_count) {
+  if (run_if != nullptr && *run_if == 0) return;
   constexpr int T = 1024;
   __shared__ int s_a[T / 32], s_b[T / 32];
   const int per = (mt + T - 1) / T;

@@ -677,30 +677,21 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
   if (!overflow) return fail("cce_bwd_kept: overflow flag required");
-  if (capacity_tiles < 1) return fail("cce_bwd_kept: capacity_tiles must be >= 1");
   if (n <= 0) return 0;
-  const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
-  if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  if (capacity_tiles < std::min<int64_t>(mt, (int64_t)nt * mt))
+    return fail("cce_bwd_kept: capacity_tiles must hold one token tile's vocab tiles (ceil(v/256))");
+  const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
+  if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
-  const int grid = num_sms();
   CCE_CUDA(cudaMemsetAsync(w.keep, 0, w.keep_bytes, stream));
-  CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, w.slot_bytes, stream));
-  CCE_CUDA(cudaMemsetAsync(w.list_count, 0, w.cnt_bytes, stream));
+  CCE_CUDA(cudaMemsetAsync(w.list_count, 0, 256, stream));
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
       tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, w.keep, counters);
   CCE_CUDA(cudaGetLastError());
-  cce::build_list_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, (int)capacity_tiles, w.list, w.slot_of,
-                                                 w.cnt_n, w.cnt_m, w.list_count, w.ok, overflow, counters);
-  CCE_CUDA(cudaGetLastError());
-  const bool pair = use_pairs();
-  if (pair) {
-    cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, w.pairs, w.pair_count);
-    CCE_CUDA(cudaGetLastError());
-  }
 
   CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h;
   const int64_t shat_rows = capacity_tiles * cce::BM;
@@ -719,59 +710,84 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     tmE3h = tmE64;
   }
   if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
+  const bool pair = use_pairs();
 
-  // S-hat of the kept tiles only (cce_lse_kernel<KEPT>, grid-stride over the list)
-  cce::Params p{};
-  p.n_total = (int)n;
-  p.n_valid = n_valid;
-  p.run_if = w.ok;
-  p.d = (int)d;
-  p.v = (int)v;
-  p.nt = nt;
-  p.n_base = 0;
-  p.mt = mt;
-  p.splits = std::max(1, (2 * grid + nt - 1) / nt);  // grid sizing only
-  p.band = choose_band(d);
-  p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
-  p.softcap = softcap;
-  p.lse = lse;
-  p.upstream = upstream;
-  p.pos = pos;
-  p.row_map = row_map;
-  p.eps = eps;
-  p.shat = w.shat;
-  p.capacity = (int)capacity_tiles;
-  p.counters = counters;
-  p.list = w.list;
-  p.list_count = w.list_count;
-  p.pairs = w.pairs;
-  p.pair_count = w.pair_count;
-  if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
+  // One pass over token tiles [g0, g0 + g): kept-tile list, S-hat of the kept tiles (KEPT), dE of
+  // those token tiles (complete), dC (written by the first pass, accumulated by later ones).
+  auto run_pass = [&](int g0, int g, bool primary, const int* run_if) -> int {
+    CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)g * mt * 4, stream));
+    CCE_CUDA(cudaMemsetAsync(w.cnt_n, 0, (size_t)(nt + mt) * 4, stream));
+    CCE_CUDA(cudaMemsetAsync(w.list_count + 3, 0, sizeof(int), stream));  // dE unit counter
+    cce::build_list_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if,
+                                                   primary ? 1 : 0, w.list, w.slot_of, w.cnt_n, w.cnt_m,
+                                                   w.list_count, w.ok, overflow, counters);
+    CCE_CUDA(cudaGetLastError());
+    const int* gate = primary ? w.ok : run_if;  // primary: only if every kept tile got a slot
+    if (pair) {
+      cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, gate, w.pairs, w.pair_count);
+      CCE_CUDA(cudaGetLastError());
+    }
+    cce::Params p{};
+    p.n_total = (int)n;
+    p.n_valid = n_valid;
+    p.run_if = gate;
+    p.d = (int)d;
+    p.v = (int)v;
+    p.nt = g;
+    p.n_base = g0;
+    p.mt = mt;
+    p.splits = std::max(1, (2 * num_sms() + g - 1) / g);  // grid sizing only
+    p.band = choose_band(d);
+    p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
+    p.softcap = softcap;
+    p.lse = lse;
+    p.upstream = upstream;
+    p.pos = pos;
+    p.row_map = row_map;
+    p.eps = eps;
+    p.shat = w.shat;
+    p.capacity = (int)capacity_tiles;
+    p.counters = counters;
+    p.list = w.list;
+    p.list_count = w.list_count;
+    p.pairs = w.pairs;
+    p.pair_count = w.pair_count;
+    if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
 
-  cce::GradParams q{};
-  q.n_total = (int)n;
-  q.n_valid = n_valid;
-  q.run_if = w.ok;
-  q.d = (int)d;
-  q.v = (int)v;
-  q.mt = mt;
-  q.ndc = ndc;
-  q.n_base = 0;
-  q.g = nt;
-  q.slot_of = w.slot_of;
-  q.cnt_n = w.cnt_n;
-  q.cnt_m = w.cnt_m;
-  q.perm = nullptr;
-  q.perm_store = perm_padded;
-  q.row_map = row_map;
-  q.e_gather = 0;
-  q.atoms3d = atoms3d ? 1 : 0;
-  q.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
-  q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
-  q.dc = static_cast<__nv_bfloat16*>(dc);
-  q.accumulate = 0;
-  if (int e = launch_de(q, w.list_count + 3, tmS128, tmC64, tmC3, tmC64, stream)) return e;
-  return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
+    cce::GradParams q{};
+    q.n_total = (int)n;
+    q.n_valid = n_valid;
+    q.run_if = gate;
+    q.d = (int)d;
+    q.v = (int)v;
+    q.mt = mt;
+    q.ndc = ndc;
+    q.n_base = g0;
+    q.g = g;
+    q.slot_of = w.slot_of;  // rows of this pass, local token-tile index
+    q.cnt_n = w.cnt_n;
+    q.cnt_m = w.cnt_m;
+    q.perm = nullptr;
+    q.perm_store = perm_padded;
+    q.row_map = row_map;
+    q.e_gather = 0;
+    q.atoms3d = atoms3d ? 1 : 0;
+    q.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
+    q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
+    q.dc = static_cast<__nv_bfloat16*>(dc);
+    q.accumulate = g0 > 0;
+    if (int e = launch_de(q, w.list_count + 3, tmS128, tmC64, tmC3, tmC64, stream)) return e;
+    return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
+  };
+  // The kept count is only known on the device: the whole-batch pass runs iff it fits; otherwise
+  // (*overflow) token-tile groups sized for the worst case (every tile kept) run instead.
+  if (int e = run_pass(0, nt, true, nullptr)) return e;
+  if ((int64_t)nt * mt > capacity_tiles) {
+    const int g = (int)std::max<int64_t>(1, capacity_tiles / mt);
+    for (int g0 = 0; g0 < nt; g0 += g)
+      if (int e = run_pass(g0, std::min(g, nt - g0), false, overflow)) return e;
+  }
+  return 0;
 }
 
 int cce_indexed_dot(const void* E, const void* C, const int64_t* targets, int64_t n, int64_t d,

@@ -239,11 +239,12 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     # S-hat slots: every token tile in one group with compact slots up to the budget; if more
     # tiles are kept than that, a fallback pass over budget-sized groups (worst case fits) runs,
     # gated on the device overflow flag -- no host read either way.
-    budget = shat_budget_tiles()
-    plans = [(nt, min(budget, nt * mt), None)]
+    key = ("filter_pass", n, d, v, int(vocab_start), filt_eps, float(softcap or 0.0))
+    cap0 = shat_capacity(key, nt, mt)
+    plans = [(nt, cap0, None)]
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
-    if plans[0][1] < nt * mt:
-        g = max(1, budget // mt)
+    if cap0 < nt * mt:
+        g = max(1, cap0 // mt)
         plans.append((g, g * mt, overflow))
     all_counters = []
     ws_bytes = max(lib.cce_bwd_workspace_bytes(n, d, v, g, cap) for g, cap, _ in plans)
@@ -260,6 +261,7 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
         LAUNCHES["count"] += 2 + 3 * (-(-nt // g))
         all_counters.append(counters)
     counters = all_counters[0] if len(plans) == 1 else torch.where(overflow.bool(), all_counters[1], all_counters[0])
+    _remember_kept(key, counters)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
     return de, dc, counters, perm
@@ -377,8 +379,10 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
         raise ValueError("backward_tiles needs filtering (eps > 0)")
     nt = -(-n // BLOCK_TOKENS)
     mt = -(-v // BLOCK_VOCAB)
-    budget = shat_budget_tiles()
-    cap = min(budget, nt * mt)
+    # S-hat slots: the whole batch in one pass if the kept tiles fit; otherwise the library falls
+    # back (device flag, no host read) to token-tile groups sized for the worst case
+    key = (n, d, v, state.vocab_start, float(eps), state.softcap)
+    cap = shat_capacity(key, nt, mt)
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
     ws_bytes = lib.cce_bwd_kept_workspace_bytes(n, d, v, cap)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -387,31 +391,68 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
                                 _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
                                 n, d, v, state.softcap, float(eps), cap, _p(ws), ws_bytes, _p(de),
                                 int(fp32_de), _p(dc), _p(counters), _p(overflow), stream), "cce_bwd_kept")
-    LAUNCHES["count"] += 6
-    del ws
-    # overflow fallback: the grouped filter pass over budget-sized token groups (worst case fits)
-    if cap < nt * mt:
-        g = max(1, budget // mt)
-        counters2 = torch.zeros(3, dtype=torch.int64, device=dev)
-        ws_bytes = lib.cce_bwd_workspace_bytes(n, d, v, g, g * mt)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        _lib.check(lib.cce_bwd(_p(e), _p(c_t), _p(state.perm_padded), 1 if state.perm is not None else 0,
-                               _p(state.row_map), _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream),
-                               n, d, v, state.softcap, float(eps), g, g * mt, _p(overflow), 0, _p(ws),
-                               ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters2), _p(None), stream),
-                   "cce_bwd")
-        LAUNCHES["count"] += 2 + 3 * (-(-nt // g))
-        counters = torch.where(overflow.bool(), counters2, counters)
+    passes = 1 + (0 if cap >= nt * mt else -(-nt // max(1, cap // mt)))
+    LAUNCHES["count"] += 2 + passes * 6
+    _remember_kept(key, counters)
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
     return de, dc, counters
 
 
+SHAT_TILE_BYTES = BLOCK_TOKENS * BLOCK_VOCAB * 2
+FIRST_CALL_MB = 1024          # S-hat allocation before any kept count has been observed
+KEPT_MARGIN = 1.15            # headroom over the last observed kept count
+_KEPT_HINT: dict = {}         # shape key -> [pinned int64[3] counters copy, CUDA event, last known kept]
+
+
 def shat_budget_tiles() -> int:
-    """S-hat slots (64 KiB each) the backward may hold: CCE_SHAT_BUDGET_MB (default 1024)."""
-    budget = int(os.environ.get("CCE_SHAT_BUDGET_MB", "1024")) << 20
-    return max(1, budget // (BLOCK_TOKENS * BLOCK_VOCAB * 2))
+    """Ceiling on S-hat slots (64 KiB each): CCE_SHAT_BUDGET_MB, else 10% of device memory."""
+    env = os.environ.get("CCE_SHAT_BUDGET_MB")
+    if env is not None:
+        budget = int(env) << 20
+    else:
+        budget = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory // 10
+    return max(1, budget // SHAT_TILE_BYTES)
+
+
+def shat_capacity(key, nt: int, mt: int) -> int:
+    """S-hat slots to allocate for this call.  A fixed CCE_SHAT_BUDGET_MB is used as is; otherwise
+    the kept-tile count of the previous call with the same shape (read from a pinned copy only
+    once its event has completed -- never a host synchronisation) plus a margin, or FIRST_CALL_MB
+    on the first call.  Too small is safe: the grouped fallback runs on the device."""
+    ceiling = shat_budget_tiles()
+    if os.environ.get("CCE_SHAT_BUDGET_MB") is not None:
+        cap = ceiling
+    else:
+        cap = min(ceiling, (FIRST_CALL_MB << 20) // SHAT_TILE_BYTES)
+        hint = _KEPT_HINT.get(key)
+        if hint is not None:
+            _harvest(hint)
+            if hint[2] is not None:
+                cap = min(ceiling, int(hint[2] * KEPT_MARGIN) + mt)
+    return min(max(cap, mt), nt * mt)
+
+
+def _harvest(hint) -> None:
+    if hint[1] is not None and hint[1].query():
+        hint[2] = int(hint[0][0])
+        hint[1] = None
+
+
+def _remember_kept(key, counters: torch.Tensor) -> None:
+    """Queue an asynchronous copy of this call's kept-tile count (read by a later call once it
+    has landed; the CPU usually runs ahead of the GPU, so the value may be a few calls old)."""
+    hint = _KEPT_HINT.get(key)
+    if hint is None:
+        hint = [torch.zeros(3, dtype=torch.int64).pin_memory(), None, None]
+        _KEPT_HINT[key] = hint
+    _harvest(hint)
+    if hint[1] is not None:
+        return  # previous copy still in flight
+    hint[0].copy_(counters, non_blocking=True)
+    hint[1] = torch.cuda.Event()
+    hint[1].record()
 
 
 def f32_to_bf16(x: torch.Tensor) -> torch.Tensor:
