@@ -250,12 +250,19 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
     options = options or CceOptions()
     E, C, X = _pair(e, c, x)
     n = E.shape[0]
-    lse_l, corr = ops.forward_local(E, C, X, IGNORE_INDEX)
-    lse, loss = ops.merge_shards(lse_l[None], corr[None], X, IGNORE_INDEX)
-    mean = perm = None
     valid = X != IGNORE_INDEX
-    if options.vocab_sorting:
-        perm, mean = ops.vocab_order(E, C, X, IGNORE_INDEX, int(valid.sum()))
+    mean = perm = state = None
+    if options.filtering:
+        # forward over the backward's tiles (compacted rows, vocab order fixed by the mean logits
+        # of the valid rows), recording per-row tile maxima: the backward then recomputes only
+        # the tiles it keeps
+        lse_l, corr, state = ops.forward_tiles(E, C, X, IGNORE_INDEX, vocab_sorting=options.vocab_sorting)
+        mean = state.mean_logits
+    else:
+        lse_l, corr = ops.forward_local(E, C, X, IGNORE_INDEX)
+        if options.vocab_sorting:
+            perm, mean = ops.vocab_order(E, C, X, IGNORE_INDEX, int(valid.sum()))
+    lse, loss = ops.merge_shards(lse_l[None], corr[None], X, IGNORE_INDEX)
     out = LossOutput(per_token_loss=loss, lse=lse, mean_logits=mean)
 
     def backward(upstream=None, stats: BackwardStats | None = None) -> Gradients:
@@ -267,10 +274,13 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
                 raise ValueError(f"upstream must have shape ({n},), got {tuple(up.shape)}")
             if bool((up[~valid] != 0).any()):
                 raise ValueError("upstream must be 0 at ignored positions")
-        de, dc, counters, _ = ops.backward(
-            E, C, X, lse, up.contiguous(), ignore_index=IGNORE_INDEX,
-            eps=options.epsilon if options.filtering else None,
-            vocab_sorting=options.vocab_sorting, perm=perm, fp32_de=True)
+        if state is not None:
+            de, dc, counters = ops.backward_tiles(state, X, lse, up.contiguous(), ignore_index=IGNORE_INDEX,
+                                                  eps=options.epsilon, fp32_de=True)
+        else:
+            de, dc, counters, _ = ops.backward(
+                E, C, X, lse, up.contiguous(), ignore_index=IGNORE_INDEX, eps=None,
+                vocab_sorting=options.vocab_sorting, perm=perm, fp32_de=True)
         if stats is not None:
             s = ops.stats_from_counters(counters, int(valid.sum()), C.shape[0])
             stats.total_tiles, stats.skipped_epsilon, stats.skipped_zero_upstream = (

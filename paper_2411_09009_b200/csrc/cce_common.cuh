@@ -94,6 +94,7 @@ struct GradParams {
   int accumulate;          // dC: add to the existing values (groups after the first)
   int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
   int de_order;            // dE: 0 chunk-major units, 1 token-tile-major
+  int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)
   int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
 };
 

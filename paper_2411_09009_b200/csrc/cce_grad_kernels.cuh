@@ -171,7 +171,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode(u, j, ln);
       const int nch = min(DE_CH, p.ndc - DE_CH * j);
       const uint32_t bytes = DE_A_BYTES + nch * DE_CHUNK_BYTES;
-      for_each_kept(p.slot_of + (size_t)ln * p.mt, p.mt, 1, [&](int m, int slot) {
+      const int32_t* srow = p.slot_of + (size_t)ln * p.mt;
+      // L2 prefetch of the C slices of kept tiles [m + prefetch, ...): lane l covers vocab tile
+      // pf_next + l, issued one batch of 32 ahead of use
+      int pf_next = 0;
+      auto prefetch_upto = [&](int m_hi) {
+        if (!p.prefetch || !plain) return;
+        m_hi = min(m_hi, p.mt);
+        while (pf_next < m_hi) {  // warp-uniform
+          const int mm = pf_next + lane;
+          if (mm < m_hi && srow[mm] >= 0)
+            for (int c = 0; c < nch; ++c)
+#pragma unroll
+              for (int h = 0; h < BN / DE_KV; ++h)
+                tma_prefetch_3d(&tmC3, 0, mm * BN + DE_KV * h, (DE_CH * j + c) * (DCH / 64));
+          pf_next = min(pf_next + 32, m_hi);
+        }
+      };
+      prefetch_upto(p.prefetch);
+      for_each_kept(srow, p.mt, 1, [&](int m, int slot) {
+        prefetch_upto(m + p.prefetch);
         for (int h = 0; h < BN / DE_KV; ++h) {
           RowGather rgc;
           rgc.load(p.perm, m * BN + DE_KV * h, DE_KV);

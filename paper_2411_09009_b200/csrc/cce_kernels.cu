@@ -294,14 +294,15 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
 // two double-buffered 256-column accumulators, chunk-major units, static round-robin.
 int launch_de(cce::GradParams q, int* sched_ctr, const CUtensorMap& tmS, const CUtensorMap& tmC,
               const CUtensorMap& tmC3, const CUtensorMap& tmCg, cudaStream_t stream) {
-  static int cfg[3] = {-1, 0, 0};
+  static int cfg[4] = {-1, 0, 0, 0};
   if (cfg[0] < 0) {
     cfg[0] = 1;
-    if (const char* e = getenv("CCE_DE")) sscanf(e, "%d,%d,%d", &cfg[0], &cfg[1], &cfg[2]);
+    if (const char* e = getenv("CCE_DE")) sscanf(e, "%d,%d,%d,%d", &cfg[0], &cfg[1], &cfg[2], &cfg[3]);
   }
   const int ch = cfg[0] == 2 ? 2 : 1;
   q.de_order = cfg[1];
   q.sched = cfg[2] ? sched_ctr : nullptr;
+  q.prefetch = cfg[3];
   const int units = q.g * ((q.ndc + ch - 1) / ch);
   const int grid = std::max(1, std::min(num_sms(), units));
   if (ch == 2) {

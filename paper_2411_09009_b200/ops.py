@@ -289,6 +289,7 @@ class TileState:
     tile_max: torch.Tensor
     vocab_start: int
     softcap: float
+    mean_logits: torch.Tensor | None = None
 
     def nbytes(self) -> int:
         own = [self.e_c, self.row_map, self.n_valid, self.pos, self.tile_max]
@@ -325,8 +326,9 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     stream = _stream(dev)
     row_map, n_valid = compact_rows(targets, ignore_index)
     e_c = gather_rows(e, row_map, n)
+    mean_logits = None
     if vocab_sorting and perm is None:
-        perm, _ = vocab_order(e, c, targets, ignore_index, n_valid)
+        perm, mean_logits = vocab_order(e, c, targets, ignore_index, n_valid)
     vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
     perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev) if perm is not None else None
     inv_perm = torch.empty(v, dtype=torch.int32, device=dev) if perm is not None else None
@@ -339,7 +341,7 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     lse_local = torch.empty(n, dtype=torch.float32, device=dev)
     correct = torch.empty(n, dtype=torch.float32, device=dev)
     state = TileState(e, e_c, c_t, row_map, n_valid, perm, perm_padded, pos, tile_max,
-                      int(vocab_start), float(softcap or 0.0))
+                      int(vocab_start), float(softcap or 0.0), mean_logits)
     if n == 0:
         return lse_local, correct, state
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)

@@ -341,3 +341,42 @@ def test_linear_cross_entropy_tile_path_matches_low_memory(cuda_device, cap, ign
     assert out[False][3][1] > 0 and out[False][3][0] > 0  # some tiles skipped, some kept
     assert O.rel_err(out[False][1], out[True][1]) < 1e-2
     assert O.rel_err(out[False][2], out[True][2]) < 1e-2
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_fake_vocab_parallel_tile_path(cuda_device, shards):
+    """Vocab-parallel training path without NCCL: every shard sorts its own rows and runs the
+    tile-recording forward; the 2N-float partials merge by log-add-exp; every shard decides its
+    tiles against the GLOBAL lse; fp32 dE partials sum to the full gradient and the filter
+    decisions equal those of the same per-shard order on the low-memory path."""
+    from paper_2411_09009_b200 import ops
+    from paper_2411_09009_b200.vocab_parallel import shard_range
+
+    rng = np.random.default_rng(40 + shards)
+    n, d, v = 700, 128, 6001
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 1.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::7] = -100
+    ed, cd, td = _dev(e, torch.bfloat16), _dev(c, torch.bfloat16), _dev(x)
+    parts = [shard_range(v, r, shards) for r in range(shards)]
+    outs = [ops.forward_tiles(ed, cd[a:b].contiguous(), td, -100, a) for a, b in parts]
+    lse, loss = ops.merge_shards(torch.stack([o[0] for o in outs]), torch.stack([o[1] for o in outs]), td, -100)
+    xo = np.where(x == -100, -1, x)
+    nl, nlse, _ = O.naive_forward(e, c, xo)
+    assert _loss_err(loss.cpu().numpy(), nl) < LOSS_TOL
+    up = _dev(O.default_upstream(xo, "mean-over-valid").astype(np.float32))
+    de = torch.zeros(n, d, device="cuda")
+    dcs, kept = [], 0
+    for (a, b), (_, _, st) in zip(parts, outs):
+        de_p, dc_p, cnt = ops.backward_tiles(st, td, lse, up, ignore_index=-100, fp32_de=True)
+        _, _, cnt_low, _ = ops.backward(ed, cd[a:b].contiguous(), td, lse, up, ignore_index=-100,
+                                        vocab_start=a, perm=st.perm, fp32_de=True)
+        assert cnt.tolist() == cnt_low.tolist()
+        kept += int(cnt[0])
+        de += de_p
+        dcs.append(dc_p.float())
+    assert kept > 0
+    fde, fdc = O.naive_backward(e, c, xo, O.default_upstream(xo, "mean-over-valid"))
+    assert O.rel_err(de.cpu().numpy(), fde) < 2e-2
+    assert O.rel_err(torch.cat(dcs).cpu().numpy(), fdc) < 2e-2
