@@ -109,9 +109,14 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * cce_bwd_kept: the backward from tile_max.  Keeps tile (n, m) iff its upstream is not all zero
  * and it holds a label or some S >= eps (the same strict test as cce_bwd, eps > 0 required);
  * recomputes S-hat for the kept tiles only, then the dE / dC passes of cce_bwd.  dC rows land
- * through perm_padded (NULL = tile order is C's order).  If more than capacity_tiles tiles are
- * kept, *overflow = 1 and nothing past the decision runs: the caller then runs cce_bwd with
- * run_if = overflow (device-gated, no host synchronisation).  counters as cce_bwd. */
+ * through perm_padded (NULL = tile order is C's order).  capacity_tiles >= ceil(v/256) S-hat
+ * slots: if the whole batch keeps more tiles than that, *overflow = 1, the whole-batch pass is
+ * skipped on the device and token-tile groups sized for the worst case run instead (each kernel
+ * gated on *overflow; dC accumulated in bf16 after the first group) -- no host synchronisation.
+ * counters as cce_bwd.
+ * de_done_event (a cudaEvent_t, may be NULL) is recorded on the stream once every dE write of the
+ * call has been enqueued, before the dC pass: a vocab-parallel caller all-reduces dE on another
+ * stream while dC runs. */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
@@ -121,7 +126,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
-                 unsigned long long* counters, int* overflow, void* stream);
+                 unsigned long long* counters, int* overflow, void* de_done_event, void* stream);
 
 /* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
  * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */

@@ -20,18 +20,22 @@
 
 namespace cce {
 
-constexpr int DE_KV = 64;                       // vocab rows (MMA K) per dE stage
-constexpr int DE_A_BYTES = BM * DE_KV * 2;      // S-hat [128 tok][64 voc] = 16 KiB (1 atom)
-constexpr int DE_CHUNK_BYTES = DE_KV * DCH * 2;  // C [64 voc][256 d]      = 32 KiB (4 atoms)
+constexpr int DE_KV = 64;                       // default vocab rows (MMA K) per dE stage
 constexpr int DE_SMEM_BUDGET = 200 * 1024;
 // CH = 256-column D chunks per unit: CH = 1 double-buffers two 256-column accumulators in TMEM,
-// CH = 2 fills TMEM with one 512-column accumulator (S-hat stage shared by both chunks).
-template <int CH>
+// CH = 2 fills TMEM with one 512-column accumulator (each S-hat stage feeds both chunks).
+// KV = vocab rows per stage: 64 (S-hat atom of 128 B rows, 128 B swizzle) or 32 (64 B rows,
+// 64 B swizzle): half the bytes per stage, twice the stages in flight.
+template <int CH, int KV>
 struct DeCfg {
-  static constexpr int STAGE_BYTES = DE_A_BYTES + CH * DE_CHUNK_BYTES;
+  static constexpr int A_BYTES = BM * KV * 2;      // S-hat [128 tok][KV voc]
+  static constexpr int CHUNK_BYTES = KV * DCH * 2;  // C [KV voc][256 d] as 4 atoms
+  static constexpr int STAGE_BYTES = A_BYTES + CH * CHUNK_BYTES;
   static constexpr int STAGES = DE_SMEM_BUDGET / STAGE_BYTES;
   static constexpr int ACC = CH == 1 ? 2 : 1;  // accumulator buffers
   static constexpr int SMEM = STAGES * STAGE_BYTES;
+  static constexpr uint64_t A_LAYOUT = KV == 32 ? kSwizzle64B : kSwizzle128B;
+  static constexpr uint32_t A_SBO = 8 * KV * 2;
 };
 constexpr int DE_QUEUE = 4;                     // scheduled units in flight
 constexpr int DC_STAGES = 4;
@@ -82,15 +86,18 @@ __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_b
 // columns, single-buffered) from the same S-hat stage, so S-hat is streamed once per chunk pair.
 // Units are ordered pair-major (the CTAs running at once share C[:, pair]) and handed out by an
 // atomic counter (p.sched): units differ in length (kept tiles per token tile, a lone last chunk).
-template <int CH>
+template <int CH, int KV>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_de_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmC,
                   const __grid_constant__ CUtensorMap tmC3, const __grid_constant__ CUtensorMap tmCg,
                   const GradParams p) {
-  using Cfg = DeCfg<CH>;
+  using Cfg = DeCfg<CH, KV>;
   constexpr int DE_STAGES = Cfg::STAGES;
   constexpr int DE_STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int DE_A_BYTES = Cfg::A_BYTES;
+  constexpr int DE_CHUNK_BYTES = Cfg::CHUNK_BYTES;
   constexpr int DE_CH = CH;
+  constexpr int DE_KV = KV;
   constexpr int ACC = Cfg::ACC;
   if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], bytes);
-            // S-hat [128 tok][64 voc]: swizzle atom h of the stored tile
+            // S-hat [128 tok][KV voc]: swizzle atom h of the stored tile
             tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
             if (plain)  // C [64 voc][256 d] per chunk as 4 atoms
               for (int c = 0; c < nch; ++c)
@@ -246,7 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < DE_KV / 16; ++ks)  // A: K-major atom; B: 4 MN-major atoms, 16 K-rows each
             for (int c = 0; c < nch; ++c)
-              mma_bf16_ss(d_tmem + c * DCH, make_sdesc(a0 + ks * 32, 0, 1024),
+              mma_bf16_ss(d_tmem + c * DCH, make_sdesc(a0 + ks * 32, 0, Cfg::A_SBO, Cfg::A_LAYOUT),
                           make_sdesc(b0 + c * DE_CHUNK_BYTES + ks * 2048, DE_KV * 128, 1024), IDESC,
                           (s | ks) != 0);
           mma_commit(&empty[stage]);

@@ -90,6 +90,25 @@ bool make_tmap3d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
   return r == CUDA_SUCCESS;
 }
 
+// 3-D view {inner, rows, cols/inner} with box {inner, box_rows, box_atoms} and the swizzle that
+// matches inner * 2 bytes (128 B or 64 B rows).
+bool make_tmap3d_inner(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int inner,
+                       int box_rows, int box_atoms) {
+  auto enc = get_encode_fn();
+  if (!enc || cols % inner != 0) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(cols / inner)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols * 2), static_cast<cuuint64_t>(inner * 2)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(inner), static_cast<cuuint32_t>(box_rows),
+                       static_cast<cuuint32_t>(box_atoms)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   inner == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int gather_box_rows() {
   static int rows = [] {
     const char* e = getenv("CCE_GATHER4_BOX_ROWS");
@@ -113,8 +132,8 @@ int num_sms() {
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
 constexpr size_t kLsePairSmem = 1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes;
-template <int CH>
-constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH>::SMEM + kCtrlBytes; }
+template <int CH, int KV>
+constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH, KV>::SMEM + kCtrlBytes; }
 constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
 
 template <typename K>
@@ -290,30 +309,43 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.total = o;
   return w;
 }
-// dE pass (B2).  Variant knobs (CCE_DE="<chunks per unit>,<order>,<dynamic>"): default 1,0,0 =
-// two double-buffered 256-column accumulators, chunk-major units, static round-robin.
-int launch_de(cce::GradParams q, int* sched_ctr, const CUtensorMap& tmS, const CUtensorMap& tmC,
-              const CUtensorMap& tmC3, const CUtensorMap& tmCg, cudaStream_t stream) {
-  static int cfg[4] = {-1, 0, 0, 0};
+// dE pass (B2).  Variant knobs (CCE_DE="<chunks per unit>,<order>,<dynamic>,<prefetch>,<kv>"):
+// default 1,0,0,0,64 = two double-buffered 256-column accumulators, chunk-major units, static
+// round-robin, no L2 prefetch, 64 vocab rows per stage.  Builds its own S-hat / C tensor maps.
+template <int CH, int KV>
+int launch_de_t(const cce::GradParams& q, int units, const void* shat, int64_t shat_rows, const void* C,
+                int64_t v, int64_t d, const CUtensorMap& tmCg, cudaStream_t stream) {
+  CUtensorMap tmS, tmC3, tmC;
+  const bool ok = make_tmap3d_inner(&tmS, shat, shat_rows, cce::BN, KV, cce::BM, 1) &&
+                  make_tmap(&tmC, C, v, d, KV) &&
+                  (d % 64 == 0 ? make_tmap3d(&tmC3, C, v, d, KV, cce::DCH / 64) : (tmC3 = tmC, true));
+  if (!ok) return fail("cce_de: cuTensorMapEncodeTiled failed");
+  if (int e = ensure_attr(cce::cce_de_kernel<CH, KV>, de_smem<CH, KV>())) return e;
+  const int grid = std::max(1, std::min(num_sms(), units));
+  cce::cce_de_kernel<CH, KV><<<grid, cce::NUM_THREADS, de_smem<CH, KV>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_de(cce::GradParams q, int* sched_ctr, const void* shat, int64_t shat_rows, const void* C,
+              const CUtensorMap& tmCg, cudaStream_t stream) {
+  static int cfg[5] = {-1, 0, 0, 0, 64};
   if (cfg[0] < 0) {
     cfg[0] = 1;
-    if (const char* e = getenv("CCE_DE")) sscanf(e, "%d,%d,%d,%d", &cfg[0], &cfg[1], &cfg[2], &cfg[3]);
+    if (const char* e = getenv("CCE_DE"))
+      sscanf(e, "%d,%d,%d,%d,%d", &cfg[0], &cfg[1], &cfg[2], &cfg[3], &cfg[4]);
   }
   const int ch = cfg[0] == 2 ? 2 : 1;
+  const int kv = (cfg[4] == 32 && q.perm == nullptr) ? 32 : 64;  // row gathers need 64-wide boxes
   q.de_order = cfg[1];
   q.sched = cfg[2] ? sched_ctr : nullptr;
   q.prefetch = cfg[3];
   const int units = q.g * ((q.ndc + ch - 1) / ch);
-  const int grid = std::max(1, std::min(num_sms(), units));
-  if (ch == 2) {
-    if (int e = ensure_attr(cce::cce_de_kernel<2>, de_smem<2>())) return e;
-    cce::cce_de_kernel<2><<<grid, cce::NUM_THREADS, de_smem<2>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
-  } else {
-    if (int e = ensure_attr(cce::cce_de_kernel<1>, de_smem<1>())) return e;
-    cce::cce_de_kernel<1><<<grid, cce::NUM_THREADS, de_smem<1>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
-  }
-  CCE_CUDA(cudaGetLastError());
-  return 0;
+  if (ch == 2)
+    return kv == 32 ? launch_de_t<2, 32>(q, units, shat, shat_rows, C, q.v, q.d, tmCg, stream)
+                    : launch_de_t<2, 64>(q, units, shat, shat_rows, C, q.v, q.d, tmCg, stream);
+  return kv == 32 ? launch_de_t<1, 32>(q, units, shat, shat_rows, C, q.v, q.d, tmCg, stream)
+                  : launch_de_t<1, 64>(q, units, shat, shat_rows, C, q.v, q.d, tmCg, stream);
 }
 
 // dC pass (B3) on single CTAs or CTA pairs (the pair needs the 3-D E map with 2-atom boxes).
@@ -607,7 +639,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
       const char* dbg = getenv("CCE_DEBUG_GRAD");
       q.debug = dbg ? atoi(dbg) : 0;
     }
-    if (int e = launch_de(q, w.slot_ctr + 1, tmS128, tmC64, tmC3, tmCg, stream)) return e;  // counter zeroed per group
+    if (int e = launch_de(q, w.slot_ctr + 1, w.shat, shat_rows, C, tmCg, stream)) return e;  // counter zeroed per group
     if (int e = launch_dc(q, dc_pair, tmS64, tmE64, tmE3, tmE3h, tmEg, stream)) return e;
   }
   return 0;
@@ -673,7 +705,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
-                 unsigned long long* counters, int* overflow, void* stream_ptr) {
+                 unsigned long long* counters, int* overflow, void* de_done_event, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
@@ -715,7 +747,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
 
   // One pass over token tiles [g0, g0 + g): kept-tile list, S-hat of the kept tiles (KEPT), dE of
   // those token tiles (complete), dC (written by the first pass, accumulated by later ones).
-  auto run_pass = [&](int g0, int g, bool primary, const int* run_if) -> int {
+  auto run_pass = [&](int g0, int g, bool primary, const int* run_if, bool last) -> int {
     CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)g * mt * 4, stream));
     CCE_CUDA(cudaMemsetAsync(w.cnt_n, 0, (size_t)(nt + mt) * 4, stream));
     CCE_CUDA(cudaMemsetAsync(w.list_count + 3, 0, sizeof(int), stream));  // dE unit counter
@@ -777,16 +809,19 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
-    if (int e = launch_de(q, w.list_count + 3, tmS128, tmC64, tmC3, tmC64, stream)) return e;
+    if (int e = launch_de(q, w.list_count + 3, w.shat, shat_rows, C_t, tmC64, stream)) return e;
+    if (last && de_done_event)  // every dE write of this call is enqueued before this point
+      CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
     return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
   };
   // The kept count is only known on the device: the whole-batch pass runs iff it fits; otherwise
   // (*overflow) token-tile groups sized for the worst case (every tile kept) run instead.
-  if (int e = run_pass(0, nt, true, nullptr)) return e;
-  if ((int64_t)nt * mt > capacity_tiles) {
+  const bool grouped = (int64_t)nt * mt > capacity_tiles;
+  if (int e = run_pass(0, nt, true, nullptr, !grouped)) return e;
+  if (grouped) {
     const int g = (int)std::max<int64_t>(1, capacity_tiles / mt);
     for (int g0 = 0; g0 < nt; g0 += g)
-      if (int e = run_pass(g0, std::min(g, nt - g0), false, overflow)) return e;
+      if (int e = run_pass(g0, std::min(g, nt - g0), false, overflow, g0 + g >= nt)) return e;
   }
   return 0;
 }

@@ -249,15 +249,17 @@ constexpr uint64_t kSwizzle128B = 2;
 //   K-major  : rows of 128 B (64 bf16 along K); SBO = 1024 (8-row group), LBO unused.
 //   MN-major : rows of 128 B (64 bf16 along M/N) indexed by K; SBO = 1024 (8 K-rows),
 //              LBO = byte distance between consecutive 64-element M/N atoms.
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                               uint64_t layout = kSwizzle128B) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= static_cast<uint64_t>(1) << 46;
-  d |= kSwizzle128B << 61;
+  d |= layout << 61;
   return d;
 }
+constexpr uint64_t kSwizzle64B = 4;  // K-major rows of 64 B (32 bf16); SBO = 8 rows = 512 B
 
 // Instruction descriptor, kind::f16 with bf16 A/B and fp32 D.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn,

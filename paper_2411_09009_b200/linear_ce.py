@@ -86,13 +86,17 @@ class _LinearCrossEntropy(torch.autograd.Function):
         up = up.contiguous()
         state, ctx.state = ctx.state, None
         if state is not None:
-            de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
-                                           fp32_de=group is not None)
-            del state
-            if group is not None:
-                from .vocab_parallel import all_reduce_de
+            if group is None:
+                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps)
+            else:
+                from .vocab_parallel import all_reduce_de_overlapped
 
-                de = all_reduce_de(de, group)
+                # dE is complete before the dC pass: its all-reduce runs on a side stream meanwhile
+                done = torch.cuda.Event()
+                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                                               fp32_de=True, de_done=done)
+                de = all_reduce_de_overlapped(de, done, group)
+            del state
         elif group is None:
             de, dc, _, _ = ops.backward(e, c, targets, lse, up, ignore_index=ignore_index,
                                         vocab_start=vocab_start, softcap=softcap, eps=eps,

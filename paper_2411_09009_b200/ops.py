@@ -356,13 +356,15 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
 
 
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
-                   eps: float = EPSILON_DEFAULT, fp32_de: bool = False):
+                   eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
+                   de_done: torch.cuda.Event | None = None):
     """Backward of the filter-from-forward path (lse_backward, kernels.py:327-486).
 
     The skip decision of every tile comes from the forward's tile maxima (the same strict test
     as the in-kernel filter), so only kept tiles are recomputed.  If the kept tiles exceed the
     S-hat budget, the full filter pass (`backward`'s grouped path) runs instead, gated on a
-    device flag.  Returns (dE, dC, counters[3]).
+    device flag.  Returns (dE, dC, counters[3]).  `de_done` (a CUDA event) is recorded on the
+    current stream once dE is complete and before the dC pass runs.
     """
     lib = _lib.load()
     e, c_t = state.e, state.c_t
@@ -392,7 +394,9 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.perm_padded), _p(state.row_map),
                                 _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
                                 n, d, v, state.softcap, float(eps), cap, _p(ws), ws_bytes, _p(de),
-                                int(fp32_de), _p(dc), _p(counters), _p(overflow), stream), "cce_bwd_kept")
+                                int(fp32_de), _p(dc), _p(counters), _p(overflow),
+                                ctypes.c_void_p(de_done.cuda_event if de_done is not None else 0),
+                                stream), "cce_bwd_kept")
     passes = 1 + (0 if cap >= nt * mt else -(-nt // max(1, cap // mt)))
     LAUNCHES["count"] += 2 + passes * 6
     _remember_kept(key, counters)

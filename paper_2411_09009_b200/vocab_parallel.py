@@ -44,6 +44,24 @@ def all_reduce_de(de_acc, group):
     return ops.f32_to_bf16(de_acc)
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def all_reduce_de_overlapped(de_acc, de_done, group):
+    """all_reduce_de on a side stream that starts at `de_done` (recorded by the backward before
+    its dC pass), so the dE all-reduce overlaps dC; the caller's stream then waits for it."""
+    main = torch.cuda.current_stream(de_acc.device)
+    side = _SIDE_STREAMS.get(de_acc.device)
+    if side is None:
+        side = _SIDE_STREAMS[de_acc.device] = torch.cuda.Stream(de_acc.device)
+    side.wait_event(de_done)
+    with torch.cuda.stream(side):
+        dist.all_reduce(de_acc, op=dist.ReduceOp.SUM, group=group)
+    de_acc.record_stream(side)
+    main.wait_stream(side)
+    return ops.f32_to_bf16(de_acc)
+
+
 def sharded_backward(e, c, targets, lse, upstream, *, ignore_index, vocab_start, softcap, eps,
                      vocab_sorting, group):
     de_acc, dc, _, _ = ops.backward(e, c, targets, lse, upstream, ignore_index=ignore_index,
