@@ -48,10 +48,13 @@ int cce_merge_shards(int num_shards, const float* lse_parts, const float* correc
 
 /* ---- vocabulary order (compute_vocab_order, kernels.py:145-160) ----
  * cce_ebar: column sums of the rows of E whose target != ignore_index (targets may be NULL =
- * all rows).  cce_vocab_order: key = C . ebar_sum / n_valid (the reference's mean_logits),
- * perm = stable descending argsort of key (ties by ascending index); n_valid is a device int. */
+ * all rows), summed in a fixed order (bit-reproducible) through a workspace of
+ * cce_ebar_workspace_bytes.  cce_vocab_order: key = C . ebar_sum / n_valid (the reference's
+ * mean_logits), perm = stable descending argsort of key (ties by ascending index); n_valid is a
+ * device int. */
+size_t cce_ebar_workspace_bytes(int64_t n, int64_t d);
 int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_t n, int64_t d,
-             float* ebar_sum, void* stream);
+             float* ebar_sum, void* ws, size_t ws_bytes, void* stream);
 size_t cce_sort_workspace_bytes(int64_t v);
 int cce_vocab_order(const void* C, const float* ebar_sum, const int* n_valid, int64_t v, int64_t d,
                     int32_t* perm, float* key_out, void* ws, size_t ws_bytes, void* stream);

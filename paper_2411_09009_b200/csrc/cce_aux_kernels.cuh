@@ -53,9 +53,12 @@ __global__ void fill_kernel(float* __restrict__ x, float v, int64_t n) {
   if (i < n) x[i] = v;
 }
 
-// Column mean of E over valid rows, fp32: ebar[d] = sum_i valid_i * E[i, d] / n_valid.
+// Column sums of E over valid rows, fp32, in a fixed order (bit-reproducible; the sort key and
+// so the vocabulary order depend on it): block (x, y) writes the partial sum of rows
+// [y * rows_per_block, +rows_per_block) to part[y][col]; ebar_reduce_kernel adds the partials in
+// y order.
 __global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* __restrict__ targets,
-                            int64_t ignore_index, int n, int d, float* __restrict__ ebar_acc,
+                            int64_t ignore_index, int n, int d, float* __restrict__ part,
                             int rows_per_block) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= d) return;
@@ -64,7 +67,15 @@ __global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* 
   float acc = 0.f;
   for (int r = r0; r < r1; ++r)
     if (targets == nullptr || targets[r] != ignore_index) acc += __bfloat162float(E[(size_t)r * d + col]);
-  atomicAdd(&ebar_acc[col], acc);
+  part[(size_t)blockIdx.y * d + col] = acc;
+}
+
+__global__ void ebar_reduce_kernel(const float* __restrict__ part, int nblk, int d, float* __restrict__ ebar) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  float acc = 0.f;
+  for (int b = 0; b < nblk; ++b) acc += part[(size_t)b * d + col];
+  ebar[col] = acc;
 }
 
 // key[v] = C[v] . ebar_sum / n_valid (fp32): the reference's mean_logits (kernels.py:305-308,

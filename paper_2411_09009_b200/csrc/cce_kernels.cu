@@ -459,15 +459,31 @@ size_t cce_sort_workspace_bytes(int64_t v) {
 // Vocabulary order for the backward (compute_vocab_order, kernels.py:145-160): stable sort of
 // the mean logit C.ebar, descending, ties by ascending index.  ebar_sum must hold the column
 // sums of the valid rows of E (see cce_ebar), n_valid their count.
+static int ebar_rows_per_block(int64_t n) { return (int)std::max<int64_t>(64, (n + 255) / 256); }
+
+size_t cce_ebar_workspace_bytes(int64_t n, int64_t d) {
+  if (n <= 0) return 0;
+  const int64_t nblk = (n + ebar_rows_per_block(n) - 1) / ebar_rows_per_block(n);
+  return (size_t)(nblk * d) * sizeof(float);
+}
+
 int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_t n, int64_t d,
-             float* ebar_sum, void* stream_ptr) {
+             float* ebar_sum, void* ws, size_t ws_bytes, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  CCE_CUDA(cudaMemsetAsync(ebar_sum, 0, d * sizeof(float), stream));
-  if (n == 0) return 0;
-  const int rows_per_block = 64;
-  dim3 grid((unsigned)((d + 127) / 128), (unsigned)((n + rows_per_block - 1) / rows_per_block));
+  if (n == 0) {
+    CCE_CUDA(cudaMemsetAsync(ebar_sum, 0, d * sizeof(float), stream));
+    return 0;
+  }
+  if (ws_bytes < cce_ebar_workspace_bytes(n, d)) return fail("cce_ebar: workspace too small");
+  // fixed-order two-pass sum (bit-reproducible): per-block partials, then an ordered reduction
+  const int rows_per_block = ebar_rows_per_block(n);
+  const int nblk = (int)((n + rows_per_block - 1) / rows_per_block);
+  float* part = static_cast<float*>(ws);
+  dim3 grid((unsigned)((d + 127) / 128), (unsigned)nblk);
   cce::ebar_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(E), targets,
-                                             ignore_index, (int)n, (int)d, ebar_sum, rows_per_block);
+                                             ignore_index, (int)n, (int)d, part, rows_per_block);
+  CCE_CUDA(cudaGetLastError());
+  cce::ebar_reduce_kernel<<<(unsigned)((d + 127) / 128), 128, 0, stream>>>(part, nblk, (int)d, ebar_sum);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }

@@ -139,14 +139,17 @@ def vocab_order(e, c, targets, ignore_index: int, n_valid):
     if not torch.is_tensor(n_valid):
         n_valid = torch.tensor([int(n_valid)], dtype=torch.int32, device=dev)
     ebar = torch.empty(d, dtype=torch.float32, device=dev)
-    _lib.check(lib.cce_ebar(_p(e), _p(targets), int(ignore_index), n, d, _p(ebar), _stream(dev)), "cce_ebar")
+    ebar_ws_bytes = lib.cce_ebar_workspace_bytes(n, d)
+    ebar_ws = torch.empty(max(ebar_ws_bytes, 16), dtype=torch.uint8, device=dev)
+    _lib.check(lib.cce_ebar(_p(e), _p(targets), int(ignore_index), n, d, _p(ebar), _p(ebar_ws),
+                            ebar_ws_bytes, _stream(dev)), "cce_ebar")
     perm = torch.empty(v, dtype=torch.int32, device=dev)
     key = torch.empty(v, dtype=torch.float32, device=dev)
     ws_bytes = lib.cce_sort_workspace_bytes(v)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.check(lib.cce_vocab_order(_p(c), _p(ebar), _p(n_valid), v, d, _p(perm), _p(key), _p(ws),
                                    ws_bytes, _stream(dev)), "cce_vocab_order")
-    LAUNCHES["count"] += 3 + 5  # ebar, sort key, iota + CUB onesweep radix sort passes
+    LAUNCHES["count"] += 4 + 5  # ebar (2), sort key, iota + CUB onesweep radix sort passes
     return perm, key
 
 
