@@ -131,6 +131,22 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
                  int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
                  unsigned long long* counters, int* overflow, void* de_done_event, void* stream);
 
+/* ---- low-memory backward: vocabulary groups (low_memory=True) ----
+ * lse_backward over groups of `group_vtiles` vocab tiles in tile order: per group, the group's
+ * classifier rows (C[perm] slice gathered into the workspace, or a view of C when perm_padded is
+ * NULL), the filter pass over every (token tile, group vocab tile) with S-hat slots for the
+ * worst case (ceil(n/128) * group_vtiles), dE accumulated into the caller-zeroed fp32 de_f32
+ * (fixed group order), and dC of the group's vocab tiles written once.  Transient memory:
+ * compacted E + one group's classifier rows + the group's S-hat slots + maps
+ * (cce_bwd_lowmem_workspace_bytes); no allocation grows with the kept-tile count.  Rows are the
+ * compacted rows (row_map, *n_valid); pos / lse / upstream per original row (cce_bwd_prep). */
+size_t cce_bwd_lowmem_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t group_vtiles);
+int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                   const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int64_t group_vtiles,
+                   void* ws, size_t ws_bytes, float* de_f32, void* dc, unsigned long long* counters,
+                   void* stream);
+
 /* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
  * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */
 int cce_gather_rows(const void* src, const int32_t* index, int64_t rows, int64_t cols, void* dst,

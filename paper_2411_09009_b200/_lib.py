@@ -48,6 +48,10 @@ SIGNATURES = {
                              c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_i64, c_void_p,
                              c_size, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                              c_void_p]),
+    "cce_bwd_lowmem_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
+    "cce_bwd_lowmem": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_i64, c_void_p, c_size,
+                               c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_gather_rows": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "cce_f32_to_bf16": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "cce_indexed_dot": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_i64, c_i64,

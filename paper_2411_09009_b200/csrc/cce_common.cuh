@@ -54,6 +54,7 @@ struct Params {
   const float* lse;        // global log-sum-exp (natural log)
   const float* upstream;   // dLoss/dloss_i, 0 at ignored rows
   const int32_t* pos;      // label position in tile order, -1 if none (FWD: nullptr = targets)
+  int pos_offset;          // BWD over a vocabulary group: pos - pos_offset is group-local
   const int32_t* perm;     // [mt*BN] tile-order position -> C row for gathers (nullptr = plain)
   const int32_t* row_map;  // compact row -> original row (padded); identity when no compaction
   int e_gather;            // 1: load E rows through row_map with gather4 (else E is compacted)
@@ -92,6 +93,7 @@ struct GradParams {
   float* de_f32;
   __nv_bfloat16* dc;       // [v][d]
   int accumulate;          // dC: add to the existing values (groups after the first)
+  int de_accumulate;       // dE (fp32 only): add to the existing values (vocabulary groups)
   int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
   int de_order;            // dE: 0 chunk-major units, 1 token-tile-major
   int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const bool has = p.cnt_n[ln] > 0;
       const int grow = (p.n_base + ln) * BM + row;
-      const bool valid = grow < rows.n;
+      const bool valid = grow < rows.n && (has || !p.de_accumulate);  // accumulate: nothing to add
       const int drow = valid ? p.row_map[grow] : 0;
 #pragma unroll 1
       for (int c = 0; c < nch * (DCH / 32); ++c) {
@@ -298,6 +298,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (valid && col < p.d) {
           const size_t off = (size_t)drow * p.d + col;
+          if (p.de_accumulate) {  // fp32 read-modify-write, fixed group order (deterministic)
+            const float* old = p.de_f32 + off;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              if (i < p.d - col) {
+                const float4 o = *reinterpret_cast<const float4*>(old + i);
+                x[i] += o.x;
+                x[i + 1] += o.y;
+                x[i + 2] += o.z;
+                x[i + 3] += o.w;
+              }
+          }
           store_row32(p.de_f32 ? p.de_f32 + off : nullptr, p.de_bf16 ? p.de_bf16 + off : nullptr, x,
                       p.d - col);
         }

@@ -842,6 +842,151 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   return 0;
 }
 
+// ---- low-memory backward: vocabulary groups ----
+namespace {
+struct LowWs {
+  __nv_bfloat16* e_c;
+  __nv_bfloat16* c_g;
+  __nv_bfloat16* shat;
+  uint8_t* block_zero;
+  int32_t* slot_of;
+  int* ctr;    // slot counter
+  int* cnt_n;  // [nt]
+  int* cnt_m;  // [group_vtiles]
+  size_t slot_bytes, ctr_bytes, total;
+};
+
+LowWs low_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t gv) {
+  const int64_t nt = (n + cce::BM - 1) / cce::BM;
+  auto up = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  uint8_t* b = static_cast<uint8_t*>(base);
+  LowWs w;
+  size_t o = 0;
+  w.e_c = reinterpret_cast<__nv_bfloat16*>(b + o); o += up((size_t)n * d * 2);
+  w.c_g = reinterpret_cast<__nv_bfloat16*>(b + o); o += up((size_t)std::min<int64_t>(gv * cce::BN, v) * d * 2);
+  w.shat = reinterpret_cast<__nv_bfloat16*>(b + o); o += up((size_t)nt * gv * cce::SHAT_TILE_BYTES);
+  w.block_zero = b + o; o += up((size_t)nt);
+  w.slot_bytes = up((size_t)nt * gv * 4);
+  w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
+  w.ctr_bytes = up(256 + (size_t)(nt + gv) * 4);
+  w.ctr = reinterpret_cast<int*>(b + o);
+  w.cnt_n = reinterpret_cast<int*>(b + o + 256);
+  w.cnt_m = w.cnt_n + nt;
+  o += w.ctr_bytes;
+  w.total = o;
+  return w;
+}
+}  // namespace
+
+size_t cce_bwd_lowmem_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t group_vtiles) {
+  return low_layout(nullptr, n, d, v, group_vtiles).total;
+}
+
+int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                   const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int64_t group_vtiles,
+                   void* ws, size_t ws_bytes, float* de_f32, void* dc, unsigned long long* counters,
+                   void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (d % 8 != 0) return fail("cce_bwd_lowmem: D must be a multiple of 8");
+  if (group_vtiles < 1) return fail("cce_bwd_lowmem: group_vtiles must be >= 1");
+  if (n <= 0) return 0;
+  const LowWs w = low_layout(ws, n, d, v, group_vtiles);
+  if (ws_bytes < w.total) return fail("cce_bwd_lowmem: workspace too small");
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
+  const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
+  const bool atoms3d = d % 64 == 0;
+  const bool pair = use_pairs();
+  // filter_ignored (kernels.py:494-510) and zero-upstream token tiles, once
+  cce::gather_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_c);
+  CCE_CUDA(cudaGetLastError());
+  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  CCE_CUDA(cudaGetLastError());
+  CUtensorMap tmE, tmE64, tmE3, tmE3h, tmS64;
+  const int64_t shat_rows = (int64_t)nt * group_vtiles * cce::BM;
+  bool ok = make_tmap(&tmE, w.e_c, n, d, cce::BM) && make_tmap(&tmE64, w.e_c, n, d, 64) &&
+            make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
+  if (ok && atoms3d)
+    ok = make_tmap3d(&tmE3, w.e_c, n, d, 64, cce::DCH / 64) && make_tmap3d(&tmE3h, w.e_c, n, d, 64, cce::DCH / 128);
+  else
+    tmE3 = tmE3h = tmE64;
+  if (!ok) return fail("cce_bwd_lowmem: cuTensorMapEncodeTiled failed");
+
+  for (int m0 = 0; m0 < mt; m0 += (int)group_vtiles) {
+    const int gm = std::min((int)group_vtiles, mt - m0);           // vocab tiles in this group
+    const int64_t r0 = (int64_t)m0 * cce::BN;
+    const int64_t rows = std::min<int64_t>((int64_t)gm * cce::BN, v - r0);  // classifier rows
+    // this group's classifier rows in tile order (C[perm] slice, or a view of C)
+    const void* cg = static_cast<const __nv_bfloat16*>(C) + r0 * d;
+    if (perm_padded) {
+      cce::gather_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, stream>>>(
+          static_cast<const __nv_bfloat16*>(C), perm_padded + r0, rows, (int)d, w.c_g);
+      CCE_CUDA(cudaGetLastError());
+      cg = w.c_g;
+    }
+    CUtensorMap tmC, tmC128h, tmC64;
+    if (!make_tmap(&tmC, cg, rows, d, cce::BN) || !make_tmap(&tmC128h, cg, rows, d, cce::BN / 2) ||
+        !make_tmap(&tmC64, cg, rows, d, cce::DE_KV))
+      return fail("cce_bwd_lowmem: cuTensorMapEncodeTiled failed");
+    CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, w.slot_bytes, stream));
+    CCE_CUDA(cudaMemsetAsync(w.ctr, 0, w.ctr_bytes, stream));
+    // (B1) recompute every tile of the group, filter, S-hat of kept tiles (capacity = worst case)
+    cce::Params p{};
+    p.n_total = (int)n;
+    p.n_valid = n_valid;
+    p.d = (int)d;
+    p.v = (int)rows;
+    p.nt = nt;
+    p.n_base = 0;
+    p.mt = gm;
+    p.band = choose_band(d);
+    p.splits = lse_splits(nt, gm, d, pair, true);
+    p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
+    p.softcap = softcap;
+    p.lse = lse;
+    p.upstream = upstream;
+    p.pos = pos;
+    p.pos_offset = (int)r0;
+    p.row_map = row_map;
+    p.block_zero = w.block_zero;
+    p.eps = eps;
+    p.shat = w.shat;
+    p.slot_of = w.slot_of;
+    p.slot_ctr = w.ctr;
+    p.capacity = nt * gm;
+    p.cnt_n = w.cnt_n;
+    p.cnt_m = w.cnt_m;
+    p.counters = counters;
+    if (int e = launch_lse<cce::BWD>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
+    // (B2) dE += S-hat C over the group (fp32 accumulate), (B3) dC of the group's vocab tiles
+    cce::GradParams q{};
+    q.n_total = (int)n;
+    q.n_valid = n_valid;
+    q.d = (int)d;
+    q.v = (int)rows;
+    q.mt = gm;
+    q.ndc = ndc;
+    q.n_base = 0;
+    q.g = nt;
+    q.slot_of = w.slot_of;
+    q.cnt_n = w.cnt_n;
+    q.cnt_m = w.cnt_m;
+    q.perm = nullptr;
+    q.perm_store = perm_padded ? perm_padded + r0 : nullptr;
+    q.row_map = row_map;
+    q.atoms3d = atoms3d ? 1 : 0;
+    q.de_f32 = de_f32;
+    q.de_accumulate = 1;
+    q.dc = static_cast<__nv_bfloat16*>(dc) + (perm_padded ? 0 : r0 * d);
+    q.accumulate = 0;
+    if (int e = launch_de(q, w.ctr + 1, w.shat, shat_rows, cg, tmC64, stream)) return e;
+    if (int e = launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream)) return e;
+  }
+  return 0;
+}
+
 int cce_indexed_dot(const void* E, const void* C, const int64_t* targets, int64_t n, int64_t d,
                     int64_t v, int64_t ignore_index, int64_t vocab_start, float softcap, float* out,
                     void* stream_ptr) {

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
         lse2 = valid ? p.lse[orow] * LOG2E : INFINITY;
         up_r = valid ? p.upstream[orow] : 0.f;
-        pos_r = valid ? p.pos[orow] : -1;
+        pos_r = valid ? p.pos[orow] - p.pos_offset : -1;  // outside the group: never matches
       }
     };
 

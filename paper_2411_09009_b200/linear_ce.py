@@ -46,7 +46,8 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 vocab_start, low_memory):
         # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
         # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
-        # low_memory / inference: plain forward, only O(N) transients survive to the backward.
+        # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
+        # backward, which then runs over vocabulary groups (ops.backward_lowmem).
         ctx.state = None
         if eps > 0 and not low_memory and (ctx.needs_input_grad[0] or ctx.needs_input_grad[1]):
             lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
@@ -97,16 +98,14 @@ class _LinearCrossEntropy(torch.autograd.Function):
                                                fp32_de=True, de_done=done)
                 de = all_reduce_de_overlapped(de, done, group)
             del state
-        elif group is None:
-            de, dc, _, _ = ops.backward(e, c, targets, lse, up, ignore_index=ignore_index,
-                                        vocab_start=vocab_start, softcap=softcap, eps=eps,
-                                        vocab_sorting=vocab_sorting)
-        else:
-            from .vocab_parallel import sharded_backward
+        else:  # low_memory=True or filtering off: vocabulary-grouped backward, bounded transients
+            de, dc, _, _ = ops.backward_lowmem(e, c, targets, lse, up, ignore_index=ignore_index,
+                                               vocab_start=vocab_start, softcap=softcap, eps=eps,
+                                               vocab_sorting=vocab_sorting, fp32_de=group is not None)
+            if group is not None:
+                from .vocab_parallel import all_reduce_de
 
-            de, dc = sharded_backward(e, c, targets, lse, up, ignore_index=ignore_index,
-                                      vocab_start=vocab_start, softcap=softcap, eps=eps,
-                                      vocab_sorting=vocab_sorting, group=group)
+                de = all_reduce_de(de, group)
         return de, dc, None, None, None, None, None, None, None, None, None
 
 
@@ -127,9 +126,11 @@ def linear_cross_entropy(
 
     e: [..., D] bf16 CUDA embeddings; c: [V, D] bf16 classifier (nn.Linear weight layout);
     targets: [...] int64.  Returns a scalar for "mean"/"sum", else per-token losses of shape
-    e.shape[:-1].  low_memory=True keeps only O(N) state between forward and backward (the
-    backward then recomputes every tile to take the filter decision) instead of the sorted
-    classifier copy and the per-tile row maxima.
+    e.shape[:-1].  low_memory=True keeps only O(N) state between forward and backward and runs
+    the backward over vocabulary groups (bounded transients: compacted E, an fp32 dE accumulator,
+    one group's classifier rows and S-hat slots) at the cost of recomputing every logit tile;
+    the default keeps the sorted classifier copy and per-tile row maxima from the forward so the
+    backward recomputes only the tiles it keeps.
     """
     if reduction not in ("mean", "sum", "none"):
         raise ValueError(f"unknown reduction {reduction!r}")

@@ -270,6 +270,75 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     return de, dc, counters, perm
 
 
+LOWMEM_SHAT_MB = 256  # S-hat slots of one vocabulary group in the low-memory backward
+LOWMEM_CG_MB = 256    # classifier rows of one vocabulary group
+
+
+def lowmem_group_vtiles(n: int, d: int, v: int) -> int:
+    """Vocab tiles per group of the low-memory backward: the worst-case S-hat of a group
+    (every token tile x every group vocab tile) within CCE_LOWMEM_SHAT_MB, and the group's
+    classifier rows within LOWMEM_CG_MB."""
+    budget = int(os.environ.get("CCE_LOWMEM_SHAT_MB", LOWMEM_SHAT_MB)) << 20
+    nt = max(1, -(-n // BLOCK_TOKENS))
+    mt = -(-v // BLOCK_VOCAB)
+    by_shat = budget // (nt * BLOCK_TOKENS * BLOCK_VOCAB * 2)
+    by_cg = (LOWMEM_CG_MB << 20) // (BLOCK_VOCAB * d * 2)
+    return max(1, min(mt, by_shat, by_cg))
+
+
+def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
+                    softcap: float = 0.0, eps: float | None = EPSILON_DEFAULT, vocab_sorting: bool = True,
+                    perm: torch.Tensor | None = None, fp32_de: bool = False):
+    """lse_backward (kernels.py:327-486) over vocabulary groups with bounded transients.
+
+    Ignored rows are compacted on the device (kernels.py:494-510); the vocabulary order is the
+    reference's (kernels.py:145-160).  Per group of vocab tiles: the group's sorted classifier
+    rows, the filter pass over every tile of the group (recompute, decision, S-hat), dE
+    accumulated in fp32, dC of the group's rows.  Transient memory is the compacted E, an fp32 dE
+    accumulator and one group's classifier rows and S-hat slots -- nothing grows with V or with
+    the kept-tile count.  Returns (dE, dC, counters[3], perm).
+    """
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    row_map, n_valid = compact_rows(targets, ignore_index)
+    if vocab_sorting and perm is None:
+        perm, _ = vocab_order(e, c, targets, ignore_index, n_valid)
+    vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
+    perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev) if perm is not None else None
+    inv_perm = torch.empty(v, dtype=torch.int32, device=dev) if perm is not None else None
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
+                                _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
+    LAUNCHES["count"] += 2 if perm is not None else 1
+    del inv_perm
+    de_acc = torch.zeros(n, d, dtype=torch.float32, device=dev)
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    if n == 0:
+        return (de_acc if fp32_de else de_acc.to(torch.bfloat16)), dc.zero_(), counters, perm
+    gv = lowmem_group_vtiles(n, d, v)
+    ws_bytes = lib.cce_bwd_lowmem_workspace_bytes(n, d, v, gv)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    filt_eps = 0.0 if (eps is None or eps == 0) else float(eps)
+    ev = _ev_begin("bwd")
+    _lib.check(lib.cce_bwd_lowmem(_p(e), _p(c), _p(perm_padded), _p(row_map), _p(n_valid), _p(pos),
+                                  _p(lse), _p(upstream), n, d, v, float(softcap or 0.0), filt_eps, gv,
+                                  _p(ws), ws_bytes, _p(de_acc), _p(dc), _p(counters), stream),
+               "cce_bwd_lowmem")
+    _ev_end("bwd", ev)
+    groups = -(-(-(-v // BLOCK_VOCAB)) // gv)
+    LAUNCHES["count"] += 2 + groups * (4 if perm is not None else 3)
+    del ws
+    LAST_COUNTERS["counters"] = counters
+    de = de_acc if fp32_de else f32_to_bf16(de_acc)
+    return de, dc, counters, perm
+
+
 @dataclass
 class TileState:
     """What the filter-from-forward path hands from the forward to the backward.

@@ -28,7 +28,9 @@ def _dev(x, dtype=None):
     return t.to(dtype) if dtype is not None else t
 
 
-PATHS = ["filter", "tiles"]  # backward filter pass (low_memory) / decision from the forward
+# backward: token-grouped filter pass (api.lse_backward) / decision from the forward (training
+# default) / vocabulary-grouped filter pass (low_memory=True, filtering off)
+PATHS = ["filter", "tiles", "lowmem"]
 
 
 def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sorting=True,
@@ -53,6 +55,9 @@ def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sortin
     if tiles:
         de, dc, cnt = ops.backward_tiles(st, td, lse, up, ignore_index=ignore_index, eps=eps)
         perm_out = st.perm
+    elif path == "lowmem":
+        de, dc, cnt, perm_out = ops.backward_lowmem(ed, cd, td, lse, up, ignore_index=ignore_index,
+                                                    softcap=softcap, eps=eps, vocab_sorting=sorting, perm=pd)
     else:
         de, dc, cnt, perm_out = ops.backward(ed, cd, td, lse, up, ignore_index=ignore_index,
                                             softcap=softcap, eps=eps, vocab_sorting=sorting, perm=pd)
@@ -118,15 +123,16 @@ def test_random_against_oracle(cuda_device, n, d, v, sigma, ign, cap, sort, path
     assert int(cnt.sum()) == st["total_tiles"]
 
 
+@pytest.mark.parametrize("path", ["filter", "lowmem"])
 @pytest.mark.parametrize("cap", [0.0, 5.0])
-def test_unfiltered_matches_f64_oracle(cuda_device, cap):
+def test_unfiltered_matches_f64_oracle(cuda_device, cap, path):
     rng = np.random.default_rng(11)
     n, d, v = 384, 256, 3000
     e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
     c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
     x = rng.integers(0, v, n)
     x[::7] = -1
-    loss, lse, de, dc, cnt, _ = _run(e, c, x, softcap=cap, eps=0.0, sorting=False)
+    loss, lse, de, dc, cnt, _ = _run(e, c, x, softcap=cap, eps=0.0, sorting=False, path=path)
     up = O.default_upstream(x, "mean-over-valid")
     fde, fdc = O.naive_backward(e, c, x, up, softcap=cap)
     assert O.rel_err(de, fde) < GRAD_TOL
@@ -240,7 +246,7 @@ def test_all_ignored_mean_is_zero_not_nan(cuda_device):
     assert torch.all(e.grad == 0) and torch.all(c.grad == 0)
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", ["filter", "tiles"])
 def test_shat_budget_overflow_falls_back_to_groups(cuda_device, monkeypatch, path):
     """A budget below the kept-tile count forces the grouped rerun; results are unchanged."""
     rng = np.random.default_rng(21)
@@ -404,3 +410,32 @@ def test_bit_reproducible(cuda_device, low):
         runs.append((loss.detach().cpu(), e.grad.cpu(), c.grad.cpu(), ops.LAST_COUNTERS["counters"].cpu()))
     for a, b in zip(*runs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("sort,cap", [(True, 0.0), (False, 10.0)])
+def test_lowmem_many_vocab_groups(cuda_device, monkeypatch, sort, cap):
+    """A zero group budget forces one-vocab-tile groups: dE accumulates over 40 groups in fp32
+    and every group writes its own dC rows; results equal the single-group run's to fp32
+    rounding and the tile counts are identical."""
+    from paper_2411_09009_b200 import ops
+
+    rng = np.random.default_rng(31)
+    n, d, v = 520, 128, 10000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 0.6 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::9] = -1
+    one = _run(e, c, x, sorting=sort, softcap=cap, path="lowmem")
+    monkeypatch.setenv("CCE_LOWMEM_SHAT_MB", "0")
+    assert ops.lowmem_group_vtiles(n, d, v) == 1
+    many = _run(e, c, x, sorting=sort, softcap=cap, path="lowmem")
+    assert np.array_equal(one[0], many[0]) and np.array_equal(one[4], many[4])
+    assert O.rel_err(many[2], one[2]) < 1e-2 and O.rel_err(many[3], one[3]) < 1e-2
+    ce, cl, idx = O.filter_ignored(e, x)
+    nl, nlse, _ = O.naive_forward(e, c, x, softcap=cap)
+    up = O.default_upstream(x, "mean-over-valid")
+    rde_c, rdc = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up[idx],
+                                        perm=many[5], softcap=cap)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(many[2], rde) < GRAD_TOL and O.rel_err(many[3], rdc) < GRAD_TOL
