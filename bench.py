@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--no-filter", action="store_true")
+    ap.add_argument("--paper-order", action="store_true",
+                    help="exempt_label_tiles=False: PAPER Alg. 3 filter ordering (not the reference's)")
     ap.add_argument("--low-memory", action="store_true",
                     help="low_memory=True: O(N) forward state, filter pass recomputes every tile")
     ap.add_argument("--cpu-tokens", type=int, default=128)
@@ -244,7 +246,7 @@ def main():
     c.requires_grad_(True)
 
     kw = dict(reduction="mean", filter_eps=eps, vocab_sorting=sort, softcap=cap or None,
-              low_memory=args.low_memory)
+              low_memory=args.low_memory, exempt_label_tiles=not args.paper_order)
     if world > 1 and not token_mode:
         kw.update(process_group=group, vocab_start=v0)
 
@@ -438,6 +440,7 @@ def main():
                 "workload": f"{args.config} head N={n} D={d} V={v}", "sigma": sigma, "softcap": cap,
                 "ignore_pad_frac": pad_frac, "filter_eps": None if args.no_filter else 2 ** -12,
                 "vocab_sorting": sort, "reduction": "mean", "low_memory": args.low_memory,
+                "filter_order": "paper (exempt_label_tiles=False)" if args.paper_order else "reference",
                 "parallelism": (f"vocab{world}" if world > 1 and not token_mode else f"token{world}"),
                 "l2": "inputs larger than L2 (C alone is %.2f GB)" % (v_loc * d * 2 / 1e9),
             },

@@ -128,8 +128,9 @@ size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t cap
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
-                 int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
-                 unsigned long long* counters, int* overflow, void* de_done_event, void* stream);
+                 int label_split, int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out,
+                 int de_fp32, void* dc, unsigned long long* counters, int* overflow, void* de_done_event,
+                 void* stream);
 
 /* ---- low-memory backward: vocabulary groups (low_memory=True) ----
  * lse_backward over groups of `group_vtiles` vocab tiles in tile order: per group, the group's
@@ -143,9 +144,25 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
 size_t cce_bwd_lowmem_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t group_vtiles);
 int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
                    const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
-                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int64_t group_vtiles,
-                   void* ws, size_t ws_bytes, float* de_f32, void* dc, unsigned long long* counters,
-                   void* stream);
+                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int label_split,
+                   int64_t group_vtiles, void* ws, size_t ws_bytes, float* de_f32, void* dc,
+                   unsigned long long* counters, void* stream);
+
+/* ---- paper ordering (label_split = 1 in cce_bwd_kept / cce_bwd_lowmem) ----
+ * PAPER.md Alg. 3 filters tiles on S alone, before the one-hot subtraction;
+ * the reference instead never skips a tile holding a label (kernels.py:447-455).
+ * With label_split = 1 the decision ignores labels and S-hat carries no -1; cce_label_terms then
+ * applies the label term exactly, as the backward of the indexed matmul:
+ *   dE[i] += coef_i C[x_i],  dC[x_i] += sum_{i: x_i} coef_i E[i],  coef_i = -up_i (1 - tanh^2)
+ * with tanh = correct_i / softcap (correct = the forward's per-row target logit; 1 without
+ * softcap).  E / C are the ORIGINAL matrices, perm_padded maps tile order to C rows (or NULL);
+ * de is bf16 or fp32 (de_fp32) per original row; dC gets one bf16 rounding per labelled row.
+ * Tokens sharing a label are summed in a fixed order (deterministic). */
+size_t cce_label_terms_workspace_bytes(int64_t n);
+int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                    const int* n_valid, const int32_t* pos, const float* upstream, const float* correct,
+                    int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes, void* de,
+                    int de_fp32, void* dc, void* stream);
 
 /* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
  * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */

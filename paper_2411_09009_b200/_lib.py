@@ -45,13 +45,17 @@ SIGNATURES = {
                               c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_bwd_kept_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_kept": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                             c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_i64, c_void_p,
-                             c_size, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                             c_void_p]),
+                             c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int, c_i64,
+                             c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                             c_void_p, c_void_p]),
     "cce_bwd_lowmem_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_lowmem": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                               c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_i64, c_void_p, c_size,
-                               c_void_p, c_void_p, c_void_p, c_void_p]),
+                               c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int, c_i64, c_void_p,
+                               c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "cce_label_terms_workspace_bytes": (c_size, [c_i64]),
+    "cce_label_terms": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_i64, c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_int,
+                                c_void_p, c_void_p]),
     "cce_gather_rows": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "cce_f32_to_bf16": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "cce_indexed_dot": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_i64, c_i64,

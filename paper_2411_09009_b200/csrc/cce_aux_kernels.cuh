@@ -1,6 +1,8 @@
 // Small helper kernels of the CCE path: split/shard LSE merges, the vocabulary sort key, the
 // backward prep (inverse permutation, label positions, zero-upstream tiles) and casts.
 #pragma once
+#include <climits>
+
 #include "cce_common.cuh"
 
 namespace cce {
@@ -262,8 +264,8 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
 __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const float* __restrict__ lse,
                                     const int32_t* __restrict__ pos, const int32_t* __restrict__ row_map,
                                     const int* __restrict__ n_valid, const uint8_t* __restrict__ block_zero,
-                                    int nt, int mt, float softcap, float eps, uint8_t* __restrict__ keep,
-                                    unsigned long long* __restrict__ counters) {
+                                    int nt, int mt, float softcap, float eps, int label_split,
+                                    uint8_t* __restrict__ keep, unsigned long long* __restrict__ counters) {
   __shared__ unsigned s_cnt[2];
   const int n = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -303,7 +305,7 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       any |= ok[k] && tile_row_big(zz[k], lse2[k], softcap, inv_cap, eps);
-      any |= pr[k] >= m * BN && pr[k] < (m + 1) * BN;
+      any |= !label_split && pr[k] >= m * BN && pr[k] < (m + 1) * BN;
     }
     const bool kept = __any_sync(0xffffffffu, any);
     if (lane == 0) {
@@ -438,6 +440,83 @@ __global__ void __launch_bounds__(1024) build_pairs_kernel(const int* __restrict
     poff += (c + 1) / 2;
   }
   if (threadIdx.x == T - 1) *pair_count = poff;
+}
+
+// ---------------------------------------------------------------------------------------
+// Label term of the paper ordering: with tiles filtered on S alone,
+// the -1 at each label is applied here, exactly, as the backward of the indexed matmul:
+//   dE[i] += coef_i * C[x_i],  dC[x_i] += sum over tokens i with label x_i of coef_i * E[i],
+//   coef_i = -upstream_i * (1 - tanh^2(z_i / cap)),  tanh = correct_i / cap (softcap), else 1.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float label_coef(const float* up, const float* correct, float softcap, int orow) {
+  float dcap = 1.f;
+  if (softcap > 0.f) {
+    const float t = correct[orow] / softcap;
+    dcap = 1.f - t * t;
+  }
+  return -up[orow] * dcap;
+}
+
+// sort keys: label position in tile order of each compact row (INT_MAX: no label here)
+__global__ void label_keys_kernel(const int32_t* __restrict__ row_map, const int* __restrict__ n_valid,
+                                  const int32_t* __restrict__ pos, int n, int32_t* __restrict__ key,
+                                  int32_t* __restrict__ val) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int32_t kk = INT_MAX, vv = 0;
+  if (k < *n_valid) {
+    vv = row_map[k];
+    const int32_t p = pos[vv];
+    if (p >= 0) kk = p;
+  }
+  key[k] = kk;
+  val[k] = vv;
+}
+
+// dC: one block per sorted entry; the first entry of each label run sums the run in sort order
+// (deterministic) and adds it to that classifier row (fp32 sum, one bf16 rounding).
+__global__ void label_dc_kernel(const int32_t* __restrict__ key, const int32_t* __restrict__ val, int n,
+                                const __nv_bfloat16* __restrict__ E, const float* __restrict__ up,
+                                const float* __restrict__ correct, float softcap,
+                                const int32_t* __restrict__ perm, int d, __nv_bfloat16* __restrict__ dc) {
+  const int k = blockIdx.x;
+  const int32_t p = key[k];
+  if (p == INT_MAX || (k > 0 && key[k - 1] == p)) return;
+  const int crow = perm ? perm[p] : p;
+  for (int col = threadIdx.x; col < d; col += blockDim.x) {
+    float acc = 0.f;
+    for (int j = k; j < n && key[j] == p; ++j) {
+      const int orow = val[j];
+      acc += label_coef(up, correct, softcap, orow) * __bfloat162float(E[(size_t)orow * d + col]);
+    }
+    __nv_bfloat16* dst = dc + (size_t)crow * d + col;
+    *dst = __float2bfloat16(__bfloat162float(*dst) + acc);
+  }
+}
+
+// dE: one warp per compact row with a label here
+__global__ void label_de_kernel(const int32_t* __restrict__ row_map, const int* __restrict__ n_valid,
+                                const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ C,
+                                const int32_t* __restrict__ perm, const float* __restrict__ up,
+                                const float* __restrict__ correct, float softcap, int n, int d,
+                                float* __restrict__ de_f32, __nv_bfloat16* __restrict__ de_bf16) {
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (k >= n || k >= *n_valid) return;
+  const int orow = row_map[k];
+  const int32_t p = pos[orow];
+  if (p < 0) return;
+  const int crow = perm ? perm[p] : p;
+  const float coef = label_coef(up, correct, softcap, orow);
+  const __nv_bfloat16* c = C + (size_t)crow * d;
+  for (int col = lane; col < d; col += 32) {
+    const float add = coef * __bfloat162float(c[col]);
+    const size_t o = (size_t)orow * d + col;
+    if (de_f32)
+      de_f32[o] += add;
+    else
+      de_bf16[o] = __float2bfloat16(__bfloat162float(de_bf16[o]) + add);
+  }
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,

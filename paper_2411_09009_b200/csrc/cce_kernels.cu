@@ -720,8 +720,9 @@ size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t cap
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
-                 int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out, int de_fp32, void* dc,
-                 unsigned long long* counters, int* overflow, void* de_done_event, void* stream_ptr) {
+                 int label_split, int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out,
+                 int de_fp32, void* dc, unsigned long long* counters, int* overflow, void* de_done_event,
+                 void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
@@ -739,7 +740,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
-      tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, w.keep, counters);
+      tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split, w.keep, counters);
   CCE_CUDA(cudaGetLastError());
 
   CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h;
@@ -794,6 +795,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     p.pos = pos;
     p.row_map = row_map;
     p.eps = eps;
+    p.label_split = label_split;
     p.shat = w.shat;
     p.capacity = (int)capacity_tiles;
     p.counters = counters;
@@ -884,9 +886,9 @@ size_t cce_bwd_lowmem_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t g
 
 int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
                    const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
-                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int64_t group_vtiles,
-                   void* ws, size_t ws_bytes, float* de_f32, void* dc, unsigned long long* counters,
-                   void* stream_ptr) {
+                   int64_t n, int64_t d, int64_t v, float softcap, float eps, int label_split,
+                   int64_t group_vtiles, void* ws, size_t ws_bytes, float* de_f32, void* dc,
+                   unsigned long long* counters, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_lowmem: D must be a multiple of 8");
   if (group_vtiles < 1) return fail("cce_bwd_lowmem: group_vtiles must be >= 1");
@@ -952,6 +954,7 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
     p.row_map = row_map;
     p.block_zero = w.block_zero;
     p.eps = eps;
+    p.label_split = label_split;
     p.shat = w.shat;
     p.slot_of = w.slot_of;
     p.slot_ctr = w.ctr;
@@ -984,6 +987,43 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
     if (int e = launch_de(q, w.ctr + 1, w.shat, shat_rows, cg, tmC64, stream)) return e;
     if (int e = launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream)) return e;
   }
+  return 0;
+}
+
+size_t cce_label_terms_workspace_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(n, 1));
+  return bytes + 4 * (size_t)std::max<int64_t>(n, 1) * 4 + 1024;
+}
+
+int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                    const int* n_valid, const int32_t* pos, const float* upstream, const float* correct,
+                    int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes, void* de,
+                    int de_fp32, void* dc, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  (void)v;
+  if (n <= 0) return 0;
+  const size_t need = cce_label_terms_workspace_bytes(n);
+  if (ws_bytes < need) return fail("cce_label_terms: workspace too small");
+  int32_t* key = static_cast<int32_t*>(ws);
+  int32_t* val = key + n;
+  int32_t* key_s = val + n;
+  int32_t* val_s = key_s + n;
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(val_s + n) + 255) & ~uintptr_t(255));
+  size_t tmp_bytes = need - 4 * (size_t)n * 4 - 1024;
+  cce::label_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(row_map, n_valid, pos, (int)n, key, val);
+  CCE_CUDA(cudaGetLastError());
+  CCE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, val, val_s, (int)n, 0, 32, stream));
+  cce::label_dc_kernel<<<(unsigned)n, 256, 0, stream>>>(key_s, val_s, (int)n, static_cast<const __nv_bfloat16*>(E),
+                                                       upstream, correct, softcap, perm_padded, (int)d,
+                                                       static_cast<__nv_bfloat16*>(dc));
+  CCE_CUDA(cudaGetLastError());
+  cce::label_de_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
+      row_map, n_valid, pos, static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap,
+      (int)n, (int)d, de_fp32 ? static_cast<float*>(de) : nullptr,
+      de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de));
+  CCE_CUDA(cudaGetLastError());
   return 0;
 }
 

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             const int col = col0 + c * 32 + j + h;
             const float s = (col < p.v) ? ex2_approx(z * LOG2E - lse2) : 0.f;
-            g2[h] = ((col == pos_r) ? s - 1.f : s) * up_r * dcap;
+            g2[h] = ((col == pos_r && !p.label_split) ? s - 1.f : s) * up_r * dcap;
           }
           pk[j >> 1] = pack_bf16x2(g2[0], g2[1]);
         }
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (col0 + c * 32 + j < p.v) zmax = fmaxf(zmax, __uint_as_float(r[j]));
         }
         const bool big = valid && tile_row_big(zmax, lse2, p.softcap, inv_cap, p.eps);
-        const bool in_tile = pos_r >= col0 && pos_r < col0 + BN;
+        const bool in_tile = !p.label_split && pos_r >= col0 && pos_r < col0 + BN;
         const uint32_t wvote = __any_sync(0xffffffffu, big || in_tile);
         if (lane == 0) s_vote[(t & 1) * 4 + quarter] = wvote;
         named_bar_sync(1, 128);

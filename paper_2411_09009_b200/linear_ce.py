@@ -43,7 +43,7 @@ def _resolve_eps(filter_eps):
 class _LinearCrossEntropy(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
-                vocab_start, low_memory):
+                vocab_start, low_memory, exempt_label_tiles):
         # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
         # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
         # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
@@ -63,6 +63,10 @@ class _LinearCrossEntropy(torch.autograd.Function):
         valid = targets != ignore_index
         ctx.save_for_backward(e, c, targets, lse)
         ctx.cfg = (ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start)
+        # paper ordering: the label term is applied apart from the filtered tiles and needs the
+        # forward's (softcapped) target logit of the rows whose label this shard owns
+        ctx.split = not exempt_label_tiles and eps > 0
+        ctx.correct = correct if ctx.split else None
         if reduction == "none":
             return loss
         total = loss.sum()
@@ -86,27 +90,30 @@ class _LinearCrossEntropy(torch.autograd.Function):
             up = valid.to(torch.float32) * (g / n_valid)
         up = up.contiguous()
         state, ctx.state = ctx.state, None
+        split, correct, ctx.correct = ctx.split, ctx.correct, None
         if state is not None:
             if group is None:
-                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps)
+                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                                               label_split=split, correct=correct)
             else:
                 from .vocab_parallel import all_reduce_de_overlapped
 
                 # dE is complete before the dC pass: its all-reduce runs on a side stream meanwhile
                 done = torch.cuda.Event()
                 de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
-                                               fp32_de=True, de_done=done)
+                                               fp32_de=True, de_done=done, label_split=split, correct=correct)
                 de = all_reduce_de_overlapped(de, done, group)
             del state
         else:  # low_memory=True or filtering off: vocabulary-grouped backward, bounded transients
             de, dc, _, _ = ops.backward_lowmem(e, c, targets, lse, up, ignore_index=ignore_index,
                                                vocab_start=vocab_start, softcap=softcap, eps=eps,
-                                               vocab_sorting=vocab_sorting, fp32_de=group is not None)
+                                               vocab_sorting=vocab_sorting, fp32_de=group is not None,
+                                               label_split=split, correct=correct)
             if group is not None:
                 from .vocab_parallel import all_reduce_de
 
                 de = all_reduce_de(de, group)
-        return de, dc, None, None, None, None, None, None, None, None, None
+        return de, dc, None, None, None, None, None, None, None, None, None, None
 
 
 def linear_cross_entropy(
@@ -121,6 +128,7 @@ def linear_cross_entropy(
     process_group=None,
     vocab_start: int = 0,
     low_memory: bool = False,
+    exempt_label_tiles: bool = True,
 ) -> torch.Tensor:
     """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
 
@@ -131,6 +139,11 @@ def linear_cross_entropy(
     one group's classifier rows and S-hat slots) at the cost of recomputing every logit tile;
     the default keeps the sorted classifier copy and per-tile row maxima from the forward so the
     backward recomputes only the tiles it keeps.
+
+    exempt_label_tiles=True is the reference's filter (a tile holding a label is never skipped,
+    kernels.py:447-455).  False is the paper's Alg. 3 ordering: tiles are filtered on the softmax
+    alone and the -1 label term is applied exactly, apart from the tiles (PAPER.md:212-214,
+    :330-335) -- label-only tiles then skip too.
     """
     if reduction not in ("mean", "sum", "none"):
         raise ValueError(f"unknown reduction {reduction!r}")
@@ -149,7 +162,7 @@ def linear_cross_entropy(
     eps = _resolve_eps(filter_eps)
     out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
                                     bool(vocab_sorting), process_group, int(vocab_start),
-                                    bool(low_memory))
+                                    bool(low_memory), bool(exempt_label_tiles))
     if reduction == "none":
         return out.reshape(lead)
     return out

@@ -270,6 +270,23 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     return de, dc, counters, perm
 
 
+def label_terms(e, c, perm_padded, row_map, n_valid, pos, upstream, correct, softcap: float, de, dc):
+    """The label term of the paper ordering, applied exactly (cce_label_terms): de[i] and
+    dc[x_i] += -upstream_i (1 - tanh^2) C[x_i] / E[i] (PAPER.md:212-214)."""
+    lib = _lib.load()
+    n, d = e.shape
+    if n == 0:
+        return
+    ws_bytes = lib.cce_label_terms_workspace_bytes(n)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=e.device)
+    _lib.check(lib.cce_label_terms(_p(e), _p(c), _p(perm_padded), _p(row_map), _p(n_valid), _p(pos),
+                                   _p(upstream), _p(correct.to(torch.float32).contiguous()), n, d, c.shape[0],
+                                   float(softcap or 0.0), _p(ws), ws_bytes, _p(de),
+                                   int(de.dtype == torch.float32), _p(dc), _stream(e.device)),
+               "cce_label_terms")
+    LAUNCHES["count"] += 3 + 4  # keys, dC, dE + CUB radix sort passes
+
+
 LOWMEM_SHAT_MB = 256  # S-hat slots of one vocabulary group in the low-memory backward
 LOWMEM_CG_MB = 256    # classifier rows of one vocabulary group
 
@@ -288,7 +305,8 @@ def lowmem_group_vtiles(n: int, d: int, v: int) -> int:
 
 def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
                     softcap: float = 0.0, eps: float | None = EPSILON_DEFAULT, vocab_sorting: bool = True,
-                    perm: torch.Tensor | None = None, fp32_de: bool = False):
+                    perm: torch.Tensor | None = None, fp32_de: bool = False,
+                    label_split: bool = False, correct: torch.Tensor | None = None):
     """lse_backward (kernels.py:327-486) over vocabulary groups with bounded transients.
 
     Ignored rows are compacted on the device (kernels.py:494-510); the vocabulary order is the
@@ -326,14 +344,17 @@ def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_st
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     filt_eps = 0.0 if (eps is None or eps == 0) else float(eps)
     ev = _ev_begin("bwd")
+    split = bool(label_split) and filt_eps > 0
     _lib.check(lib.cce_bwd_lowmem(_p(e), _p(c), _p(perm_padded), _p(row_map), _p(n_valid), _p(pos),
-                                  _p(lse), _p(upstream), n, d, v, float(softcap or 0.0), filt_eps, gv,
-                                  _p(ws), ws_bytes, _p(de_acc), _p(dc), _p(counters), stream),
-               "cce_bwd_lowmem")
+                                  _p(lse), _p(upstream), n, d, v, float(softcap or 0.0), filt_eps,
+                                  int(split), gv, _p(ws), ws_bytes, _p(de_acc), _p(dc), _p(counters),
+                                  stream), "cce_bwd_lowmem")
+    del ws
+    if split:
+        label_terms(e, c, perm_padded, row_map, n_valid, pos, upstream, correct, softcap, de_acc, dc)
     _ev_end("bwd", ev)
     groups = -(-(-(-v // BLOCK_VOCAB)) // gv)
     LAUNCHES["count"] += 2 + groups * (4 if perm is not None else 3)
-    del ws
     LAST_COUNTERS["counters"] = counters
     de = de_acc if fp32_de else f32_to_bf16(de_acc)
     return de, dc, counters, perm
@@ -351,6 +372,7 @@ class TileState:
     """
 
     e: torch.Tensor
+    c: torch.Tensor
     e_c: torch.Tensor
     c_t: torch.Tensor
     row_map: torch.Tensor
@@ -412,7 +434,7 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     tile_max = torch.empty(lib.cce_tile_max_bytes(n, v) // 4, dtype=torch.float32, device=dev)
     lse_local = torch.empty(n, dtype=torch.float32, device=dev)
     correct = torch.empty(n, dtype=torch.float32, device=dev)
-    state = TileState(e, e_c, c_t, row_map, n_valid, perm, perm_padded, pos, tile_max,
+    state = TileState(e, c, e_c, c_t, row_map, n_valid, perm, perm_padded, pos, tile_max,
                       int(vocab_start), float(softcap or 0.0), mean_logits)
     if n == 0:
         return lse_local, correct, state
@@ -429,7 +451,8 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
 
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
                    eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
-                   de_done: torch.cuda.Event | None = None):
+                   de_done: torch.cuda.Event | None = None, label_split: bool = False,
+                   correct: torch.Tensor | None = None):
     """Backward of the filter-from-forward path (lse_backward, kernels.py:327-486).
 
     The skip decision of every tile comes from the forward's tile maxima (the same strict test
@@ -465,12 +488,18 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     ev = _ev_begin("bwd")
     _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.perm_padded), _p(state.row_map),
                                 _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
-                                n, d, v, state.softcap, float(eps), cap, _p(ws), ws_bytes, _p(de),
-                                int(fp32_de), _p(dc), _p(counters), _p(overflow),
-                                ctypes.c_void_p(de_done.cuda_event if de_done is not None else 0),
-                                stream), "cce_bwd_kept")
+                                n, d, v, state.softcap, float(eps), int(bool(label_split)), cap, _p(ws),
+                                ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters), _p(overflow),
+                                ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
+                                                else 0), stream), "cce_bwd_kept")
     passes = 1 + (0 if cap >= nt * mt else -(-nt // max(1, cap // mt)))
     LAUNCHES["count"] += 2 + passes * 6
+    del ws
+    if label_split:
+        label_terms(e, state.c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream,
+                    correct, state.softcap, de, dc)
+        if de_done is not None:
+            de_done.record()
     _remember_kept(key, counters)
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters

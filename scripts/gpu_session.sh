@@ -17,6 +17,8 @@ for s in "$@"; do
         CCE_BENCH_BACKEND=gloo CCE_BENCH_SAME_DEVICE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
           --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline --mode $mode \
           >> $out/multirank.log 2>&1; echo "exit $mode $?" >> $out/multirank.log; done ;;
+    benchpaper) for a in "" "--low-memory" "--config gemma2-9b"; do
+        timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --paper-order $a >> $out/benchpaper.log 2>&1; echo "exit $a $?" >> $out/benchpaper.log; done ;;
     benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \

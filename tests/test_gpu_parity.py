@@ -439,3 +439,75 @@ def test_lowmem_many_vocab_groups(cuda_device, monkeypatch, sort, cap):
     rde = np.zeros_like(e)
     rde[idx] = rde_c
     assert O.rel_err(many[2], rde) < GRAD_TOL and O.rel_err(many[3], rdc) < GRAD_TOL
+
+
+@pytest.mark.parametrize("path", ["tiles", "lowmem"])
+@pytest.mark.parametrize("n,d,v,sigma,ign,cap,sort", [
+    (512, 128, 12000, 0.6, 0.2, 0.0, True),
+    (300, 256, 20000, 0.4, 0.0, 8.0, False),
+    (640, 64, 9001, 1.0, 0.1, 0.0, True),
+])
+def test_paper_ordering_against_oracle(cuda_device, path, n, d, v, sigma, ign, cap, sort):
+    """exempt_label_tiles=False: tiles filtered on S alone, the label term applied exactly apart
+    from the tiles.  Parity against the oracle's restatement with
+    the GPU's vocabulary order; tile counts equal the oracle's."""
+    from paper_2411_09009_b200 import ops
+
+    rng = np.random.default_rng(n + v)
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * sigma / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    if ign:
+        x[rng.random(n) < ign] = -1
+    ed, cd, td = _dev(e, torch.bfloat16), _dev(c, torch.bfloat16), _dev(x.astype(np.int64))
+    if path == "tiles":
+        lse_l, corr, st = ops.forward_tiles(ed, cd, td, -1, 0, cap, vocab_sorting=sort)
+    else:
+        lse_l, corr = ops.forward_local(ed, cd, td, -1, 0, cap)
+    lse, loss = ops.merge_shards(lse_l[None], corr[None], td, -1)
+    up_np = O.default_upstream(x, "mean-over-valid")
+    up = _dev(up_np.astype(np.float32))
+    if path == "tiles":
+        de, dc, cnt = ops.backward_tiles(st, td, lse, up, ignore_index=-1, label_split=True, correct=corr)
+        perm = None if st.perm is None else st.perm.cpu().numpy()
+    else:
+        de, dc, cnt, pm = ops.backward_lowmem(ed, cd, td, lse, up, ignore_index=-1, softcap=cap,
+                                              vocab_sorting=sort, label_split=True, correct=corr)
+        perm = None if pm is None else pm.cpu().numpy()
+    torch.cuda.synchronize()
+    nl, nlse, _ = O.naive_forward(e, c, x, softcap=cap)
+    ce, cl, idx = O.filter_ignored(e, x)
+    rde_c, rdc, st_ref = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up_np[idx],
+                                                perm=perm, softcap=cap, return_stats=True,
+                                                exempt_labels=False)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    k = cnt.cpu().numpy()
+    assert int(k[1]) == st_ref["skipped_epsilon"] and int(k.sum()) == st_ref["total_tiles"]
+    assert O.rel_err(de.float().cpu().numpy(), rde) < GRAD_TOL
+    assert O.rel_err(dc.float().cpu().numpy(), rdc) < GRAD_TOL
+
+
+def test_paper_ordering_autograd_skips_label_only_tiles(cuda_device):
+    """linear_cross_entropy(exempt_label_tiles=False): same loss, at least as many skipped tiles as
+    the reference rule, gradients within the filtering error of the exact ones."""
+    from paper_2411_09009_b200 import linear_cross_entropy, ops
+
+    rng = np.random.default_rng(3)
+    n, d, v = 1024, 128, 30000
+    e0 = torch.from_numpy(O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))).cuda().bfloat16()
+    c0 = torch.from_numpy(O.round_to_bf16((rng.standard_normal((v, d)) * 0.5 / math.sqrt(d)).astype(np.float32))).cuda().bfloat16()
+    t = torch.from_numpy(rng.integers(0, v, n)).cuda()
+    out = {}
+    for exempt in (True, False):
+        e = e0.clone().requires_grad_(True)
+        c = c0.clone().requires_grad_(True)
+        loss = linear_cross_entropy(e, c, t, exempt_label_tiles=exempt)
+        loss.backward()
+        out[exempt] = (loss.item(), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy(),
+                       ops.LAST_COUNTERS["counters"].cpu().tolist())
+    assert out[False][0] == pytest.approx(out[True][0], rel=1e-6)
+    assert out[False][3][1] > out[True][3][1]
+    fde, fdc = O.naive_backward(e0.float().cpu().numpy(), c0.float().cpu().numpy(), t.cpu().numpy(),
+                                O.default_upstream(t.cpu().numpy(), "mean-over-valid"))
+    assert O.rel_err(out[False][1], fde) < 3e-2 and O.rel_err(out[False][2], fdc) < 3e-2

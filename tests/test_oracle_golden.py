@@ -204,3 +204,33 @@ def test_softcap_blocked_matches_naive():
     nde, ndc = O.naive_backward(e, c, x, O.default_upstream(x, "mean-over-valid"), softcap=5.0)
     assert np.max(np.abs(loss - nl)) < 1e-4
     assert O.rel_err(de, nde) < 1e-4 and O.rel_err(dc, ndc) < 1e-4
+
+
+def test_paper_ordering_restatement():
+    """exempt_labels=False (Alg. 3: filter on S, then the label term): without filtering
+    it is the unfiltered gradient; when every label tile is kept anyway it equals the reference's
+    label-tile exemption; otherwise it skips at least as many tiles."""
+    rng = np.random.default_rng(5)
+    n, d, v = 300, 32, 10000  # mean S = 1e-4 < eps: only label tiles survive the reference rule
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 0.1 / np.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::7] = -1
+    _, lse, _ = O.naive_forward(e, c, x)
+    up = O.default_upstream(x, "mean-over-valid")
+    a = O.lse_backward_blocked(e, c, x, lse.astype(np.float32), up, eps=None, exempt_labels=False,
+                               dtype=np.float64)
+    b = O.naive_backward(e, c, x, up)
+    assert O.rel_err(a[0], b[0]) < 1e-6 and O.rel_err(a[1], b[1]) < 1e-6  # lse passed as f32
+    ex = O.lse_backward_blocked(e, c, x, lse.astype(np.float32), up, return_stats=True)
+    sp = O.lse_backward_blocked(e, c, x, lse.astype(np.float32), up, exempt_labels=False,
+                                return_stats=True)
+    assert sp[2]["skipped_epsilon"] > ex[2]["skipped_epsilon"]  # label-only tiles now skip
+    # sharp logits: every label tile holds a big S, so both orderings keep the same tiles
+    c2 = O.round_to_bf16((rng.standard_normal((v, d)) * 3.0 / np.sqrt(d)).astype(np.float32))
+    _, lse2, _ = O.naive_forward(e, c2, x)
+    ex2 = O.lse_backward_blocked(e, c2, x, lse2.astype(np.float32), up, return_stats=True)
+    sp2 = O.lse_backward_blocked(e, c2, x, lse2.astype(np.float32), up, exempt_labels=False,
+                                 return_stats=True)
+    if ex2[2] == sp2[2]:
+        assert O.rel_err(ex2[0], sp2[0]) < 1e-6 and O.rel_err(ex2[1], sp2[1]) < 1e-6

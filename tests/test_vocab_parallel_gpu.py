@@ -36,7 +36,7 @@ def _inputs(n, d, v, seed=3):
     return e, c, x
 
 
-def _worker(rank, world, port, q, n, d, v, filt, cap):
+def _worker(rank, world, port, q, n, d, v, filt, cap, split=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -52,7 +52,8 @@ def _worker(rank, world, port, q, n, d, v, filt, cap):
         c = torch.from_numpy(c_np[v0:v1]).cuda().bfloat16().requires_grad_(True)
         t = torch.from_numpy(x_np).cuda()
         loss = linear_cross_entropy(e, c, t, filter_eps="auto" if filt else None, softcap=cap or None,
-                                    process_group=dist.group.WORLD, vocab_start=v0)
+                                    process_group=dist.group.WORLD, vocab_start=v0,
+                                    exempt_label_tiles=not split)
         loss.backward()
         torch.cuda.synchronize()
         q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy()))
@@ -60,15 +61,16 @@ def _worker(rank, world, port, q, n, d, v, filt, cap):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("filt,cap", [(False, 0.0), (True, 0.0), (True, 20.0)])
-def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap):
+@pytest.mark.parametrize("filt,cap,split", [(False, 0.0, False), (True, 0.0, False), (True, 20.0, False),
+                                            (True, 0.0, True)])
+def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap, split):
     import torch.multiprocessing as mp
 
     world, n, d, v = 2, 600, 128, 5001
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, d, v, filt, cap)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, d, v, filt, cap, split)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
