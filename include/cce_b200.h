@@ -107,7 +107,9 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * vocab sorting, else C).  pos[i] (per ORIGINAL row, cce_bwd_prep) is the label position in tile
  * order or -1.  lse_local / correct are per ORIGINAL row (undefined / 0 at ignored rows).
  * tile_max: [ceil(n/128)][ceil(v/256)][128] fp32 (cce_tile_max_bytes), the max raw logit of
- * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).
+ * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).  perm_padded: NULL
+ * when C_t is already in tile order; else C_t is the classifier in natural order and its rows are
+ * gathered through perm_padded (TMA tile::gather4, CTA pairs only).
  *
  * cce_bwd_kept: the backward from tile_max.  Keeps tile (n, m) iff its upstream is not all zero
  * and it holds a label or some S >= eps (the same strict test as cce_bwd, eps > 0 required);
@@ -121,9 +123,10 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * call has been enqueued, before the dC pass: a vocab-parallel caller all-reduces dE on another
  * stream while dC runs. */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
-int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
-                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
-                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream);
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+                  const int* n_valid, const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap,
+                  void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
+                  void* stream);
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles);
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
@@ -163,6 +166,16 @@ int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, co
                     const int* n_valid, const int32_t* pos, const float* upstream, const float* correct,
                     int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes, void* de,
                     int de_fp32, void* dc, void* stream);
+
+/* ---- reductions (default_upstream, core.py:181-200; linear_cross_entropy's reduction) ----
+ * reduction: 0 none, 1 sum, 2 mean over valid rows (an all-ignored batch gives 0, not NaN).
+ * cce_reduce_loss: *out = sum of the per-row losses (or that / n_valid); one block, fixed order.
+ * cce_upstream: up[i] = 0 at ignored rows, else grad[i] (none, grad is [n]) or grad[0] (sum) or
+ * grad[0] / n_valid (mean).  Device scalars throughout: no host synchronisation. */
+int cce_reduce_loss(const float* loss, const int64_t* targets, int64_t ignore_index, int64_t n,
+                    int reduction, float* out, void* stream);
+int cce_upstream(const float* grad, const int64_t* targets, int64_t ignore_index, int64_t n, int reduction,
+                 float* up, void* stream);
 
 /* dst[i] = src[index[i]] for bf16 rows of `cols` elements: materialises the vocabulary-sorted
  * classifier C[perm] so the backward loads plain tiles (c_sorted = 1). */

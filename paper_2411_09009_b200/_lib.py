@@ -41,8 +41,8 @@ SIGNATURES = {
                         c_void_p, c_int, c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p,
                         c_void_p, c_void_p]),
     "cce_tile_max_bytes": (c_size, [c_i64, c_i64]),
-    "cce_fwd_tiles": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
-                              c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "cce_fwd_tiles": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64,
+                              c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_bwd_kept_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_kept": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int, c_i64,
@@ -56,6 +56,8 @@ SIGNATURES = {
     "cce_label_terms": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_i64, c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_int,
                                 c_void_p, c_void_p]),
+    "cce_reduce_loss": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_int, c_void_p, c_void_p]),
+    "cce_upstream": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_int, c_void_p, c_void_p]),
     "cce_gather_rows": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "cce_f32_to_bf16": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "cce_indexed_dot": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_i64, c_i64,

@@ -318,71 +318,86 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
   if (threadIdx.x == 0 && s_cnt[0]) atomicAdd(&counters[1], (unsigned long long)s_cnt[0]);
 }
 
-// One block of 1024 threads: the kept flags of token tiles [n_lo, n_lo + g), in vocab-tile-major
-// order, become the kept-tile list (slot = list position, so concurrently running CTAs of the
-// KEPT pass share C tiles) and slot_of / cnt_n / cnt_m of that group (local token-tile index
-// n - n_lo; slot_of pre-filled with -1, counts zeroed).  primary: also counters[0] += kept and
-// the capacity flags (*ok = 1, *overflow = 0 when every kept tile got a slot, else *ok = 0 and
-// *overflow = 1).  Runs only if run_if is null or *run_if != 0.
-__global__ void __launch_bounds__(1024) build_list_kernel(
-    const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g, int capacity, const int* run_if,
-    int primary, int2* __restrict__ list, int32_t* __restrict__ slot_of, int* __restrict__ cnt_n,
-    int* __restrict__ cnt_m, int* __restrict__ list_count, int* __restrict__ ok, int* __restrict__ overflow,
-    unsigned long long* __restrict__ counters) {
-  if (run_if != nullptr && *run_if == 0) return;
-  constexpr int T = 1024, U = 8;
-  __shared__ int s_warp[T / 32];
-  const long long total = (long long)g * mt;
-  const long long per = ((total + T - 1) / T + U - 1) / U * U;
-  const long long i0 = (long long)threadIdx.x * per;
-  const long long i1 = min(total, i0 + per);
-  auto flag = [&](long long i) -> int {
-    const int m = (int)(i / g), n = n_lo + (int)(i - (long long)m * g);
-    return keep[(size_t)m * nt + n];
-  };
-  int c = 0;
-  for (long long i = i0; i < i1; i += U) {
-    int f[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) f[k] = (i + k < i1) ? flag(i + k) : 0;
-#pragma unroll
-    for (int k = 0; k < U; ++k) c += f[k];
-  }
-  // block exclusive scan of c
+// block-wide sum (any block size that is a multiple of 32, <= 1024)
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* s_tmp) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = c;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_tmp[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (wid == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? s_tmp[lane] : T(0);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) s_tmp[0] = r;
+  }
+  __syncthreads();
+  r = s_tmp[0];
+  __syncthreads();
+  return r;
+}
+
+// Kept-tile list of the token tiles [n_lo, n_lo + g) in vocab-tile-major order (slot = list
+// position, so concurrently running CTAs of the KEPT pass share C tiles), in three parallel
+// steps: list_count_kernel (block per vocab tile) -> list_scan_kernel (one block: offsets,
+// list_count, capacity flags, counter resets) -> list_fill_kernel (block per vocab tile: list,
+// every slot_of entry (slot or -1), cnt_n).  All run only if run_if is null or *run_if != 0.
+__global__ void list_count_kernel(const uint8_t* __restrict__ keep, int nt, int n_lo, int g,
+                                  const int* run_if, int* __restrict__ cnt_m) {
+  if (run_if != nullptr && *run_if == 0) return;
+  __shared__ int s_w[32];
+  const uint8_t* row = keep + (size_t)blockIdx.x * nt + n_lo;
+  int c = 0;
+  for (int i = threadIdx.x; i < g; i += blockDim.x) c += row[i];
+  c = block_sum(c, s_w);
+  if (threadIdx.x == 0) cnt_m[blockIdx.x] = c;
+}
+
+// cnt_m -> off_m (exclusive), *list_count; primary: counters[0] += kept and *ok / *overflow
+// (every kept tile got a slot or not); resets cnt_n[0..g) and the dE unit counter.
+__global__ void __launch_bounds__(1024) list_scan_kernel(const int* __restrict__ cnt_m, int mt, int g,
+                                                         int capacity, const int* run_if, int primary,
+                                                         int* __restrict__ off_m, int* __restrict__ cnt_n,
+                                                         int* __restrict__ list_count, int* __restrict__ ok,
+                                                         int* __restrict__ overflow, int* __restrict__ sched,
+                                                         unsigned long long* __restrict__ counters) {
+  if (run_if != nullptr && *run_if == 0) return;
+  constexpr int T = 1024;
+  __shared__ int s_part[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < g; i += T) cnt_n[i] = 0;
+  if (threadIdx.x == 0 && sched) *sched = 0;
+  const int per = (mt + T - 1) / T;
+  const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
+  int local = 0;
+  for (int m = m0; m < m1; ++m) local += cnt_m[m];
+  int incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) s_warp[wid] = incl;
+  if (lane == 31) s_part[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    int x = s_warp[lane];
+    int x = s_part[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    s_warp[lane] = x;  // inclusive over warps
+    s_part[lane] = x;
   }
   __syncthreads();
-  int slot = (wid ? s_warp[wid - 1] : 0) + incl - c;
-  const int kept_total = s_warp[T / 32 - 1];
-  if (c)
-    for (long long i = i0; i < i1; ++i) {
-      if (!flag(i)) continue;
-      const int m = (int)(i / g), ln = (int)(i - (long long)m * g);
-      if (slot < capacity) {
-        list[slot] = make_int2(n_lo + ln, m);
-        slot_of[(size_t)ln * mt + m] = slot;
-        atomicAdd(&cnt_n[ln], 1);
-        atomicAdd(&cnt_m[m], 1);
-      }
-      ++slot;
-    }
+  int run = (wid ? s_part[wid - 1] : 0) + incl - local;
+  for (int m = m0; m < m1; ++m) {
+    off_m[m] = run;
+    run += cnt_m[m];
+  }
   if (threadIdx.x == 0) {
+    const int kept_total = s_part[31];
     *list_count = kept_total;
     if (primary) {
       const bool fits = kept_total <= capacity;
@@ -390,6 +405,49 @@ __global__ void __launch_bounds__(1024) build_list_kernel(
       *overflow = fits ? 0 : 1;
       atomicAdd(&counters[0], (unsigned long long)kept_total);
     }
+  }
+}
+
+// block per vocab tile m: slots off_m + rank in token-tile order; slot_of row-major [g][mt] with
+// the local token-tile index; tiles past the capacity get no slot (only possible when the
+// caller's gate then skips every consumer).
+__global__ void list_fill_kernel(const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g,
+                                 int capacity, const int* run_if, const int* __restrict__ off_m,
+                                 int2* __restrict__ list, int32_t* __restrict__ slot_of,
+                                 int* __restrict__ cnt_n) {
+  if (run_if != nullptr && *run_if == 0) return;
+  __shared__ int s_w[32];
+  __shared__ int s_base;
+  const int m = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint8_t* row = keep + (size_t)m * nt + n_lo;
+  if (threadIdx.x == 0) s_base = off_m[m];
+  __syncthreads();
+  for (int b = 0; b < g; b += blockDim.x) {
+    const int ln = b + threadIdx.x;
+    const bool f = ln < g && row[ln];
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_w[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+    for (int w = 0; w < wid; ++w) before += s_w[w];
+    const int slot = s_base + before + __popc(bal & ((1u << lane) - 1));
+    if (ln < g) {
+      int so = -1;
+      if (f && slot < capacity) {
+        list[slot] = make_int2(n_lo + ln, m);
+        so = slot;
+        atomicAdd(&cnt_n[ln], 1);
+      }
+      slot_of[(size_t)ln * mt + m] = so;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+      s_base += t;
+    }
+    __syncthreads();
   }
 }
 
@@ -516,6 +574,46 @@ __global__ void label_de_kernel(const int32_t* __restrict__ row_map, const int* 
       de_f32[o] += add;
     else
       de_bf16[o] = __float2bfloat16(__bfloat162float(de_bf16[o]) + add);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Reductions of linear_cross_entropy (default_upstream, core.py:181-200), one block, fixed order
+// ---------------------------------------------------------------------------------------
+// out = sum(loss) (reduction 1) or sum(loss) / n_valid, 0 when nothing is valid (reduction 2)
+__global__ void __launch_bounds__(1024) reduce_loss_kernel(const float* __restrict__ loss,
+                                                           const int64_t* __restrict__ targets,
+                                                           int64_t ignore_index, int n, int reduction,
+                                                           float* __restrict__ out) {
+  __shared__ float s_f[32];
+  __shared__ int s_i[32];
+  float acc = 0.f;
+  int cnt = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    acc += loss[i];
+    cnt += targets[i] != ignore_index;
+  }
+  const float total = block_sum(acc, s_f);
+  const int nv = block_sum(cnt, s_i);
+  if (threadIdx.x == 0) *out = reduction == 1 ? total : (nv > 0 ? total / (float)nv : 0.f);
+}
+
+// up[i] = valid_i * g (reduction 1), valid_i * g / n_valid (2), valid_i * g[i] (0: g is [n])
+__global__ void __launch_bounds__(1024) upstream_kernel(const float* __restrict__ g,
+                                                        const int64_t* __restrict__ targets,
+                                                        int64_t ignore_index, int n, int reduction,
+                                                        float* __restrict__ up) {
+  __shared__ int s_i[32];
+  int cnt = 0;
+  if (reduction == 2)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) cnt += targets[i] != ignore_index;
+  const int nv = reduction == 2 ? block_sum(cnt, s_i) : 1;
+  const float scale = reduction == 2 ? (nv > 0 ? 1.f / (float)nv : 0.f) : 1.f;
+  const float g0 = reduction == 0 ? 0.f : *g;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const bool valid = targets[i] != ignore_index;
+    const float gi = reduction == 0 ? g[i] : g0;
+    up[i] = valid ? gi * scale : 0.f;
   }
 }
 

@@ -279,6 +279,7 @@ struct KeptWs {
   int* ok;
   int* cnt_n;
   int* cnt_m;
+  int* off_m;
   size_t keep_bytes, slot_bytes, cnt_bytes;
   size_t total;
 };
@@ -299,12 +300,13 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
   w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
   w.block_zero = b + o; o += up((size_t)nt);
   // zeroed together: list_count, ok, cnt_n[nt], cnt_m[mt]
-  w.cnt_bytes = up(256 + (size_t)(nt + mt) * 4);
+  w.cnt_bytes = up(256 + (size_t)(nt + 2 * mt) * 4);
   w.list_count = reinterpret_cast<int*>(b + o);
   w.ok = w.list_count + 1;
   w.pair_count = w.list_count + 2;
   w.cnt_n = reinterpret_cast<int*>(b + o + 256);
   w.cnt_m = w.cnt_n + nt;
+  w.off_m = w.cnt_m + mt;
   o += w.cnt_bytes;
   w.total = o;
   return w;
@@ -669,9 +671,10 @@ size_t cce_tile_max_bytes(int64_t n, int64_t v) {
   return (size_t)(nt * mt * cce::BM) * sizeof(float);
 }
 
-int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
-                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
-                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream_ptr) {
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+                  const int* n_valid, const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap,
+                  void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
+                  void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (n < 0 || d <= 0 || v <= 0) return fail("cce_fwd_tiles: bad sizes");
   if (d % 8 != 0) return fail("cce_fwd_tiles: D must be a multiple of 8 (16-byte TMA row pitch)");
@@ -682,10 +685,11 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   const bool pair = use_pairs();
   const int splits = lse_splits(nt, mt, d, pair, false);
   if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd_tiles: workspace too small");
-  CUtensorMap tmE, tmC, tmC128;
+  CUtensorMap tmE, tmC, tmC128, tmCg;
   if (!make_tmap(&tmE, E_c, n, d, cce::BM) || !make_tmap(&tmC, C_t, v, d, cce::BN) ||
-      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2))
+      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2) || !make_tmap(&tmCg, C_t, v, d, 1))
     return fail("cce_fwd_tiles: cuTensorMapEncodeTiled failed");
+  if (perm_padded && !pair) return fail("cce_fwd_tiles: row gathers need CTA pairs");
   cce::Params p{};
   p.n_total = (int)n;
   p.n_valid = n_valid;
@@ -703,8 +707,9 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   p.tile_max = tile_max;
+  p.perm = perm_padded;  // C_t rows gathered through perm (tile::gather4) instead of a sorted copy
   cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
-  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
+  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmCg, tmC128, stream)) return e;
   cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
       static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());
@@ -735,8 +740,6 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
   if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
-  CCE_CUDA(cudaMemsetAsync(w.keep, 0, w.keep_bytes, stream));
-  CCE_CUDA(cudaMemsetAsync(w.list_count, 0, 256, stream));
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
@@ -765,12 +768,15 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   // One pass over token tiles [g0, g0 + g): kept-tile list, S-hat of the kept tiles (KEPT), dE of
   // those token tiles (complete), dC (written by the first pass, accumulated by later ones).
   auto run_pass = [&](int g0, int g, bool primary, const int* run_if, bool last) -> int {
-    CCE_CUDA(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)g * mt * 4, stream));
-    CCE_CUDA(cudaMemsetAsync(w.cnt_n, 0, (size_t)(nt + mt) * 4, stream));
-    CCE_CUDA(cudaMemsetAsync(w.list_count + 3, 0, sizeof(int), stream));  // dE unit counter
-    cce::build_list_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if,
-                                                   primary ? 1 : 0, w.list, w.slot_of, w.cnt_n, w.cnt_m,
-                                                   w.list_count, w.ok, overflow, counters);
+    // kept list, slot_of (every entry written) and counts of this pass; counters reset inside
+    cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, g0, g, run_if, w.cnt_m);
+    CCE_CUDA(cudaGetLastError());
+    cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, g, (int)capacity_tiles, run_if, primary ? 1 : 0,
+                                                  w.off_m, w.cnt_n, w.list_count, w.ok, overflow,
+                                                  w.list_count + 3, counters);
+    CCE_CUDA(cudaGetLastError());
+    cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if, w.off_m,
+                                                  w.list, w.slot_of, w.cnt_n);
     CCE_CUDA(cudaGetLastError());
     const int* gate = primary ? w.ok : run_if;  // primary: only if every kept tile got a slot
     if (pair) {
@@ -1023,6 +1029,25 @@ int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, co
       row_map, n_valid, pos, static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap,
       (int)n, (int)d, de_fp32 ? static_cast<float*>(de) : nullptr,
       de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de));
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int cce_reduce_loss(const float* loss, const int64_t* targets, int64_t ignore_index, int64_t n,
+                    int reduction, float* out, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (reduction != 1 && reduction != 2) return fail("cce_reduce_loss: reduction must be 1 (sum) or 2 (mean)");
+  cce::reduce_loss_kernel<<<1, 1024, 0, stream>>>(loss, targets, ignore_index, (int)n, reduction, out);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int cce_upstream(const float* grad, const int64_t* targets, int64_t ignore_index, int64_t n, int reduction,
+                 float* up, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (reduction < 0 || reduction > 2) return fail("cce_upstream: reduction must be 0, 1 or 2");
+  if (n == 0) return 0;
+  cce::upstream_kernel<<<1, 1024, 0, stream>>>(grad, targets, ignore_index, (int)n, reduction, up);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }

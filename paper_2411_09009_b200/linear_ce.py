@@ -60,7 +60,6 @@ class _LinearCrossEntropy(torch.autograd.Function):
             from .vocab_parallel import gather_and_merge
 
             lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group)
-        valid = targets != ignore_index
         ctx.save_for_backward(e, c, targets, lse)
         ctx.cfg = (ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start)
         # paper ordering: the label term is applied apart from the filtered tiles and needs the
@@ -69,26 +68,13 @@ class _LinearCrossEntropy(torch.autograd.Function):
         ctx.correct = correct if ctx.split else None
         if reduction == "none":
             return loss
-        total = loss.sum()
-        if reduction == "sum":
-            return total
-        n_valid = valid.sum()
-        return torch.where(n_valid > 0, total / n_valid.clamp_min(1), torch.zeros_like(total))
+        return ops.reduce_loss(loss, targets, ignore_index, reduction)  # mean: 0 if nothing valid
 
     @staticmethod
     def backward(ctx, grad_out):
         e, c, targets, lse = ctx.saved_tensors
         ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start = ctx.cfg
-        valid = targets != ignore_index
-        g = grad_out.to(torch.float32)
-        if reduction == "none":
-            up = torch.where(valid, g, torch.zeros_like(g))
-        elif reduction == "sum":
-            up = valid.to(torch.float32) * g
-        else:  # mean over valid tokens (default_upstream, core.py:181-200)
-            n_valid = valid.sum().clamp_min(1).to(torch.float32)
-            up = valid.to(torch.float32) * (g / n_valid)
-        up = up.contiguous()
+        up = ops.upstream(grad_out, targets, ignore_index, reduction)  # default_upstream, core.py:181-200
         state, ctx.state = ctx.state, None
         split, correct, ctx.correct = ctx.split, ctx.correct, None
         if state is not None:

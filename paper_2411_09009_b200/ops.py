@@ -440,10 +440,11 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
         return lse_local, correct, state
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    fwd_gather = perm is not None and os.environ.get("CCE_FWD_GATHER") == "1"  # experiment knob
     ev = _ev_begin("fwd")
-    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), n, d, v,
-                                 float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
-                                 _p(tile_max), stream), "cce_fwd_tiles")
+    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c if fwd_gather else c_t), _p(perm_padded if fwd_gather else None),
+                                 _p(row_map), _p(n_valid), _p(pos), n, d, v, float(softcap or 0.0), _p(ws),
+                                 ws_bytes, _p(lse_local), _p(correct), _p(tile_max), stream), "cce_fwd_tiles")
     _ev_end("fwd", ev)
     LAUNCHES["count"] += 3
     return lse_local, correct, state
@@ -560,6 +561,30 @@ def _remember_kept(key, counters: torch.Tensor) -> None:
     hint[0].copy_(counters, non_blocking=True)
     hint[1] = torch.cuda.Event()
     hint[1].record()
+
+
+REDUCTIONS = {"none": 0, "sum": 1, "mean": 2}
+
+
+def reduce_loss(loss: torch.Tensor, targets: torch.Tensor, ignore_index: int, reduction: str) -> torch.Tensor:
+    """Scalar sum / mean-over-valid of per-row losses (0 at ignored rows); device-side."""
+    lib = _lib.load()
+    out = torch.empty((), dtype=torch.float32, device=loss.device)
+    _lib.check(lib.cce_reduce_loss(_p(loss), _p(targets), int(ignore_index), loss.shape[0],
+                                   REDUCTIONS[reduction], _p(out), _stream(loss.device)), "cce_reduce_loss")
+    LAUNCHES["count"] += 1
+    return out
+
+
+def upstream(grad: torch.Tensor, targets: torch.Tensor, ignore_index: int, reduction: str) -> torch.Tensor:
+    """dLoss/dloss_i for each row (default_upstream, core.py:181-200), 0 at ignored rows."""
+    lib = _lib.load()
+    g = grad.to(torch.float32).contiguous()
+    up = torch.empty(targets.shape[0], dtype=torch.float32, device=targets.device)
+    _lib.check(lib.cce_upstream(_p(g), _p(targets), int(ignore_index), targets.shape[0],
+                                REDUCTIONS[reduction], _p(up), _stream(targets.device)), "cce_upstream")
+    LAUNCHES["count"] += 1
+    return up
 
 
 def f32_to_bf16(x: torch.Tensor) -> torch.Tensor:

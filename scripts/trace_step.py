@@ -39,8 +39,9 @@ for ev in evs:
 tot_gap = sum(r[2] for r in rows if r[2] > 0)
 span = rows[-1][0] + rows[-1][1] - rows[0][0]
 print(f"span {span/1e3:.2f} ms for 2 steps, kernel-busy {sum(r[1] for r in rows)/1e3:.2f} ms, gaps {tot_gap/1e3:.2f} ms")
+full = os.environ.get("TRACE_ALL") == "1"
 for s, dur, gap, name in rows:
-    if dur > 50 or gap > 50:
+    if full or dur > 50 or gap > 50:
         print(f"  gap {gap:8.1f} us  dur {dur:9.1f} us  {name}")
 # CPU-side ops that took long (syncs)
 cpu = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CPU], key=lambda e: -e.cpu_time_total)[:15]
