@@ -96,6 +96,8 @@ struct GradParams {
   __nv_bfloat16* dc;       // [v][d]
   int accumulate;          // dC: add to the existing values (groups after the first)
   int de_accumulate;       // dE (fp32 only): add to the existing values (vocabulary groups)
+  const int2* list;        // dC: vocab-tile-major kept list (slot = index, .x = token tile), or nullptr
+  const int* off_m;        //     first slot of each vocab tile (its cnt_m slots are consecutive)
   int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
   int de_order;            // dE: 0 chunk-major units, 1 token-tile-major
   int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)

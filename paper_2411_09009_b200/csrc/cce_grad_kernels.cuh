@@ -62,6 +62,19 @@ __device__ __forceinline__ void for_each_kept(const int32_t* slot_of, int count,
   }
 }
 
+// Visit the kept tiles of one vocab tile through the vocab-tile-major kept list: slots
+// [off, off + cnt) in token-tile order; lanes fetch 32 entries at a time, every lane calls
+// f(local token tile, slot).
+template <typename F>
+__device__ __forceinline__ void for_each_listed(const int2* list, int off, int cnt, int n_base, F&& f) {
+  const int lane = threadIdx.x & 31;
+  for (int base = 0; base < cnt; base += 32) {
+    const int my = base + lane < cnt ? list[off + base + lane].x : 0;
+    const int k_end = min(32, cnt - base);
+    for (int k = 0; k < k_end; ++k) f(__shfl_sync(0xffffffffu, my, k) - n_base, off + base + k);
+  }
+}
+
 __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_bf16, const float* x,
                                             int lim) {
   // 32 consecutive values; lim = number of valid columns (multiple of 8)
@@ -390,7 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     for (int u = start; u < units; u += stride) {
       const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
-      for_each_kept(p.slot_of + m, G, p.mt, [&](int ln, int slot) {
+      auto tile = [&](int ln, int slot) {
         const int n = p.n_base + ln;
         for (int h = 0; h < 2; ++h) {
           RowGather rge;
@@ -426,7 +439,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           advance_stage(stage, phase, DC_STAGES);
         }
-      });
+      };
+      if (p.off_m != nullptr)  // contiguous slots of this vocab tile from the kept list
+        for_each_listed(p.list, p.off_m[m], p.cnt_m[m], p.n_base, tile);
+      else
+        for_each_kept(p.slot_of + m, G, p.mt, tile);
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // pairs: the leader issues for both CTAs

@@ -833,6 +833,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
+    q.list = w.list;
+    q.off_m = w.off_m;
     if (int e = launch_de(q, w.list_count + 3, w.shat, shat_rows, C_t, tmC64, stream)) return e;
     if (last && de_done_event)  // every dE write of this call is enqueued before this point
       CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
