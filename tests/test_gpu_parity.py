@@ -140,12 +140,13 @@ def test_unfiltered_matches_f64_oracle(cuda_device, cap, path):
     assert int(cnt[1]) == 0 and int(cnt[0]) == 3 * 12
 
 
-def test_uniform_classifier_and_margin(cuda_device):  # test_kernels.py:132-136, :354-371
+@pytest.mark.parametrize("path", PATHS)
+def test_uniform_classifier_and_margin(cuda_device, path):  # test_kernels.py:132-136, :354-371
     rng = np.random.default_rng(2)
     e = O.round_to_bf16(rng.standard_normal((24, 16)).astype(np.float32))
     c = np.zeros((16, 16), np.float32)
     x = rng.integers(0, 16, 24)
-    loss, lse, de, dc, _, _ = _run(e, c, x)
+    loss, lse, de, dc, _, _ = _run(e, c, x, path=path)
     assert np.allclose(loss, math.log(16), atol=1e-5)
     fde, fdc = O.naive_backward(e, c, x, O.default_upstream(x, "mean-over-valid"))
     assert O.rel_err(de, fde) < GRAD_TOL and O.rel_err(dc, fdc) < GRAD_TOL
@@ -153,7 +154,7 @@ def test_uniform_classifier_and_margin(cuda_device):  # test_kernels.py:132-136,
     e1 = np.ones((1, d), np.float32)
     c1 = np.zeros((v, d), np.float32)
     c1[13] = 10.0 / d
-    loss, _, _, _, _, _ = _run(e1, c1, np.array([13]))
+    loss, _, _, _, _, _ = _run(e1, c1, np.array([13]), path=path)
     assert loss[0] == pytest.approx(math.log(1.0 + (v - 1) * math.exp(-10.0)), abs=1e-4)
 
 
@@ -511,3 +512,26 @@ def test_paper_ordering_autograd_skips_label_only_tiles(cuda_device):
     fde, fdc = O.naive_backward(e0.float().cpu().numpy(), c0.float().cpu().numpy(), t.cpu().numpy(),
                                 O.default_upstream(t.cpu().numpy(), "mean-over-valid"))
     assert O.rel_err(out[False][1], fde) < 3e-2 and O.rel_err(out[False][2], fdc) < 3e-2
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("d", [8, 24, 200])
+def test_hidden_sizes_not_multiple_of_64(cuda_device, path, d):
+    """D % 64 != 0: 2-D TMA boxes instead of the 3-D atom views, partial last K-block."""
+    rng = np.random.default_rng(d)
+    n, v = 257, 3001
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 1.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::13] = -1
+    loss, lse, de, dc, cnt, perm = _run(e, c, x, path=path)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    assert _loss_err(loss, nl) < LOSS_TOL
+    ce, cl, idx = O.filter_ignored(e, x)
+    up = O.default_upstream(x, "mean-over-valid")
+    rde_c, rdc, st = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up[idx], perm=perm,
+                                            return_stats=True)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
+    assert int(cnt[1]) == st["skipped_epsilon"]
