@@ -535,3 +535,28 @@ def test_hidden_sizes_not_multiple_of_64(cuda_device, path, d):
     rde[idx] = rde_c
     assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
     assert int(cnt[1]) == st["skipped_epsilon"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 127, 129])
+@pytest.mark.parametrize("low", [False, True])
+def test_tiny_batches_through_public_api(cuda_device, n, low):
+    """Empty batches (kernels.py:275-276, :380-381), single tokens and ragged token tiles."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    rng = np.random.default_rng(n + 7)
+    d, v = 64, 700
+    e_np = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c_np = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    e = torch.from_numpy(e_np).cuda().bfloat16().requires_grad_(True)
+    c = torch.from_numpy(c_np).cuda().bfloat16().requires_grad_(True)
+    loss = linear_cross_entropy(e, c, torch.from_numpy(x).cuda(), low_memory=low)
+    loss.backward()
+    if n == 0:
+        assert loss.item() == 0.0 and e.grad.shape == (0, d) and torch.all(c.grad == 0)
+        return
+    nl, _, _ = O.naive_forward(e_np, c_np, x)
+    assert loss.item() == pytest.approx(float(nl.mean()), rel=1e-3, abs=1e-3)
+    de, dc = O.naive_backward(e_np, c_np, x, O.default_upstream(x, "mean-over-valid"))
+    assert O.rel_err(e.grad.float().cpu().numpy(), de) < 2e-2
+    assert O.rel_err(c.grad.float().cpu().numpy(), dc) < 2e-2
