@@ -332,13 +332,31 @@ int launch_de_t(const cce::GradParams& q, int units, const void* shat, int64_t s
 int launch_de(cce::GradParams q, int* sched_ctr, const void* shat, int64_t shat_rows, const void* C,
               const CUtensorMap& tmCg, cudaStream_t stream) {
   static int cfg[5] = {-1, 0, 0, 0, 64};
+  static bool fixed = false;
   if (cfg[0] < 0) {
     cfg[0] = 1;
-    if (const char* e = getenv("CCE_DE"))
+    if (const char* e = getenv("CCE_DE")) {
       sscanf(e, "%d,%d,%d,%d,%d", &cfg[0], &cfg[1], &cfg[2], &cfg[3], &cfg[4]);
+      fixed = true;
+    }
   }
-  const int ch = cfg[0] == 2 ? 2 : 1;
-  const int kv = (cfg[4] == 32 && q.perm == nullptr) ? 32 : 64;  // row gathers need 64-wide boxes
+  int ch = cfg[0] == 2 ? 2 : 1;
+  int kv = cfg[4];
+  if (!fixed) {
+    // measured (profiles/r1/de_variants_s46*): one 512-column accumulator fed by 32-row stages
+    // (less operand traffic per flop) wins once there are enough units to balance the grid
+    // (Gemma-2-9B: 11.5 vs 13.1 ms); with few units (Gemma-2-2B: 288) the double-buffered
+    // 256-column form wins (1.65 vs 2.05 ms)
+    const int units512 = q.g * ((q.ndc + 1) / 2);
+    if (units512 >= 8 * num_sms()) {
+      ch = 2;
+      kv = 32;
+    } else {
+      ch = 1;
+      kv = 64;
+    }
+  }
+  kv = (kv == 32 && q.perm == nullptr) ? 32 : 64;  // row gathers need 64-wide boxes
   q.de_order = cfg[1];
   q.sched = cfg[2] ? sched_ctr : nullptr;
   q.prefetch = cfg[3];
