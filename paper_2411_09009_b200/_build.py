@@ -33,21 +33,31 @@ def up_to_date() -> bool:
     return all(src.stat().st_mtime <= t for src in SOURCES + HEADERS if src.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Build libcce_b200.so (or, for A/B experiments, a variant with extra -D defines into `out`,
+    selected at run time with CCE_LIB=<file name>)."""
+    lib = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(CSRC), "-I", str(PKG.parent / "include"),
-           "-o", str(tmp), *map(str, SOURCES)]
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in (defines or [])], "-I", str(CSRC),
+           "-I", str(PKG.parent / "include"), "-o", str(tmp), *map(str, SOURCES)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    # python -m paper_2411_09009_b200._build [--force] [--variant NAME DEFINE=VALUE ...]
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        print(build(force=True, verbose=True, defines=defs, out=PKG / f"libcce_b200_{name}.so"))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
+        print(LIB)

@@ -7,9 +7,13 @@ load, every op raises.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "libcce_b200.so"
+# CCE_LIB selects another in-tree build of the same ABI (A/B experiments: `_build.py --variant`)
+if os.environ.get("CCE_LIB"):
+    _LIB_PATH = Path(__file__).resolve().parent / os.environ["CCE_LIB"]
 _lib = None
 
 c_void_p = ctypes.c_void_p

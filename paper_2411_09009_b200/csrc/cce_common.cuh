@@ -17,7 +17,10 @@ constexpr int B_BYTES = BN * BK * 2;      // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_THREADS = 192;          // warp0 TMA, warp1 MMA, warps 2..5 epilogue
 constexpr int LSE_STAGES = 4;
-constexpr int LSE_STAGES_PAIR = 6;
+#ifndef CCE_LSE_STAGES_PAIR
+#define CCE_LSE_STAGES_PAIR 6
+#endif
+constexpr int LSE_STAGES_PAIR = CCE_LSE_STAGES_PAIR;
 constexpr int PAIR_STAGE_BYTES = A_BYTES + (BN / 2) * BK * 2;  // 128 E rows + 128 of 256 C rows
 constexpr int TMEM_COLS = 512;
 constexpr int DCH = 256;                  // D columns per gradient chunk (MMA N of dE / dC)

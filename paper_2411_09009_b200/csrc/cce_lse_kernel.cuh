@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else
               mbar_arrive_cluster(&full[stage], 0);
             const uint32_t lb = leader_addr(&full[stage]);
-            tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
+tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
             if (!gather_c) tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * (BN / 2));
           } else {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
