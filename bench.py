@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--no-filter", action="store_true")
+    ap.add_argument("--force-dist", action="store_true", help="init the process group even for 1 rank")
     ap.add_argument("--paper-order", action="store_true",
                     help="exempt_label_tiles=False: PAPER Alg. 3 filter ordering (not the reference's)")
     ap.add_argument("--low-memory", action="store_true",
@@ -209,7 +210,9 @@ def main():
     dev = torch.device("cuda", 0 if same_dev else local)
     torch.cuda.set_device(dev)
     group = None
-    if world > 1:
+    # --force-dist: the distributed (vocab-parallel) path even for one rank -- exercises the NCCL
+    # collectives on a single GPU (functional check)
+    if world > 1 or args.force_dist:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -227,7 +230,8 @@ def main():
     gen.manual_seed(0 + (rank if token_mode else 0))
     e = torch.randn(n, d, device=dev, generator=gen).to(torch.bfloat16)
     gen.manual_seed(1)
-    if world > 1 and not token_mode:
+    dist_vocab = (world > 1 or args.force_dist) and not token_mode
+    if dist_vocab:
         v0, v1 = shard_range(v, rank, world)
         c_full_rows = v1 - v0
         # deterministic shard of the same global classifier: generate only this shard's rows
@@ -247,7 +251,7 @@ def main():
 
     kw = dict(reduction="mean", filter_eps=eps, vocab_sorting=sort, softcap=cap or None,
               low_memory=args.low_memory, exempt_label_tiles=not args.paper_order)
-    if world > 1 and not token_mode:
+    if dist_vocab:
         kw.update(process_group=group, vocab_start=v0)
 
     def step(ei, ci, ti):
@@ -258,7 +262,7 @@ def main():
         return loss
 
     def barrier():
-        if world > 1:
+        if group is not None:
             dist.barrier()
 
     # ---- memory (instrument.py:3-10 definition: transients only; inputs E, C, targets and the
@@ -465,7 +469,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if group is not None:
         dist.destroy_process_group()
 
 

@@ -466,10 +466,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
+      // the next unit's kept count is loaded one unit ahead (units are short: ~8 us at Gemma-2B)
+      int cnt = start < units ? p.cnt_m[(start >> 1) / p.ndc] : 0;
       for (int u = start; u < units; u += stride, ++t) {
-        const int m = (u >> 1) / p.ndc;
+        const int un = u + stride;
+        const int cnt_next = un < units ? p.cnt_m[(un >> 1) / p.ndc] : 0;
         const int buf = t & 1;
-        const int ksteps = 2 * p.cnt_m[m];
+        const int ksteps = 2 * cnt;
+        cnt = cnt_next;
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * DCH;
@@ -512,11 +516,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int u = start; u < units; u += stride, ++t) {
       const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
       const int buf = t & 1;
-      mbar_wait(&acc_full[buf], (t >> 1) & 1);
-      tc_fence_after();
+      // per-unit loads issued before the wait so their latency hides behind it
       const bool has = p.cnt_m[m] > 0;
       const int vpos = m * BN + vh * 128 + row;
       const int my_vrow = vpos < p.v ? (p.perm_store ? p.perm_store[vpos] : vpos) : -1;
+      mbar_wait(&acc_full[buf], (t >> 1) & 1);
+      tc_fence_after();
       if (has || !p.accumulate) {
 #pragma unroll 1
         for (int c = 0; c < DCH / 64; ++c) {

@@ -19,6 +19,8 @@ for s in "$@"; do
           >> $out/multirank.log 2>&1; echo "exit $mode $?" >> $out/multirank.log; done ;;
     benchpaper) for a in "" "--low-memory" "--config gemma2-9b"; do
         timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --paper-order $a >> $out/benchpaper.log 2>&1; echo "exit $a $?" >> $out/benchpaper.log; done ;;
+    nccl1) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+        --master-port 29519 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu-baseline --force-dist > $out/nccl1.log 2>&1; echo "exit $?" >> $out/nccl1.log ;;
     benchvar) for a in "--no-sort" "--no-filter" "--sigma 2" "--config gpt2" ; do
         timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e $a >> $out/benchvar.log 2>&1; echo "exit $a $?" >> $out/benchvar.log; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \

@@ -90,3 +90,35 @@ def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap, s
     assert np.array_equal(res[0][2], res[1][2])  # every rank holds the same all-reduced dE
     dc = np.concatenate([r[3] for r in res])
     assert O.rel_err(dc, fdc) < tol
+
+
+@pytest.mark.parametrize("low", [False, True])
+def test_single_rank_nccl_group_matches_no_group(cuda_device, low):
+    """The vocab-parallel path through real NCCL collectives (a world of one: NCCL refuses two
+    ranks on one device): all_gather_into_tensor of the LSE partials, the dE all-reduce on a side
+    stream overlapping dC.  Results must equal the single-GPU path bit for bit."""
+    import torch.distributed as dist
+
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    store = dist.TCPStore("127.0.0.1", _free_port(), 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        e_np, c_np, x_np = _inputs(700, 128, 6001)
+        out = []
+        for group in (None, dist.group.WORLD):
+            e = torch.from_numpy(e_np).cuda().bfloat16().requires_grad_(True)
+            c = torch.from_numpy(c_np).cuda().bfloat16().requires_grad_(True)
+            loss = linear_cross_entropy(e, c, torch.from_numpy(x_np).cuda(), process_group=group,
+                                        low_memory=low)
+            loss.backward()
+            torch.cuda.synchronize()
+            out.append((loss.detach().cpu(), e.grad.cpu(), c.grad.cpu()))
+        assert torch.equal(out[0][0], out[1][0])
+        assert torch.equal(out[0][2], out[1][2])
+        # dE: the group path all-reduces fp32 partials, then rounds once (no-group rounds in-kernel)
+        assert O.rel_err(out[1][1].float().numpy(), out[0][1].float().numpy()) < 1e-2
+    finally:
+        dist.destroy_process_group()
