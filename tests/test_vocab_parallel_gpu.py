@@ -122,3 +122,52 @@ def test_single_rank_nccl_group_matches_no_group(cuda_device, low):
         assert O.rel_err(out[1][1].float().numpy(), out[0][1].float().numpy()) < 1e-2
     finally:
         dist.destroy_process_group()
+
+
+def _token_worker(rank, world, port, q, n, d, v):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_09009_b200.vocab_parallel import token_parallel_loss
+
+        e_np, c_np, x_np = _inputs(n, d, v)
+        rows = slice(rank * n // world, (rank + 1) * n // world)
+        e = torch.from_numpy(e_np[rows]).cuda().bfloat16().requires_grad_(True)
+        c = torch.from_numpy(c_np).cuda().bfloat16().requires_grad_(True)
+        loss = token_parallel_loss(e, c, torch.from_numpy(x_np[rows]).cuda(), ignore_index=-100)
+        loss.backward()
+        torch.cuda.synchronize()
+        q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_token_parallel_two_ranks(cuda_device):
+    """Token-sharded data parallelism: no communication inside the loss except the valid-count
+    scalar; the per-rank losses sum to the global mean, each rank's dE rows equal the full batch's,
+    and the per-rank dC (the caller's DDP would all-reduce them) sum to the full dC."""
+    import torch.multiprocessing as mp
+
+    world, n, d, v = 2, 640, 128, 5001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_token_worker, args=(r, world, port, q, n, d, v)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    e_np, c_np, x_np = _inputs(n, d, v)
+    xo = np.where(x_np == -100, -1, x_np)
+    nl, _, _ = O.naive_forward(e_np, c_np, xo)
+    ref = float(nl[xo != -1].mean())
+    assert abs(sum(r[1] for r in res) - ref) <= 1e-3 * abs(ref)
+    fde, fdc = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"))
+    de = np.concatenate([r[2] for r in res])
+    assert O.rel_err(de, fde) < 2e-2
+    assert O.rel_err(res[0][3] + res[1][3], fdc) < 2e-2
