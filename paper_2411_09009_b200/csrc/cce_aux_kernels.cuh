@@ -451,6 +451,89 @@ __global__ void list_fill_kernel(const uint8_t* __restrict__ keep, int nt, int m
   }
 }
 
+// Fallback passes (token-tile groups after an overflow, gated on run_if): the whole kept list of
+// the group -- counts, offsets, list / slot_of / cnt_n, and the CTA-pair list -- in ONE block, so
+// a pass that does not run costs one launch here instead of four.
+__global__ void __launch_bounds__(1024) list_single_kernel(
+    const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g, int capacity, const int* run_if,
+    int* __restrict__ cnt_m, int* __restrict__ off_m, int2* __restrict__ list, int32_t* __restrict__ slot_of,
+    int* __restrict__ cnt_n, int* __restrict__ list_count, int* __restrict__ sched, int2* __restrict__ pairs,
+    int* __restrict__ pair_count) {
+  if (run_if != nullptr && *run_if == 0) return;
+  constexpr int T = 1024, W = T / 32;
+  __shared__ int s_a[W], s_b[W];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < g; i += T) cnt_n[i] = 0;
+  if (threadIdx.x == 0 && sched) *sched = 0;
+  for (int m = wid; m < mt; m += W) {  // kept count per vocab tile
+    const uint8_t* row = keep + (size_t)m * nt + n_lo;
+    int c = 0;
+    for (int b = 0; b < g; b += 32) c += __popc(__ballot_sync(0xffffffffu, b + lane < g && row[b + lane]));
+    if (lane == 0) cnt_m[m] = c;
+  }
+  __syncthreads();
+  // exclusive scans of the counts (slots) and of the pair counts ((c + 1) / 2)
+  const int per = (mt + T - 1) / T;
+  const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
+  int la = 0, lb = 0;
+  for (int m = m0; m < m1; ++m) {
+    la += cnt_m[m];
+    lb += (cnt_m[m] + 1) / 2;
+  }
+  int ia = la, ib = lb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += ya; ib += yb; }
+  }
+  if (lane == 31) { s_a[wid] = ia; s_b[wid] = ib; }
+  __syncthreads();
+  if (wid == 0) {
+    int xa = s_a[lane], xb = s_b[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+      if (lane >= o) { xa += ya; xb += yb; }
+    }
+    s_a[lane] = xa;
+    s_b[lane] = xb;
+  }
+  __syncthreads();
+  int ra = (wid ? s_a[wid - 1] : 0) + ia - la, rb = (wid ? s_b[wid - 1] : 0) + ib - lb;
+  for (int m = m0; m < m1; ++m) {
+    const int c = cnt_m[m];
+    off_m[m] = ra;
+    for (int j = 0; 2 * j < c; ++j) pairs[rb + j] = make_int2(ra + 2 * j, min(2, c - 2 * j));
+    ra += c;
+    rb += (c + 1) / 2;
+  }
+  if (threadIdx.x == T - 1) {
+    *list_count = ra;
+    *pair_count = rb;
+  }
+  __syncthreads();
+  for (int m = wid; m < mt; m += W) {  // slots in vocab-tile-major, token-tile order
+    const uint8_t* row = keep + (size_t)m * nt + n_lo;
+    int slot0 = off_m[m];
+    for (int b = 0; b < g; b += 32) {
+      const int ln = b + lane;
+      const bool f = ln < g && row[ln];
+      const uint32_t bal = __ballot_sync(0xffffffffu, f);
+      const int slot = slot0 + __popc(bal & ((1u << lane) - 1));
+      if (ln < g) {
+        int so = -1;
+        if (f && slot < capacity) {
+          list[slot] = make_int2(n_lo + ln, m);
+          so = slot;
+          atomicAdd(&cnt_n[ln], 1);
+        }
+        slot_of[(size_t)ln * mt + m] = so;
+      }
+      slot0 += __popc(bal);
+    }
+  }
+}
+
 // One block: CTA-pair work list of the KEPT pass.  The kept tiles of vocab tile m hold the
 // consecutive slots [off_m, off_m + cnt_m) (build_list_kernel); pair j of m takes slots
 // off_m + 2j and, if it exists, off_m + 2j + 1.  pairs[k] = (first slot, tiles in the pair).

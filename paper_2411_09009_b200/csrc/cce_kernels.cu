@@ -786,21 +786,30 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   // One pass over token tiles [g0, g0 + g): kept-tile list, S-hat of the kept tiles (KEPT), dE of
   // those token tiles (complete), dC (written by the first pass, accumulated by later ones).
   auto run_pass = [&](int g0, int g, bool primary, const int* run_if, bool last) -> int {
-    // kept list, slot_of (every entry written) and counts of this pass; counters reset inside
-    cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, g0, g, run_if, w.cnt_m);
-    CCE_CUDA(cudaGetLastError());
-    cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, g, (int)capacity_tiles, run_if, primary ? 1 : 0,
-                                                  w.off_m, w.cnt_n, w.list_count, w.ok, overflow,
-                                                  w.list_count + 3, counters);
-    CCE_CUDA(cudaGetLastError());
-    cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if, w.off_m,
-                                                  w.list, w.slot_of, w.cnt_n);
-    CCE_CUDA(cudaGetLastError());
-    const int* gate = primary ? w.ok : run_if;  // primary: only if every kept tile got a slot
-    if (pair) {
-      cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, gate, w.pairs, w.pair_count);
+    // kept list, slot_of (every entry written), counts and pairs of this pass; counters reset
+    // inside.  The whole-batch pass uses three parallel kernels (+ pairs); fallback passes one
+    // block (they usually do not run, and then cost one launch)
+    if (primary) {
+      cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, g0, g, run_if, w.cnt_m);
+      CCE_CUDA(cudaGetLastError());
+      cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, g, (int)capacity_tiles, run_if, 1, w.off_m,
+                                                    w.cnt_n, w.list_count, w.ok, overflow, w.list_count + 3,
+                                                    counters);
+      CCE_CUDA(cudaGetLastError());
+      cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if, w.off_m,
+                                                    w.list, w.slot_of, w.cnt_n);
+      CCE_CUDA(cudaGetLastError());
+      if (pair) {
+        cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, w.ok, w.pairs, w.pair_count);
+        CCE_CUDA(cudaGetLastError());
+      }
+    } else {
+      cce::list_single_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if,
+                                                      w.cnt_m, w.off_m, w.list, w.slot_of, w.cnt_n,
+                                                      w.list_count, w.list_count + 3, w.pairs, w.pair_count);
       CCE_CUDA(cudaGetLastError());
     }
+    const int* gate = primary ? w.ok : run_if;  // primary: only if every kept tile got a slot
     cce::Params p{};
     p.n_total = (int)n;
     p.n_valid = n_valid;

@@ -542,7 +542,13 @@ def shat_capacity(key, nt: int, mt: int) -> int:
     return min(max(cap, mt), nt * mt)
 
 
+def _capturing() -> bool:
+    return torch.cuda.is_current_stream_capturing()
+
+
 def _harvest(hint) -> None:
+    if _capturing():  # no event queries inside a CUDA-graph capture: use what is already known
+        return
     if hint[1] is not None and hint[1].query():
         hint[2] = int(hint[0][0])
         hint[1] = None
@@ -551,6 +557,8 @@ def _harvest(hint) -> None:
 def _remember_kept(key, counters: torch.Tensor) -> None:
     """Queue an asynchronous copy of this call's kept-tile count (read by a later call once it
     has landed; the CPU usually runs ahead of the GPU, so the value may be a few calls old)."""
+    if _capturing():  # a graph replays with the capacity fixed at capture time
+        return
     hint = _KEPT_HINT.get(key)
     if hint is None:
         hint = [torch.zeros(3, dtype=torch.int64).pin_memory(), None, None]

@@ -1,0 +1,79 @@
+"""Per-kernel breakdown of one default training step at the Gemma-2-2B head (device times from a
+torch.profiler trace of 3 steps, median per kernel), with algorithmic flops / bytes per kernel and
+the fraction of the measured peaks (MEASURED_PEAKS.json).  Writes markdown to stdout."""
+import json, math, os, statistics, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from torch.profiler import profile, ProfilerActivity
+from paper_2411_09009_b200 import linear_cross_entropy, ops
+
+N, D, V = 8192, 2304, 256000
+dev = torch.device("cuda")
+g = torch.Generator(device=dev).manual_seed(0)
+e = torch.randn(N, D, device=dev, generator=g).bfloat16().requires_grad_(True)
+c = (torch.randn(V, D, device=dev, generator=g) / math.sqrt(D)).bfloat16().requires_grad_(True)
+t = torch.randint(0, V, (N,), device=dev, generator=g)
+
+
+def step():
+    e.grad = c.grad = None
+    linear_cross_entropy(e, c, t).backward()
+
+
+for _ in range(4):
+    step()
+torch.cuda.synchronize()
+steps = 3
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+kept = int(ops.LAST_COUNTERS["counters"][0])
+evs = sorted([x for x in prof.events() if x.device_type == torch.autograd.DeviceType.CUDA],
+             key=lambda x: x.time_range.start)
+span = (evs[-1].time_range.end - evs[0].time_range.start) / steps / 1e3
+per = {}
+for x in evs:
+    per.setdefault(x.name, []).append((x.time_range.end - x.time_range.start) / 1e3)
+peaks = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json"))) \
+    if os.path.exists(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")) else \
+    {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+tile = 128 * 256
+work = {  # name fragment -> (flops, bytes) per step (algorithmic)
+    "cce_lse_kernel<0": (2.0 * N * V * D, None),
+    "cce_lse_kernel<2": (2.0 * D * kept * tile, None),
+    "cce_de_kernel": (2.0 * D * kept * tile, None),
+    "cce_dc_kernel": (2.0 * D * kept * tile, None),
+    "sort_key_kernel": (None, V * D * 2.0),
+    "gather_rows_kernel": (None, 2 * (V + N) * D * 2.0),
+    "decide_tiles_kernel": (None, (N // 128) * (V // 256) * 512.0),
+}
+rows = []
+for name, ds in per.items():
+    ms = sum(ds) / steps
+    short = name.split("(")[0].replace("void ", "").replace("cce::", "")
+    flops = byts = None
+    for k, (f, b) in work.items():
+        if k in name:
+            flops, byts = f, b
+    rows.append((ms, short, flops, byts))
+rows.sort(reverse=True)
+print(f"Gemma-2-2B head, default path, {steps} steps: {span:.2f} ms/step, kept tiles {kept} of "
+      f"{(N // 128) * (V // 256)}; peaks: {peaks['bf16_tflops']} TFLOP/s bf16, {peaks['hbm_gbs']} GB/s\n")
+print("| kernel | ms/step | share | achieved | of peak |")
+print("|---|---|---|---|---|")
+busy = 0.0
+for ms, short, f, b in rows:
+    busy += ms
+    if ms < 0.004:
+        continue
+    ach = frac = ""
+    if f:
+        ach = f"{f / (ms / 1e3) / 1e12:.0f} TFLOP/s"
+        frac = f"{f / (ms / 1e3) / 1e12 / peaks['bf16_tflops']:.0%}"
+    elif b:
+        ach = f"{b / (ms / 1e3) / 1e9:.0f} GB/s"
+        frac = f"{b / (ms / 1e3) / 1e9 / peaks['hbm_gbs']:.0%}"
+    print(f"| `{short[:60]}` | {ms:.3f} | {ms / span:.1%} | {ach} | {frac} |")
+print(f"| (all kernels) | {busy:.3f} | {busy / span:.1%} | | |")
+print(f"| (gaps between kernels) | {span - busy:.3f} | {(span - busy) / span:.1%} | | |")
