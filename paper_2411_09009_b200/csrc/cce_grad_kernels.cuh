@@ -368,11 +368,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   const GradParams p) {
   constexpr int B_BYTES = DC_B_BYTES / CG;  // this CTA's part of E[64 tok][256 d]
   constexpr int SBYTES = DC_A_BYTES + B_BYTES;
+  // same smem footprint for both forms: pairs (32 KB stages) get 6 stages instead of 4
+  constexpr int STAGES = (DC_STAGES * DC_STAGE_BYTES) / SBYTES;
+  constexpr int DC_STAGES = STAGES;
+  constexpr int DC_STAGE_BYTES = SBYTES;
   if (skip_launch(p.run_if)) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* stg = smem + DC_STAGES * DC_STAGE_BYTES;
+  uint8_t* stg = smem + cce::DC_STAGES * cce::DC_STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + DC_STG_BYTES);
   uint64_t* empty = full + DC_STAGES;
   uint64_t* acc_full = empty + DC_STAGES;
