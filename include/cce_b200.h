@@ -107,9 +107,7 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * vocab sorting, else C).  pos[i] (per ORIGINAL row, cce_bwd_prep) is the label position in tile
  * order or -1.  lse_local / correct are per ORIGINAL row (undefined / 0 at ignored rows).
  * tile_max: [ceil(n/128)][ceil(v/256)][128] fp32 (cce_tile_max_bytes), the max raw logit of
- * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).  perm_padded: NULL
- * when C_t is already in tile order; else C_t is the classifier in natural order and its rows are
- * gathered through perm_padded (TMA tile::gather4, CTA pairs only).
+ * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).
  *
  * cce_bwd_kept: the backward from tile_max.  Keeps tile (n, m) iff its upstream is not all zero
  * and it holds a label or some S >= eps (the same strict test as cce_bwd, eps > 0 required);
@@ -123,10 +121,9 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * call has been enqueued, before the dC pass: a vocab-parallel caller all-reduces dE on another
  * stream while dC runs. */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
-int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
-                  const int* n_valid, const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap,
-                  void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
-                  void* stream);
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream);
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles);
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,

@@ -689,10 +689,9 @@ size_t cce_tile_max_bytes(int64_t n, int64_t v) {
   return (size_t)(nt * mt * cce::BM) * sizeof(float);
 }
 
-int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
-                  const int* n_valid, const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap,
-                  void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
-                  void* stream_ptr) {
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (n < 0 || d <= 0 || v <= 0) return fail("cce_fwd_tiles: bad sizes");
   if (d % 8 != 0) return fail("cce_fwd_tiles: D must be a multiple of 8 (16-byte TMA row pitch)");
@@ -703,11 +702,10 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, 
   const bool pair = use_pairs();
   const int splits = lse_splits(nt, mt, d, pair, false);
   if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd_tiles: workspace too small");
-  CUtensorMap tmE, tmC, tmC128, tmCg;
+  CUtensorMap tmE, tmC, tmC128;
   if (!make_tmap(&tmE, E_c, n, d, cce::BM) || !make_tmap(&tmC, C_t, v, d, cce::BN) ||
-      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2) || !make_tmap(&tmCg, C_t, v, d, 1))
+      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2))
     return fail("cce_fwd_tiles: cuTensorMapEncodeTiled failed");
-  if (perm_padded && !pair) return fail("cce_fwd_tiles: row gathers need CTA pairs");
   cce::Params p{};
   p.n_total = (int)n;
   p.n_valid = n_valid;
@@ -725,9 +723,8 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* perm_padded, 
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   p.tile_max = tile_max;
-  p.perm = perm_padded;  // C_t rows gathered through perm (tile::gather4) instead of a sorted copy
   cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
-  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmCg, tmC128, stream)) return e;
+  if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
   cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
       static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());

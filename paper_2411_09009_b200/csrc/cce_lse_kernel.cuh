@@ -169,8 +169,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           cur_n = t.n;
         }
         rgc.load(p.perm, t.m * BN, BN);
-      } else {
-        rgc.load(p.perm, t.m * BN + rank * (BN / 2), BN / 2);  // this CTA's half of the C tile
       }
       for (int kb = 0; kb < p.num_kb; ++kb) {
         uint8_t* sa = smem + stage * SBYTES;
@@ -184,20 +182,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_arrive_cluster(&full[stage], 0);
             const uint32_t lb = leader_addr(&full[stage]);
 tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
-            if (!gather_c) tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * (BN / 2));
+            tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * (BN / 2));
           } else {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           }
         }
         __syncwarp();
-        if (CG == 2 && gather_c) {  // C rows through perm: each lane its 4-row groups
-          const uint32_t lb = leader_addr(&full[stage]);
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            if (j < rgc.groups)
-              tma_gather4_pair(&tmCg, lb, sa + A_BYTES + (lane + 32 * j) * 512, kb * BK, rgc.idx[j].x,
-                               rgc.idx[j].y, rgc.idx[j].z, rgc.idx[j].w);
-        }
         if (CG == 1) {
           load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, t.n * BM);
           load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);

@@ -172,17 +172,6 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* m, uint32_t 
       : "memory");
 }
 
-// Pair row gather: four rows into this CTA's smem, completion on the leader's barrier.
-__device__ __forceinline__ void tma_gather4_pair(const CUtensorMap* m, uint32_t leader_bar, void* dst,
-                                                 int32_t c0, int32_t r0, int32_t r1, int32_t r2,
-                                                 int32_t r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
-
 // ----------------------------------------------------------------------------------------
 // tcgen05: TMEM allocation, MMA, commit, loads
 // ----------------------------------------------------------------------------------------

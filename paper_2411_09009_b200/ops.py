@@ -440,11 +440,10 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
         return lse_local, correct, state
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
-    fwd_gather = perm is not None and os.environ.get("CCE_FWD_GATHER") == "1"  # experiment knob
     ev = _ev_begin("fwd")
-    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c if fwd_gather else c_t), _p(perm_padded if fwd_gather else None),
-                                 _p(row_map), _p(n_valid), _p(pos), n, d, v, float(softcap or 0.0), _p(ws),
-                                 ws_bytes, _p(lse_local), _p(correct), _p(tile_max), stream), "cce_fwd_tiles")
+    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), n, d, v,
+                                 float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
+                                 _p(tile_max), stream), "cce_fwd_tiles")
     _ev_end("fwd", ev)
     LAUNCHES["count"] += 3
     return lse_local, correct, state
