@@ -108,10 +108,20 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * order or -1.  lse_local / correct are per ORIGINAL row (undefined / 0 at ignored rows).
  * tile_max: [ceil(n/128)][ceil(v/256)][128] fp32 (cce_tile_max_bytes), the max raw logit of
  * each compact row in each tile.  ws as cce_fwd (cce_fwd_workspace_bytes).
+ * Label tiles (optional, lab_buf != NULL): a tile holding some row's label is always kept by the
+ * backward (kernels.py:447-455), so the forward stores it -- fp16 of z' - z'max(row), <= 0 and
+ * exact near the row max -- in one of lab_capacity 64 KiB slots of lab_buf; lab_slot
+ * [ceil(n/128)][ceil(v/256)] (-1 = none) and lab_list [lab_capacity] (token tile, vocab tile) int2
+ * map them, *lab_count counts the slots handed out (tiles past the capacity are simply
+ * recomputed).  lab_buf is the head of the S-hat buffer later passed to cce_bwd_kept.
  *
  * cce_bwd_kept: the backward from tile_max.  Keeps tile (n, m) iff its upstream is not all zero
  * and it holds a label or some S >= eps (the same strict test as cce_bwd, eps > 0 required);
- * recomputes S-hat for the kept tiles only, then the dE / dC passes of cce_bwd.  dC rows land
+ * kept tiles stored by the forward become S-hat in place, the other kept tiles are recomputed,
+ * then the dE / dC passes of cce_bwd.  shat: [lab_capacity + capacity_tiles][128][256] bf16, the
+ * label region first (lab_slot / lab_list / lab_count from cce_fwd_tiles, or lab_slot NULL: none).
+ * stats (optional, 2 ints): label tiles stored, tiles the whole-batch pass recomputes (sizing
+ * hints for the next call).  dC rows land
  * through perm_padded (NULL = tile order is C's order).  capacity_tiles >= ceil(v/256) S-hat
  * slots: if the whole batch keeps more tiles than that, *overflow = 1, the whole-batch pass is
  * skipped on the device and token-tile groups sized for the worst case run instead (each kernel
@@ -123,14 +133,17 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
-                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream);
-size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles);
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
+                  int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream);
+size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
+                                    int64_t lab_capacity);
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
-                 int label_split, int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out,
-                 int de_fp32, void* dc, unsigned long long* counters, int* overflow, void* de_done_event,
-                 void* stream);
+                 int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
+                 const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
+                 void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
+                 int* stats, void* de_done_event, void* stream);
 
 /* ---- low-memory backward: vocabulary groups (low_memory=True) ----
  * lse_backward over groups of `group_vtiles` vocab tiles in tile order: per group, the group's

@@ -256,7 +256,8 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
         # forward over the backward's tiles (compacted rows, vocab order fixed by the mean logits
         # of the valid rows), recording per-row tile maxima: the backward then recomputes only
         # the tiles it keeps
-        lse_l, corr, state = ops.forward_tiles(E, C, X, IGNORE_INDEX, vocab_sorting=options.vocab_sorting)
+        lse_l, corr, state = ops.forward_tiles(E, C, X, IGNORE_INDEX, vocab_sorting=options.vocab_sorting,
+                                               eps=options.epsilon)
         mean = state.mean_logits
     else:
         lse_l, corr = ops.forward_local(E, C, X, IGNORE_INDEX)

@@ -344,141 +344,50 @@ __device__ __forceinline__ T block_sum(T v, T* s_tmp) {
 // steps: list_count_kernel (block per vocab tile) -> list_scan_kernel (one block: offsets,
 // list_count, capacity flags, counter resets) -> list_fill_kernel (block per vocab tile: list,
 // every slot_of entry (slot or -1), cnt_n).  All run only if run_if is null or *run_if != 0.
-__global__ void list_count_kernel(const uint8_t* __restrict__ keep, int nt, int n_lo, int g,
-                                  const int* run_if, int* __restrict__ cnt_m) {
+__global__ void list_count_kernel(const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g,
+                                  const int* run_if, const int32_t* __restrict__ lab_slot,
+                                  int* __restrict__ cnt_m, int* __restrict__ rcnt_m) {
   if (run_if != nullptr && *run_if == 0) return;
   __shared__ int s_w[32];
-  const uint8_t* row = keep + (size_t)blockIdx.x * nt + n_lo;
-  int c = 0;
-  for (int i = threadIdx.x; i < g; i += blockDim.x) c += row[i];
+  const int m = blockIdx.x;
+  const uint8_t* row = keep + (size_t)m * nt + n_lo;
+  int c = 0, r = 0;
+  for (int i = threadIdx.x; i < g; i += blockDim.x) {
+    const int k = row[i];
+    c += k;
+    r += k && (lab_slot == nullptr || lab_slot[(size_t)(n_lo + i) * mt + m] < 0);
+  }
   c = block_sum(c, s_w);
-  if (threadIdx.x == 0) cnt_m[blockIdx.x] = c;
+  r = block_sum(r, s_w);
+  if (threadIdx.x == 0) {
+    cnt_m[m] = c;
+    rcnt_m[m] = r;
+  }
 }
 
-// cnt_m -> off_m (exclusive), *list_count; primary: counters[0] += kept and *ok / *overflow
-// (every kept tile got a slot or not); resets cnt_n[0..g) and the dE unit counter.
-__global__ void __launch_bounds__(1024) list_scan_kernel(const int* __restrict__ cnt_m, int mt, int g,
+// cnt_m -> off_m and rcnt_m -> roff_m (exclusive); *list_count = kept tiles, *rlist_count = tiles
+// to recompute; primary: counters[0] += kept and *ok / *overflow (every tile to recompute got a
+// slot or not); resets cnt_n[0..g) and the dE unit counter.
+__global__ void __launch_bounds__(1024) list_scan_kernel(const int* __restrict__ cnt_m,
+                                                         const int* __restrict__ rcnt_m, int mt, int g,
                                                          int capacity, const int* run_if, int primary,
-                                                         int* __restrict__ off_m, int* __restrict__ cnt_n,
-                                                         int* __restrict__ list_count, int* __restrict__ ok,
+                                                         int* __restrict__ off_m, int* __restrict__ roff_m,
+                                                         int* __restrict__ cnt_n, int* __restrict__ list_count,
+                                                         int* __restrict__ rlist_count, int* __restrict__ ok,
                                                          int* __restrict__ overflow, int* __restrict__ sched,
                                                          unsigned long long* __restrict__ counters) {
   if (run_if != nullptr && *run_if == 0) return;
   constexpr int T = 1024;
-  __shared__ int s_part[32];
+  __shared__ int s_a[32], s_b[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < g; i += T) cnt_n[i] = 0;
   if (threadIdx.x == 0 && sched) *sched = 0;
-  const int per = (mt + T - 1) / T;
-  const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
-  int local = 0;
-  for (int m = m0; m < m1; ++m) local += cnt_m[m];
-  int incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_part[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    int x = s_part[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    s_part[lane] = x;
-  }
-  __syncthreads();
-  int run = (wid ? s_part[wid - 1] : 0) + incl - local;
-  for (int m = m0; m < m1; ++m) {
-    off_m[m] = run;
-    run += cnt_m[m];
-  }
-  if (threadIdx.x == 0) {
-    const int kept_total = s_part[31];
-    *list_count = kept_total;
-    if (primary) {
-      const bool fits = kept_total <= capacity;
-      *ok = fits ? 1 : 0;
-      *overflow = fits ? 0 : 1;
-      atomicAdd(&counters[0], (unsigned long long)kept_total);
-    }
-  }
-}
-
-// block per vocab tile m: slots off_m + rank in token-tile order; slot_of row-major [g][mt] with
-// the local token-tile index; tiles past the capacity get no slot (only possible when the
-// caller's gate then skips every consumer).
-__global__ void list_fill_kernel(const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g,
-                                 int capacity, const int* run_if, const int* __restrict__ off_m,
-                                 int2* __restrict__ list, int32_t* __restrict__ slot_of,
-                                 int* __restrict__ cnt_n) {
-  if (run_if != nullptr && *run_if == 0) return;
-  __shared__ int s_w[32];
-  __shared__ int s_base;
-  const int m = blockIdx.x;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint8_t* row = keep + (size_t)m * nt + n_lo;
-  if (threadIdx.x == 0) s_base = off_m[m];
-  __syncthreads();
-  for (int b = 0; b < g; b += blockDim.x) {
-    const int ln = b + threadIdx.x;
-    const bool f = ln < g && row[ln];
-    const uint32_t bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) s_w[wid] = __popc(bal);
-    __syncthreads();
-    int before = 0;
-    for (int w = 0; w < wid; ++w) before += s_w[w];
-    const int slot = s_base + before + __popc(bal & ((1u << lane) - 1));
-    if (ln < g) {
-      int so = -1;
-      if (f && slot < capacity) {
-        list[slot] = make_int2(n_lo + ln, m);
-        so = slot;
-        atomicAdd(&cnt_n[ln], 1);
-      }
-      slot_of[(size_t)ln * mt + m] = so;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
-      s_base += t;
-    }
-    __syncthreads();
-  }
-}
-
-// Fallback passes (token-tile groups after an overflow, gated on run_if): the whole kept list of
-// the group -- counts, offsets, list / slot_of / cnt_n, and the CTA-pair list -- in ONE block, so
-// a pass that does not run costs one launch here instead of four.
-__global__ void __launch_bounds__(1024) list_single_kernel(
-    const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g, int capacity, const int* run_if,
-    int* __restrict__ cnt_m, int* __restrict__ off_m, int2* __restrict__ list, int32_t* __restrict__ slot_of,
-    int* __restrict__ cnt_n, int* __restrict__ list_count, int* __restrict__ sched, int2* __restrict__ pairs,
-    int* __restrict__ pair_count) {
-  if (run_if != nullptr && *run_if == 0) return;
-  constexpr int T = 1024, W = T / 32;
-  __shared__ int s_a[W], s_b[W];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < g; i += T) cnt_n[i] = 0;
-  if (threadIdx.x == 0 && sched) *sched = 0;
-  for (int m = wid; m < mt; m += W) {  // kept count per vocab tile
-    const uint8_t* row = keep + (size_t)m * nt + n_lo;
-    int c = 0;
-    for (int b = 0; b < g; b += 32) c += __popc(__ballot_sync(0xffffffffu, b + lane < g && row[b + lane]));
-    if (lane == 0) cnt_m[m] = c;
-  }
-  __syncthreads();
-  // exclusive scans of the counts (slots) and of the pair counts ((c + 1) / 2)
   const int per = (mt + T - 1) / T;
   const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
   int la = 0, lb = 0;
   for (int m = m0; m < m1; ++m) {
     la += cnt_m[m];
-    lb += (cnt_m[m] + 1) / 2;
+    lb += rcnt_m[m];
   }
   int ia = la, ib = lb;
 #pragma unroll
@@ -501,35 +410,268 @@ __global__ void __launch_bounds__(1024) list_single_kernel(
   __syncthreads();
   int ra = (wid ? s_a[wid - 1] : 0) + ia - la, rb = (wid ? s_b[wid - 1] : 0) + ib - lb;
   for (int m = m0; m < m1; ++m) {
-    const int c = cnt_m[m];
     off_m[m] = ra;
-    for (int j = 0; 2 * j < c; ++j) pairs[rb + j] = make_int2(ra + 2 * j, min(2, c - 2 * j));
-    ra += c;
-    rb += (c + 1) / 2;
+    roff_m[m] = rb;
+    ra += cnt_m[m];
+    rb += rcnt_m[m];
+  }
+  if (threadIdx.x == 0) {
+    const int kept_total = s_a[31], recompute = s_b[31];
+    *list_count = kept_total;
+    *rlist_count = recompute;
+    if (primary) {
+      const bool fits = recompute <= capacity;
+      *ok = fits ? 1 : 0;
+      *overflow = fits ? 0 : 1;
+      atomicAdd(&counters[0], (unsigned long long)kept_total);
+    }
+  }
+}
+
+// block per vocab tile m, token-tile order: every kept tile gets a unified slot -- its stored
+// label slot (lab_slot >= 0), else lab_capacity + its place in the recompute list; the all-kept
+// list (for dC) holds (token tile, slot) at off_m[m] + rank, the recompute list (for KEPT) holds
+// (token tile, vocab tile) at roff_m[m] + rank; slot_of row-major [g][mt] with the local token-tile
+// index (every entry written).  Recompute tiles past the capacity get no slot (only when the
+// caller's gate then skips every consumer).
+__global__ void list_fill_kernel(const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g,
+                                 int capacity, int lab_capacity, const int32_t* __restrict__ lab_slot,
+                                 const int* run_if, const int* __restrict__ off_m, const int* __restrict__ roff_m,
+                                 int2* __restrict__ alist, int2* __restrict__ rlist, int32_t* __restrict__ slot_of,
+                                 int* __restrict__ cnt_n) {
+  if (run_if != nullptr && *run_if == 0) return;
+  __shared__ int s_a[32], s_b[32];
+  __shared__ int s_base, s_rbase;
+  const int m = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint8_t* row = keep + (size_t)m * nt + n_lo;
+  if (threadIdx.x == 0) {
+    s_base = off_m[m];
+    s_rbase = roff_m[m];
+  }
+  __syncthreads();
+  for (int b = 0; b < g; b += blockDim.x) {
+    const int ln = b + threadIdx.x;
+    const bool f = ln < g && row[ln];
+    const int ls = f && lab_slot ? lab_slot[(size_t)(n_lo + ln) * mt + m] : -1;
+    const bool rc = f && ls < 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, f), rbal = __ballot_sync(0xffffffffu, rc);
+    if (lane == 0) {
+      s_a[wid] = __popc(bal);
+      s_b[wid] = __popc(rbal);
+    }
+    __syncthreads();
+    int before = 0, rbefore = 0;
+    for (int w = 0; w < wid; ++w) {
+      before += s_a[w];
+      rbefore += s_b[w];
+    }
+    const int apos = s_base + before + __popc(bal & ((1u << lane) - 1));
+    const int rpos = s_rbase + rbefore + __popc(rbal & ((1u << lane) - 1));
+    if (ln < g) {
+      int so = -1;
+      if (f) {
+        if (ls >= 0) {
+          so = ls;
+        } else if (rpos < capacity) {
+          so = lab_capacity + rpos;
+          rlist[rpos] = make_int2(n_lo + ln, m);
+        }
+        if (so >= 0) {
+          alist[apos] = make_int2(n_lo + ln, so);
+          atomicAdd(&cnt_n[ln], 1);
+        }
+      }
+      slot_of[(size_t)ln * mt + m] = so;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int ta = 0, tb = 0;
+      for (int w = 0; w < nw; ++w) {
+        ta += s_a[w];
+        tb += s_b[w];
+      }
+      s_base += ta;
+      s_rbase += tb;
+    }
+    __syncthreads();
+  }
+}
+
+// In-place S-hat of the stored label tiles: fp16 d = z' - z'max(row) -> bf16
+// up * (S - onehot) * (1 - tanh^2), S = exp(z'max + d - lse) (same formula as the KEPT epilogue,
+// from the stored logits instead of a recompute).  One block of 8 warps per slot; a warp takes a
+// row at a time (lane = 8 consecutive columns: one coalesced 512 B row per access), two rows in
+// flight.  Tiles of zero-upstream token tiles are never kept and are left alone.
+__global__ void __launch_bounds__(256) label_shat_kernel(
+    __half* buf, const int2* __restrict__ lab_list, const int* __restrict__ lab_count, int lab_capacity,
+    const uint8_t* __restrict__ block_zero, int mt, const float* __restrict__ tile_max,
+    const float* __restrict__ lse, const float* __restrict__ upstream, const int32_t* __restrict__ pos,
+    const int32_t* __restrict__ row_map, const int* __restrict__ n_valid, int v, float softcap, int label_split) {
+  const int s = blockIdx.x;
+  if (s >= min(*lab_count, lab_capacity)) return;
+  const int2 nm = lab_list[s];
+  if (block_zero[nm.x]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = *n_valid;
+  const bool use_softcap = softcap > 0.f;
+  const float inv_cap = use_softcap ? 1.0f / softcap : 0.f;
+  const int col_base = nm.y * BN + lane * 8;
+  constexpr int R = 2;  // rows per iteration (independent loads in flight)
+  for (int r0 = warp * R; r0 < BM; r0 += 8 * R) {
+    uint4 in[R];
+    float lse2[R], up[R], zc0[R];
+    int pr[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      const int grow = nm.x * BM + row;
+      const bool valid = grow < nv;
+      const int orow = valid ? row_map[grow] : 0;
+      lse2[i] = valid ? lse[orow] * LOG2E : INFINITY;
+      up[i] = valid ? upstream[orow] : 0.f;
+      pr[i] = (valid && !label_split) ? pos[orow] : -1;
+      const float zmax = tile_max[((size_t)nm.x * mt + nm.y) * BM + row];
+      zc0[i] = use_softcap ? softcap * softcap_tanh(zmax, inv_cap) : zmax;
+      in[i] = reinterpret_cast<const uint4*>(buf + ((size_t)s * BM + row) * BN)[lane];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const __half2* h2 = reinterpret_cast<const __half2*>(&in[i]);
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 d = __half22float2(h2[k]);
+        float g[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = col_base + 2 * k + h;
+          g[h] = 0.f;
+          if (col < v) {  // padded columns hold -inf
+            const float zc = zc0[i] + (h ? d.y : d.x);
+            const float sv = ex2_approx(zc * LOG2E - lse2[i]);
+            float dcap = 1.f;
+            if (use_softcap) {
+              const float th = zc * inv_cap;
+              dcap = 1.f - th * th;
+            }
+            g[h] = ((col == pr[i]) ? sv - 1.f : sv) * up[i] * dcap;
+          }
+        }
+        o[k] = pack_bf16x2(g[0], g[1]);
+      }
+      reinterpret_cast<uint4*>(buf + ((size_t)s * BM + r0 + i) * BN)[lane] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// Fallback passes (token-tile groups after an overflow, gated on run_if): everything
+// list_count / list_scan / list_fill / build_pairs produce for the group, in ONE block, so a pass
+// that does not run costs one launch here instead of four.
+__global__ void __launch_bounds__(1024) list_single_kernel(
+    const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g, int capacity, int lab_capacity,
+    const int32_t* __restrict__ lab_slot, const int* run_if, int* __restrict__ cnt_m, int* __restrict__ rcnt_m,
+    int* __restrict__ off_m, int* __restrict__ roff_m, int2* __restrict__ alist, int2* __restrict__ rlist,
+    int32_t* __restrict__ slot_of, int* __restrict__ cnt_n, int* __restrict__ list_count,
+    int* __restrict__ rlist_count, int* __restrict__ sched, int2* __restrict__ pairs, int* __restrict__ pair_count) {
+  if (run_if != nullptr && *run_if == 0) return;
+  constexpr int T = 1024, W = T / 32;
+  __shared__ int s_a[W], s_b[W], s_c[W];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < g; i += T) cnt_n[i] = 0;
+  if (threadIdx.x == 0 && sched) *sched = 0;
+  auto is_lab = [&](int ln, int m) { return lab_slot != nullptr && lab_slot[(size_t)(n_lo + ln) * mt + m] >= 0; };
+  for (int m = wid; m < mt; m += W) {  // counts per vocab tile: kept, to recompute
+    const uint8_t* row = keep + (size_t)m * nt + n_lo;
+    int c = 0, r = 0;
+    for (int b = 0; b < g; b += 32) {
+      const bool f = b + lane < g && row[b + lane];
+      c += __popc(__ballot_sync(0xffffffffu, f));
+      r += __popc(__ballot_sync(0xffffffffu, f && !is_lab(b + lane, m)));
+    }
+    if (lane == 0) {
+      cnt_m[m] = c;
+      rcnt_m[m] = r;
+    }
+  }
+  __syncthreads();
+  // exclusive scans: kept slots, recompute slots, recompute pairs ((r + 1) / 2)
+  const int per = (mt + T - 1) / T;
+  const int m0 = threadIdx.x * per, m1 = min(mt, m0 + per);
+  int la = 0, lb = 0, lc = 0;
+  for (int m = m0; m < m1; ++m) {
+    la += cnt_m[m];
+    lb += rcnt_m[m];
+    lc += (rcnt_m[m] + 1) / 2;
+  }
+  int ia = la, ib = lb, ic = lc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+    const int yc = __shfl_up_sync(0xffffffffu, ic, o);
+    if (lane >= o) { ia += ya; ib += yb; ic += yc; }
+  }
+  if (lane == 31) { s_a[wid] = ia; s_b[wid] = ib; s_c[wid] = ic; }
+  __syncthreads();
+  if (wid == 0) {
+    int xa = s_a[lane], xb = s_b[lane], xc = s_c[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+      const int yc = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) { xa += ya; xb += yb; xc += yc; }
+    }
+    s_a[lane] = xa;
+    s_b[lane] = xb;
+    s_c[lane] = xc;
+  }
+  __syncthreads();
+  int ra = (wid ? s_a[wid - 1] : 0) + ia - la, rb = (wid ? s_b[wid - 1] : 0) + ib - lb;
+  int rc = (wid ? s_c[wid - 1] : 0) + ic - lc;
+  for (int m = m0; m < m1; ++m) {
+    const int r = rcnt_m[m];
+    off_m[m] = ra;
+    roff_m[m] = rb;
+    for (int j = 0; 2 * j < r; ++j) pairs[rc + j] = make_int2(rb + 2 * j, min(2, r - 2 * j));
+    ra += cnt_m[m];
+    rb += r;
+    rc += (r + 1) / 2;
   }
   if (threadIdx.x == T - 1) {
     *list_count = ra;
-    *pair_count = rb;
+    *rlist_count = rb;
+    *pair_count = rc;
   }
   __syncthreads();
   for (int m = wid; m < mt; m += W) {  // slots in vocab-tile-major, token-tile order
     const uint8_t* row = keep + (size_t)m * nt + n_lo;
-    int slot0 = off_m[m];
+    int a0 = off_m[m], r0 = roff_m[m];
     for (int b = 0; b < g; b += 32) {
       const int ln = b + lane;
       const bool f = ln < g && row[ln];
-      const uint32_t bal = __ballot_sync(0xffffffffu, f);
-      const int slot = slot0 + __popc(bal & ((1u << lane) - 1));
+      const int ls = f && lab_slot ? lab_slot[(size_t)(n_lo + ln) * mt + m] : -1;
+      const bool rcp = f && ls < 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, f), rbal = __ballot_sync(0xffffffffu, rcp);
+      const int apos = a0 + __popc(bal & ((1u << lane) - 1));
+      const int rpos = r0 + __popc(rbal & ((1u << lane) - 1));
       if (ln < g) {
         int so = -1;
-        if (f && slot < capacity) {
-          list[slot] = make_int2(n_lo + ln, m);
-          so = slot;
-          atomicAdd(&cnt_n[ln], 1);
+        if (f) {
+          if (ls >= 0) {
+            so = ls;
+          } else if (rpos < capacity) {
+            so = lab_capacity + rpos;
+            rlist[rpos] = make_int2(n_lo + ln, m);
+          }
+          if (so >= 0) {
+            alist[apos] = make_int2(n_lo + ln, so);
+            atomicAdd(&cnt_n[ln], 1);
+          }
         }
         slot_of[(size_t)ln * mt + m] = so;
       }
-      slot0 += __popc(bal);
+      a0 += __popc(bal);
+      r0 += __popc(rbal);
     }
   }
 }

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdint>
 
@@ -53,6 +54,14 @@ struct Params {
   float2* part;      // [splits][n_total]  (running max, running sum) in log2 units
   float* correct;    // [n_total] target logit (written by the tile that owns the label)
   float* tile_max;   // [nt][mt][BM] max raw logit of each row in each tile, or nullptr
+  // label tiles (FWD, optional): a tile holding some row's label is always kept by the backward
+  // (kernels.py:447-455), so the forward stores it -- fp16 of z' - z'max(row) -- in a slot of
+  // lab_buf ([lab_capacity][BM][BN]) and the backward turns it into S-hat without a recompute
+  __half* lab_buf;
+  int lab_capacity;
+  int* lab_count;          // slots handed out (may exceed lab_capacity: those tiles get none)
+  int32_t* lab_slot;       // [nt][mt] slot of a stored label tile, -1 (pre-filled) if none
+  int2* lab_list;          // [lab_capacity] (token tile, vocab tile) of each slot
   // backward filter pass (lse / upstream / pos are indexed by ORIGINAL row)
   const float* lse;        // global log-sum-exp (natural log)
   const float* upstream;   // dLoss/dloss_i, 0 at ignored rows

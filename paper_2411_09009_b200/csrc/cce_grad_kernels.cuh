@@ -65,16 +65,17 @@ __device__ __forceinline__ void for_each_kept(const int32_t* slot_of, int count,
   }
 }
 
-// Visit the kept tiles of one vocab tile through the vocab-tile-major kept list: slots
-// [off, off + cnt) in token-tile order; lanes fetch 32 entries at a time, every lane calls
-// f(local token tile, slot).
+// Visit the kept tiles of one vocab tile through the vocab-tile-major kept list: entries
+// [off, off + cnt) = (token tile, slot) in token-tile order; lanes fetch 32 entries at a time,
+// every lane calls f(local token tile, slot).
 template <typename F>
 __device__ __forceinline__ void for_each_listed(const int2* list, int off, int cnt, int n_base, F&& f) {
   const int lane = threadIdx.x & 31;
   for (int base = 0; base < cnt; base += 32) {
-    const int my = base + lane < cnt ? list[off + base + lane].x : 0;
+    const int2 my = base + lane < cnt ? list[off + base + lane] : make_int2(0, 0);
     const int k_end = min(32, cnt - base);
-    for (int k = 0; k < k_end; ++k) f(__shfl_sync(0xffffffffu, my, k) - n_base, off + base + k);
+    for (int k = 0; k < k_end; ++k)
+      f(__shfl_sync(0xffffffffu, my.x, k) - n_base, __shfl_sync(0xffffffffu, my.y, k));
   }
 }
 

@@ -268,45 +268,52 @@ int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CU
 }
 
 struct KeptWs {
-  __nv_bfloat16* shat;
   uint8_t* keep;
-  int2* list;
+  int2* alist;     // all kept tiles, vocab-tile-major: (token tile, slot)
+  int2* rlist;     // tiles to recompute: (token tile, vocab tile)
   int2* pairs;
   int* pair_count;
   int32_t* slot_of;
   uint8_t* block_zero;
   int* list_count;
+  int* rlist_count;
   int* ok;
   int* cnt_n;
   int* cnt_m;
+  int* rcnt_m;
   int* off_m;
+  int* roff_m;
   size_t keep_bytes, slot_bytes, cnt_bytes;
   size_t total;
 };
 
-KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity) {
+// capacity = S-hat slots for recomputed tiles; lab_capacity = stored label-tile slots
+KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity, int64_t lab_capacity) {
   const int64_t mt = (v + cce::BN - 1) / cce::BN;
   const int64_t nt = (n + cce::BM - 1) / cce::BM;
   auto up = [](size_t x) { return (x + 1023) & ~size_t(1023); };
   uint8_t* b = static_cast<uint8_t*>(base);
   KeptWs w;
   size_t o = 0;
-  w.shat = reinterpret_cast<__nv_bfloat16*>(b + o); o += up((size_t)capacity * cce::SHAT_TILE_BYTES);
   w.keep_bytes = up((size_t)nt * mt);
   w.keep = b + o; o += w.keep_bytes;
-  w.list = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
+  w.alist = reinterpret_cast<int2*>(b + o); o += up((size_t)(capacity + lab_capacity) * sizeof(int2));
+  w.rlist = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
   w.pairs = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
   w.slot_bytes = up((size_t)nt * mt * 4);
   w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
   w.block_zero = b + o; o += up((size_t)nt);
-  // zeroed together: list_count, ok, cnt_n[nt], cnt_m[mt]
-  w.cnt_bytes = up(256 + (size_t)(nt + 2 * mt) * 4);
+  w.cnt_bytes = up(256 + (size_t)(nt + 4 * mt) * 4);
   w.list_count = reinterpret_cast<int*>(b + o);
   w.ok = w.list_count + 1;
   w.pair_count = w.list_count + 2;
+  // list_count + 3: dE unit counter
+  w.rlist_count = w.list_count + 4;
   w.cnt_n = reinterpret_cast<int*>(b + o + 256);
   w.cnt_m = w.cnt_n + nt;
-  w.off_m = w.cnt_m + mt;
+  w.rcnt_m = w.cnt_m + mt;
+  w.off_m = w.rcnt_m + mt;
+  w.roff_m = w.off_m + mt;
   o += w.cnt_bytes;
   w.total = o;
   return w;
@@ -691,9 +698,11 @@ size_t cce_tile_max_bytes(int64_t n, int64_t v) {
 
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
-                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* stream_ptr) {
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
+                  int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (n < 0 || d <= 0 || v <= 0) return fail("cce_fwd_tiles: bad sizes");
+  if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail("cce_fwd_tiles: label tiles need slot maps");
   if (d % 8 != 0) return fail("cce_fwd_tiles: D must be a multiple of 8 (16-byte TMA row pitch)");
   if (!row_map || !n_valid || !pos || !tile_max) return fail("cce_fwd_tiles: row_map, n_valid, pos, tile_max required");
   if (n == 0) return 0;
@@ -723,6 +732,15 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   p.tile_max = tile_max;
+  if (lab_buf) {
+    CCE_CUDA(cudaMemsetAsync(lab_slot, 0xFF, (size_t)nt * mt * sizeof(int32_t), stream));
+    CCE_CUDA(cudaMemsetAsync(lab_count, 0, sizeof(int), stream));
+    p.lab_buf = static_cast<__half*>(lab_buf);
+    p.lab_capacity = (int)lab_capacity;
+    p.lab_count = lab_count;
+    p.lab_slot = lab_slot;
+    p.lab_list = static_cast<int2*>(lab_list);
+  }
   cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
   cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
@@ -732,27 +750,30 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
 }
 
 
-size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles) {
+size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
+                                    int64_t lab_capacity) {
   (void)d;
-  return kept_layout(nullptr, n, v, capacity_tiles).total;
+  return kept_layout(nullptr, n, v, capacity_tiles, lab_capacity).total;
 }
 
 int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
-                 int label_split, int64_t capacity_tiles, void* ws, size_t ws_bytes, void* de_out,
-                 int de_fp32, void* dc, unsigned long long* counters, int* overflow, void* de_done_event,
-                 void* stream_ptr) {
+                 int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
+                 const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
+                 void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
+                 int* stats, void* de_done_event, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
-  if (!overflow) return fail("cce_bwd_kept: overflow flag required");
+  if (!overflow || !shat) return fail("cce_bwd_kept: overflow flag and S-hat buffer required");
+  if (lab_slot == nullptr) lab_capacity = 0;
   if (n <= 0) return 0;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   if (capacity_tiles < std::min<int64_t>(mt, (int64_t)nt * mt))
     return fail("cce_bwd_kept: capacity_tiles must hold one token tile's vocab tiles (ceil(v/256))");
-  const KeptWs w = kept_layout(ws, n, v, capacity_tiles);
+  const KeptWs w = kept_layout(ws, n, v, capacity_tiles, lab_capacity);
   if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
@@ -760,15 +781,23 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
       tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split, w.keep, counters);
   CCE_CUDA(cudaGetLastError());
+  // S-hat slots: [stored label tiles (lab_capacity) | recomputed tiles (capacity_tiles)]
+  __nv_bfloat16* shat_all = static_cast<__nv_bfloat16*>(shat);
+  __nv_bfloat16* shat_rec = shat_all + (size_t)lab_capacity * cce::BM * cce::BN;
+  if (lab_capacity > 0) {  // stored label tiles -> S-hat, in place
+    cce::label_shat_kernel<<<(unsigned)lab_capacity, 256, 0, stream>>>(
+        reinterpret_cast<__half*>(shat_all), static_cast<const int2*>(lab_list), lab_count, (int)lab_capacity,
+        w.block_zero, mt, tile_max, lse, upstream, pos, row_map, n_valid, (int)v, softcap, label_split);
+    CCE_CUDA(cudaGetLastError());
+  }
 
-  CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h;
-  const int64_t shat_rows = capacity_tiles * cce::BM;
+  CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS64, tmC3, tmE3, tmE3h;
+  const int64_t shat_rows = (capacity_tiles + lab_capacity) * cce::BM;
   const bool atoms3d = d % 64 == 0;
   bool ok = make_tmap(&tmE, E_c, n, d, cce::BM) && make_tmap(&tmC, C_t, v, d, cce::BN) &&
             make_tmap(&tmC64, C_t, v, d, cce::DE_KV) && make_tmap(&tmE64, E_c, n, d, 64) &&
             make_tmap(&tmC128h, C_t, v, d, cce::BN / 2) &&
-            make_tmap3d(&tmS128, w.shat, shat_rows, cce::BN, 128, 1) &&
-            make_tmap3d(&tmS64, w.shat, shat_rows, cce::BN, 64, 2);
+            make_tmap3d(&tmS64, shat_all, shat_rows, cce::BN, 64, 2);
   if (ok && atoms3d)
     ok = make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) && make_tmap3d(&tmE3, E_c, n, d, 64, cce::DCH / 64) &&
          make_tmap3d(&tmE3h, E_c, n, d, 64, cce::DCH / 128);
@@ -780,33 +809,35 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
   const bool pair = use_pairs();
 
-  // One pass over token tiles [g0, g0 + g): kept-tile list, S-hat of the kept tiles (KEPT), dE of
-  // those token tiles (complete), dC (written by the first pass, accumulated by later ones).
+  // One pass over token tiles [g0, g0 + g): kept lists, S-hat of the tiles to recompute (KEPT),
+  // dE of those token tiles (complete), dC (written by the first pass, accumulated by later ones).
   auto run_pass = [&](int g0, int g, bool primary, const int* run_if, bool last) -> int {
-    // kept list, slot_of (every entry written), counts and pairs of this pass; counters reset
-    // inside.  The whole-batch pass uses three parallel kernels (+ pairs); fallback passes one
-    // block (they usually do not run, and then cost one launch)
+    // lists, slot_of (every entry written), counts and pairs of this pass; counters reset inside.
+    // The whole-batch pass uses parallel kernels, fallback passes one block (they usually do not
+    // run, and then cost one launch)
     if (primary) {
-      cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, g0, g, run_if, w.cnt_m);
+      cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, run_if, lab_slot, w.cnt_m, w.rcnt_m);
       CCE_CUDA(cudaGetLastError());
-      cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, g, (int)capacity_tiles, run_if, 1, w.off_m,
-                                                    w.cnt_n, w.list_count, w.ok, overflow, w.list_count + 3,
-                                                    counters);
+      cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, w.rcnt_m, mt, g, (int)capacity_tiles, run_if, 1,
+                                                    w.off_m, w.roff_m, w.cnt_n, w.list_count, w.rlist_count,
+                                                    w.ok, overflow, w.list_count + 3, counters);
       CCE_CUDA(cudaGetLastError());
-      cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if, w.off_m,
-                                                    w.list, w.slot_of, w.cnt_n);
+      cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, (int)lab_capacity,
+                                                    lab_slot, run_if, w.off_m, w.roff_m, w.alist, w.rlist,
+                                                    w.slot_of, w.cnt_n);
       CCE_CUDA(cudaGetLastError());
       if (pair) {
-        cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, mt, w.ok, w.pairs, w.pair_count);
+        cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.rcnt_m, mt, w.ok, w.pairs, w.pair_count);
         CCE_CUDA(cudaGetLastError());
       }
     } else {
-      cce::list_single_kernel<<<1, 1024, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, run_if,
-                                                      w.cnt_m, w.off_m, w.list, w.slot_of, w.cnt_n,
-                                                      w.list_count, w.list_count + 3, w.pairs, w.pair_count);
+      cce::list_single_kernel<<<1, 1024, 0, stream>>>(
+          w.keep, nt, mt, g0, g, (int)capacity_tiles, (int)lab_capacity, lab_slot, run_if, w.cnt_m, w.rcnt_m,
+          w.off_m, w.roff_m, w.alist, w.rlist, w.slot_of, w.cnt_n, w.list_count, w.rlist_count,
+          w.list_count + 3, w.pairs, w.pair_count);
       CCE_CUDA(cudaGetLastError());
     }
-    const int* gate = primary ? w.ok : run_if;  // primary: only if every kept tile got a slot
+    const int* gate = primary ? w.ok : run_if;  // primary: only if every tile to recompute got a slot
     cce::Params p{};
     p.n_total = (int)n;
     p.n_valid = n_valid;
@@ -826,11 +857,11 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     p.row_map = row_map;
     p.eps = eps;
     p.label_split = label_split;
-    p.shat = w.shat;
+    p.shat = shat_rec;
     p.capacity = (int)capacity_tiles;
     p.counters = counters;
-    p.list = w.list;
-    p.list_count = w.list_count;
+    p.list = w.rlist;
+    p.list_count = w.rlist_count;
     p.pairs = w.pairs;
     p.pair_count = w.pair_count;
     if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
@@ -845,7 +876,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.ndc = ndc;
     q.n_base = g0;
     q.g = g;
-    q.slot_of = w.slot_of;  // rows of this pass, local token-tile index
+    q.slot_of = w.slot_of;  // rows of this pass, local token-tile index; unified slots
     q.cnt_n = w.cnt_n;
     q.cnt_m = w.cnt_m;
     q.perm = nullptr;
@@ -857,17 +888,24 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
-    q.list = w.list;
+    q.list = w.alist;
     q.off_m = w.off_m;
-    if (int e = launch_de(q, w.list_count + 3, w.shat, shat_rows, C_t, tmC64, stream)) return e;
+    if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, C_t, tmC64, stream)) return e;
     if (last && de_done_event)  // every dE write of this call is enqueued before this point
       CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
     return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
   };
-  // The kept count is only known on the device: the whole-batch pass runs iff it fits; otherwise
-  // (*overflow) token-tile groups sized for the worst case (every tile kept) run instead.
+  // The counts are only known on the device: the whole-batch pass runs iff its tiles to
+  // recompute fit; otherwise (*overflow) token-tile groups sized for the worst case run instead.
   const bool grouped = (int64_t)nt * mt > capacity_tiles;
   if (int e = run_pass(0, nt, true, nullptr, !grouped)) return e;
+  if (stats) {  // label tiles stored by the forward, tiles the whole-batch pass had to recompute
+    if (lab_capacity > 0)
+      CCE_CUDA(cudaMemcpyAsync(stats, lab_count, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+    else
+      CCE_CUDA(cudaMemsetAsync(stats, 0, sizeof(int), stream));
+    CCE_CUDA(cudaMemcpyAsync(stats + 1, w.rlist_count, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+  }
   if (grouped) {
     const int g = (int)std::max<int64_t>(1, capacity_tiles / mt);
     for (int g0 = 0; g0 < nt; g0 += g)

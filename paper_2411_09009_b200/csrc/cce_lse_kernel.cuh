@@ -344,6 +344,15 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
           have_corr = false;
         }
         const bool tile_has_t = tpos >= col0 && tpos < col0 + BN;
+        // label tile of this CTA's token tile?  (decided before the sweep: labels are known)
+        bool is_lab = false;
+        if (p.lab_buf != nullptr) {
+          const uint32_t wv = __ballot_sync(0xffffffffu, tile_has_t);
+          if (lane == 0) s_vote[(t & 1) * 4 + quarter] = wv;
+          named_bar_sync(1, 128);
+          const uint32_t* vv = s_vote + (t & 1) * 4;
+          is_lab = tr.ok && (vv[0] | vv[1] | vv[2] | vv[3]) != 0;
+        }
         float zmax = -INFINITY;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -373,6 +382,48 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
             for (int j = 0; j < 32; ++j) acc += ex2_approx(y[j] - nm);
             run_s = run_s * ex2_approx(run_m - nm) + acc;
             run_m = nm;
+          }
+        }
+        if (is_lab) {
+          // claim a slot, then re-read the accumulator: fp16 of z' - z'max(row), <= 0 and exact
+          // near the row max where S lives (padded columns -inf)
+          if (epi_tid == 0) {
+            int slot = atomicAdd(p.lab_count, 1);
+            if (slot < p.lab_capacity) {
+              p.lab_slot[(size_t)tr.n * p.mt + tr.m] = slot;
+              p.lab_list[slot] = make_int2(tr.n, tr.m);
+            } else {
+              slot = -1;
+            }
+            s_slot[t & 1] = slot;
+          }
+          named_bar_sync(1, 128);
+          const int slot = s_slot[t & 1];
+          if (slot >= 0) {
+            const float zcmax = use_softcap ? p.softcap * softcap_tanh(zmax, inv_cap) : zmax;
+            uint4* dst = reinterpret_cast<uint4*>(p.lab_buf + ((size_t)slot * BM + row) * BN);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              uint32_t r[32];
+              tmem_ld32(tacc + c * 32, r);
+              tmem_ld_wait();
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                float dd[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  float z = __uint_as_float(r[j + h]);
+                  if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
+                  dd[h] = (col0 + c * 32 + j + h < p.v) ? z - zcmax : -INFINITY;
+                }
+                const __half2 h2 = __floats2half2_rn(dd[0], dd[1]);
+                pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
           }
         }
         release_acc(buf);

@@ -51,7 +51,8 @@ class _LinearCrossEntropy(torch.autograd.Function):
         ctx.state = None
         if eps > 0 and not low_memory and (ctx.needs_input_grad[0] or ctx.needs_input_grad[1]):
             lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
-                                                              softcap, vocab_sorting)
+                                                              softcap, vocab_sorting, eps=eps,
+                                                              label_split=not exempt_label_tiles)
         else:
             lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
         if group is None:

@@ -384,9 +384,18 @@ class TileState:
     vocab_start: int
     softcap: float
     mean_logits: torch.Tensor | None = None
+    # S-hat slots [stored label tiles (lab_cap) | recomputed tiles (rcap)], allocated by the forward
+    shat: torch.Tensor | None = None
+    lab_cap: int = 0
+    rcap: int = 0
+    lab_slot: torch.Tensor | None = None
+    lab_list: torch.Tensor | None = None
+    lab_count: torch.Tensor | None = None
+    keys: tuple = ()
 
     def nbytes(self) -> int:
         own = [self.e_c, self.row_map, self.n_valid, self.pos, self.tile_max]
+        own += [t for t in (self.shat, self.lab_slot, self.lab_list, self.lab_count) if t is not None]
         if self.perm is not None:
             own += [self.c_t, self.perm, self.perm_padded]
         return sum(t.numel() * t.element_size() for t in own)
@@ -404,7 +413,8 @@ def gather_rows(src: torch.Tensor, index: torch.Tensor, rows: int) -> torch.Tens
 
 
 def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
-                  vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+                  vocab_sorting: bool = True, perm: torch.Tensor | None = None,
+                  eps: float = EPSILON_DEFAULT, label_split: bool = False, store_labels: bool = True):
     """Forward of the filter-from-forward path: (lse_local, correct, TileState).
 
     Same results as forward_local (indexed_matmul + lse_forward, kernels.py:204-319), computed
@@ -438,12 +448,31 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
                       int(vocab_start), float(softcap or 0.0), mean_logits)
     if n == 0:
         return lse_local, correct, state
+    # S-hat slots for the backward, allocated here because the forward fills the label region:
+    # tiles holding a label are always kept (kernels.py:447-455), so their logits are stored now
+    # and turned into S-hat without a recompute
+    nt = -(-n // BLOCK_TOKENS)
+    mt = -(-v // BLOCK_VOCAB)
+    store_labels = store_labels and os.environ.get("CCE_STORE_LABELS", "1") != "0"
+    rkey = ("recompute", n, d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
+            bool(store_labels))
+    lkey = ("labels", n, d, v, int(vocab_start))
+    state.rcap = shat_capacity(rkey, nt, mt)
+    state.lab_cap = label_capacity(lkey, nt, mt) if store_labels else 0
+    state.keys = (rkey, lkey)
+    state.shat = torch.empty((state.lab_cap + state.rcap) * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
+    if state.lab_cap:
+        state.lab_slot = torch.empty(nt * mt, dtype=torch.int32, device=dev)
+        state.lab_list = torch.empty(state.lab_cap, 2, dtype=torch.int32, device=dev)
+        state.lab_count = torch.empty(1, dtype=torch.int32, device=dev)
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     ev = _ev_begin("fwd")
     _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), n, d, v,
                                  float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
-                                 _p(tile_max), stream), "cce_fwd_tiles")
+                                 _p(tile_max), _p(state.shat if state.lab_cap else None), state.lab_cap,
+                                 _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), stream),
+               "cce_fwd_tiles")
     _ev_end("fwd", ev)
     LAUNCHES["count"] += 3
     return lse_local, correct, state
@@ -478,29 +507,38 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
         raise ValueError("backward_tiles needs filtering (eps > 0)")
     nt = -(-n // BLOCK_TOKENS)
     mt = -(-v // BLOCK_VOCAB)
-    # S-hat slots: the whole batch in one pass if the kept tiles fit; otherwise the library falls
-    # back (device flag, no host read) to token-tile groups sized for the worst case
-    key = (n, d, v, state.vocab_start, float(eps), state.softcap)
-    cap = shat_capacity(key, nt, mt)
+    # S-hat slots (from the forward): label tiles stored there, the rest recomputed -- in one pass
+    # if they fit; otherwise the library falls back (device flag, no host read) to token-tile
+    # groups sized for the worst case
+    if state.shat is None:
+        state.rcap = shat_capacity(("recompute-", n, d, v, state.vocab_start, float(eps), state.softcap), nt, mt)
+        state.shat = torch.empty(state.rcap * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
+    cap, lab_cap = state.rcap, state.lab_cap
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
-    ws_bytes = lib.cce_bwd_kept_workspace_bytes(n, d, v, cap)
+    stats = torch.zeros(2, dtype=torch.int32, device=dev)
+    ws_bytes = lib.cce_bwd_kept_workspace_bytes(n, d, v, cap, lab_cap)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     ev = _ev_begin("bwd")
     _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.perm_padded), _p(state.row_map),
                                 _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
-                                n, d, v, state.softcap, float(eps), int(bool(label_split)), cap, _p(ws),
-                                ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters), _p(overflow),
+                                n, d, v, state.softcap, float(eps), int(bool(label_split)), _p(state.shat),
+                                lab_cap, _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), cap,
+                                _p(ws), ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters), _p(overflow),
+                                _p(stats),
                                 ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
                                                 else 0), stream), "cce_bwd_kept")
     passes = 1 + (0 if cap >= nt * mt else -(-nt // max(1, cap // mt)))
-    LAUNCHES["count"] += 2 + passes * 6
+    LAUNCHES["count"] += 3 + (1 if lab_cap else 0) + 6 + (passes - 1) * 4
     del ws
     if label_split:
         label_terms(e, state.c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream,
                     correct, state.softcap, de, dc)
         if de_done is not None:
             de_done.record()
-    _remember_kept(key, counters)
+    if state.keys:
+        _remember_count(state.keys[0], stats, 1)
+        if lab_cap:
+            _remember_count(state.keys[1], stats, 0)
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
@@ -510,7 +548,7 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
 SHAT_TILE_BYTES = BLOCK_TOKENS * BLOCK_VOCAB * 2
 FIRST_CALL_MB = 1024          # S-hat allocation before any kept count has been observed
 KEPT_MARGIN = 1.15            # headroom over the last observed kept count
-_KEPT_HINT: dict = {}         # shape key -> [pinned int64[3] counters copy, CUDA event, last known kept]
+_KEPT_HINT: dict = {}         # shape key -> [pinned copy of a device count vector, CUDA event, last known value, index]
 
 
 def shat_budget_tiles() -> int:
@@ -549,25 +587,46 @@ def _harvest(hint) -> None:
     if _capturing():  # no event queries inside a CUDA-graph capture: use what is already known
         return
     if hint[1] is not None and hint[1].query():
-        hint[2] = int(hint[0][0])
+        hint[2] = int(hint[0][hint[3]])
         hint[1] = None
+
+
+LABEL_MARGIN = 1.1
+
+
+def label_capacity(key, nt: int, mt: int) -> int:
+    """Stored label-tile slots: the worst case (every valid row's label in its own vocab tile,
+    ceil(n/128) * min(ceil(v/256), 128)) until a label count of this shape has been observed, then
+    that count plus a margin.  Too small is safe: tiles without a slot are recomputed."""
+    worst = nt * min(mt, BLOCK_TOKENS)
+    hint = _KEPT_HINT.get(key)
+    if hint is not None:
+        _harvest(hint)
+        if hint[2] is not None:
+            return min(worst, int(hint[2] * LABEL_MARGIN) + nt)
+    return worst
+
+
+def _remember_count(key, counts: torch.Tensor, index: int) -> None:
+    """Queue an asynchronous copy of a device count (read by a later call once it has landed)."""
+    if _capturing():
+        return
+    hint = _KEPT_HINT.get(key)
+    if hint is None:
+        hint = [torch.zeros(counts.shape, dtype=counts.dtype).pin_memory(), None, None, index]
+        _KEPT_HINT[key] = hint
+    _harvest(hint)
+    if hint[1] is not None:
+        return  # previous copy still in flight
+    hint[0].copy_(counts, non_blocking=True)
+    hint[1] = torch.cuda.Event()
+    hint[1].record()
 
 
 def _remember_kept(key, counters: torch.Tensor) -> None:
     """Queue an asynchronous copy of this call's kept-tile count (read by a later call once it
     has landed; the CPU usually runs ahead of the GPU, so the value may be a few calls old)."""
-    if _capturing():  # a graph replays with the capacity fixed at capture time
-        return
-    hint = _KEPT_HINT.get(key)
-    if hint is None:
-        hint = [torch.zeros(3, dtype=torch.int64).pin_memory(), None, None]
-        _KEPT_HINT[key] = hint
-    _harvest(hint)
-    if hint[1] is not None:
-        return  # previous copy still in flight
-    hint[0].copy_(counters, non_blocking=True)
-    hint[1] = torch.cuda.Event()
-    hint[1].record()
+    _remember_count(key, counters, 0)
 
 
 REDUCTIONS = {"none": 0, "sum": 1, "mean": 2}

@@ -255,6 +255,7 @@ def test_shat_budget_overflow_falls_back_to_groups(cuda_device, monkeypatch, pat
     e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
     c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
     x = rng.integers(0, v, n)
+    monkeypatch.setenv("CCE_STORE_LABELS", "0")  # every kept tile is recomputed (label tiles too)
     base = _run(e, c, x, path=path)
     from paper_2411_09009_b200 import ops
 
@@ -615,3 +616,31 @@ def test_cuda_graph_capture_and_replay(cuda_device):
     torch.cuda.synchronize()
     assert torch.equal(got[0], ref_loss.detach())
     assert torch.equal(got[1], e_s.grad) and torch.equal(got[2], c_s.grad)
+
+
+def test_stored_label_tiles_with_overflowing_recompute(cuda_device, monkeypatch):
+    """Label tiles stored by the forward plus more non-label kept tiles than the recompute slots:
+    the grouped fallback mixes stored and recomputed slots; results equal the unconstrained run."""
+    from paper_2411_09009_b200 import ops
+
+    rng = np.random.default_rng(23)
+    n, d, v = 2000, 64, 20000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::9] = -1
+    base = _run(e, c, x, path="tiles")
+    assert int(ops.LAST_OVERFLOW["flag"].item()) == 0
+    monkeypatch.setenv("CCE_SHAT_BUDGET_MB", "1")  # recompute slots = one token tile's vocab tiles
+    small = _run(e, c, x, path="tiles")
+    assert int(ops.LAST_OVERFLOW["flag"].item()) == 1
+    for a, b in zip(base[:4], small[:4]):
+        assert O.rel_err(a, b) < 1e-2
+    assert np.array_equal(base[4], small[4])
+    ce, cl, idx = O.filter_ignored(e, x)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    up = O.default_upstream(x, "mean-over-valid")
+    rde_c, rdc = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up[idx], perm=small[5])
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(small[2], rde) < GRAD_TOL and O.rel_err(small[3], rdc) < GRAD_TOL
