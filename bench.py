@@ -318,6 +318,7 @@ def main():
     kev = {k: sum(a.elapsed_time(b) for a, b in evs) / args.steps for k, evs in ops.KERNEL_EVENTS.items()}
     ops.KERNEL_EVENTS = None
     counters = ops.LAST_COUNTERS["counters"].tolist()
+    stats = ops.LAST_STATS["stats"].tolist() if "stats" in ops.LAST_STATS else None
     if world > 1:
         mt = torch.tensor([ms], device=dev)
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
@@ -405,9 +406,11 @@ def main():
     tile_area = 128 * 256
     tiles_path = not (args.low_memory or args.no_filter)  # forward on compacted rows
     flops_fwd = 2.0 * (n_valid if tiles_path else n) * v_loc * d
-    # backward recompute: every tile (low_memory filter pass) or the kept tiles only (decision
-    # taken from the forward's tile maxima); then dE and dC over the kept tiles
-    flops_recompute = 2.0 * d * kept * tile_area if tiles_path else 2.0 * n_valid * v_loc * d
+    # backward recompute: every tile (low_memory filter pass) or, on the training path, only the
+    # kept tiles the forward did not store (label tiles are stored and need no recompute); then
+    # dE and dC over all kept tiles
+    recomputed = stats[1] if (tiles_path and stats) else kept
+    flops_recompute = 2.0 * d * recomputed * tile_area if tiles_path else 2.0 * n_valid * v_loc * d
     flops_bwd = flops_recompute + 4.0 * d * kept * tile_area
     # dominant single kernel: the forward logit-tile kernel (cce_fwd is one tcgen05 launch plus two
     # tiny ones); the backward entry is three kernels (B1 filter, B2 dE, B3 dC) and is reported
@@ -451,7 +454,9 @@ def main():
             "gpu_launches": launches,
             "kernel_ms": kev,
             "skip": {"kept_tiles": kept, "eps_skipped": counters[1], "zero_up_skipped": counters[2],
-                     "total_tiles": total_tiles, "skip_rate": 1 - kept / max(1, total_tiles)},
+                     "total_tiles": total_tiles, "skip_rate": 1 - kept / max(1, total_tiles),
+                     "label_tiles_stored": stats[0] if (tiles_path and stats) else 0,
+                     "recomputed_tiles": recomputed if tiles_path else total_tiles},
             "step_tflops": step_flops / (ms / 1e3) / 1e12,
             "step_frac": step_flops / (ms / 1e3) / 1e12 / peaks["bf16_tflops"],
             "bwd_tflops": flops_bwd / (kev.get("bwd", float("nan")) / 1e3) / 1e12,

@@ -26,6 +26,7 @@ EPSILON_DEFAULT = 2.0 ** -12   # core.py:27
 KERNEL_EVENTS: dict[str, list] | None = None
 LAST_COUNTERS: dict = {}
 LAST_OVERFLOW: dict = {}  # device flag of the last backward: 1 if the fallback pass ran
+LAST_STATS: dict = {}     # tile-path backward: [label tiles stored by the forward, tiles recomputed]
 LAUNCHES = {"count": 0}   # kernels launched from libcce_b200.so (bench.py's gpu_launches)
 
 
@@ -535,6 +536,7 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
                     correct, state.softcap, de, dc)
         if de_done is not None:
             de_done.record()
+    LAST_STATS["stats"] = stats  # [label tiles stored by the forward, tiles recomputed]
     if state.keys:
         _remember_count(state.keys[0], stats, 1)
         if lab_cap:

@@ -29,6 +29,7 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
         step()
     torch.cuda.synchronize()
 kept = int(ops.LAST_COUNTERS["counters"][0])
+recomputed = int(ops.LAST_STATS["stats"][1])  # label tiles are stored by the forward
 evs = sorted([x for x in prof.events() if x.device_type == torch.autograd.DeviceType.CUDA],
              key=lambda x: x.time_range.start)
 span = (evs[-1].time_range.end - evs[0].time_range.start) / steps / 1e3
@@ -41,7 +42,8 @@ peaks = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_P
 tile = 128 * 256
 work = {  # name fragment -> (flops, bytes) per step (algorithmic)
     "cce_lse_kernel<0": (2.0 * N * V * D, None),
-    "cce_lse_kernel<2": (2.0 * D * kept * tile, None),
+    "cce_lse_kernel<2": (2.0 * D * recomputed * tile, None),
+    "label_shat_kernel": (None, (kept - recomputed) * tile * 4.0),
     "cce_de_kernel": (2.0 * D * kept * tile, None),
     "cce_dc_kernel": (2.0 * D * kept * tile, None),
     "sort_key_kernel": (None, V * D * 2.0),
@@ -59,7 +61,7 @@ for name, ds in per.items():
     rows.append((ms, short, flops, byts))
 rows.sort(reverse=True)
 print(f"Gemma-2-2B head, default path, {steps} steps: {span:.2f} ms/step, kept tiles {kept} of "
-      f"{(N // 128) * (V // 256)}; peaks: {peaks['bf16_tflops']} TFLOP/s bf16, {peaks['hbm_gbs']} GB/s\n")
+      f"{(N // 128) * (V // 256)} ({kept - recomputed} stored by the forward, {recomputed} recomputed); peaks: {peaks['bf16_tflops']} TFLOP/s bf16, {peaks['hbm_gbs']} GB/s\n")
 print("| kernel | ms/step | share | achieved | of peak |")
 print("|---|---|---|---|---|")
 busy = 0.0
