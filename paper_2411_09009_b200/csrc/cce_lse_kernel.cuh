@@ -280,14 +280,16 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
     // [slot][128][256]
     auto store_shat = [&](uint32_t tacc, int col0, int slot) {
       uint4* dst = reinterpret_cast<uint4*>(p.shat + ((size_t)slot * BM + row) * BN);
+      // 64 columns per step: each thread writes a full 128 B line of its row at once
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tacc + c * 32, r);
+      for (int c = 0; c < BN / 64; ++c) {
+        uint32_t r[64];
+        tmem_ld32(tacc + c * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32(tacc + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
         tmem_ld_wait();
-        uint32_t pk[16];
+        uint32_t pk[32];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
+        for (int j = 0; j < 64; j += 2) {
           float g2[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -298,15 +300,15 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
               z = p.softcap * th;
               dcap = 1.f - th * th;
             }
-            const int col = col0 + c * 32 + j + h;
+            const int col = col0 + c * 64 + j + h;
             const float s = (col < p.v) ? ex2_approx(z * LOG2E - lse2) : 0.f;
             g2[h] = ((col == pos_r && !p.label_split) ? s - 1.f : s) * up_r * dcap;
           }
           pk[j >> 1] = pack_bf16x2(g2[0], g2[1]);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        for (int q = 0; q < 8; ++q)
+          dst[c * 8 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
     };
 
@@ -402,27 +404,29 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
           if (slot >= 0) {
             const float zcmax = use_softcap ? p.softcap * softcap_tanh(zmax, inv_cap) : zmax;
             uint4* dst = reinterpret_cast<uint4*>(p.lab_buf + ((size_t)slot * BM + row) * BN);
+            // 64 columns per step: each thread writes a full 128 B line of its row at once
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-              uint32_t r[32];
-              tmem_ld32(tacc + c * 32, r);
+            for (int c = 0; c < BN / 64; ++c) {
+              uint32_t r[64];
+              tmem_ld32(tacc + c * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+              tmem_ld32(tacc + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
               tmem_ld_wait();
-              uint32_t pk[16];
+              uint32_t pk[32];
 #pragma unroll
-              for (int j = 0; j < 32; j += 2) {
+              for (int j = 0; j < 64; j += 2) {
                 float dd[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   float z = __uint_as_float(r[j + h]);
                   if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
-                  dd[h] = (col0 + c * 32 + j + h < p.v) ? z - zcmax : -INFINITY;
+                  dd[h] = (col0 + c * 64 + j + h < p.v) ? z - zcmax : -INFINITY;
                 }
                 const __half2 h2 = __floats2half2_rn(dd[0], dd[1]);
                 pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
               }
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                dst[c * 4 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+              for (int q = 0; q < 8; ++q)
+                dst[c * 8 + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
           }
         }
