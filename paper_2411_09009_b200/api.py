@@ -124,16 +124,27 @@ def _labels(x, vocab: int | None = None) -> torch.Tensor:
 
 
 def _pair(e, c, x=None):
+    """(E, C, X) on the device in the kernels' layout; a hidden size that is not a multiple of 8 is
+    zero-padded (logits unchanged) and _trim cuts the gradients back to the caller's D."""
     E = _matrix(e, "embeddings", 0)
     C = _matrix(c, "classifier", 1)
     if E.shape[1] != C.shape[1]:
         raise ValueError(f"feature dims differ: embeddings {E.shape[1]} vs classifier {C.shape[1]}")
+    E, C = ops.adapt_operands(E, C)
     X = None
     if x is not None:
         X = _labels(x, C.shape[0])
         if X.shape[0] != E.shape[0]:
             raise ValueError(f"label count {X.shape[0]} != token count {E.shape[0]}")
     return E, C, X
+
+
+def _hidden(e) -> int:
+    return int(e.shape[1]) if hasattr(e, "shape") else int(torch.as_tensor(e).shape[1])
+
+
+def _trim(g: torch.Tensor, d: int) -> torch.Tensor:
+    return g if g.shape[1] == d else g[:, :d].contiguous()
 
 
 def default_upstream(x, reduction: str, dtype=torch.float32) -> torch.Tensor:
@@ -240,7 +251,8 @@ def lse_backward(e, c, x, lse, upstream, blocks: BlockSpec | None = None,
         s = ops.stats_from_counters(counters, int((X != IGNORE_INDEX).sum()), C.shape[0])
         stats.total_tiles, stats.skipped_epsilon, stats.skipped_zero_upstream = (
             s.total_tiles, s.skipped_epsilon, s.skipped_zero_upstream)
-    return Gradients(d_e=de, d_c=dc.float())
+    d = _hidden(e)
+    return Gradients(d_e=_trim(de, d), d_c=_trim(dc.float(), d))
 
 
 def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | None = None):
@@ -249,7 +261,7 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
     blocks = blocks or BlockSpec()
     options = options or CceOptions()
     E, C, X = _pair(e, c, x)
-    n = E.shape[0]
+    n, d = E.shape[0], _hidden(e)
     valid = X != IGNORE_INDEX
     mean = perm = state = None
     if options.filtering:
@@ -286,7 +298,7 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
             s = ops.stats_from_counters(counters, int(valid.sum()), C.shape[0])
             stats.total_tiles, stats.skipped_epsilon, stats.skipped_zero_upstream = (
                 s.total_tiles, s.skipped_epsilon, s.skipped_zero_upstream)
-        return Gradients(d_e=de, d_c=dc.float())
+        return Gradients(d_e=_trim(de, d), d_c=_trim(dc.float(), d))
 
     return out, backward
 

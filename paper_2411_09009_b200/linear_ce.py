@@ -119,8 +119,9 @@ def linear_cross_entropy(
 ) -> torch.Tensor:
     """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
 
-    e: [..., D] bf16 CUDA embeddings; c: [V, D] bf16 classifier (nn.Linear weight layout);
-    targets: [...] int64.  Returns a scalar for "mean"/"sum", else per-token losses of shape
+    e: [..., D] CUDA embeddings; c: [V, D] classifier (nn.Linear weight layout); targets: [...]
+    integer labels.  The kernels compute in bf16: fp32/fp16 operands are cast (gradients come
+    back in the operands' dtype) and any D is accepted (zero-padded to a multiple of 8).  Returns a scalar for "mean"/"sum", else per-token losses of shape
     e.shape[:-1].  low_memory=True keeps only O(N) state between forward and backward and runs
     the backward over vocabulary groups (bounded transients: compacted E, an fp32 dE accumulator,
     one group's classifier rows and S-hat slots) at the cost of recomputing every logit tile;
@@ -139,8 +140,7 @@ def linear_cross_entropy(
     t2 = targets.reshape(-1)
     if t2.shape[0] != e2.shape[0]:
         raise ValueError(f"label count {t2.shape[0]} != token count {e2.shape[0]}")
-    if not e2.is_contiguous():
-        e2 = e2.contiguous()
+    e2, c = ops.adapt_operands(e2, c)  # bf16, contiguous, hidden size padded to a multiple of 8
     ops.check_operands(e2, c, t2.to(torch.int64) if t2.dtype != torch.int64 else t2)
     t2 = t2.to(torch.int64).contiguous()
     cap = float(softcap) if softcap else 0.0

@@ -78,6 +78,25 @@ def check_operands(e: torch.Tensor, c: torch.Tensor, targets: torch.Tensor | Non
             raise ValueError(f"targets must be int64, got {targets.dtype}")
 
 
+def adapt_operands(e: torch.Tensor, c: torch.Tensor):
+    """Bring caller operands to the kernels' layout: floating inputs are cast to bf16 (the compute
+    type), a strided classifier is made contiguous, and a hidden size that is not a multiple of 8
+    (16-byte TMA rows; the reference tests use d=4, test_kernels.py:361) is zero-padded -- zero
+    columns add nothing to any logit, and autograd slices the padding off dE / dC.  Anything that
+    is not a float, not 2-D or has mismatched feature dims is left for check_operands to reject."""
+    def cast(t):
+        if t.is_floating_point() and t.dtype != torch.bfloat16:
+            t = t.to(torch.bfloat16)
+        return t if t.is_contiguous() else t.contiguous()
+
+    e, c = cast(e), cast(c)
+    if e.dim() == 2 and c.dim() == 2 and e.shape[1] == c.shape[1] and e.shape[1] % 8:
+        pad = 8 - e.shape[1] % 8
+        e = torch.nn.functional.pad(e, (0, pad))
+        c = torch.nn.functional.pad(c, (0, pad))
+    return e, c
+
+
 def forward_local(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0):
     """Per-row log-sum-exp over this shard's vocabulary and the owned target logit.
 

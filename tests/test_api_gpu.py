@@ -130,3 +130,36 @@ def test_lse_forward_and_indexed_matmul(cuda_device):  # test_kernels.py:26-39, 
     assert O.rel_err(mean.cpu().numpy(), c.astype(np.float64) @ e.astype(np.float64).mean(0)) < 1e-4
     ones = api.indexed_matmul(np.ones((5, 8), np.float32), np.ones((3, 8), np.float32), np.array([0, 1, 2, 0, -1]))
     assert ones.tolist() == [8, 8, 8, 8, 0]
+
+
+@pytest.mark.parametrize("margin,kernel_tol", [(20.0, 5e-6), (10.0, 1e-5)])
+def test_cce_loss_margin_closed_form_d4(cuda_device, margin, kernel_tol):  # test_kernels.py:354-371
+    """The reference's own case at its own hidden size d=4 (zero-padded to 8 for the TMA rows)."""
+    api = _api()
+    v, d = 64, 4
+    c = np.zeros((v, d), np.float32)
+    c[13] = margin / d
+    out, back = api.cce_loss(np.ones((1, d), np.float32), c, np.array([13]))
+    expected = math.log(1.0 + (v - 1) * math.exp(-margin))
+    assert float(out.per_token_loss[0]) == pytest.approx(expected, abs=kernel_tol)
+    g = back()
+    assert tuple(g.d_e.shape) == (1, d) and tuple(g.d_c.shape) == (v, d)
+
+
+@pytest.mark.parametrize("d", [1, 4, 12, 30])
+@pytest.mark.parametrize("filtering", [False, True])
+def test_cce_loss_hidden_size_not_multiple_of_8(cuda_device, d, filtering):
+    api = _api()
+    e, c, x = _make(d, 300, 1100, 40 + d, sigma=3.0)
+    x[::7] = -1
+    opts = api.CceOptions(filtering=filtering)
+    out, back = api.cce_loss(e, c, x, options=opts)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    valid = x != -1
+    assert np.max(np.abs(out.per_token_loss.cpu().numpy()[valid] - nl[valid])) < 1e-3 * max(1.0, np.abs(nl).max())
+    g = back()
+    assert tuple(g.d_e.shape) == (300, d) and tuple(g.d_c.shape) == (1100, d)
+    fde, fdc = O.naive_backward(e, c, x, O.default_upstream(x, "mean-over-valid"))
+    tol = 2e-2 if filtering else 1e-2
+    assert O.rel_err(g.d_e.float().cpu().numpy(), fde) < tol
+    assert O.rel_err(g.d_c.float().cpu().numpy(), fdc) < tol

@@ -644,3 +644,34 @@ def test_stored_label_tiles_with_overflowing_recompute(cuda_device, monkeypatch)
     rde = np.zeros_like(e)
     rde[idx] = rde_c
     assert O.rel_err(small[2], rde) < GRAD_TOL and O.rel_err(small[3], rdc) < GRAD_TOL
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16])
+@pytest.mark.parametrize("d", [6, 64])
+@pytest.mark.parametrize("low", [False, True])
+def test_linear_cross_entropy_adapts_operands(cuda_device, dtype, d, low):
+    """Drop-in operands: fp32/fp16 tensors (computed in bf16, gradients returned in the operand
+    dtype), a strided classifier view and a hidden size that is not a multiple of 8."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    rng = np.random.default_rng(d)
+    n, v = 333, 2100
+    e_np = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c_np = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::9] = -100
+    e = torch.from_numpy(e_np).cuda().to(dtype).requires_grad_(True)
+    c_big = torch.zeros(v, d + 5, dtype=dtype, device="cuda")
+    c_big[:, :d] = torch.from_numpy(c_np).cuda().to(dtype)
+    c_big.requires_grad_(True)
+    c = c_big[:, :d]  # strided view
+    loss = linear_cross_entropy(e, c, torch.from_numpy(x).cuda(), low_memory=low)
+    loss.backward()
+    assert e.grad.dtype == dtype and e.grad.shape == (n, d) and c_big.grad.dtype == dtype
+    assert torch.all(c_big.grad[:, d:] == 0)
+    xo = np.where(x == -100, -1, x)
+    nl, _, _ = O.naive_forward(e_np, c_np, xo)
+    assert loss.item() == pytest.approx(float(nl[xo != -1].mean()), rel=1e-3, abs=1e-3)
+    fde, fdc = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"))
+    assert O.rel_err(e.grad.float().cpu().numpy(), fde) < 2e-2
+    assert O.rel_err(c_big.grad[:, :d].float().cpu().numpy(), fdc) < 2e-2
