@@ -347,6 +347,7 @@ __device__ __forceinline__ T block_sum(T v, T* s_tmp) {
 __global__ void list_count_kernel(const uint8_t* __restrict__ keep, int nt, int mt, int n_lo, int g,
                                   const int* run_if, const int32_t* __restrict__ lab_slot,
                                   int* __restrict__ cnt_m, int* __restrict__ rcnt_m) {
+  griddep_wait();
   if (run_if != nullptr && *run_if == 0) return;
   __shared__ int s_w[32];
   const int m = blockIdx.x;
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(1024) list_scan_kernel(const int* __restrict__
                                                          int* __restrict__ rlist_count, int* __restrict__ ok,
                                                          int* __restrict__ overflow, int* __restrict__ sched,
                                                          unsigned long long* __restrict__ counters) {
+  griddep_wait();
   if (run_if != nullptr && *run_if == 0) return;
   constexpr int T = 1024;
   __shared__ int s_a[32], s_b[32];
@@ -439,6 +441,7 @@ __global__ void list_fill_kernel(const uint8_t* __restrict__ keep, int nt, int m
                                  const int* run_if, const int* __restrict__ off_m, const int* __restrict__ roff_m,
                                  int2* __restrict__ alist, int2* __restrict__ rlist, int32_t* __restrict__ slot_of,
                                  int* __restrict__ cnt_n) {
+  griddep_wait();
   if (run_if != nullptr && *run_if == 0) return;
   __shared__ int s_a[32], s_b[32];
   __shared__ int s_base, s_rbase;
@@ -574,6 +577,7 @@ __global__ void __launch_bounds__(1024) list_single_kernel(
     int* __restrict__ off_m, int* __restrict__ roff_m, int2* __restrict__ alist, int2* __restrict__ rlist,
     int32_t* __restrict__ slot_of, int* __restrict__ cnt_n, int* __restrict__ list_count,
     int* __restrict__ rlist_count, int* __restrict__ sched, int2* __restrict__ pairs, int* __restrict__ pair_count) {
+  griddep_wait();
   if (run_if != nullptr && *run_if == 0) return;
   constexpr int T = 1024, W = T / 32;
   __shared__ int s_a[W], s_b[W], s_c[W];
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(1024) list_single_kernel(
 __global__ void __launch_bounds__(1024) build_pairs_kernel(const int* __restrict__ cnt_m, int mt,
                                                            const int* run_if, int2* __restrict__ pairs,
                                                            int* __restrict__ pair_count) {
+  griddep_wait();
   if (run_if != nullptr && *run_if == 0) return;
   constexpr int T = 1024;
   __shared__ int s_a[T / 32], s_b[T / 32];

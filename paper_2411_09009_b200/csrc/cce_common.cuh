@@ -111,7 +111,7 @@ struct GradParams {
   const int2* list;        // dC: vocab-tile-major kept list (slot = index, .x = token tile), or nullptr
   const int* off_m;        //     first slot of each vocab tile (its cnt_m slots are consecutive)
   int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
-  int de_order;            // dE: 0 chunk-major units, 1 token-tile-major
+  int de_order;            // dE: 0 chunk-major units, 1 token-tile-major, K>=2 groups of K chunks
   int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)
   int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
 };
@@ -129,7 +129,23 @@ struct Rows {
   }
 };
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may be scheduled
+// before its predecessor in the stream has finished; every thread waits here, before touching
+// anything upstream kernels wrote (and before exiting, so completion stays transitive along a
+// chain of gated-off kernels).  Without the attribute the wait returns at once.
+#ifndef CCE_PDL_TRIGGER
+#define CCE_PDL_TRIGGER 1
+#endif
+__device__ __forceinline__ void griddep_wait() {
+#if CCE_PDL_TRIGGER
+  // let the next kernel be scheduled now; its own griddep_wait still orders it after this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ bool skip_launch(const int* run_if) {
+  griddep_wait();
   return run_if != nullptr && *run_if == 0;
 }
 

@@ -163,6 +163,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (p.de_order == 0) {
       j = u / G;
       ln = u % G;
+    } else if (p.de_order >= 2) {
+      // groups of K = de_order chunk pairs, token-tile-major inside a group: the K CTAs of one
+      // token tile run side by side (static round-robin, grid a multiple of K) and read each
+      // S-hat tile at the same time, so it comes from HBM once per group instead of once per chunk
+      const int K = p.de_order;
+      const int g = u / (G * K);
+      const int kg = min(K, npair - g * K);
+      const int r = u - g * G * K;
+      ln = r / kg;
+      j = g * K + r % kg;
     } else {
       ln = u / npair;
       j = u % npair;

@@ -136,6 +136,56 @@ template <int CH, int KV>
 constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH, KV>::SMEM + kCtrlBytes; }
 constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
 
+// Launches inside the kept backward's pass chain use programmatic dependent launch (every kernel
+// there begins with griddepcontrol.wait): the next kernel is scheduled while its predecessor
+// drains, which matters for the worst-case fallback chain -- a few dozen gated-off launches per
+// step that otherwise cost a full launch gap each.  CCE_PDL=0 turns it off.
+thread_local bool g_pdl = false;
+
+bool pdl_allowed() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CCE_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(bool on) : prev(g_pdl) { g_pdl = on && pdl_allowed(); }
+  ~PdlScope() { g_pdl = prev; }
+};
+
+// cudaLaunchKernelEx with an optional cluster dimension and the PDL attribute when g_pdl is set
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int cluster,
+             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  unsigned na = 0;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (g_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  CCE_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  return 0;
+}
+
 template <typename K>
 int ensure_attr(K kernel, size_t bytes) {
   // cudaFuncSetAttribute is cheap; call it every launch so multi-device use stays correct.
@@ -243,28 +293,14 @@ int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CU
   if (!pair) {
     if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 1>, kLseSmem)) return e;
     const int units = p.nt * p.splits;
-    cce::cce_lse_kernel<MODE, 1><<<std::max(1, std::min(num_sms(), units)), cce::NUM_THREADS, kLseSmem,
-                                   stream>>>(tmE, tmEg, tmC256, tmCg, p);
-    CCE_CUDA(cudaGetLastError());
-    return 0;
+    return launch_k(cce::cce_lse_kernel<MODE, 1>, dim3(std::max(1, std::min(num_sms(), units))),
+                    dim3(cce::NUM_THREADS), kLseSmem, stream, 1, tmE, tmEg, tmC256, tmCg, p);
   }
   if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 2>, kLsePairSmem)) return e;
   const int pair_units = ((p.nt + 1) / 2) * p.splits;
   const int grid = 2 * std::max(1, std::min(num_sms() / 2, pair_units));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(cce::NUM_THREADS);
-  cfg.dynamicSmemBytes = kLsePairSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CCE_CUDA(cudaLaunchKernelEx(&cfg, cce::cce_lse_kernel<MODE, 2>, tmE, tmEg, tmC128, tmCg, p));
-  return 0;
+  return launch_k(cce::cce_lse_kernel<MODE, 2>, dim3(grid), dim3(cce::NUM_THREADS), kLsePairSmem, stream, 2,
+                  tmE, tmEg, tmC128, tmCg, p);
 }
 
 struct KeptWs {
@@ -330,10 +366,10 @@ int launch_de_t(const cce::GradParams& q, int units, const void* shat, int64_t s
                   (d % 64 == 0 ? make_tmap3d(&tmC3, C, v, d, KV, cce::DCH / 64) : (tmC3 = tmC, true));
   if (!ok) return fail("cce_de: cuTensorMapEncodeTiled failed");
   if (int e = ensure_attr(cce::cce_de_kernel<CH, KV>, de_smem<CH, KV>())) return e;
-  const int grid = std::max(1, std::min(num_sms(), units));
-  cce::cce_de_kernel<CH, KV><<<grid, cce::NUM_THREADS, de_smem<CH, KV>(), stream>>>(tmS, tmC, tmC3, tmCg, q);
-  CCE_CUDA(cudaGetLastError());
-  return 0;
+  int grid = std::max(1, std::min(num_sms(), units));
+  if (q.de_order >= 2 && q.sched == nullptr && grid >= q.de_order) grid -= grid % q.de_order;
+  return launch_k(cce::cce_de_kernel<CH, KV>, dim3(grid), dim3(cce::NUM_THREADS), de_smem<CH, KV>(), stream, 1,
+                  tmS, tmC, tmC3, tmCg, q);
 }
 
 int launch_de(cce::GradParams q, int* sched_ctr, const void* shat, int64_t shat_rows, const void* C,
@@ -382,26 +418,12 @@ int launch_dc(const cce::GradParams& q, bool pair, const CUtensorMap& tmS64, con
   const int units = q.mt * q.ndc * 2;
   if (!pair) {
     if (int e = ensure_attr(cce::cce_dc_kernel<1>, kDcSmem)) return e;
-    cce::cce_dc_kernel<1><<<std::min(num_sms(), units), cce::NUM_THREADS, kDcSmem, stream>>>(tmS64, tmE64, tmE3,
-                                                                                              tmEg, q);
-    CCE_CUDA(cudaGetLastError());
-    return 0;
+    return launch_k(cce::cce_dc_kernel<1>, dim3(std::min(num_sms(), units)), dim3(cce::NUM_THREADS), kDcSmem,
+                    stream, 1, tmS64, tmE64, tmE3, tmEg, q);
   }
   if (int e = ensure_attr(cce::cce_dc_kernel<2>, kDcSmem)) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * std::max(1, std::min(num_sms() / 2, units / 2)));
-  cfg.blockDim = dim3(cce::NUM_THREADS);
-  cfg.dynamicSmemBytes = kDcSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CCE_CUDA(cudaLaunchKernelEx(&cfg, cce::cce_dc_kernel<2>, tmS64, tmE64, tmE3h, tmE64, q));
-  return 0;
+  return launch_k(cce::cce_dc_kernel<2>, dim3(2 * std::max(1, std::min(num_sms() / 2, units / 2))),
+                  dim3(cce::NUM_THREADS), kDcSmem, stream, 2, tmS64, tmE64, tmE3h, tmE64, q);
 }
 
 }  // namespace
@@ -816,26 +838,27 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     // The whole-batch pass uses parallel kernels, fallback passes one block (they usually do not
     // run, and then cost one launch)
     if (primary) {
-      cce::list_count_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, run_if, lab_slot, w.cnt_m, w.rcnt_m);
-      CCE_CUDA(cudaGetLastError());
-      cce::list_scan_kernel<<<1, 1024, 0, stream>>>(w.cnt_m, w.rcnt_m, mt, g, (int)capacity_tiles, run_if, 1,
-                                                    w.off_m, w.roff_m, w.cnt_n, w.list_count, w.rlist_count,
-                                                    w.ok, overflow, w.list_count + 3, counters);
-      CCE_CUDA(cudaGetLastError());
-      cce::list_fill_kernel<<<mt, 128, 0, stream>>>(w.keep, nt, mt, g0, g, (int)capacity_tiles, (int)lab_capacity,
-                                                    lab_slot, run_if, w.off_m, w.roff_m, w.alist, w.rlist,
-                                                    w.slot_of, w.cnt_n);
-      CCE_CUDA(cudaGetLastError());
-      if (pair) {
-        cce::build_pairs_kernel<<<1, 1024, 0, stream>>>(w.rcnt_m, mt, w.ok, w.pairs, w.pair_count);
-        CCE_CUDA(cudaGetLastError());
-      }
+      if (int e = launch_k(cce::list_count_kernel, dim3(mt), dim3(128), 0, stream, 1, w.keep, nt, mt, g0, g,
+                           run_if, lab_slot, w.cnt_m, w.rcnt_m))
+        return e;
+      if (int e = launch_k(cce::list_scan_kernel, dim3(1), dim3(1024), 0, stream, 1, w.cnt_m, w.rcnt_m, mt, g,
+                           (int)capacity_tiles, run_if, 1, w.off_m, w.roff_m, w.cnt_n, w.list_count,
+                           w.rlist_count, w.ok, overflow, w.list_count + 3, counters))
+        return e;
+      if (int e = launch_k(cce::list_fill_kernel, dim3(mt), dim3(128), 0, stream, 1, w.keep, nt, mt, g0, g,
+                           (int)capacity_tiles, (int)lab_capacity, lab_slot, run_if, w.off_m, w.roff_m, w.alist,
+                           w.rlist, w.slot_of, w.cnt_n))
+        return e;
+      if (pair)
+        if (int e = launch_k(cce::build_pairs_kernel, dim3(1), dim3(1024), 0, stream, 1, w.rcnt_m, mt,
+                             (const int*)w.ok, w.pairs, w.pair_count))
+          return e;
     } else {
-      cce::list_single_kernel<<<1, 1024, 0, stream>>>(
-          w.keep, nt, mt, g0, g, (int)capacity_tiles, (int)lab_capacity, lab_slot, run_if, w.cnt_m, w.rcnt_m,
-          w.off_m, w.roff_m, w.alist, w.rlist, w.slot_of, w.cnt_n, w.list_count, w.rlist_count,
-          w.list_count + 3, w.pairs, w.pair_count);
-      CCE_CUDA(cudaGetLastError());
+      if (int e = launch_k(cce::list_single_kernel, dim3(1), dim3(1024), 0, stream, 1, w.keep, nt, mt, g0, g,
+                           (int)capacity_tiles, (int)lab_capacity, lab_slot, run_if, w.cnt_m, w.rcnt_m, w.off_m,
+                           w.roff_m, w.alist, w.rlist, w.slot_of, w.cnt_n, w.list_count, w.rlist_count,
+                           w.list_count + 3, w.pairs, w.pair_count))
+        return e;
     }
     const int* gate = primary ? w.ok : run_if;  // primary: only if every tile to recompute got a slot
     cce::Params p{};
@@ -898,6 +921,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   // The counts are only known on the device: the whole-batch pass runs iff its tiles to
   // recompute fit; otherwise (*overflow) token-tile groups sized for the worst case run instead.
   const bool grouped = (int64_t)nt * mt > capacity_tiles;
+  PdlScope pdl_scope(true);
   if (int e = run_pass(0, nt, true, nullptr, !grouped)) return e;
   if (stats) {  // label tiles stored by the forward, tiles the whole-batch pass had to recompute
     if (lab_capacity > 0)
@@ -906,7 +930,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
       CCE_CUDA(cudaMemsetAsync(stats, 0, sizeof(int), stream));
     CCE_CUDA(cudaMemcpyAsync(stats + 1, w.rlist_count, sizeof(int), cudaMemcpyDeviceToDevice, stream));
   }
-  if (grouped) {
+  if (grouped && !getenv("CCE_MEASURE_NO_FALLBACK")) {  // the env switch is for A/B timing only
     const int g = (int)std::max<int64_t>(1, capacity_tiles / mt);
     for (int g0 = 0; g0 < nt; g0 += g)
       if (int e = run_pass(g0, std::min(g, nt - g0), false, overflow, g0 + g >= nt)) return e;
