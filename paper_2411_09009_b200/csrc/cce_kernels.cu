@@ -129,6 +129,31 @@ int num_sms() {
   return sms;
 }
 
+// A non-blocking side stream and fork/join events per device (created once; stream-capture
+// safe: the fork/join is expressed with event record / wait only).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+SideStream* side_stream() {
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& x = per_dev[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      x.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &x;
+}
+
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
 constexpr size_t kLsePairSmem = 1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes;
@@ -806,11 +831,22 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   // S-hat slots: [stored label tiles (lab_capacity) | recomputed tiles (capacity_tiles)]
   __nv_bfloat16* shat_all = static_cast<__nv_bfloat16*>(shat);
   __nv_bfloat16* shat_rec = shat_all + (size_t)lab_capacity * cce::BM * cce::BN;
-  if (lab_capacity > 0) {  // stored label tiles -> S-hat, in place
-    cce::label_shat_kernel<<<(unsigned)lab_capacity, 256, 0, stream>>>(
+  // Stored label tiles -> S-hat, in place.  HBM-bound and independent of the kept lists, so it
+  // runs on a side stream beside the list kernels and the tensor-bound recompute pass; dE joins.
+  const char* side_env = getenv("CCE_LABEL_SIDE");  // 0: same stream (A/B timing)
+  SideStream* side = (lab_capacity > 0 && (!side_env || atoi(side_env) != 0)) ? side_stream() : nullptr;
+  if (lab_capacity > 0) {
+    cudaStream_t ls = stream;
+    if (side) {
+      CCE_CUDA(cudaEventRecord(side->fork, stream));
+      CCE_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+      ls = side->s;
+    }
+    cce::label_shat_kernel<<<(unsigned)lab_capacity, 256, 0, ls>>>(
         reinterpret_cast<__half*>(shat_all), static_cast<const int2*>(lab_list), lab_count, (int)lab_capacity,
         w.block_zero, mt, tile_max, lse, upstream, pos, row_map, n_valid, (int)v, softcap, label_split);
     CCE_CUDA(cudaGetLastError());
+    if (side) CCE_CUDA(cudaEventRecord(side->join, side->s));
   }
 
   CUtensorMap tmE, tmC, tmC64, tmC128h, tmE64, tmS64, tmC3, tmE3, tmE3h;
@@ -913,6 +949,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.accumulate = g0 > 0;
     q.list = w.alist;
     q.off_m = w.off_m;
+    if (primary && side) CCE_CUDA(cudaStreamWaitEvent(stream, side->join, 0));  // label S-hat ready
     if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, C_t, tmC64, stream)) return e;
     if (last && de_done_event)  // every dE write of this call is enqueued before this point
       CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
