@@ -129,7 +129,12 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * counters as cce_bwd.
  * de_done_event (a cudaEvent_t, may be NULL) is recorded on the stream once every dE write of the
  * call has been enqueued, before the dC pass: a vocab-parallel caller all-reduces dE on another
- * stream while dC runs. */
+ * stream while dC runs.
+ * dc may alias C_t (dc == C_t): the sorted copy is last read by the dE pass, so its storage can
+ * become the dC output and no transient holds a second V x D matrix.  C is then the caller's
+ * classifier in its own row order and the fallback groups read it through perm_padded (row
+ * gathers) instead of C_t, which an earlier group's dC pass has overwritten.  C may be NULL when
+ * dc does not alias C_t. */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
@@ -137,7 +142,7 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
                   int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream);
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
                                     int64_t lab_capacity);
-int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,

@@ -803,7 +803,7 @@ size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t cap
   return kept_layout(nullptr, n, v, capacity_tiles, lab_capacity).total;
 }
 
-int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, const int32_t* row_map,
+int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t* perm_padded, const int32_t* row_map,
                  const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
@@ -814,6 +814,11 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
   if (!overflow || !shat) return fail("cce_bwd_kept: overflow flag and S-hat buffer required");
+  // dc aliasing C_t: the fallback passes (which may follow an earlier group's dC pass) read the
+  // caller's C through the permutation instead of the sorted copy
+  const bool aliased = dc == C_t;
+  if (aliased && (C == nullptr || perm_padded == nullptr))
+    return fail("cce_bwd_kept: dc aliases C_t, so C and perm_padded are required");
   if (lab_slot == nullptr) lab_capacity = 0;
   if (n <= 0) return 0;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
@@ -864,6 +869,9 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     tmE3 = tmE64;
     tmE3h = tmE64;
   }
+  CUtensorMap tmCo, tmCog;  // the caller's C (row gathers through perm_padded) for aliased fallbacks
+  if (ok && aliased)
+    ok = make_tmap(&tmCo, C, v, d, cce::BN) && make_tmap(&tmCog, C, v, d, gather_box_rows());
   if (!ok) return fail("cce_bwd_kept: cuTensorMapEncodeTiled failed");
   const bool pair = use_pairs();
 
@@ -923,7 +931,13 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     p.list_count = w.rlist_count;
     p.pairs = w.pairs;
     p.pair_count = w.pair_count;
-    if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) return e;
+    const bool gathered = aliased && !primary;  // C_t may already hold dC: gather from C
+    if (gathered) {
+      p.perm = perm_padded;
+      if (int e = launch_lse<cce::KEPT>(p, false, tmE, tmE, tmCo, tmCog, tmC128h, stream)) return e;
+    } else if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) {
+      return e;
+    }
 
     cce::GradParams q{};
     q.n_total = (int)n;
@@ -938,7 +952,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.slot_of = w.slot_of;  // rows of this pass, local token-tile index; unified slots
     q.cnt_n = w.cnt_n;
     q.cnt_m = w.cnt_m;
-    q.perm = nullptr;
+    q.perm = gathered ? perm_padded : nullptr;
     q.perm_store = perm_padded;
     q.row_map = row_map;
     q.e_gather = 0;
@@ -950,7 +964,9 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const int32_t* perm_padded, c
     q.list = w.alist;
     q.off_m = w.off_m;
     if (primary && side) CCE_CUDA(cudaStreamWaitEvent(stream, side->join, 0));  // label S-hat ready
-    if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, C_t, tmC64, stream)) return e;
+    if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, gathered ? C : C_t, gathered ? tmCog : tmC64,
+                          stream))
+      return e;
     if (last && de_done_event)  // every dE write of this call is enqueued before this point
       CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
     return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);

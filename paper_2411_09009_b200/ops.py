@@ -418,7 +418,7 @@ class TileState:
         own += [t for t in (self.shat, self.lab_slot, self.lab_list, self.lab_count) if t is not None]
         if self.perm is not None:
             own += [self.c_t, self.perm, self.perm_padded]
-        return sum(t.numel() * t.element_size() for t in own)
+        return sum(t.numel() * t.element_size() for t in own if t is not None)
 
 
 def gather_rows(src: torch.Tensor, index: torch.Tensor, rows: int) -> torch.Tensor:
@@ -519,7 +519,12 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     lse = lse.to(torch.float32).contiguous()
     upstream = upstream.to(torch.float32).contiguous()
     de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev)
-    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    # The sorted classifier copy is last read by the dE pass, so its storage becomes the dC output
+    # (the library reads C through the permutation wherever C_t may already hold dC): no second
+    # V x D matrix is ever live.  CCE_ALIAS_DC=0 allocates dC separately (A/B).
+    alias = state.perm is not None and os.environ.get("CCE_ALIAS_DC", "1") != "0"
+    dc = c_t if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    state.c_t = None
     counters = torch.zeros(3, dtype=torch.int64, device=dev)
     if n == 0:
         return de, dc.zero_(), counters
@@ -539,7 +544,8 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     ws_bytes = lib.cce_bwd_kept_workspace_bytes(n, d, v, cap, lab_cap)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     ev = _ev_begin("bwd")
-    _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.perm_padded), _p(state.row_map),
+    _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.c if alias else None),
+                                _p(state.perm_padded), _p(state.row_map),
                                 _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
                                 n, d, v, state.softcap, float(eps), int(bool(label_split)), _p(state.shat),
                                 lab_cap, _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), cap,

@@ -675,3 +675,31 @@ def test_linear_cross_entropy_adapts_operands(cuda_device, dtype, d, low):
     fde, fdc = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"))
     assert O.rel_err(e.grad.float().cpu().numpy(), fde) < 2e-2
     assert O.rel_err(c_big.grad[:, :d].float().cpu().numpy(), fdc) < 2e-2
+
+
+@pytest.mark.parametrize("budget", [None, "1"])
+@pytest.mark.parametrize("store", ["1", "0"])
+def test_dc_aliasing_sorted_copy_is_bit_identical(cuda_device, monkeypatch, budget, store):
+    """dC written into the storage of the sorted classifier copy (the default) equals a separate dC
+    buffer bit for bit: on the whole-batch pass, and on the overflow fallback groups, which then
+    read C through the permutation with row gathers (an earlier group's dC pass has overwritten
+    C_t).  dE is checked the same way."""
+    from paper_2411_09009_b200 import ops
+
+    rng = np.random.default_rng(31)
+    n, d, v = 3000, 64, 20000  # non-label kept tiles exceed the capacity floor (one token tile: 79)
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 3.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::11] = -1
+    monkeypatch.setenv("CCE_STORE_LABELS", store)
+    if budget:
+        monkeypatch.setenv("CCE_SHAT_BUDGET_MB", budget)
+    monkeypatch.setenv("CCE_ALIAS_DC", "0")
+    sep = _run(e, c, x, path="tiles")
+    flag_sep = int(ops.LAST_OVERFLOW["flag"].item())
+    monkeypatch.setenv("CCE_ALIAS_DC", "1")
+    ali = _run(e, c, x, path="tiles")
+    assert int(ops.LAST_OVERFLOW["flag"].item()) == flag_sep == (1 if budget else 0)
+    for a, b in zip(sep[:5], ali[:5]):
+        assert np.array_equal(a, b)
