@@ -129,19 +129,18 @@ int num_sms() {
   return sms;
 }
 
-// A non-blocking side stream and fork/join events per device (created once; stream-capture
-// safe: the fork/join is expressed with event record / wait only).
+// A non-blocking side stream and fork/join events per host thread and device (created once;
+// stream-capture safe: the fork/join is expressed with event record / wait only).  Per thread,
+// so concurrent callers never re-record each other's join event between record and wait.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 SideStream* side_stream() {
-  static std::mutex mu;
-  static SideStream per_dev[64];
+  thread_local SideStream per_dev[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
   SideStream& x = per_dev[dev];
   if (!x.s) {
     if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||

@@ -20,7 +20,7 @@ def step():
     e.grad = c.grad = None
     linear_cross_entropy(e, c, t, softcap=cap or None).backward()
 
-for _ in range(3):
+for _ in range(int(os.environ.get("TRACE_WARM", "3"))):  # e.g. 40: settle the power state first
     step()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
