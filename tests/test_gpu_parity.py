@@ -703,3 +703,58 @@ def test_dc_aliasing_sorted_copy_is_bit_identical(cuda_device, monkeypatch, budg
     assert int(ops.LAST_OVERFLOW["flag"].item()) == flag_sep == (1 if budget else 0)
     for a, b in zip(sep[:5], ali[:5]):
         assert np.array_equal(a, b)
+
+
+def test_concurrent_callers_on_two_streams(cuda_device):
+    """Two host threads, each on its own CUDA stream, run training steps at the same time
+    (reference: safe to call concurrently on disjoint outputs).  Every result equals
+    the sequential run bit for bit: the side stream / fork-join events and the launch attributes
+    are per thread, the workspaces per call."""
+    import threading
+
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    def make(seed, n, d, v):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        e = torch.randn(n, d, device="cuda", generator=g).bfloat16()
+        c = (torch.randn(v, d, device="cuda", generator=g) * 2.0 / math.sqrt(d)).bfloat16()
+        t = torch.randint(0, v, (n,), device="cuda", generator=g)
+        return e, c, t
+
+    def step(e, c, t):
+        ee = e.clone().requires_grad_(True)
+        cc = c.clone().requires_grad_(True)
+        loss = linear_cross_entropy(ee, cc, t)
+        loss.backward()
+        return loss.detach(), ee.grad, cc.grad
+
+    jobs = [make(1, 1000, 128, 9000), make(2, 1500, 256, 7000)]
+    for _ in range(3):  # learn the S-hat capacities, so every run takes the whole-batch pass
+        for j in jobs:
+            step(*j)
+    torch.cuda.synchronize()
+    ref = [step(*j) for j in jobs]
+    torch.cuda.synchronize()
+    out = [[None] * 4 for _ in jobs]
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for k in range(4):
+                    out[i][k] = step(*jobs[i])
+            s.synchronize()
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(len(jobs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+    for i in range(len(jobs)):
+        for k in range(4):
+            for a, b in zip(ref[i], out[i][k]):
+                assert torch.equal(a, b), (i, k)
