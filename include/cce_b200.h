@@ -134,21 +134,27 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * become the dC output and no transient holds a second V x D matrix.  C is then the caller's
  * classifier in its own row order and the fallback groups read it through perm_padded (row
  * gathers) instead of C_t, which an earlier group's dC pass has overwritten.  C may be NULL when
- * dc does not alias C_t. */
+ * dc does not alias C_t.
+ * Vocabulary groups (cce_fwd_tiles and cce_bwd_kept): C_t may hold only the sorted rows
+ * [pos_offset, pos_offset + v) of the vocabulary, pos_offset a multiple of 256; label positions
+ * pos are global and pos - pos_offset is group-local, tile_max is the group's own
+ * [ceil(n/128)][ceil(v/256)][128] block and perm_padded points at the group's first entry.  With
+ * de_accumulate (fp32 dE only) the call adds its dE into de_out instead of writing it, so the
+ * groups of one backward accumulate in a fixed order. */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
-                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
                   size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
                   int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream);
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
                                     int64_t lab_capacity);
 int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t* perm_padded, const int32_t* row_map,
-                 const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                 const int* n_valid, const int32_t* pos, int64_t pos_offset, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
                  const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
-                 void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
-                 int* stats, void* de_done_event, void* stream);
+                 void* de_out, int de_fp32, int de_accumulate, void* dc, unsigned long long* counters,
+                 int* overflow, int* stats, void* de_done_event, void* stream);
 
 /* ---- low-memory backward: vocabulary groups (low_memory=True) ----
  * lse_backward over groups of `group_vtiles` vocab tiles in tile order: per group, the group's

@@ -262,7 +262,7 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
 // Grid (ceil(mt / 64), nt), 256 threads: warp w takes vocab tiles blockIdx.x * 64 + w + 8j, lane l
 // rows 4l .. 4l + 3.  counters[1] += eps-skipped, counters[2] += zero-upstream-skipped tiles.
 __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const float* __restrict__ lse,
-                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ row_map,
+                                    const int32_t* __restrict__ pos, int pos_offset, const int32_t* __restrict__ row_map,
                                     const int* __restrict__ n_valid, const uint8_t* __restrict__ block_zero,
                                     int nt, int mt, float softcap, float eps, int label_split,
                                     uint8_t* __restrict__ keep, unsigned long long* __restrict__ counters) {
@@ -295,7 +295,7 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
     ok[k] = grow < nv;
     const int orow = ok[k] ? row_map[grow] : 0;
     lse2[k] = ok[k] ? lse[orow] * LOG2E : INFINITY;
-    pr[k] = ok[k] ? pos[orow] : -1;
+    pr[k] = ok[k] ? pos[orow] - pos_offset : -1;  // vocabulary group: group-local position
   }
   unsigned skipped = 0;
   for (int m = m_lo + warp; m < m_hi; m += 8) {

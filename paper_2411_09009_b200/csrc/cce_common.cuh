@@ -66,7 +66,7 @@ struct Params {
   const float* lse;        // global log-sum-exp (natural log)
   const float* upstream;   // dLoss/dloss_i, 0 at ignored rows
   const int32_t* pos;      // label position in tile order, -1 if none (FWD: nullptr = targets)
-  int pos_offset;          // BWD over a vocabulary group: pos - pos_offset is group-local
+  int pos_offset;          // over a vocabulary group: pos - pos_offset is group-local
   int label_split;         // 1: paper ordering -- filter on S alone, S-hat without the -1 (the
                            //    label term is applied separately, cce_label_terms)
   const int32_t* perm;     // [mt*BN] tile-order position -> C row for gathers (nullptr = plain)

@@ -743,7 +743,7 @@ size_t cce_tile_max_bytes(int64_t n, int64_t v) {
 }
 
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
-                  const int32_t* pos, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
                   size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
                   int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
@@ -774,6 +774,7 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
   p.softcap = softcap;
   p.pos = pos;
+  p.pos_offset = (int)pos_offset;
   p.row_map = row_map;
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
@@ -803,12 +804,12 @@ size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t cap
 }
 
 int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t* perm_padded, const int32_t* row_map,
-                 const int* n_valid, const int32_t* pos, const float* lse, const float* upstream,
+                 const int* n_valid, const int32_t* pos, int64_t pos_offset, const float* lse, const float* upstream,
                  const float* tile_max, int64_t n, int64_t d, int64_t v, float softcap, float eps,
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
                  const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
-                 void* de_out, int de_fp32, void* dc, unsigned long long* counters, int* overflow,
-                 int* stats, void* de_done_event, void* stream_ptr) {
+                 void* de_out, int de_fp32, int de_accumulate, void* dc, unsigned long long* counters,
+                 int* overflow, int* stats, void* de_done_event, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
@@ -819,6 +820,9 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
   if (aliased && (C == nullptr || perm_padded == nullptr))
     return fail("cce_bwd_kept: dc aliases C_t, so C and perm_padded are required");
   if (lab_slot == nullptr) lab_capacity = 0;
+  if (de_accumulate && !de_fp32) return fail("cce_bwd_kept: de_accumulate needs the fp32 dE");
+  if (lab_capacity > 0 && pos_offset != 0)
+    return fail("cce_bwd_kept: stored label tiles are not supported over a vocabulary group (pos_offset)");
   if (n <= 0) return 0;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
@@ -830,7 +834,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
-      tile_max, lse, pos, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split, w.keep, counters);
+      tile_max, lse, pos, (int)pos_offset, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split,
+      w.keep, counters);
   CCE_CUDA(cudaGetLastError());
   // S-hat slots: [stored label tiles (lab_capacity) | recomputed tiles (capacity_tiles)]
   __nv_bfloat16* shat_all = static_cast<__nv_bfloat16*>(shat);
@@ -920,6 +925,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     p.lse = lse;
     p.upstream = upstream;
     p.pos = pos;
+    p.pos_offset = (int)pos_offset;
     p.row_map = row_map;
     p.eps = eps;
     p.label_split = label_split;
@@ -958,6 +964,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     q.atoms3d = atoms3d ? 1 : 0;
     q.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
     q.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
+    q.de_accumulate = de_accumulate ? 1 : 0;  // vocabulary groups after the first add into dE
     q.dc = static_cast<__nv_bfloat16*>(dc);
     q.accumulate = g0 > 0;
     q.list = w.alist;

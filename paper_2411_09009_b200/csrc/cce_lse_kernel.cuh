@@ -263,7 +263,7 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
         tpos = -1;
         if (valid) {
           if (p.pos) {
-            tpos = p.pos[orow];
+            tpos = p.pos[orow] - p.pos_offset;  // vocabulary group: group-local position
           } else {
             const int64_t tg = p.targets[orow];
             if (tg != p.ignore_index) tpos = tg - p.vocab_start;

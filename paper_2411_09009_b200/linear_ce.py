@@ -19,6 +19,8 @@ full loss, dE is all-reduced, dC stays local (see vocab_parallel.py).
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import ops
@@ -49,10 +51,15 @@ class _LinearCrossEntropy(torch.autograd.Function):
         # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
         # backward, which then runs over vocabulary groups (ops.backward_lowmem).
         ctx.state = None
-        if eps > 0 and not low_memory and (ctx.needs_input_grad[0] or ctx.needs_input_grad[1]):
+        training = ctx.needs_input_grad[0] or ctx.needs_input_grad[1]
+        if eps > 0 and not low_memory and training:
             lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
                                                               softcap, vocab_sorting, eps=eps,
                                                               label_split=not exempt_label_tiles)
+        elif eps > 0 and low_memory and training and os.environ.get("CCE_LOWMEM_RECOMPUTE", "0") == "0":
+            # bounded memory: the same decision from the forward, over vocabulary groups
+            lse_local, correct, ctx.state = ops.forward_grouped(e, c, targets, ignore_index, vocab_start,
+                                                                softcap, vocab_sorting)
         else:
             lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
         if group is None:
@@ -78,7 +85,17 @@ class _LinearCrossEntropy(torch.autograd.Function):
         up = ops.upstream(grad_out, targets, ignore_index, reduction)  # default_upstream, core.py:181-200
         state, ctx.state = ctx.state, None
         split, correct, ctx.correct = ctx.split, ctx.correct, None
-        if state is not None:
+        if isinstance(state, ops.GroupState):
+            done = torch.cuda.Event() if group is not None else None
+            de, dc, _ = ops.backward_grouped(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                                             fp32_de=group is not None, de_done=done, label_split=split,
+                                             correct=correct)
+            del state
+            if group is not None:
+                from .vocab_parallel import all_reduce_de_overlapped
+
+                de = all_reduce_de_overlapped(de, done, group)
+        elif state is not None:
             if group is None:
                 de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
                                                label_split=split, correct=correct)
@@ -122,11 +139,12 @@ def linear_cross_entropy(
     e: [..., D] CUDA embeddings; c: [V, D] classifier (nn.Linear weight layout); targets: [...]
     integer labels.  The kernels compute in bf16: fp32/fp16 operands are cast (gradients come
     back in the operands' dtype) and any D is accepted (zero-padded to a multiple of 8).  Returns a scalar for "mean"/"sum", else per-token losses of shape
-    e.shape[:-1].  low_memory=True keeps only O(N) state between forward and backward and runs
-    the backward over vocabulary groups (bounded transients: compacted E, an fp32 dE accumulator,
-    one group's classifier rows and S-hat slots) at the cost of recomputing every logit tile;
-    the default keeps the sorted classifier copy and per-tile row maxima from the forward so the
-    backward recomputes only the tiles it keeps.
+    e.shape[:-1].  The default keeps the sorted classifier copy and per-tile row maxima from the
+    forward, so the backward recomputes only the tiles it keeps.  low_memory=True bounds the
+    transients: forward and backward run over vocabulary groups of the sorted order, only one
+    group's classifier rows and S-hat slots exist at a time, and dE accumulates in fp32 (the
+    per-tile row maxima and the compacted E are kept from the forward; with filter_eps=None,
+    or CCE_LOWMEM_RECOMPUTE=1, only O(N) state is kept and the backward recomputes every tile).
 
     exempt_label_tiles=True is the reference's filter (a tile holding a label is never skipped,
     kernels.py:447-455).  False is the paper's Alg. 3 ordering: tiles are filtered on the softmax

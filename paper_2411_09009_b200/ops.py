@@ -488,7 +488,7 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     ev = _ev_begin("fwd")
-    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), n, d, v,
+    _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_t), _p(row_map), _p(n_valid), _p(pos), 0, n, d, v,
                                  float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
                                  _p(tile_max), _p(state.shat if state.lab_cap else None), state.lab_cap,
                                  _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), stream),
@@ -546,10 +546,10 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     ev = _ev_begin("bwd")
     _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_t), _p(state.c if alias else None),
                                 _p(state.perm_padded), _p(state.row_map),
-                                _p(state.n_valid), _p(state.pos), _p(lse), _p(upstream), _p(state.tile_max),
+                                _p(state.n_valid), _p(state.pos), 0, _p(lse), _p(upstream), _p(state.tile_max),
                                 n, d, v, state.softcap, float(eps), int(bool(label_split)), _p(state.shat),
                                 lab_cap, _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), cap,
-                                _p(ws), ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters), _p(overflow),
+                                _p(ws), ws_bytes, _p(de), int(fp32_de), 0, _p(dc), _p(counters), _p(overflow),
                                 _p(stats),
                                 ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
                                                 else 0), stream), "cce_bwd_kept")
@@ -570,6 +570,156 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
     return de, dc, counters
+
+
+@dataclass
+class GroupState:
+    """What the grouped backward needs from forward_grouped: like TileState, but the sorted
+    classifier is never materialised -- each vocabulary group's rows are gathered into a small
+    buffer, once in the forward and once in the backward -- and the tile maxima are laid out
+    group by group ([group][token tile][vocab tile of the group][128])."""
+    e: torch.Tensor
+    c: torch.Tensor
+    e_c: torch.Tensor
+    row_map: torch.Tensor
+    n_valid: torch.Tensor
+    perm: torch.Tensor | None
+    perm_padded: torch.Tensor | None
+    pos: torch.Tensor
+    tile_max: torch.Tensor
+    groups: list  # (first sorted row, end row) per group; starts are multiples of 256
+    vocab_start: int
+    softcap: float
+    mean_logits: torch.Tensor | None = None
+
+    def nbytes(self) -> int:
+        own = [self.e_c, self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded]
+        return sum(t.numel() * t.element_size() for t in own if t is not None)
+
+
+def _group_rows(c, perm, v0: int, v1: int) -> torch.Tensor:
+    """The classifier rows of sorted positions [v0, v1): gathered, or a view without sorting."""
+    return gather_rows(c, perm[v0:v1], v1 - v0) if perm is not None else c[v0:v1]
+
+
+def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
+                    vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+    """Forward of the bounded-memory training path: (lse_local, correct, GroupState).
+
+    The same sweep as forward_tiles (compacted rows, the reference's vocabulary order, per-row
+    maxima of every 128 x 256 tile), run over vocabulary groups of the sorted order so that only
+    one group's classifier rows are ever gathered (lowmem_group_vtiles budgets).  Each group is a
+    vocabulary shard of its own: its (lse, correct) partials merge with the log-add-exp kernel of
+    the vocab-parallel path (kernels.py:121-137).
+    """
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    row_map, n_valid = compact_rows(targets, ignore_index)
+    e_c = gather_rows(e, row_map, n)
+    mean_logits = None
+    if vocab_sorting and perm is None:
+        perm, mean_logits = vocab_order(e, c, targets, ignore_index, n_valid)
+    vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
+    perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev) if perm is not None else None
+    inv_perm = torch.empty(v, dtype=torch.int32, device=dev) if perm is not None else None
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
+                                _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
+    LAUNCHES["count"] += 2 if perm is not None else 1
+    del inv_perm
+    nt = -(-n // BLOCK_TOKENS)
+    mt = -(-v // BLOCK_VOCAB)
+    gv = lowmem_group_vtiles(n, d, v)
+    groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gv) * BLOCK_VOCAB)) for m0 in range(0, mt, gv)]
+    tile_max = torch.empty(max(nt, 1) * mt * BLOCK_TOKENS, dtype=torch.float32, device=dev)
+    state = GroupState(e, c, e_c, row_map, n_valid, perm, perm_padded, pos, tile_max, groups,
+                       int(vocab_start), float(softcap or 0.0), mean_logits)
+    lse_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
+    corr_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
+    if n == 0:
+        return lse_parts.sum(0), corr_parts.sum(0), state
+    ws_bytes = max(lib.cce_fwd_workspace_bytes(n, d, v1 - v0) for v0, v1 in groups)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    ev = _ev_begin("fwd")
+    for g, (v0, v1) in enumerate(groups):
+        c_g = _group_rows(c, perm, v0, v1)
+        tm_g = tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
+        _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0,
+                                     float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]),
+                                     _p(corr_parts[g]), _p(tm_g), _p(None), 0, _p(None), _p(None), _p(None),
+                                     stream), "cce_fwd_tiles")
+        LAUNCHES["count"] += 3 + (1 if perm is not None else 0)
+    # the groups are vocabulary shards of this call: log-add-exp of their partials; the target
+    # logit sits in exactly one group (0 elsewhere)
+    lse_local, loss = merge_shards(lse_parts, corr_parts, targets, ignore_index)
+    correct = corr_parts.sum(0)
+    del loss
+    _ev_end("fwd", ev)
+    return lse_local, correct, state
+
+
+def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index: int,
+                     eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
+                     de_done: torch.cuda.Event | None = None, label_split: bool = False,
+                     correct: torch.Tensor | None = None):
+    """Backward of the bounded-memory training path (lse_backward, kernels.py:327-486): per
+    vocabulary group, the group's rows are gathered again, the skip decision is taken from the
+    forward's tile maxima and only the kept tiles are recomputed (cce_bwd_kept with the group's
+    S-hat slots sized for its worst case, so no overflow path exists); dE accumulates over the
+    groups in fp32 in a fixed order, dC rows are written by their own group.
+    Returns (dE, dC, counters[3])."""
+    lib = _lib.load()
+    e, c = state.e, state.c
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    de = torch.zeros(n, d, dtype=torch.float32, device=dev)
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    if n == 0:
+        return (de if fp32_de else de.to(torch.bfloat16)), dc.zero_(), counters
+    if not eps:
+        raise ValueError("backward_grouped needs filtering (eps > 0)")
+    nt = -(-n // BLOCK_TOKENS)
+    gtiles = max(-(-(v1 - v0) // BLOCK_VOCAB) for v0, v1 in state.groups)
+    cap = nt * gtiles  # every tile of the largest group: the whole-batch pass always fits
+    shat = torch.empty(cap * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
+    ws_bytes = max(lib.cce_bwd_kept_workspace_bytes(n, d, v1 - v0, cap, 0) for v0, v1 in state.groups)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    split = bool(label_split)
+    ev = _ev_begin("bwd")
+    last = len(state.groups) - 1
+    for g, (v0, v1) in enumerate(state.groups):
+        vg = v1 - v0
+        c_g = _group_rows(c, state.perm, v0, v1)
+        tm_g = state.tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
+        perm_g = state.perm_padded[v0:] if state.perm_padded is not None else None
+        dc_g = dc if state.perm_padded is not None else dc[v0:v1]
+        done = de_done.cuda_event if (de_done is not None and g == last and not split) else 0
+        _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_g), _p(None), _p(perm_g), _p(state.row_map),
+                                    _p(state.n_valid), _p(state.pos), v0, _p(lse), _p(upstream), _p(tm_g),
+                                    n, d, vg, state.softcap, float(eps), int(split), _p(shat), 0, _p(None),
+                                    _p(None), _p(None), cap, _p(ws), ws_bytes, _p(de), 1, int(g > 0),
+                                    _p(dc_g), _p(counters), _p(overflow), _p(None), ctypes.c_void_p(done),
+                                    stream), "cce_bwd_kept")
+        LAUNCHES["count"] += 3 + 6 + (1 if state.perm is not None else 0)
+    del ws, shat
+    if split:
+        label_terms(e, c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream, correct,
+                    state.softcap, de, dc)
+        if de_done is not None:
+            de_done.record()
+    _ev_end("bwd", ev)
+    LAST_COUNTERS["counters"] = counters
+    LAST_OVERFLOW["flag"] = overflow
+    return (de if fp32_de else f32_to_bf16(de)), dc, counters
 
 
 SHAT_TILE_BYTES = BLOCK_TOKENS * BLOCK_VOCAB * 2

@@ -18,7 +18,8 @@ t = torch.randint(0, v, (n,), device=dev, generator=g)
 
 def step():
     e.grad = c.grad = None
-    linear_cross_entropy(e, c, t, softcap=cap or None).backward()
+    linear_cross_entropy(e, c, t, softcap=cap or None,
+                         low_memory=os.environ.get("TRACE_LOW", "0") == "1").backward()
 
 for _ in range(int(os.environ.get("TRACE_WARM", "3"))):  # e.g. 40: settle the power state first
     step()
