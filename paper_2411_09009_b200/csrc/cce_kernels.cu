@@ -410,12 +410,13 @@ int launch_de(cce::GradParams q, int* sched_ctr, const void* shat, int64_t shat_
   int ch = cfg[0] == 2 ? 2 : 1;
   int kv = cfg[4];
   if (!fixed) {
-    // measured (profiles/r1/de_variants_s46*): one 512-column accumulator fed by 32-row stages
-    // (less operand traffic per flop) wins once there are enough units to balance the grid
-    // (Gemma-2-9B: 11.5 vs 13.1 ms); with few units (Gemma-2-2B: 288) the double-buffered
-    // 256-column form wins (1.65 vs 2.05 ms)
+    // measured (profiles/r1/de_variants_s46*, ab/ab_de_ch2_threshold.txt): one 512-column
+    // accumulator fed by 32-row stages (less operand traffic per flop) wins once there are
+    // enough units to balance the grid (Gemma-2-9B: 11.5 vs 13.1 ms; Llama-3-8B, 1024 units:
+    // 11.1 vs 12.0 ms); with few units (Gemma-2-2B: 320) the double-buffered 256-column form
+    // wins (1.65 vs 2.05 ms)
     const int units512 = q.g * ((q.ndc + 1) / 2);
-    if (units512 >= 8 * num_sms()) {
+    if (units512 >= 6 * num_sms()) {
       ch = 2;
       kv = 32;
     } else {

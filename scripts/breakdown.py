@@ -7,18 +7,21 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 from paper_2411_09009_b200 import linear_cross_entropy, ops
 
-N, D, V = 8192, 2304, 256000
+import bench
+
+CFG = os.environ.get("BREAKDOWN_CONFIG", "gemma2-2b")
+N, D, V, CAP, PAD, SIGMA = bench.CONFIGS[CFG]
 LOW = os.environ.get("BREAKDOWN_LOW", "0") == "1"  # low_memory=True (vocabulary groups)
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
 e = torch.randn(N, D, device=dev, generator=g).bfloat16().requires_grad_(True)
-c = (torch.randn(V, D, device=dev, generator=g) / math.sqrt(D)).bfloat16().requires_grad_(True)
+c = (torch.randn(V, D, device=dev, generator=g) * SIGMA / math.sqrt(D)).bfloat16().requires_grad_(True)
 t = torch.randint(0, V, (N,), device=dev, generator=g)
 
 
 def step():
     e.grad = c.grad = None
-    linear_cross_entropy(e, c, t, low_memory=LOW).backward()
+    linear_cross_entropy(e, c, t, softcap=CAP or None, low_memory=LOW).backward()
 
 
 for _ in range(4):
@@ -68,7 +71,7 @@ for name, ds in per.items():
             flops, byts = f, b
     rows.append((ms, short, flops, byts))
 rows.sort(reverse=True)
-print(f"Gemma-2-2B head, {'low_memory=True' if LOW else 'default path'}, {steps} steps: {span:.2f} ms/step, kept tiles {kept} of "
+print(f"{CFG} head N={N} D={D} V={V}, {'low_memory=True' if LOW else 'default path'}, {steps} steps: {span:.2f} ms/step, kept tiles {kept} of "
       f"{(N // 128) * (V // 256)} ({kept - recomputed} stored by the forward, {recomputed} recomputed); peaks: {peaks['bf16_tflops']} TFLOP/s bf16, {peaks['hbm_gbs']} GB/s\n")
 print("| kernel | ms/step (exclusive) | share | achieved | of peak |")
 print("|---|---|---|---|---|")
