@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(1024) list_single_kernel(
 }
 
 // One block: CTA-pair work list of the KEPT pass.  The kept tiles of vocab tile m hold the
-// consecutive slots [off_m, off_m + cnt_m) (build_list_kernel); pair j of m takes slots
+// consecutive slots [off_m, off_m + cnt_m) (list_fill_kernel); pair j of m takes slots
 // off_m + 2j and, if it exists, off_m + 2j + 1.  pairs[k] = (first slot, tiles in the pair).
 __global__ void __launch_bounds__(1024) build_pairs_kernel(const int* __restrict__ cnt_m, int mt,
                                                            const int* run_if, int2* __restrict__ pairs,
