@@ -805,3 +805,24 @@ def test_grouped_many_vocab_groups(cuda_device, monkeypatch, sort, cap, split):
     assert abs(b[0] - float(nl[xo != -1].mean())) <= 1e-3 * max(1.0, abs(b[0]))
     fde, fdc = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"), softcap=cap)
     assert O.rel_err(b[1], fde) < 2e-2 and O.rel_err(b[2], fdc) < 2e-2
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_llama70b_hidden_size(cuda_device, path):
+    """D = 8192 (Llama-3-70B head width): 128 K-blocks per logit tile, a token band of 5 tiles,
+    32 dE/dC chunks, the 512-column dE form never chosen at this N."""
+    rng = np.random.default_rng(70)
+    n, d, v = 600, 8192, 6000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::9] = -1
+    loss, lse, de, dc, cnt, perm = _run(e, c, x, path=path)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    assert _loss_err(loss, nl) < LOSS_TOL
+    ce, cl, idx = O.filter_ignored(e, x)
+    up = O.default_upstream(x, "mean-over-valid")
+    rde_c, rdc = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up[idx], perm=perm)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
