@@ -268,8 +268,10 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
         # forward over the backward's tiles (compacted rows, vocab order fixed by the mean logits
         # of the valid rows), recording per-row tile maxima: the backward then recomputes only
         # the tiles it keeps
+        # the backward closure may run more than once (kernels.py:549-580): no stored label tiles
+        # (they become S-hat in place) and no dC in the sorted copy's storage (reuse_state)
         lse_l, corr, state = ops.forward_tiles(E, C, X, IGNORE_INDEX, vocab_sorting=options.vocab_sorting,
-                                               eps=options.epsilon)
+                                               eps=options.epsilon, store_labels=False)
         mean = state.mean_logits
     else:
         lse_l, corr = ops.forward_local(E, C, X, IGNORE_INDEX)
@@ -289,7 +291,7 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
                 raise ValueError("upstream must be 0 at ignored positions")
         if state is not None:
             de, dc, counters = ops.backward_tiles(state, X, lse, up.contiguous(), ignore_index=IGNORE_INDEX,
-                                                  eps=options.epsilon, fp32_de=True)
+                                                  eps=options.epsilon, fp32_de=True, reuse_state=True)
         else:
             de, dc, counters, _ = ops.backward(
                 E, C, X, lse, up.contiguous(), ignore_index=IGNORE_INDEX, eps=None,

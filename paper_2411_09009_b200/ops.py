@@ -501,14 +501,16 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
                    eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
                    de_done: torch.cuda.Event | None = None, label_split: bool = False,
-                   correct: torch.Tensor | None = None):
+                   correct: torch.Tensor | None = None, reuse_state: bool = False):
     """Backward of the filter-from-forward path (lse_backward, kernels.py:327-486).
 
     The skip decision of every tile comes from the forward's tile maxima (the same strict test
     as the in-kernel filter), so only kept tiles are recomputed.  If the kept tiles exceed the
     S-hat budget, the full filter pass (`backward`'s grouped path) runs instead, gated on a
     device flag.  Returns (dE, dC, counters[3]).  `de_done` (a CUDA event) is recorded on the
-    current stream once dE is complete and before the dC pass runs.
+    current stream once dE is complete and before the dC pass runs.  Unless `reuse_state` (the
+    state may see another backward, as the reference's backward closure allows), dC is written
+    into the sorted classifier copy's storage and the state is spent.
     """
     lib = _lib.load()
     e, c_t = state.e, state.c_t
@@ -522,9 +524,12 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     # The sorted classifier copy is last read by the dE pass, so its storage becomes the dC output
     # (the library reads C through the permutation wherever C_t may already hold dC): no second
     # V x D matrix is ever live.  CCE_ALIAS_DC=0 allocates dC separately (A/B).
-    alias = state.perm is not None and os.environ.get("CCE_ALIAS_DC", "1") != "0"
+    if reuse_state and state.lab_cap:
+        raise ValueError("reuse_state needs a forward without stored label tiles (store_labels=False)")
+    alias = state.perm is not None and not reuse_state and os.environ.get("CCE_ALIAS_DC", "1") != "0"
     dc = c_t if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
-    state.c_t = None
+    if alias:
+        state.c_t = None  # spent: its storage is now dC
     counters = torch.zeros(3, dtype=torch.int64, device=dev)
     if n == 0:
         return de, dc.zero_(), counters

@@ -163,3 +163,20 @@ def test_cce_loss_hidden_size_not_multiple_of_8(cuda_device, d, filtering):
     tol = 2e-2 if filtering else 1e-2
     assert O.rel_err(g.d_e.float().cpu().numpy(), fde) < tol
     assert O.rel_err(g.d_c.float().cpu().numpy(), fdc) < tol
+
+
+def test_backward_closure_callable_twice(cuda_device):  # kernels.py:549-580: a plain closure
+    """The reference's backward closure can be called again (e.g. with another upstream); the
+    second call must equal a fresh run, whatever the first call did with its buffers."""
+    api = _api()
+    e, c, x = _make(64, 700, 5000, 12, sigma=2.0)
+    x[::5] = -1
+    up2 = np.where(x == -1, 0.0, np.linspace(0.1, 1.0, 700)).astype(np.float32)
+    out, back = api.cce_loss(e, c, x)
+    g1 = back()
+    g2 = back(up2)
+    _, back_fresh = api.cce_loss(e, c, x)
+    f2 = back_fresh(up2)
+    assert torch.equal(g2.d_e, f2.d_e) and torch.equal(g2.d_c, f2.d_c)
+    g1b = back()
+    assert torch.equal(g1.d_e, g1b.d_e) and torch.equal(g1.d_c, g1b.d_c)
