@@ -473,7 +473,12 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     # and turned into S-hat without a recompute
     nt = -(-n // BLOCK_TOKENS)
     mt = -(-v // BLOCK_VOCAB)
-    store_labels = store_labels and os.environ.get("CCE_STORE_LABELS", "1") != "0"
+    # storing a label tile costs the forward's epilogue a fixed amount per tile, recomputing it
+    # costs the backward 2 * 128 * 256 * D: measured break-even between D = 768 (GPT-2: 1.35 vs
+    # 1.39 ms per step without) and D = 2304 (Gemma-2-2B: 11.5 vs 12.1 ms with), so small heads
+    # recompute (profiles/r1/ab/ab_store_labels_by_d.txt).  CCE_STORE_LABELS=0 / 1 forces it.
+    env = os.environ.get("CCE_STORE_LABELS")
+    store_labels = store_labels and (env == "1" if env in ("0", "1") else d >= LABEL_STORE_MIN_D)
     rkey = ("recompute", n, d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
             bool(store_labels))
     lkey = ("labels", n, d, v, int(vocab_start))
@@ -728,6 +733,7 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
 
 
 SHAT_TILE_BYTES = BLOCK_TOKENS * BLOCK_VOCAB * 2
+LABEL_STORE_MIN_D = 1536      # hidden size from which the forward stores label tiles
 FIRST_CALL_MB = 1024          # S-hat allocation before any kept count has been observed
 KEPT_MARGIN = 1.15            # headroom over the last observed kept count
 _KEPT_HINT: dict = {}         # shape key -> [pinned copy of a device count vector, CUDA event, last known value, index]

@@ -12,6 +12,9 @@ GOLDEN = ROOT / "tests" / "golden"
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running")
+    # The forward stores label tiles only from D >= 1536 (ops.LABEL_STORE_MIN_D); the parity
+    # cases use small D, so force the store path on for them (tests that need it off set "0").
+    os.environ.setdefault("CCE_STORE_LABELS", "1")
 
 
 def golden_cases():

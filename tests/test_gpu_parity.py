@@ -826,3 +826,26 @@ def test_llama70b_hidden_size(cuda_device, path):
     rde = np.zeros_like(e)
     rde[idx] = rde_c
     assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
+
+
+@pytest.mark.parametrize("d,stored", [(768, False), (1536, True)])
+def test_label_store_rule_by_hidden_size(cuda_device, monkeypatch, d, stored):
+    """Without CCE_STORE_LABELS the forward stores label tiles from D >= 1536 only; both forms
+    give the oracle's loss and gradients."""
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.delenv("CCE_STORE_LABELS", raising=False)
+    rng = np.random.default_rng(d)
+    n, v = 300, 3000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    td = _dev(x.astype(np.int64))
+    _, _, st = ops.forward_tiles(_dev(e, torch.bfloat16), _dev(c, torch.bfloat16), td, -1)
+    assert (st.lab_cap > 0) == stored
+    loss, lse, de, dc, cnt, perm = _run(e, c, x, path="tiles")
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    assert _loss_err(loss, nl) < LOSS_TOL
+    rde, rdc = O.lse_backward_blocked(e, c, x, nlse.astype(np.float32), O.default_upstream(x, "mean-over-valid"),
+                                      perm=perm)
+    assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
