@@ -259,8 +259,10 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
 // row's largest S = exp(z' - lse) is >= eps (block_skip_decision, kernels.py:140-142, strict <).
 // tile_max[(n * mt + m) * 128 + r] is the forward's max raw logit of row r in tile (n, m);
 // tile_row_big is the same test the in-kernel filter (cce_lse_kernel<BWD>) applies.
-// Grid (ceil(mt / 64), nt), 256 threads: warp w takes vocab tiles blockIdx.x * 64 + w + 8j, lane l
-// rows 4l .. 4l + 3.  counters[1] += eps-skipped, counters[2] += zero-upstream-skipped tiles.
+// Grid (ceil(mt / DECIDE_VT), nt), 256 threads: warp w takes vocab tiles blockIdx.x * DECIDE_VT +
+// w + 8j, lane l rows 4l .. 4l + 3.  counters[1] += eps-skipped, counters[2] += zero-upstream-
+// skipped tiles.  16 vocab tiles per block keeps the grid wide for vocabulary groups too.
+constexpr int DECIDE_VT = 16;
 __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const float* __restrict__ lse,
                                     const int32_t* __restrict__ pos, int pos_offset, const int32_t* __restrict__ row_map,
                                     const int* __restrict__ n_valid, const uint8_t* __restrict__ block_zero,
@@ -271,8 +273,8 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nv = *n_valid;
   const int nt_dev = (nv + BM - 1) / BM;
-  const int m_lo = blockIdx.x * 64;
-  const int m_hi = min(mt, m_lo + 64);
+  const int m_lo = blockIdx.x * DECIDE_VT;
+  const int m_hi = min(mt, m_lo + DECIDE_VT);
   if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   if (n >= nt_dev) {  // token tile past the compacted rows: not a tile of this backward

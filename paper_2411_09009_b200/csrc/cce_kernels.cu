@@ -834,7 +834,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
   cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
-  cce::decide_tiles_kernel<<<dim3((unsigned)((mt + 63) / 64), (unsigned)nt), 256, 0, stream>>>(
+  cce::decide_tiles_kernel<<<dim3((unsigned)((mt + cce::DECIDE_VT - 1) / cce::DECIDE_VT), (unsigned)nt), 256, 0,
+                              stream>>>(
       tile_max, lse, pos, (int)pos_offset, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split,
       w.keep, counters);
   CCE_CUDA(cudaGetLastError());
