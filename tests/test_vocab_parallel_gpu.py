@@ -36,7 +36,7 @@ def _inputs(n, d, v, seed=3):
     return e, c, x
 
 
-def _worker(rank, world, port, q, n, d, v, filt, cap, split=False):
+def _worker(rank, world, port, q, n, d, v, filt, cap, split=False, low=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -53,7 +53,7 @@ def _worker(rank, world, port, q, n, d, v, filt, cap, split=False):
         t = torch.from_numpy(x_np).cuda()
         loss = linear_cross_entropy(e, c, t, filter_eps="auto" if filt else None, softcap=cap or None,
                                     process_group=dist.group.WORLD, vocab_start=v0,
-                                    exempt_label_tiles=not split)
+                                    exempt_label_tiles=not split, low_memory=low)
         loss.backward()
         torch.cuda.synchronize()
         q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy()))
@@ -61,16 +61,18 @@ def _worker(rank, world, port, q, n, d, v, filt, cap, split=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("filt,cap,split", [(False, 0.0, False), (True, 0.0, False), (True, 20.0, False),
-                                            (True, 0.0, True)])
-def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap, split):
+@pytest.mark.parametrize("filt,cap,split,low", [(False, 0.0, False, False), (True, 0.0, False, False),
+                                                (True, 20.0, False, False), (True, 0.0, True, False),
+                                                (True, 0.0, False, True), (True, 20.0, True, True)])
+def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap, split, low):
     import torch.multiprocessing as mp
 
     world, n, d, v = 2, 600, 128, 5001
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, d, v, filt, cap, split)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, d, v, filt, cap, split, low))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
