@@ -112,6 +112,7 @@ struct GradParams {
   const int* off_m;        //     first slot of each vocab tile (its cnt_m slots are consecutive)
   int* sched;              // dE: unit counter (zeroed before the launch), nullptr = static
   int de_order;            // dE: 0 chunk-major units, 1 token-tile-major, K>=2 groups of K chunks
+  int dc_block;            // dC: 0 vocab-tile-major units, B > 0 blocks of B vocab tiles, chunk-major
   int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)
   int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
 };

@@ -79,6 +79,26 @@ __device__ __forceinline__ void for_each_listed(const int2* list, int off, int c
   }
 }
 
+// dC unit -> (vocab tile m, D chunk dc, vocab half vh).  blk = 0: vocabulary-tile-major (the
+// 2 * ndc units of one vocab tile side by side: its S-hat tiles are shared through L2, E rows are
+// re-read per vocab tile -- free while E fits L2).  blk > 0: blocks of blk vocab tiles, D-chunk-
+// major inside a block, so concurrent CTAs share the block's S-hat tiles and one E chunk (large N:
+// E no longer fits L2).
+__device__ __forceinline__ void dc_unit(int u, int mt, int ndc, int blk, int& m, int& dc, int& vh) {
+  vh = u & 1;
+  const int w = u >> 1;
+  if (blk <= 0) {
+    dc = w % ndc;
+    m = w / ndc;
+    return;
+  }
+  const int b = w / (blk * ndc);
+  const int r = w - b * blk * ndc;
+  const int bb = min(blk, mt - b * blk);  // vocab tiles of this block (the last may be short)
+  dc = r / bb;
+  m = b * blk + r % bb;
+}
+
 __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_bf16, const float* x,
                                             int lim) {
   // 32 consecutive values; lim = number of valid columns (multiple of 8)
@@ -432,7 +452,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = start; u < units; u += stride) {
-      const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
+      int vh, dc, m;
+      dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
       auto tile = [&](int ln, int slot) {
         const int n = p.n_base + ln;
         for (int h = 0; h < 2; ++h) {
@@ -482,10 +503,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int t = 0;
       // the next unit's kept count is loaded one unit ahead (units are short: ~8 us at Gemma-2B)
-      int cnt = start < units ? p.cnt_m[(start >> 1) / p.ndc] : 0;
+      auto unit_cnt = [&](int uu) {
+        int mm, dd, hh;
+        dc_unit(uu, p.mt, p.ndc, p.dc_block, mm, dd, hh);
+        return p.cnt_m[mm];
+      };
+      int cnt = start < units ? unit_cnt(start) : 0;
       for (int u = start; u < units; u += stride, ++t) {
         const int un = u + stride;
-        const int cnt_next = un < units ? p.cnt_m[(un >> 1) / p.ndc] : 0;
+        const int cnt_next = un < units ? unit_cnt(un) : 0;
         const int buf = t & 1;
         const int ksteps = 2 * cnt;
         cnt = cnt_next;
@@ -529,7 +555,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t* wstg = stg + quarter * 32 * DC_STG_PITCH;
     int t = 0;
     for (int u = start; u < units; u += stride, ++t) {
-      const int vh = u & 1, dc = (u >> 1) % p.ndc, m = (u >> 1) / p.ndc;
+      int vh, dc, m;
+      dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
       const int buf = t & 1;
       // per-unit loads issued before the wait so their latency hides behind it
       const bool has = p.cnt_m[m] > 0;

@@ -437,10 +437,14 @@ int launch_de(cce::GradParams q, int* sched_ctr, const void* shat, int64_t shat_
 }
 
 // dC pass (B3) on single CTAs or CTA pairs (the pair needs the 3-D E map with 2-atom boxes).
-int launch_dc(const cce::GradParams& q, bool pair, const CUtensorMap& tmS64, const CUtensorMap& tmE64,
+int launch_dc(cce::GradParams q, bool pair, const CUtensorMap& tmS64, const CUtensorMap& tmE64,
               const CUtensorMap& tmE3, const CUtensorMap& tmE3h, const CUtensorMap& tmEg,
               cudaStream_t stream) {
   const int units = q.mt * q.ndc * 2;
+  {
+    const char* e = getenv("CCE_DC_BLOCK");
+    q.dc_block = e ? atoi(e) : 0;
+  }
   if (!pair) {
     if (int e = ensure_attr(cce::cce_dc_kernel<1>, kDcSmem)) return e;
     return launch_k(cce::cce_dc_kernel<1>, dim3(std::min(num_sms(), units)), dim3(cce::NUM_THREADS), kDcSmem,
