@@ -57,24 +57,47 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
+        # nvidia-smi --id takes the physical index; torch's index is remapped by
+        # CUDA_VISIBLE_DEVICES, so address the GPU by UUID when torch exposes it
+        self.id = str(index)
+        try:
+            import torch
+
+            u = str(torch.cuda.get_device_properties(index).uuid)
+            if u and u != "None":
+                self.id = u if u.startswith("GPU-") else "GPU-" + u
+        except Exception:
+            pass
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.window = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", f"--id={self.id}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment to start: wait for its first line so that the timed
+            # region (marked by start() / stop()) is covered from its beginning
+            t_end = time.monotonic() + 3.0
+            while not self.lines and time.monotonic() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
 
+    def start(self):
+        self.window = [time.monotonic(), None]
+
+    def stop(self):
+        if self.window is not None:
+            self.window[1] = time.monotonic()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -87,7 +110,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None and self.window[1] is not None:
+            lo, hi = self.window
+            lines = [x for x in self.lines if lo <= x[0] <= hi + 0.03]  # samples of the timed region
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -303,13 +330,17 @@ def main():
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clk:
+        barrier()  # every rank's sampler is running before the timed region starts
+        torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        clk.start()
         t0.record()
         for _ in range(args.steps):
             step(e, c, t)
         t1.record()
         torch.cuda.synchronize()
+        clk.stop()
     barrier()
     ms = t0.elapsed_time(t1) / args.steps
     launches = (ops.LAUNCHES["count"] - launches0) // args.steps
