@@ -97,8 +97,101 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+@dataclass(frozen=True)
+class EmbeddingMatrix:
+    """Token embeddings [n_tokens, dim] (core.py:52-67): any array or tensor; checked on use."""
+    data: object
+
+    @property
+    def n_tokens(self) -> int:
+        return int(_shape(self.data)[0])
+
+    @property
+    def dim(self) -> int:
+        return int(_shape(self.data)[1])
+
+
+@dataclass(frozen=True)
+class ClassifierMatrix:
+    """Classifier rows [vocab, dim] (core.py:70-85)."""
+    data: object
+
+    @property
+    def vocab(self) -> int:
+        return int(_shape(self.data)[0])
+
+    @property
+    def dim(self) -> int:
+        return int(_shape(self.data)[1])
+
+
+@dataclass(frozen=True)
+class TokenBatch:
+    """Target labels, IGNORE_INDEX or a vocabulary row (core.py:88-114); validated on creation
+    like the reference (1-D, >= -1)."""
+    labels: object
+
+    def __post_init__(self):
+        t = torch.as_tensor(self.labels)
+        if t.dim() != 1:
+            raise ValueError(f"labels must be 1-D, got shape {tuple(t.shape)}")
+        if t.numel() and int(t.min()) < IGNORE_INDEX:
+            raise ValueError("labels must be -1 (ignore) or non-negative")
+
+    @property
+    def n_tokens(self) -> int:
+        return int(_shape(self.labels)[0])
+
+    @property
+    def valid_mask(self) -> torch.Tensor:
+        return torch.as_tensor(self.labels) != IGNORE_INDEX
+
+    def check_vocab(self, vocab: int) -> None:
+        t = torch.as_tensor(self.labels)
+        if t.numel() and int(t.max()) >= vocab:
+            raise ValueError(f"label {int(t.max())} out of range for vocab size {vocab}")
+
+
+@dataclass(frozen=True)
+class BlockSchedule:
+    """The (token block, vocab block) pairs a pass visits, each once (kernels.py:48-63).  On the
+    GPU the visit order is the persistent kernels' static unit schedule (a11); `order` keeps the
+    reference's vocabulary: "row-major" = one fixed sweep (what the B200 kernels do: results are
+    bit-reproducible), "work-stealing" = dynamic hand-out."""
+    pairs: tuple
+    order: str = "row-major"
+
+    @classmethod
+    def for_grid(cls, n_tiles: int, m_tiles: int, order: str = "row-major") -> "BlockSchedule":
+        return cls(tuple((n, m) for n in range(n_tiles) for m in range(m_tiles)), order)
+
+
+def round_to_bf16(x):
+    """bf16 round-to-nearest-even, returned as float32 (core.py:208-226): scalars give a float,
+    tensors a tensor, anything else a numpy array.  NaN stays NaN, +-inf stay infinite."""
+    t = torch.as_tensor(x, dtype=torch.float32)
+    r = t.to(torch.bfloat16).to(torch.float32)
+    if isinstance(x, torch.Tensor):
+        return r
+    if r.dim() == 0:
+        return float(r)
+    return r.numpy()
+
+
+def _shape(x):
+    return tuple(x.shape) if hasattr(x, "shape") else tuple(torch.as_tensor(x).shape)
+
+
+def _unwrap(x):
+    if isinstance(x, (EmbeddingMatrix, ClassifierMatrix)):
+        return x.data
+    if isinstance(x, TokenBatch):
+        return x.labels
+    return x
+
+
 def _matrix(x, name: str, min_rows: int) -> torch.Tensor:
-    t = torch.as_tensor(x)
+    t = torch.as_tensor(_unwrap(x))
     if t.dim() != 2:
         raise ValueError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
     if t.shape[0] < min_rows:
@@ -112,7 +205,7 @@ def _matrix(x, name: str, min_rows: int) -> torch.Tensor:
 
 
 def _labels(x, vocab: int | None = None) -> torch.Tensor:
-    t = torch.as_tensor(x).to(torch.int64)
+    t = torch.as_tensor(_unwrap(x)).to(torch.int64)
     if t.dim() != 1:
         raise ValueError(f"labels must be 1-D, got shape {tuple(t.shape)}")
     if t.numel() and int(t.min()) < IGNORE_INDEX:
@@ -139,7 +232,7 @@ def _pair(e, c, x=None):
 
 
 def _hidden(e) -> int:
-    return int(e.shape[1]) if hasattr(e, "shape") else int(torch.as_tensor(e).shape[1])
+    return int(_shape(_unwrap(e))[1])
 
 
 def _trim(g: torch.Tensor, d: int) -> torch.Tensor:
@@ -148,7 +241,7 @@ def _trim(g: torch.Tensor, d: int) -> torch.Tensor:
 
 def default_upstream(x, reduction: str, dtype=torch.float32) -> torch.Tensor:
     """core.py:181-200: 'sum' = 1 per valid token, 'mean-over-valid' = 1/#valid, 'none' raises."""
-    labels = torch.as_tensor(x)
+    labels = torch.as_tensor(_unwrap(x))
     if reduction == "none":
         raise ValueError('reduction "none" requires an explicit upstream vector')
     valid = labels != IGNORE_INDEX
@@ -188,16 +281,23 @@ def compute_vocab_order(mean_logits, m_b: int = ops.BLOCK_VOCAB) -> VocabOrder:
 
 
 def filter_ignored(e, x):
-    """kernels.py:494-510: (compact_e, compact_x, index_map)."""
-    E = torch.as_tensor(e)
-    X = torch.as_tensor(x)
+    """kernels.py:494-510: (compact_e, compact_x, index_map); wrapped inputs
+    (EmbeddingMatrix / TokenBatch) come back wrapped, like the reference's."""
+    E = torch.as_tensor(_unwrap(e))
+    X = torch.as_tensor(_unwrap(x))
     if E.shape[0] != X.shape[0]:
         raise ValueError(f"label count {X.shape[0]} != token count {E.shape[0]}")
     valid = X != IGNORE_INDEX
     if bool(valid.all()):
-        return E, X, torch.arange(X.shape[0], device=X.device)
-    idx = torch.nonzero(valid).squeeze(1)
-    return E[idx], X[idx], idx
+        ce, cx, idx = E, X, torch.arange(X.shape[0], device=X.device)
+    else:
+        idx = torch.nonzero(valid).squeeze(1)
+        ce, cx = E[idx], X[idx]
+    if isinstance(e, EmbeddingMatrix):
+        ce = EmbeddingMatrix(ce)
+    if isinstance(x, TokenBatch):
+        cx = TokenBatch(cx)
+    return ce, cx, idx
 
 
 def indexed_matmul(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | None = None):
@@ -305,8 +405,8 @@ def cce_loss(e, c, x, blocks: BlockSpec | None = None, options: CceOptions | Non
 
 
 __all__ = [
-    "BackwardStats", "BlockSpec", "CceOptions", "EPSILON_DEFAULT", "Gradients", "IGNORE_INDEX",
-    "LossOutput", "VocabOrder", "block_skip_decision", "cce_loss", "compute_vocab_order",
-    "default_upstream", "filter_ignored", "indexed_matmul", "log_add_exp", "lse_backward",
-    "lse_forward",
+    "BackwardStats", "BlockSchedule", "BlockSpec", "CceOptions", "ClassifierMatrix", "EPSILON_DEFAULT",
+    "EmbeddingMatrix", "Gradients", "IGNORE_INDEX", "LossOutput", "TokenBatch", "VocabOrder",
+    "block_skip_decision", "cce_loss", "compute_vocab_order", "default_upstream", "filter_ignored",
+    "indexed_matmul", "log_add_exp", "lse_backward", "lse_forward", "round_to_bf16",
 ]

@@ -68,3 +68,41 @@ def test_no_cpu_fallback():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="CUDA"):
         api.cce_loss(np.zeros((2, 8), np.float32), np.zeros((3, 8), np.float32), np.array([0, 1]))
+
+
+def test_reference_wrapper_types():  # core.py:52-114
+    import numpy as np
+
+    e = api.EmbeddingMatrix(np.zeros((5, 8), np.float32))
+    c = api.ClassifierMatrix(np.zeros((7, 8), np.float32))
+    x = api.TokenBatch(np.array([0, -1, 3, 6, -1]))
+    assert (e.n_tokens, e.dim, c.vocab, c.dim, x.n_tokens) == (5, 8, 7, 8, 5)
+    assert x.valid_mask.tolist() == [True, False, True, True, False]
+    x.check_vocab(7)
+    with pytest.raises(ValueError, match="out of range"):
+        x.check_vocab(6)
+    with pytest.raises(ValueError):
+        api.TokenBatch(np.array([0, -2]))
+    with pytest.raises(ValueError):
+        api.TokenBatch(np.zeros((2, 2), np.int64))
+    ce, cx, idx = api.filter_ignored(e, x)  # kernels.py:494-510, wrapped in, wrapped out
+    assert isinstance(ce, api.EmbeddingMatrix) and isinstance(cx, api.TokenBatch)
+    assert idx.tolist() == [0, 2, 3] and ce.n_tokens == 3
+    assert api.default_upstream(x, "sum").tolist() == [1.0, 0.0, 1.0, 1.0, 0.0]
+
+
+def test_block_schedule_covers_grid_once():  # test_kernels.py:228-232
+    sched = api.BlockSchedule.for_grid(3, 5)
+    assert len(sched.pairs) == 15 and len(set(sched.pairs)) == 15
+    assert sched.order == "row-major"
+
+
+def test_round_to_bf16_known_values():  # test_core.py:76-99 (round-to-nearest-even)
+    import numpy as np
+
+    assert api.round_to_bf16(1.0) == 1.0
+    assert api.round_to_bf16(1.0 + 2.0 ** -8) == 1.0            # tie -> even
+    assert api.round_to_bf16(1.0 + 3 * 2.0 ** -8) == 1.0 + 2.0 ** -6  # tie -> even (up)
+    assert api.round_to_bf16(1.0 + 2.0 ** -7) == 1.0 + 2.0 ** -7  # exact
+    r = api.round_to_bf16(np.array([np.nan, np.inf, -np.inf, 3.14159], np.float32))
+    assert np.isnan(r[0]) and r[1] == np.inf and r[2] == -np.inf and r[3] == np.float32(3.140625)

@@ -180,3 +180,16 @@ def test_backward_closure_callable_twice(cuda_device):  # kernels.py:549-580: a 
     assert torch.equal(g2.d_e, f2.d_e) and torch.equal(g2.d_c, f2.d_c)
     g1b = back()
     assert torch.equal(g1.d_e, g1b.d_e) and torch.equal(g1.d_c, g1b.d_c)
+
+
+def test_cce_loss_accepts_reference_wrapper_types(cuda_device):  # core.py:52-114, kernels.py:513
+    api = _api()
+    e, c, x = _make(32, 300, 2000, 14)
+    x[::4] = -1
+    out_w, back_w = api.cce_loss(api.EmbeddingMatrix(e), api.ClassifierMatrix(c), api.TokenBatch(x))
+    out_p, back_p = api.cce_loss(e, c, x)
+    assert torch.equal(out_w.per_token_loss, out_p.per_token_loss)
+    gw, gp = back_w(), back_p()
+    assert torch.equal(gw.d_e, gp.d_e) and torch.equal(gw.d_c, gp.d_c)
+    lse, mean = api.lse_forward(api.EmbeddingMatrix(e), api.ClassifierMatrix(c))
+    assert torch.equal(lse, api.lse_forward(e, c)[0])
