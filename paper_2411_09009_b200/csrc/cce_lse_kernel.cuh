@@ -356,17 +356,23 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
           is_lab = tr.ok && (vv[0] | vv[1] | vv[2] | vv[3]) != 0;
         }
         float zmax = -INFINITY;
+#ifndef CCE_FWD_LDW
+#define CCE_FWD_LDW 32
+#endif
+        constexpr int LW = CCE_FWD_LDW;  // TMEM columns per load-wait step (32 or 64)
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tacc + c * 32, r);
+        for (int c = 0; c < BN / LW; ++c) {
+          uint32_t r[LW];
+#pragma unroll
+          for (int q = 0; q < LW / 32; ++q)
+            tmem_ld32(tacc + c * LW + q * 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
           tmem_ld_wait();
-          float y[32];
+          float y[LW];
           float cm = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
+          for (int j = 0; j < LW; ++j) {
             float z = __uint_as_float(r[j]);
-            const int col = col0 + c * 32 + j;
+            const int col = col0 + c * LW + j;
             const bool in_v = col < p.v;
             if (in_v) zmax = fmaxf(zmax, z);
             if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
@@ -381,7 +387,7 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
           if (nm != -INFINITY) {
             float acc = 0.f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc += ex2_approx(y[j] - nm);
+            for (int j = 0; j < LW; ++j) acc += ex2_approx(y[j] - nm);
             run_s = run_s * ex2_approx(run_m - nm) + acc;
             run_m = nm;
           }
