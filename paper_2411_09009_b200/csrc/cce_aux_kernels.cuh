@@ -14,6 +14,7 @@ namespace cce {
 // Merge the per-split (max2, sum2) partials of each row into this shard's natural-log LSE.
 __global__ void combine_splits_kernel(const float2* __restrict__ part, int splits, int n,
                                       float* __restrict__ lse_local) {
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float m = -INFINITY;
@@ -33,6 +34,7 @@ __global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
                                     const float* __restrict__ correct_parts,
                                     const int64_t* __restrict__ targets, int64_t ignore_index,
                                     int n, float* __restrict__ lse_out, float* __restrict__ loss_out) {
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float m = -INFINITY;
@@ -51,6 +53,7 @@ __global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
 
 // zero a float buffer (used for `correct` so rows whose label lives in another shard read 0)
 __global__ void fill_kernel(float* __restrict__ x, float v, int64_t n) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = v;
 }
@@ -62,6 +65,7 @@ __global__ void fill_kernel(float* __restrict__ x, float v, int64_t n) {
 __global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* __restrict__ targets,
                             int64_t ignore_index, int n, int d, float* __restrict__ part,
                             int rows_per_block) {
+  griddep_wait();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= d) return;
   const int r0 = blockIdx.y * rows_per_block;
@@ -73,6 +77,7 @@ __global__ void ebar_kernel(const __nv_bfloat16* __restrict__ E, const int64_t* 
 }
 
 __global__ void ebar_reduce_kernel(const float* __restrict__ part, int nblk, int d, float* __restrict__ ebar) {
+  griddep_wait();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= d) return;
   float acc = 0.f;
@@ -85,6 +90,7 @@ __global__ void ebar_reduce_kernel(const float* __restrict__ part, int nblk, int
 // row, 4 independent 16-byte loads in flight per lane.
 __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float* __restrict__ ebar_sum,
                                 const int* __restrict__ n_valid, int v, int d, float* __restrict__ key) {
+  griddep_wait();
   extern __shared__ float s_ebar[];
   for (int j = threadIdx.x; j < d; j += blockDim.x) s_ebar[j] = ebar_sum[j];
   __syncthreads();
@@ -126,6 +132,7 @@ __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float
 // pre-filled (entries past the count stay as they are, e.g. 0, so padded gathers stay in bounds).
 __global__ void compact_rows_kernel(const int64_t* __restrict__ targets, int64_t ignore_index, int n,
                                     int32_t* __restrict__ row_map, int* __restrict__ n_valid) {
+  griddep_wait();
   constexpr int T = 1024;
   __shared__ int s_warp[T / 32];
   __shared__ int s_base;
@@ -163,6 +170,7 @@ __global__ void indexed_dot_kernel(const __nv_bfloat16* __restrict__ E, const __
                                    const int64_t* __restrict__ targets, int64_t ignore_index,
                                    int64_t vocab_start, int n, int d, int v, float softcap,
                                    float* __restrict__ out) {
+  griddep_wait();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -190,6 +198,7 @@ __global__ void indexed_dot_kernel(const __nv_bfloat16* __restrict__ E, const __
 }
 
 __global__ void iota_kernel(int32_t* __restrict__ x, int n) {
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = i;
 }
@@ -197,6 +206,7 @@ __global__ void iota_kernel(int32_t* __restrict__ x, int n) {
 // inv[perm[j]] = j for j < v ; padding positions of perm (>= v) point at row 0.
 __global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int v, int vpad,
                                    int32_t* __restrict__ perm_padded, int32_t* __restrict__ inv) {
+  griddep_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= vpad) return;
   if (j < v) {
@@ -212,6 +222,7 @@ __global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int v, int 
 __global__ void label_pos_kernel(const int64_t* __restrict__ targets, int64_t ignore_index,
                                  int64_t vocab_start, int v, const int32_t* __restrict__ inv,
                                  int n, int32_t* __restrict__ pos) {
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t tg = targets[i];
@@ -226,6 +237,7 @@ __global__ void label_pos_kernel(const int64_t* __restrict__ targets, int64_t ig
 // block_zero[b] = every upstream of compact token tile b is exactly zero (kernels.py:434-438)
 __global__ void block_zero_kernel(const float* __restrict__ up, const int32_t* __restrict__ row_map,
                                   const int* __restrict__ n_valid, uint8_t* __restrict__ bz) {
+  griddep_wait();
   const int b = blockIdx.x;
   const int i = b * BM + threadIdx.x;
   const bool nz = (i < *n_valid) && (up[row_map[i]] != 0.f);
@@ -238,6 +250,7 @@ __global__ void block_zero_kernel(const float* __restrict__ up, const int32_t* _
 // plain TMA box instead of 64 tile::gather4 transfers.
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const int32_t* __restrict__ index,
                                    int64_t rows, int cols, __nv_bfloat16* __restrict__ dst) {
+  griddep_wait();
   const int warps = blockDim.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -268,6 +281,7 @@ __global__ void decide_tiles_kernel(const float* __restrict__ tile_max, const fl
                                     const int* __restrict__ n_valid, const uint8_t* __restrict__ block_zero,
                                     int nt, int mt, float softcap, float eps, int label_split,
                                     uint8_t* __restrict__ keep, unsigned long long* __restrict__ counters) {
+  griddep_wait();
   __shared__ unsigned s_cnt[2];
   const int n = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -513,6 +527,7 @@ __global__ void __launch_bounds__(256) label_shat_kernel(
     const uint8_t* __restrict__ block_zero, int mt, const float* __restrict__ tile_max,
     const float* __restrict__ lse, const float* __restrict__ upstream, const int32_t* __restrict__ pos,
     const int32_t* __restrict__ row_map, const int* __restrict__ n_valid, int v, float softcap, int label_split) {
+  griddep_wait();
   const int s = blockIdx.x;
   if (s >= min(*lab_count, lab_capacity)) return;
   const int2 nm = lab_list[s];
@@ -751,6 +766,7 @@ __device__ __forceinline__ float label_coef(const float* up, const float* correc
 __global__ void label_keys_kernel(const int32_t* __restrict__ row_map, const int* __restrict__ n_valid,
                                   const int32_t* __restrict__ pos, int n, int32_t* __restrict__ key,
                                   int32_t* __restrict__ val) {
+  griddep_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int32_t kk = INT_MAX, vv = 0;
@@ -769,6 +785,7 @@ __global__ void label_dc_kernel(const int32_t* __restrict__ key, const int32_t* 
                                 const __nv_bfloat16* __restrict__ E, const float* __restrict__ up,
                                 const float* __restrict__ correct, float softcap,
                                 const int32_t* __restrict__ perm, int d, __nv_bfloat16* __restrict__ dc) {
+  griddep_wait();
   const int k = blockIdx.x;
   const int32_t p = key[k];
   if (p == INT_MAX || (k > 0 && key[k - 1] == p)) return;
@@ -790,6 +807,7 @@ __global__ void label_de_kernel(const int32_t* __restrict__ row_map, const int* 
                                 const int32_t* __restrict__ perm, const float* __restrict__ up,
                                 const float* __restrict__ correct, float softcap, int n, int d,
                                 float* __restrict__ de_f32, __nv_bfloat16* __restrict__ de_bf16) {
+  griddep_wait();
   const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (k >= n || k >= *n_valid) return;
@@ -817,6 +835,7 @@ __global__ void __launch_bounds__(1024) reduce_loss_kernel(const float* __restri
                                                            const int64_t* __restrict__ targets,
                                                            int64_t ignore_index, int n, int reduction,
                                                            float* __restrict__ out) {
+  griddep_wait();
   __shared__ float s_f[32];
   __shared__ int s_i[32];
   float acc = 0.f;
@@ -835,6 +854,7 @@ __global__ void __launch_bounds__(1024) upstream_kernel(const float* __restrict_
                                                         const int64_t* __restrict__ targets,
                                                         int64_t ignore_index, int n, int reduction,
                                                         float* __restrict__ up) {
+  griddep_wait();
   __shared__ int s_i[32];
   int cnt = 0;
   if (reduction == 2)
@@ -851,6 +871,7 @@ __global__ void __launch_bounds__(1024) upstream_kernel(const float* __restrict_
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                    int64_t n4) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const float4 v = reinterpret_cast<const float4*>(x)[i];

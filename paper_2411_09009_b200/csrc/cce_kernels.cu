@@ -164,7 +164,7 @@ constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES +
 // there begins with griddepcontrol.wait): the next kernel is scheduled while its predecessor
 // drains, which matters for the worst-case fallback chain -- a few dozen gated-off launches per
 // step that otherwise cost a full launch gap each.  CCE_PDL=0 turns it off.
-thread_local bool g_pdl = false;
+thread_local bool g_pdl = true;  // every launch of this library; CCE_PDL=0 turns it off
 
 bool pdl_allowed() {
   static int v = -1;
@@ -199,7 +199,7 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (g_pdl) {
+  if (g_pdl && pdl_allowed()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -209,6 +209,12 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   CCE_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   return 0;
 }
+
+// kernel<<<grid, block, smem, stream>>>(args) with the launch attributes of launch_k
+#define PDL_LAUNCH(kernel, grid, block, smem, stream, ...)                                      \
+  do {                                                                                         \
+    if (int e_ = launch_k(kernel, grid, block, (size_t)(smem), stream, 1, __VA_ARGS__)) return e_; \
+  } while (0)
 
 template <typename K>
 int ensure_attr(K kernel, size_t bytes) {
@@ -506,11 +512,10 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   const int units = nt * splits;
-  cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
+  PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   (void)units;
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
-  cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-      static_cast<const float2*>(ws), splits, (int)n, lse_local);
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -520,8 +525,7 @@ int cce_merge_shards(int num_shards, const float* lse_parts, const float* correc
                      float* loss_out, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (n == 0) return 0;
-  cce::merge_shards_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-      num_shards, lse_parts, correct_parts, targets, ignore_index, (int)n, lse_out, loss_out);
+  PDL_LAUNCH(cce::merge_shards_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, num_shards, lse_parts, correct_parts, targets, ignore_index, (int)n, lse_out, loss_out);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -558,10 +562,10 @@ int cce_ebar(const void* E, const int64_t* targets, int64_t ignore_index, int64_
   const int nblk = (int)((n + rows_per_block - 1) / rows_per_block);
   float* part = static_cast<float*>(ws);
   dim3 grid((unsigned)((d + 127) / 128), (unsigned)nblk);
-  cce::ebar_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(E), targets,
+  PDL_LAUNCH(cce::ebar_kernel, dim3(grid), dim3(128), 0, stream, static_cast<const __nv_bfloat16*>(E), targets,
                                              ignore_index, (int)n, (int)d, part, rows_per_block);
   CCE_CUDA(cudaGetLastError());
-  cce::ebar_reduce_kernel<<<(unsigned)((d + 127) / 128), 128, 0, stream>>>(part, nblk, (int)d, ebar_sum);
+  PDL_LAUNCH(cce::ebar_reduce_kernel, dim3((unsigned)((d + 127) / 128)), dim3(128), 0, stream, part, nblk, (int)d, ebar_sum);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -580,10 +584,9 @@ int cce_vocab_order(const void* C, const float* ebar_sum, const int* n_valid, in
   size_t tmp_bytes = need - 3 * (size_t)v * 4 - 1024;
   CCE_CUDA(cudaFuncSetAttribute(cce::sort_key_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(d * sizeof(float))));
-  cce::sort_key_kernel<<<(unsigned)std::min<int64_t>((v + 7) / 8, 4 * num_sms()), 256, d * sizeof(float), stream>>>(
-      static_cast<const __nv_bfloat16*>(C), ebar_sum, n_valid, (int)v, (int)d, key);
+  PDL_LAUNCH(cce::sort_key_kernel, dim3((unsigned)std::min<int64_t>((v + 7) / 8, 4 * num_sms())), dim3(256), d * sizeof(float), stream, static_cast<const __nv_bfloat16*>(C), ebar_sum, n_valid, (int)v, (int)d, key);
   CCE_CUDA(cudaGetLastError());
-  cce::iota_kernel<<<(unsigned)((v + 255) / 256), 256, 0, stream>>>(idx, (int)v);
+  PDL_LAUNCH(cce::iota_kernel, dim3((unsigned)((v + 255) / 256)), dim3(256), 0, stream, idx, (int)v);
   CCE_CUDA(cudaGetLastError());
   CCE_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, key, key_sorted, idx, perm,
                                                      (int)v, 0, 32, stream));
@@ -597,7 +600,7 @@ int cce_compact_rows(const int64_t* targets, int64_t ignore_index, int64_t n, in
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   const int64_t npad = ((n + cce::BM - 1) / cce::BM) * cce::BM;
   CCE_CUDA(cudaMemsetAsync(row_map, 0, std::max<int64_t>(npad, 1) * sizeof(int32_t), stream));
-  cce::compact_rows_kernel<<<1, 1024, 0, stream>>>(targets, ignore_index, (int)n, row_map, n_valid);
+  PDL_LAUNCH(cce::compact_rows_kernel, dim3(1), dim3(1024), 0, stream, targets, ignore_index, (int)n, row_map, n_valid);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -608,13 +611,11 @@ int cce_bwd_prep(const int32_t* perm, int64_t v, const int64_t* targets, int64_t
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   const int64_t vpad = ((v + cce::BN - 1) / cce::BN) * cce::BN;
   if (perm) {
-    cce::invert_perm_kernel<<<(unsigned)((vpad + 255) / 256), 256, 0, stream>>>(
-        perm, (int)v, (int)vpad, perm_padded, inv_perm);
+    PDL_LAUNCH(cce::invert_perm_kernel, dim3((unsigned)((vpad + 255) / 256)), dim3(256), 0, stream, perm, (int)v, (int)vpad, perm_padded, inv_perm);
     CCE_CUDA(cudaGetLastError());
   }
   if (n > 0) {
-    cce::label_pos_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-        targets, ignore_index, vocab_start, (int)v, perm ? inv_perm : nullptr, (int)n, pos);
+    PDL_LAUNCH(cce::label_pos_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, targets, ignore_index, vocab_start, (int)v, perm ? inv_perm : nullptr, (int)n, pos);
     CCE_CUDA(cudaGetLastError());
   }
   return 0;
@@ -646,12 +647,11 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
   // compact E (filter_ignored) unless rows are gathered on the fly; zero-upstream tile flags
   const void* e_src = E;
   if (!e_gather) {
-    cce::gather_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_compact);
+    PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_compact);
     CCE_CUDA(cudaGetLastError());
     e_src = w.e_compact;
   }
-  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  PDL_LAUNCH(cce::block_zero_kernel, dim3(nt), dim3(cce::BM), 0, stream, upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   CUtensorMap tmE, tmEg, tmC, tmCg, tmC128, tmE64, tmS128, tmS64, tmC3, tmE3, tmE3h, tmC128h, tmC64;
   const int64_t shat_rows = capacity_tiles * cce::BM;
@@ -793,10 +793,9 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
     p.lab_slot = lab_slot;
     p.lab_list = static_cast<int2*>(lab_list);
   }
-  cce::fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(correct, 0.f, n);
+  PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
-  cce::combine_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-      static_cast<const float2*>(ws), splits, (int)n, lse_local);
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -836,11 +835,9 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
   const KeptWs w = kept_layout(ws, n, v, capacity_tiles, lab_capacity);
   if (ws_bytes < w.total) return fail("cce_bwd_kept: workspace too small");
   const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
-  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  PDL_LAUNCH(cce::block_zero_kernel, dim3(nt), dim3(cce::BM), 0, stream, upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
-  cce::decide_tiles_kernel<<<dim3((unsigned)((mt + cce::DECIDE_VT - 1) / cce::DECIDE_VT), (unsigned)nt), 256, 0,
-                              stream>>>(
-      tile_max, lse, pos, (int)pos_offset, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split,
+  PDL_LAUNCH(cce::decide_tiles_kernel, dim3(dim3((unsigned)((mt + cce::DECIDE_VT - 1) / cce::DECIDE_VT), (unsigned)nt)), dim3(256), 0, stream, tile_max, lse, pos, (int)pos_offset, row_map, n_valid, w.block_zero, nt, mt, softcap, eps, label_split,
       w.keep, counters);
   CCE_CUDA(cudaGetLastError());
   // S-hat slots: [stored label tiles (lab_capacity) | recomputed tiles (capacity_tiles)]
@@ -857,8 +854,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
       CCE_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
       ls = side->s;
     }
-    cce::label_shat_kernel<<<(unsigned)lab_capacity, 256, 0, ls>>>(
-        reinterpret_cast<__half*>(shat_all), static_cast<const int2*>(lab_list), lab_count, (int)lab_capacity,
+    PDL_LAUNCH(cce::label_shat_kernel, dim3((unsigned)lab_capacity), dim3(256), 0, ls, reinterpret_cast<__half*>(shat_all), static_cast<const int2*>(lab_list), lab_count, (int)lab_capacity,
         w.block_zero, mt, tile_max, lse, upstream, pos, row_map, n_valid, (int)v, softcap, label_split);
     CCE_CUDA(cudaGetLastError());
     if (side) CCE_CUDA(cudaEventRecord(side->join, side->s));
@@ -1060,10 +1056,9 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
   const bool atoms3d = d % 64 == 0;
   const bool pair = use_pairs();
   // filter_ignored (kernels.py:494-510) and zero-upstream token tiles, once
-  cce::gather_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_c);
+  PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(E), row_map, n, (int)d, w.e_c);
   CCE_CUDA(cudaGetLastError());
-  cce::block_zero_kernel<<<nt, cce::BM, 0, stream>>>(upstream, row_map, n_valid, w.block_zero);
+  PDL_LAUNCH(cce::block_zero_kernel, dim3(nt), dim3(cce::BM), 0, stream, upstream, row_map, n_valid, w.block_zero);
   CCE_CUDA(cudaGetLastError());
   CUtensorMap tmE, tmE64, tmE3, tmE3h, tmS64;
   const int64_t shat_rows = (int64_t)nt * group_vtiles * cce::BM;
@@ -1082,8 +1077,7 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
     // this group's classifier rows in tile order (C[perm] slice, or a view of C)
     const void* cg = static_cast<const __nv_bfloat16*>(C) + r0 * d;
     if (perm_padded) {
-      cce::gather_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(C), perm_padded + r0, rows, (int)d, w.c_g);
+      PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(C), perm_padded + r0, rows, (int)d, w.c_g);
       CCE_CUDA(cudaGetLastError());
       cg = w.c_g;
     }
@@ -1171,15 +1165,14 @@ int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, co
   int32_t* val_s = key_s + n;
   void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(val_s + n) + 255) & ~uintptr_t(255));
   size_t tmp_bytes = need - 4 * (size_t)n * 4 - 1024;
-  cce::label_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(row_map, n_valid, pos, (int)n, key, val);
+  PDL_LAUNCH(cce::label_keys_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, row_map, n_valid, pos, (int)n, key, val);
   CCE_CUDA(cudaGetLastError());
   CCE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, val, val_s, (int)n, 0, 32, stream));
-  cce::label_dc_kernel<<<(unsigned)n, 256, 0, stream>>>(key_s, val_s, (int)n, static_cast<const __nv_bfloat16*>(E),
+  PDL_LAUNCH(cce::label_dc_kernel, dim3((unsigned)n), dim3(256), 0, stream, key_s, val_s, (int)n, static_cast<const __nv_bfloat16*>(E),
                                                        upstream, correct, softcap, perm_padded, (int)d,
                                                        static_cast<__nv_bfloat16*>(dc));
   CCE_CUDA(cudaGetLastError());
-  cce::label_de_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
-      row_map, n_valid, pos, static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap,
+  PDL_LAUNCH(cce::label_de_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, row_map, n_valid, pos, static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap,
       (int)n, (int)d, de_fp32 ? static_cast<float*>(de) : nullptr,
       de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de));
   CCE_CUDA(cudaGetLastError());
@@ -1190,7 +1183,7 @@ int cce_reduce_loss(const float* loss, const int64_t* targets, int64_t ignore_in
                     int reduction, float* out, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (reduction != 1 && reduction != 2) return fail("cce_reduce_loss: reduction must be 1 (sum) or 2 (mean)");
-  cce::reduce_loss_kernel<<<1, 1024, 0, stream>>>(loss, targets, ignore_index, (int)n, reduction, out);
+  PDL_LAUNCH(cce::reduce_loss_kernel, dim3(1), dim3(1024), 0, stream, loss, targets, ignore_index, (int)n, reduction, out);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1200,7 +1193,7 @@ int cce_upstream(const float* grad, const int64_t* targets, int64_t ignore_index
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (reduction < 0 || reduction > 2) return fail("cce_upstream: reduction must be 0, 1 or 2");
   if (n == 0) return 0;
-  cce::upstream_kernel<<<1, 1024, 0, stream>>>(grad, targets, ignore_index, (int)n, reduction, up);
+  PDL_LAUNCH(cce::upstream_kernel, dim3(1), dim3(1024), 0, stream, grad, targets, ignore_index, (int)n, reduction, up);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1211,8 +1204,7 @@ int cce_indexed_dot(const void* E, const void* C, const int64_t* targets, int64_
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_indexed_dot: D must be a multiple of 8");
   if (n == 0) return 0;
-  cce::indexed_dot_kernel<<<(unsigned)((n + 7) / 8), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(E), static_cast<const __nv_bfloat16*>(C), targets,
+  PDL_LAUNCH(cce::indexed_dot_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(E), static_cast<const __nv_bfloat16*>(C), targets,
       ignore_index, vocab_start, (int)n, (int)d, (int)v, softcap, out);
   CCE_CUDA(cudaGetLastError());
   return 0;
@@ -1223,8 +1215,7 @@ int cce_gather_rows(const void* src, const int32_t* index, int64_t rows, int64_t
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (cols % 8 != 0) return fail("cce_gather_rows: cols must be a multiple of 8");
   if (rows == 0) return 0;
-  cce::gather_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(src), index, rows, (int)cols, static_cast<__nv_bfloat16*>(dst));
+  PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(src), index, rows, (int)cols, static_cast<__nv_bfloat16*>(dst));
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1234,8 +1225,7 @@ int cce_f32_to_bf16(const float* x, void* y, int64_t count, void* stream_ptr) {
   if (count % 4 != 0) return fail("cce_f32_to_bf16: count must be a multiple of 4");
   const int64_t n4 = count / 4;
   if (n4 == 0) return 0;
-  cce::f32_to_bf16_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, stream>>>(
-      x, static_cast<__nv_bfloat16*>(y), n4);
+  PDL_LAUNCH(cce::f32_to_bf16_kernel, dim3((unsigned)((n4 + 255) / 256)), dim3(256), 0, stream, x, static_cast<__nv_bfloat16*>(y), n4);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
