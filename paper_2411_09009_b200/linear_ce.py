@@ -161,6 +161,13 @@ def linear_cross_entropy(
     e2, c = ops.adapt_operands(e2, c)  # bf16, contiguous, hidden size padded to a multiple of 8
     ops.check_operands(e2, c, t2.to(torch.int64) if t2.dtype != torch.int64 else t2)
     t2 = t2.to(torch.int64).contiguous()
+    if process_group is None and (os.environ.get("CCE_CHECK_LABELS") == "1" or torch.is_anomaly_enabled()):
+        # the reference's check_vocab (core.py:110-114) needs a host read, so it runs only in debug
+        # mode; otherwise a label outside [0, V) counts as a row whose target logit is absent
+        # (loss = LSE), exactly as a label owned by another vocabulary shard
+        bad = (t2 != ignore_index) & ((t2 < 0) | (t2 >= c.shape[0]))
+        if bool(bad.any()):
+            raise ValueError(f"label out of range for vocab size {c.shape[0]}")
     cap = float(softcap) if softcap else 0.0
     if cap < 0:
         raise ValueError("softcap must be positive")

@@ -877,3 +877,26 @@ def test_extreme_logit_scale(cuda_device, path):
     x1 = rng.integers(0, 700, 130)
     loss1, lse1, de1, dc1, _, _ = _run(e1, c1, x1, path=path)
     assert np.allclose(loss1, math.log(700), atol=2e-4) and np.all(np.isfinite(de1))
+
+
+def test_out_of_range_labels(cuda_device, monkeypatch):
+    """Debug mode (CCE_CHECK_LABELS=1 or torch anomaly mode) raises like the reference's
+    check_vocab (core.py:110-114); otherwise such a row's loss is its LSE (target logit absent)."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    rng = np.random.default_rng(5)
+    n, d, v = 200, 64, 900
+    e = torch.from_numpy(O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))).cuda().bfloat16()
+    c = torch.from_numpy(O.round_to_bf16((rng.standard_normal((v, d)) / 8).astype(np.float32))).cuda().bfloat16()
+    t = torch.from_numpy(rng.integers(0, v, n)).cuda()
+    t[7] = v + 5
+    monkeypatch.setenv("CCE_CHECK_LABELS", "1")
+    with pytest.raises(ValueError, match="out of range"):
+        linear_cross_entropy(e, c, t)
+    monkeypatch.delenv("CCE_CHECK_LABELS")
+    with torch.autograd.detect_anomaly():
+        with pytest.raises(ValueError, match="out of range"):
+            linear_cross_entropy(e, c, t)
+    per = linear_cross_entropy(e, c, t, reduction="none")
+    lse = torch.logsumexp(e.float() @ c.float().T, dim=1)
+    assert abs(per[7].item() - lse[7].item()) < 1e-3
