@@ -168,6 +168,9 @@ def linear_cross_entropy(
         bad = (t2 != ignore_index) & ((t2 < 0) | (t2 >= c.shape[0]))
         if bool(bad.any()):
             raise ValueError(f"label out of range for vocab size {c.shape[0]}")
+        for name, x in (("embeddings", e2), ("classifier", c)):  # core.py:47
+            if not bool(torch.isfinite(x).all()):
+                raise ValueError(f"{name} contains non-finite entries")
     cap = float(softcap) if softcap else 0.0
     if cap < 0:
         raise ValueError("softcap must be positive")

@@ -900,3 +900,9 @@ def test_out_of_range_labels(cuda_device, monkeypatch):
     per = linear_cross_entropy(e, c, t, reduction="none")
     lse = torch.logsumexp(e.float() @ c.float().T, dim=1)
     assert abs(per[7].item() - lse[7].item()) < 1e-3
+    t[7] = 3
+    e_bad = e.clone()
+    e_bad[3, 5] = float("nan")
+    monkeypatch.setenv("CCE_CHECK_LABELS", "1")
+    with pytest.raises(ValueError, match="non-finite"):
+        linear_cross_entropy(e_bad, c, t)
