@@ -906,3 +906,37 @@ def test_out_of_range_labels(cuda_device, monkeypatch):
     monkeypatch.setenv("CCE_CHECK_LABELS", "1")
     with pytest.raises(ValueError, match="non-finite"):
         linear_cross_entropy(e_bad, c, t)
+
+
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+@pytest.mark.parametrize("low", [False, True])
+def test_reductions_on_both_training_paths(cuda_device, reduction, low):
+    """reduction mean / sum / none (a non-uniform upstream) on the default and the low-memory
+    (vocabulary-grouped) paths, softcap on, against the oracle."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    rng = np.random.default_rng(61)
+    n, d, v, cap = 700, 128, 6000, 15.0
+    e_np = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c_np = O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[::6] = -100
+    e = torch.from_numpy(e_np).cuda().bfloat16().requires_grad_(True)
+    c = torch.from_numpy(c_np).cuda().bfloat16().requires_grad_(True)
+    out = linear_cross_entropy(e, c, torch.from_numpy(x).cuda(), softcap=cap, reduction=reduction, low_memory=low)
+    xo = np.where(x == -100, -1, x)
+    valid = xo != -1
+    nl, _, _ = O.naive_forward(e_np, c_np, xo, softcap=cap)
+    if reduction == "none":
+        w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+        (out * torch.from_numpy(w).cuda()).sum().backward()
+        assert np.max(np.abs(out.detach().cpu().numpy()[valid] - nl[valid])) < 1e-3 * max(1.0, np.abs(nl).max())
+        up = np.where(valid, w, 0.0).astype(np.float32)
+    else:
+        out.backward()
+        ref = float(nl[valid].sum()) / (valid.sum() if reduction == "mean" else 1)
+        assert out.item() == pytest.approx(ref, rel=1e-3)
+        up = O.default_upstream(xo, "mean-over-valid" if reduction == "mean" else "sum")
+    fde, fdc = O.naive_backward(e_np, c_np, xo, up, softcap=cap)
+    assert O.rel_err(e.grad.float().cpu().numpy(), fde) < 2e-2
+    assert O.rel_err(c.grad.float().cpu().numpy(), fdc) < 2e-2
