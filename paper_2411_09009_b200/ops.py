@@ -737,6 +737,7 @@ LABEL_STORE_MIN_D = 1536      # hidden size from which the forward stores label 
 FIRST_CALL_MB = 1024          # S-hat allocation before any kept count has been observed
 KEPT_MARGIN = 1.15            # headroom over the last observed kept count
 _KEPT_HINT: dict = {}         # shape key -> [pinned copy of a device count vector, CUDA event, last known value, index]
+KEPT_HINT_MAX = 256           # shape keys remembered (least recently used dropped first)
 
 
 def shat_budget_tiles() -> int:
@@ -799,10 +800,12 @@ def _remember_count(key, counts: torch.Tensor, index: int) -> None:
     """Queue an asynchronous copy of a device count (read by a later call once it has landed)."""
     if _capturing():
         return
-    hint = _KEPT_HINT.get(key)
+    hint = _KEPT_HINT.pop(key, None)
     if hint is None:
         hint = [torch.zeros(counts.shape, dtype=counts.dtype).pin_memory(), None, None, index]
-        _KEPT_HINT[key] = hint
+        while len(_KEPT_HINT) >= KEPT_HINT_MAX:  # shapes that vary every step: drop the oldest
+            _KEPT_HINT.pop(next(iter(_KEPT_HINT)))
+    _KEPT_HINT[key] = hint  # (re)inserted last: the dict's order is least recently used first
     _harvest(hint)
     if hint[1] is not None:
         return  # previous copy still in flight

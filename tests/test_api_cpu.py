@@ -106,3 +106,21 @@ def test_round_to_bf16_known_values():  # test_core.py:76-99 (round-to-nearest-e
     assert api.round_to_bf16(1.0 + 2.0 ** -7) == 1.0 + 2.0 ** -7  # exact
     r = api.round_to_bf16(np.array([np.nan, np.inf, -np.inf, 3.14159], np.float32))
     assert np.isnan(r[0]) and r[1] == np.inf and r[2] == -np.inf and r[3] == np.float32(3.140625)
+
+
+def test_capacity_hint_cache_is_bounded(monkeypatch):
+    """Shapes that change every step cannot grow the pinned capacity-hint cache without bound."""
+    import torch
+
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.setattr(ops, "_KEPT_HINT", {})
+    monkeypatch.setattr(ops, "KEPT_HINT_MAX", 8)
+    monkeypatch.setattr(ops, "_capturing", lambda: False)
+    monkeypatch.setattr(torch.Tensor, "pin_memory", lambda self: self)  # no CUDA here
+    monkeypatch.setattr(torch.cuda, "Event", lambda: type("E", (), {"record": lambda s: None,
+                                                                     "query": lambda s: True})())
+    for i in range(50):
+        ops._remember_count(("shape", i), torch.tensor([i, 2 * i]), 1)
+    assert len(ops._KEPT_HINT) == 8
+    assert ("shape", 49) in ops._KEPT_HINT and ("shape", 0) not in ops._KEPT_HINT
