@@ -140,7 +140,9 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * pos are global and pos - pos_offset is group-local, tile_max is the group's own
  * [ceil(n/128)][ceil(v/256)][128] block and perm_padded points at the group's first entry.  With
  * de_accumulate (fp32 dE only) the call adds its dE into de_out instead of writing it, so the
- * groups of one backward accumulate in a fixed order. */
+ * groups of one backward accumulate in a fixed order.
+ * de_out or dc may be NULL (not both): that pass is skipped (an input that needs no gradient,
+ * e.g. a frozen classifier). */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,

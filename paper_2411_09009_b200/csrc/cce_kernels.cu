@@ -820,7 +820,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
   if (!overflow || !shat) return fail("cce_bwd_kept: overflow flag and S-hat buffer required");
   // dc aliasing C_t: the fallback passes (which may follow an earlier group's dC pass) read the
   // caller's C through the permutation instead of the sorted copy
-  const bool aliased = dc == C_t;
+  if (de_out == nullptr && dc == nullptr) return fail("cce_bwd_kept: neither dE nor dC requested");
+  const bool aliased = dc != nullptr && dc == C_t;
   if (aliased && (C == nullptr || perm_padded == nullptr))
     return fail("cce_bwd_kept: dc aliases C_t, so C and perm_padded are required");
   if (lab_slot == nullptr) lab_capacity = 0;
@@ -972,11 +973,13 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     q.list = w.alist;
     q.off_m = w.off_m;
     if (primary && side) CCE_CUDA(cudaStreamWaitEvent(stream, side->join, 0));  // label S-hat ready
-    if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, gathered ? C : C_t, gathered ? tmCog : tmC64,
-                          stream))
-      return e;
+    if (de_out != nullptr)  // NULL: the caller does not want dE (e.g. its input needs no grad)
+      if (int e = launch_de(q, w.list_count + 3, shat_all, shat_rows, gathered ? C : C_t,
+                            gathered ? tmCog : tmC64, stream))
+        return e;
     if (last && de_done_event)  // every dE write of this call is enqueued before this point
       CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
+    if (dc == nullptr) return 0;  // NULL: no dC wanted (a frozen classifier)
     return launch_dc(q, pair && atoms3d, tmS64, tmE64, tmE3, tmE3h, tmE64, stream);
   };
   // The counts are only known on the device: the whole-batch pass runs iff its tiles to
@@ -1165,17 +1168,18 @@ int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, co
   int32_t* val_s = key_s + n;
   void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(val_s + n) + 255) & ~uintptr_t(255));
   size_t tmp_bytes = need - 4 * (size_t)n * 4 - 1024;
-  PDL_LAUNCH(cce::label_keys_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, row_map, n_valid, pos, (int)n, key, val);
-  CCE_CUDA(cudaGetLastError());
-  CCE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, val, val_s, (int)n, 0, 32, stream));
-  PDL_LAUNCH(cce::label_dc_kernel, dim3((unsigned)n), dim3(256), 0, stream, key_s, val_s, (int)n, static_cast<const __nv_bfloat16*>(E),
-                                                       upstream, correct, softcap, perm_padded, (int)d,
-                                                       static_cast<__nv_bfloat16*>(dc));
-  CCE_CUDA(cudaGetLastError());
-  PDL_LAUNCH(cce::label_de_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, row_map, n_valid, pos, static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap,
-      (int)n, (int)d, de_fp32 ? static_cast<float*>(de) : nullptr,
-      de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de));
-  CCE_CUDA(cudaGetLastError());
+  if (dc != nullptr) {  // NULL: no dC wanted
+    PDL_LAUNCH(cce::label_keys_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, row_map, n_valid,
+               pos, (int)n, key, val);
+    CCE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, val, val_s, (int)n, 0, 32, stream));
+    PDL_LAUNCH(cce::label_dc_kernel, dim3((unsigned)n), dim3(256), 0, stream, key_s, val_s, (int)n,
+               static_cast<const __nv_bfloat16*>(E), upstream, correct, softcap, perm_padded, (int)d,
+               static_cast<__nv_bfloat16*>(dc));
+  }
+  if (de != nullptr)  // NULL: no dE wanted
+    PDL_LAUNCH(cce::label_de_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, stream, row_map, n_valid, pos,
+               static_cast<const __nv_bfloat16*>(C), perm_padded, upstream, correct, softcap, (int)n, (int)d,
+               de_fp32 ? static_cast<float*>(de) : nullptr, de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de));
   return 0;
 }
 

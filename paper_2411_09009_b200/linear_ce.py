@@ -85,28 +85,32 @@ class _LinearCrossEntropy(torch.autograd.Function):
         up = ops.upstream(grad_out, targets, ignore_index, reduction)  # default_upstream, core.py:181-200
         state, ctx.state = ctx.state, None
         split, correct, ctx.correct = ctx.split, ctx.correct, None
+        # a pass whose input needs no gradient is skipped (e.g. a frozen classifier: no dC pass)
+        want = dict(want_de=ctx.needs_input_grad[0], want_dc=ctx.needs_input_grad[1])
         if isinstance(state, ops.GroupState):
             done = torch.cuda.Event() if group is not None else None
             de, dc, _ = ops.backward_grouped(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
                                              fp32_de=group is not None, de_done=done, label_split=split,
-                                             correct=correct)
+                                             correct=correct, **want)
             del state
-            if group is not None:
+            if group is not None and de is not None:
                 from .vocab_parallel import all_reduce_de_overlapped
 
                 de = all_reduce_de_overlapped(de, done, group)
         elif state is not None:
             if group is None:
                 de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
-                                               label_split=split, correct=correct)
+                                               label_split=split, correct=correct, **want)
             else:
                 from .vocab_parallel import all_reduce_de_overlapped
 
                 # dE is complete before the dC pass: its all-reduce runs on a side stream meanwhile
                 done = torch.cuda.Event()
                 de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
-                                               fp32_de=True, de_done=done, label_split=split, correct=correct)
-                de = all_reduce_de_overlapped(de, done, group)
+                                               fp32_de=True, de_done=done, label_split=split, correct=correct,
+                                               **want)
+                if de is not None:
+                    de = all_reduce_de_overlapped(de, done, group)
             del state
         else:  # low_memory=True or filtering off: vocabulary-grouped backward, bounded transients
             de, dc, _, _ = ops.backward_lowmem(e, c, targets, lse, up, ignore_index=ignore_index,

@@ -302,7 +302,7 @@ def label_terms(e, c, perm_padded, row_map, n_valid, pos, upstream, correct, sof
     _lib.check(lib.cce_label_terms(_p(e), _p(c), _p(perm_padded), _p(row_map), _p(n_valid), _p(pos),
                                    _p(upstream), _p(correct.to(torch.float32).contiguous()), n, d, c.shape[0],
                                    float(softcap or 0.0), _p(ws), ws_bytes, _p(de),
-                                   int(de.dtype == torch.float32), _p(dc), _stream(e.device)),
+                                   int(de is not None and de.dtype == torch.float32), _p(dc), _stream(e.device)),
                "cce_label_terms")
     LAUNCHES["count"] += 3 + 4  # keys, dC, dE + CUB radix sort passes
 
@@ -506,7 +506,8 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
                    eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
                    de_done: torch.cuda.Event | None = None, label_split: bool = False,
-                   correct: torch.Tensor | None = None, reuse_state: bool = False):
+                   correct: torch.Tensor | None = None, reuse_state: bool = False,
+                   want_de: bool = True, want_dc: bool = True):
     """Backward of the filter-from-forward path (lse_backward, kernels.py:327-486).
 
     The skip decision of every tile comes from the forward's tile maxima (the same strict test
@@ -515,7 +516,8 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     device flag.  Returns (dE, dC, counters[3]).  `de_done` (a CUDA event) is recorded on the
     current stream once dE is complete and before the dC pass runs.  Unless `reuse_state` (the
     state may see another backward, as the reference's backward closure allows), dC is written
-    into the sorted classifier copy's storage and the state is spent.
+    into the sorted classifier copy's storage and the state is spent.  want_de / want_dc False
+    skip that pass (an input that needs no gradient) and return None in its place.
     """
     lib = _lib.load()
     e, c_t = state.e, state.c_t
@@ -525,19 +527,20 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     stream = _stream(dev)
     lse = lse.to(torch.float32).contiguous()
     upstream = upstream.to(torch.float32).contiguous()
-    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev)
+    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev) if want_de else None
     # The sorted classifier copy is last read by the dE pass, so its storage becomes the dC output
     # (the library reads C through the permutation wherever C_t may already hold dC): no second
     # V x D matrix is ever live.  CCE_ALIAS_DC=0 allocates dC separately (A/B).
     if reuse_state and state.lab_cap:
         raise ValueError("reuse_state needs a forward without stored label tiles (store_labels=False)")
-    alias = state.perm is not None and not reuse_state and os.environ.get("CCE_ALIAS_DC", "1") != "0"
-    dc = c_t if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    alias = (want_dc and state.perm is not None and not reuse_state
+             and os.environ.get("CCE_ALIAS_DC", "1") != "0")
+    dc = (c_t if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)) if want_dc else None
     if alias:
         state.c_t = None  # spent: its storage is now dC
     counters = torch.zeros(3, dtype=torch.int64, device=dev)
     if n == 0:
-        return de, dc.zero_(), counters
+        return de, (dc.zero_() if dc is not None else None), counters
     if not eps:
         raise ValueError("backward_tiles needs filtering (eps > 0)")
     nt = -(-n // BLOCK_TOKENS)
@@ -674,7 +677,7 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
 def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index: int,
                      eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
                      de_done: torch.cuda.Event | None = None, label_split: bool = False,
-                     correct: torch.Tensor | None = None):
+                     correct: torch.Tensor | None = None, want_de: bool = True, want_dc: bool = True):
     """Backward of the bounded-memory training path (lse_backward, kernels.py:327-486): per
     vocabulary group, the group's rows are gathered again, the skip decision is taken from the
     forward's tile maxima and only the kept tiles are recomputed (cce_bwd_kept with the group's
@@ -689,11 +692,12 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
     stream = _stream(dev)
     lse = lse.to(torch.float32).contiguous()
     upstream = upstream.to(torch.float32).contiguous()
-    de = torch.zeros(n, d, dtype=torch.float32, device=dev)
-    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    de = torch.zeros(n, d, dtype=torch.float32, device=dev) if want_de else None
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev) if want_dc else None
     counters = torch.zeros(3, dtype=torch.int64, device=dev)
     if n == 0:
-        return (de if fp32_de else de.to(torch.bfloat16)), dc.zero_(), counters
+        return ((de if fp32_de else de.to(torch.bfloat16)) if de is not None else None,
+                dc.zero_() if dc is not None else None, counters)
     if not eps:
         raise ValueError("backward_grouped needs filtering (eps > 0)")
     nt = -(-n // BLOCK_TOKENS)
@@ -711,7 +715,7 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
         c_g = _group_rows(c, state.perm, v0, v1)
         tm_g = state.tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
         perm_g = state.perm_padded[v0:] if state.perm_padded is not None else None
-        dc_g = dc if state.perm_padded is not None else dc[v0:v1]
+        dc_g = None if dc is None else (dc if state.perm_padded is not None else dc[v0:v1])
         done = de_done.cuda_event if (de_done is not None and g == last and not split) else 0
         _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_g), _p(None), _p(perm_g), _p(state.row_map),
                                     _p(state.n_valid), _p(state.pos), v0, _p(lse), _p(upstream), _p(tm_g),
@@ -729,7 +733,7 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
-    return (de if fp32_de else f32_to_bf16(de)), dc, counters
+    return (de if (fp32_de or de is None) else f32_to_bf16(de)), dc, counters
 
 
 SHAT_TILE_BYTES = BLOCK_TOKENS * BLOCK_VOCAB * 2

@@ -940,3 +940,29 @@ def test_reductions_on_both_training_paths(cuda_device, reduction, low):
     fde, fdc = O.naive_backward(e_np, c_np, xo, up, softcap=cap)
     assert O.rel_err(e.grad.float().cpu().numpy(), fde) < 2e-2
     assert O.rel_err(c.grad.float().cpu().numpy(), fdc) < 2e-2
+
+
+@pytest.mark.parametrize("low", [False, True])
+@pytest.mark.parametrize("frozen", ["c", "e"])
+@pytest.mark.parametrize("split", [False, True])
+def test_frozen_input_skips_its_pass(cuda_device, low, frozen, split):
+    """A classifier (or embedding) that needs no gradient: the backward skips that pass and the
+    other gradient equals the full run bit for bit."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    rng = np.random.default_rng(77)
+    n, d, v = 600, 128, 9000
+    e0 = torch.from_numpy(O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))).cuda().bfloat16()
+    c0 = torch.from_numpy(O.round_to_bf16((rng.standard_normal((v, d)) * 2.0 / math.sqrt(d)).astype(np.float32))).cuda().bfloat16()
+    t = torch.from_numpy(rng.integers(0, v, n)).cuda()
+    grads = {}
+    for freeze in (None, frozen):
+        e = e0.clone().requires_grad_(freeze != "e")
+        c = c0.clone().requires_grad_(freeze != "c")
+        linear_cross_entropy(e, c, t, low_memory=low, exempt_label_tiles=not split).backward()
+        grads[freeze] = (e.grad, c.grad)
+    full, part = grads[None], grads[frozen]
+    if frozen == "c":
+        assert part[1] is None and torch.equal(part[0], full[0])
+    else:
+        assert part[0] is None and torch.equal(part[1], full[1])
