@@ -173,6 +173,40 @@ def cpu_desc(tokens: int) -> dict:
     return {"cores": os.cpu_count(), "cpu": model}
 
 
+def zipf_head(e, c, v, v0, gen, dev, alpha=4.0, zipf_s=1.0):
+    """D3: token frequencies follow a Zipf law.  A fixed unit direction u is added
+    to every embedding (weight alpha) and to classifier row j (weight b_j / alpha), so logits gain
+    the shared bias b_j = -s log(rank_j) (random ranks, centred); targets are sampled from the
+    resulting softmax (Gumbel-max, 1024 rows at a time).  With vocab_sorting the frequent rows
+    gather in the first tiles, which is where the non-trivial gradients live."""
+    import torch
+
+    n, d = e.shape
+    g2 = torch.Generator(device=dev)
+    g2.manual_seed(7)
+    u = torch.randn(d, device=dev, generator=g2)
+    u = u / u.norm()
+    rank = torch.randperm(v, device=dev, generator=g2).float() + 1.0
+    b = -zipf_s * torch.log(rank)
+    b = b - b.mean()
+    rows = slice(v0, v0 + c.shape[0])
+    e = (e.float() + alpha * u).to(torch.bfloat16)
+    c = (c.float() + (b[rows] / alpha)[:, None] * u).to(torch.bfloat16)
+    # targets from the full vocabulary (every rank builds the same global classifier bias)
+    c_full = c if c.shape[0] == v else None
+    t = torch.empty(n, dtype=torch.int64, device=dev)
+    for r0 in range(0, n, 1024):
+        r1 = min(n, r0 + 1024)
+        if c_full is not None:
+            z = e[r0:r1].float() @ c_full.float().T
+        else:  # vocab-parallel: only the bias drives the sampling (cheap, shard-independent)
+            z = b[None, :].expand(r1 - r0, -1).clone()
+        gum = -torch.log(-torch.log(torch.rand(z.shape, device=dev, generator=g2).clamp_min(1e-20)))
+        t[r0:r1] = (z + gum).argmax(dim=1)
+        del z, gum
+    return e, c, t
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -208,6 +242,10 @@ def main():
     ap.add_argument("--mode", default="vocab", choices=["vocab", "token"])
     ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
     ap.add_argument("--no-sort", action="store_true")
+    ap.add_argument("--dist", default="iid", choices=["iid", "zipf"],
+                    help="iid: E, C Gaussian, uniform targets (D1); zipf: a shared direction carries a "
+                         "log-Zipf bias per vocabulary row and targets are sampled from the softmax "
+                         "(SURVEY §8(d) D3, where vocabulary sorting groups the non-trivial tiles)")
     ap.add_argument("--no-filter", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="init the process group even for 1 rank")
     ap.add_argument("--paper-order", action="store_true",
@@ -269,6 +307,8 @@ def main():
         c = (torch.randn(v, d, device=dev, generator=gen) * (sigma / math.sqrt(d))).to(torch.bfloat16)
     gen.manual_seed(2 + (rank if token_mode else 0))
     t = torch.randint(0, v, (n,), device=dev, generator=gen)
+    if args.dist == "zipf":
+        e, c, t = zipf_head(e, c, v, v0, gen, dev)
     if pad_frac:
         seq = 4096
         pos = torch.arange(n, device=dev) % seq
@@ -475,7 +515,7 @@ def main():
             "scaling": "weak" if (world == 1 or token_mode) else "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random E ~ N(0,1), C ~ N(0, sigma^2/D), uniform targets)",
             "config": {
-                "workload": f"{args.config} head N={n} D={d} V={v}", "sigma": sigma, "softcap": cap,
+                "workload": f"{args.config} head N={n} D={d} V={v}", "dist": args.dist, "sigma": sigma, "softcap": cap,
                 "ignore_pad_frac": pad_frac, "filter_eps": None if args.no_filter else 2 ** -12,
                 "vocab_sorting": sort, "reduction": "mean", "low_memory": args.low_memory,
                 "filter_order": "paper (exempt_label_tiles=False)" if args.paper_order else "reference",
