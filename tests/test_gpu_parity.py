@@ -966,3 +966,33 @@ def test_frozen_input_skips_its_pass(cuda_device, low, frozen, split):
         assert part[1] is None and torch.equal(part[0], full[0])
     else:
         assert part[0] is None and torch.equal(part[1], full[1])
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_zipf_structured_head(cuda_device, path):
+    """a shared log-Zipf row bias with targets sampled from the softmax.  Kept
+    tiles concentrate in the first sorted vocabulary tiles (many token tiles per vocab tile);
+    parity with the oracle, and sorting skips more tiles than the natural order."""
+    rng = np.random.default_rng(88)
+    n, d, v, alpha = 700, 128, 40000, 4.0
+    u = rng.standard_normal(d)
+    u /= np.linalg.norm(u)
+    b = -1.5 * np.log(rng.permutation(v) + 1.0)  # Zipf exponent 1.5: the tail tiles are filterable
+    b -= b.mean()
+    e = O.round_to_bf16((rng.standard_normal((n, d)) + alpha * u).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) / math.sqrt(d) + (b / alpha)[:, None] * u).astype(np.float32))
+    z = e.astype(np.float64) @ c.astype(np.float64).T
+    x = np.argmax(z - np.log(-np.log(rng.uniform(1e-12, 1.0, z.shape))), axis=1)
+    x[::10] = -1
+    loss, lse, de, dc, cnt, perm = _run(e, c, x, path=path)
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    assert _loss_err(loss, nl) < LOSS_TOL
+    ce, cl, idx = O.filter_ignored(e, x)
+    up = O.default_upstream(x, "mean-over-valid")
+    rde_c, rdc = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up[idx], perm=perm)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
+    if path == "tiles":
+        unsorted = _run(e, c, x, path=path, sorting=False)
+        assert int(cnt[1]) > int(unsorted[4][1])  # more eps-skipped tiles with the sorted order
