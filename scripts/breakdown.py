@@ -17,6 +17,10 @@ g = torch.Generator(device=dev).manual_seed(0)
 e = torch.randn(N, D, device=dev, generator=g).bfloat16().requires_grad_(True)
 c = (torch.randn(V, D, device=dev, generator=g) * SIGMA / math.sqrt(D)).bfloat16().requires_grad_(True)
 t = torch.randint(0, V, (N,), device=dev, generator=g)
+if os.environ.get("BREAKDOWN_DIST", "iid") == "zipf":  # SURVEY D3 (bench.zipf_head)
+    e, c, t = bench.zipf_head(e.detach(), c.detach(), V, 0, g, dev)
+    e.requires_grad_(True)
+    c.requires_grad_(True)
 
 
 def step():
@@ -81,6 +85,8 @@ for ms, short, f, b in rows:
     if ms < 0.004:
         continue
     ach = frac = ""
+    if ms < 0.05:  # gated-off fallback launches and tiny kernels: no meaningful rate
+        f = b = None
     if f:
         ach = f"{f / (ms / 1e3) / 1e12:.0f} TFLOP/s"
         frac = f"{f / (ms / 1e3) / 1e12 / peaks['bf16_tflops']:.0%}"
