@@ -513,7 +513,8 @@ def main():
             "metric": "fwd+bwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak" if (world == 1 or token_mode) else "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random E ~ N(0,1), C ~ N(0, sigma^2/D), uniform targets)",
+            "vs_baseline": None, "dtype": "bf16", "data": ("synthetic (random E ~ N(0,1), C ~ N(0, sigma^2/D), uniform targets)" if args.dist == "iid" else
+                     "synthetic (D3: E, C Gaussian plus a shared log-Zipf row bias, targets sampled from the softmax)"),
             "config": {
                 "workload": f"{args.config} head N={n} D={d} V={v}", "dist": args.dist, "sigma": sigma, "softcap": cap,
                 "ignore_pad_frac": pad_frac, "filter_eps": None if args.no_filter else 2 ** -12,
