@@ -59,7 +59,8 @@ class _LinearCrossEntropy(torch.autograd.Function):
         elif eps > 0 and low_memory and training and os.environ.get("CCE_LOWMEM_RECOMPUTE", "0") == "0":
             # bounded memory: the same decision from the forward, over vocabulary groups
             lse_local, correct, ctx.state = ops.forward_grouped(e, c, targets, ignore_index, vocab_start,
-                                                                softcap, vocab_sorting)
+                                                                softcap, vocab_sorting, eps=eps,
+                                                                label_split=not exempt_label_tiles)
         else:
             lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
         if group is None:

@@ -323,6 +323,34 @@ def lowmem_group_vtiles(n: int, d: int, v: int) -> int:
     return max(1, min(mt, by_shat, by_cg))
 
 
+GROUP_MARGIN = 1.3  # headroom of the learned kept density when sizing vocabulary groups
+
+
+def grouped_plan(n: int, d: int, v: int, key) -> tuple[int, int]:
+    """(vocab tiles per group, S-hat slots per group) for low_memory=True.  Until a kept count of
+    this shape has been observed: the worst case (every tile of a group kept, lowmem_group_vtiles).
+    Afterwards the same memory -- CCE_LOWMEM_SHAT_MB of slots plus the group's rows of the
+    worst-case plan -- is split by the learned kept density, so groups grow (fewer passes over the
+    fp32 dE, fewer launches); a group that keeps more than its slots takes the on-device overflow
+    path of cce_bwd_kept."""
+    nt = max(1, -(-n // BLOCK_TOKENS))
+    mt = -(-v // BLOCK_VOCAB)
+    gv0 = lowmem_group_vtiles(n, d, v)
+    worst = (gv0, nt * gv0)
+    hint = _KEPT_HINT.get(key)
+    if hint is None or os.environ.get("CCE_LOWMEM_WORST", "0") == "1":
+        return worst
+    _harvest(hint)
+    if hint[2] is None:
+        return worst
+    rows_bytes = BLOCK_VOCAB * d * 2
+    budget = nt * gv0 * SHAT_TILE_BYTES + gv0 * rows_bytes  # the worst-case plan's memory
+    per_vtile = GROUP_MARGIN * (hint[2] / mt) * SHAT_TILE_BYTES + rows_bytes
+    gv = int(max(gv0, min(mt, budget // max(per_vtile, 1))))
+    slots = min(nt * gv, max(gv, int(GROUP_MARGIN * hint[2] * gv / mt) + gv))
+    return gv, slots
+
+
 def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
                     softcap: float = 0.0, eps: float | None = EPSILON_DEFAULT, vocab_sorting: bool = True,
                     perm: torch.Tensor | None = None, fp32_de: bool = False,
@@ -604,6 +632,8 @@ class GroupState:
     vocab_start: int
     softcap: float
     mean_logits: torch.Tensor | None = None
+    slots: int = 0   # S-hat slots per group (grouped_plan)
+    key: tuple = ()  # shape key of the learned kept count
 
     def nbytes(self) -> int:
         own = [self.e_c, self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded]
@@ -616,7 +646,8 @@ def _group_rows(c, perm, v0: int, v1: int) -> torch.Tensor:
 
 
 def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
-                    vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+                    vocab_sorting: bool = True, perm: torch.Tensor | None = None,
+                    eps: float = EPSILON_DEFAULT, label_split: bool = False):
     """Forward of the bounded-memory training path: (lse_local, correct, GroupState).
 
     The same sweep as forward_tiles (compacted rows, the reference's vocabulary order, per-row
@@ -645,11 +676,13 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
     del inv_perm
     nt = -(-n // BLOCK_TOKENS)
     mt = -(-v // BLOCK_VOCAB)
-    gv = lowmem_group_vtiles(n, d, v)
+    key = ("grouped", n, d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
+           perm is not None)
+    gv, slots = grouped_plan(n, d, v, key)
     groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gv) * BLOCK_VOCAB)) for m0 in range(0, mt, gv)]
     tile_max = torch.empty(max(nt, 1) * mt * BLOCK_TOKENS, dtype=torch.float32, device=dev)
     state = GroupState(e, c, e_c, row_map, n_valid, perm, perm_padded, pos, tile_max, groups,
-                       int(vocab_start), float(softcap or 0.0), mean_logits)
+                       int(vocab_start), float(softcap or 0.0), mean_logits, slots, key)
     lse_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
     corr_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
     if n == 0:
@@ -657,7 +690,9 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
     ws_bytes = max(lib.cce_fwd_workspace_bytes(n, d, v1 - v0) for v0, v1 in groups)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     ev = _ev_begin("fwd")
+    c_g = None
     for g, (v0, v1) in enumerate(groups):
+        c_g = None  # release the previous group's rows before gathering the next (one buffer live)
         c_g = _group_rows(c, perm, v0, v1)
         tm_g = tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
         _lib.check(lib.cce_fwd_tiles(_p(e_c), _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0,
@@ -702,7 +737,9 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
         raise ValueError("backward_grouped needs filtering (eps > 0)")
     nt = -(-n // BLOCK_TOKENS)
     gtiles = max(-(-(v1 - v0) // BLOCK_VOCAB) for v0, v1 in state.groups)
-    cap = nt * gtiles  # every tile of the largest group: the whole-batch pass always fits
+    # slots from grouped_plan: every tile of the group until a kept count is known, then the
+    # learned density (a group that keeps more takes cce_bwd_kept's on-device overflow path)
+    cap = max(gtiles, min(nt * gtiles, state.slots or nt * gtiles))
     shat = torch.empty(cap * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
     ws_bytes = max(lib.cce_bwd_kept_workspace_bytes(n, d, v1 - v0, cap, 0) for v0, v1 in state.groups)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -710,8 +747,10 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
     split = bool(label_split)
     ev = _ev_begin("bwd")
     last = len(state.groups) - 1
+    c_g = None
     for g, (v0, v1) in enumerate(state.groups):
         vg = v1 - v0
+        c_g = None  # one group's rows live at a time
         c_g = _group_rows(c, state.perm, v0, v1)
         tm_g = state.tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
         perm_g = state.perm_padded[v0:] if state.perm_padded is not None else None
@@ -725,6 +764,8 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
                                     stream), "cce_bwd_kept")
         LAUNCHES["count"] += 3 + 6 + (1 if state.perm is not None else 0)
     del ws, shat
+    if state.key:
+        _remember_count(state.key, counters, 0)  # kept tiles of all groups: sizes the next call
     if split:
         label_terms(e, c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream, correct,
                     state.softcap, de, dc)

@@ -996,3 +996,28 @@ def test_zipf_structured_head(cuda_device, path):
     if path == "tiles":
         unsorted = _run(e, c, x, path=path, sorting=False)
         assert int(cnt[1]) > int(unsorted[4][1])  # more eps-skipped tiles with the sorted order
+
+
+def test_grouped_learned_plan_overflows_safely(cuda_device, monkeypatch):
+    """low_memory=True sizes its vocabulary groups from the previous call's kept count.  A call
+    that keeps far more tiles than learned (same shape, denser logits) overflows the groups'
+    S-hat slots and takes the on-device fallback: results still match the reference's filtered
+    lse_backward with the GPU's tile geometry and order."""
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.setenv("CCE_LOWMEM_SHAT_MB", "2")  # several groups at this size
+    rng = np.random.default_rng(101)
+    n, d, v = 300, 64, 100000  # labels touch ~28% of the tiles: the sparse calls keep little
+    x = rng.integers(0, v, n)
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    flags = []
+    for sigma in (0.3, 0.3, 3.0):  # sparse, sparse (learned plan), dense (overflow)
+        c = O.round_to_bf16((rng.standard_normal((v, d)) * sigma / math.sqrt(d)).astype(np.float32))
+        loss, lse, de, dc, cnt, perm = _run(e, c, x, path="grouped")
+        flags.append(int(ops.LAST_OVERFLOW["flag"].item()))
+        nl, nlse, _ = O.naive_forward(e, c, x)
+        assert _loss_err(loss, nl) < LOSS_TOL
+        rde, rdc = O.lse_backward_blocked(e, c, x, nlse.astype(np.float32),
+                                          O.default_upstream(x, "mean-over-valid"), perm=perm)
+        assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
+    assert flags == [0, 0, 1]  # only the dense call overflowed the learned slots
