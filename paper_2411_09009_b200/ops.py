@@ -311,11 +311,14 @@ LOWMEM_SHAT_MB = 256  # S-hat slots of one vocabulary group in the low-memory ba
 LOWMEM_CG_MB = 256    # classifier rows of one vocabulary group
 
 
-def lowmem_group_vtiles(n: int, d: int, v: int) -> int:
+GROUPED_SHAT_MB = 128  # low_memory=True (vocabulary groups sized from the learned density)
+
+
+def lowmem_group_vtiles(n: int, d: int, v: int, default_mb: int = LOWMEM_SHAT_MB) -> int:
     """Vocab tiles per group of the low-memory backward: the worst-case S-hat of a group
-    (every token tile x every group vocab tile) within CCE_LOWMEM_SHAT_MB, and the group's
-    classifier rows within LOWMEM_CG_MB."""
-    budget = int(os.environ.get("CCE_LOWMEM_SHAT_MB", LOWMEM_SHAT_MB)) << 20
+    (every token tile x every group vocab tile) within CCE_LOWMEM_SHAT_MB (else default_mb), and
+    the group's classifier rows within LOWMEM_CG_MB."""
+    budget = int(os.environ.get("CCE_LOWMEM_SHAT_MB", default_mb)) << 20
     nt = max(1, -(-n // BLOCK_TOKENS))
     mt = -(-v // BLOCK_VOCAB)
     by_shat = budget // (nt * BLOCK_TOKENS * BLOCK_VOCAB * 2)
@@ -335,7 +338,9 @@ def grouped_plan(n: int, d: int, v: int, key) -> tuple[int, int]:
     path of cce_bwd_kept."""
     nt = max(1, -(-n // BLOCK_TOKENS))
     mt = -(-v // BLOCK_VOCAB)
-    gv0 = lowmem_group_vtiles(n, d, v)
+    # 128 MB measured best for this mode: 13.3 ms / 275 MiB vs 13.0 ms / 443 MiB at 256 MB
+    # (Gemma-2-2B, profiles/r1/ab/ab_lowmem_budget.txt)
+    gv0 = lowmem_group_vtiles(n, d, v, GROUPED_SHAT_MB)
     worst = (gv0, nt * gv0)
     hint = _KEPT_HINT.get(key)
     if hint is None or os.environ.get("CCE_LOWMEM_WORST", "0") == "1":
