@@ -814,7 +814,7 @@ def shat_capacity(key, nt: int, mt: int) -> int:
         if hint is not None:
             _harvest(hint)
             if hint[2] is not None:
-                cap = min(ceiling, int(hint[2] * KEPT_MARGIN) + mt)
+                cap = min(ceiling, max(int(hint[2] * KEPT_MARGIN), mt))  # floor: one token tile's tiles
     return min(max(cap, mt), nt * mt)
 
 
