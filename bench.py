@@ -262,7 +262,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2411_09009_b200 import linear_cross_entropy, ops
+    from paper_2411_09009_b200 import _lib, linear_cross_entropy, ops
     from paper_2411_09009_b200.vocab_parallel import shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -366,7 +366,7 @@ def main():
 
     # ---- timed region: device time with CUDA events, max over ranks
     ops.KERNEL_EVENTS = {}
-    launches0 = ops.LAUNCHES["count"]
+    launches0 = _lib.load().cce_launch_count()  # counted inside libcce_b200.so
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clk:
@@ -383,7 +383,7 @@ def main():
         clk.stop()
     barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    launches = (ops.LAUNCHES["count"] - launches0) // args.steps
+    launches = (_lib.load().cce_launch_count() - launches0) // args.steps
     # per-step device time of each C entry point (the backward has a primary and a device-gated
     # fallback call per step, so calls are summed per step, not averaged)
     kev = {k: sum(a.elapsed_time(b) for a, b in evs) / args.steps for k, evs in ops.KERNEL_EVENTS.items()}

@@ -28,6 +28,8 @@ extern "C" {
 /* Message of the last failing call on this thread. */
 const char* cce_last_error(void);
 int cce_abi_version(void);
+/* Kernels launched by this library so far (all threads; CUB's sort kernels not included). */
+unsigned long long cce_launch_count(void);
 
 /* ---- forward: indexed_matmul (kernels.py:204-251) + lse_forward (kernels.py:254-319) ----
  * One fused persistent tcgen05 kernel: per token row, the log-sum-exp over this shard's

@@ -26,6 +26,7 @@ c_size = ctypes.c_size_t
 SIGNATURES = {
     "cce_last_error": (ctypes.c_char_p, []),
     "cce_abi_version": (c_int, []),
+    "cce_launch_count": (ctypes.c_ulonglong, []),
     "cce_fwd_workspace_bytes": (c_size, [c_i64, c_i64, c_i64]),
     "cce_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_f32,
                         c_void_p, c_size, c_void_p, c_void_p, c_void_p]),

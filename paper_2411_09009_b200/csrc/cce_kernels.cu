@@ -14,6 +14,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -181,6 +182,9 @@ struct PdlScope {
   ~PdlScope() { g_pdl = prev; }
 };
 
+// every kernel this library launches (cce_launch_count): the bench's gpu_launches claim
+std::atomic<unsigned long long> g_launches{0};
+
 // cudaLaunchKernelEx with an optional cluster dimension and the PDL attribute when g_pdl is set
 template <typename... KArgs, typename... Args>
 int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int cluster,
@@ -207,6 +211,7 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.attrs = attr;
   cfg.numAttrs = na;
   CCE_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return 0;
 }
 
@@ -468,6 +473,8 @@ extern "C" {
 const char* cce_last_error(void) { return g_last_error.c_str(); }
 
 int cce_abi_version(void) { return 1; }
+
+unsigned long long cce_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 size_t cce_fwd_workspace_bytes(int64_t n, int64_t d, int64_t v) {
   const int nt = (int)((n + cce::BM - 1) / cce::BM);

@@ -27,7 +27,6 @@ KERNEL_EVENTS: dict[str, list] | None = None
 LAST_COUNTERS: dict = {}
 LAST_OVERFLOW: dict = {}  # device flag of the last backward: 1 if the fallback pass ran
 LAST_STATS: dict = {}     # tile-path backward: [label tiles stored by the forward, tiles recomputed]
-LAUNCHES = {"count": 0}   # kernels launched from libcce_b200.so (bench.py's gpu_launches)
 
 
 def _ev_begin(name: str):
@@ -118,7 +117,6 @@ def forward_local(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
                            float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
                            _stream(dev)), "cce_fwd")
     _ev_end("fwd", ev)
-    LAUNCHES["count"] += 3
     return lse_local, correct
 
 
@@ -132,7 +130,6 @@ def merge_shards(lse_parts, correct_parts, targets, ignore_index: int):
         _lib.check(lib.cce_merge_shards(p, _p(lse_parts.contiguous()), _p(correct_parts.contiguous()),
                                         _p(targets), int(ignore_index), n, _p(lse), _p(loss),
                                         _stream(lse_parts.device)), "cce_merge_shards")
-        LAUNCHES["count"] += 1
     return lse, loss
 
 
@@ -169,7 +166,6 @@ def vocab_order(e, c, targets, ignore_index: int, n_valid):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.check(lib.cce_vocab_order(_p(c), _p(ebar), _p(n_valid), v, d, _p(perm), _p(key), _p(ws),
                                    ws_bytes, _stream(dev)), "cce_vocab_order")
-    LAUNCHES["count"] += 4 + 5  # ebar (2), sort key, iota + CUB onesweep radix sort passes
     return perm, key
 
 
@@ -210,7 +206,6 @@ def compact_rows(targets, ignore_index: int):
     n_valid = torch.empty(1, dtype=torch.int32, device=dev)
     _lib.check(lib.cce_compact_rows(_p(targets), int(ignore_index), n, _p(row_map), _p(n_valid),
                                     _stream(dev)), "cce_compact_rows")
-    LAUNCHES["count"] += 1
     return row_map, n_valid
 
 
@@ -243,7 +238,6 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
                                 _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
-    LAUNCHES["count"] += 2 if perm is not None else 1
     de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev)
     dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
     if n == 0:
@@ -257,7 +251,6 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     if perm is not None and not gather:
         c_src = torch.empty_like(c)
         _lib.check(lib.cce_gather_rows(_p(c), _p(perm), v, d, _p(c_src), stream), "cce_gather_rows")
-        LAUNCHES["count"] += 1
         c_sorted = 1
     # S-hat slots: every token tile in one group with compact slots up to the budget; if more
     # tiles are kept than that, a fallback pass over budget-sized groups (worst case fits) runs,
@@ -281,7 +274,6 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
                                _p(dc), _p(counters), _p(overflow if run_if is None else None), stream),
                    "cce_bwd")
         _ev_end("bwd", ev)
-        LAUNCHES["count"] += 2 + 3 * (-(-nt // g))
         all_counters.append(counters)
     counters = all_counters[0] if len(plans) == 1 else torch.where(overflow.bool(), all_counters[1], all_counters[0])
     _remember_kept(key, counters)
@@ -304,7 +296,6 @@ def label_terms(e, c, perm_padded, row_map, n_valid, pos, upstream, correct, sof
                                    float(softcap or 0.0), _p(ws), ws_bytes, _p(de),
                                    int(de is not None and de.dtype == torch.float32), _p(dc), _stream(e.device)),
                "cce_label_terms")
-    LAUNCHES["count"] += 3 + 4  # keys, dC, dE + CUB radix sort passes
 
 
 LOWMEM_SHAT_MB = 256  # S-hat slots of one vocabulary group in the low-memory backward
@@ -385,7 +376,6 @@ def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_st
     pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
                                 _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
-    LAUNCHES["count"] += 2 if perm is not None else 1
     del inv_perm
     de_acc = torch.zeros(n, d, dtype=torch.float32, device=dev)
     dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev)
@@ -406,8 +396,6 @@ def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_st
     if split:
         label_terms(e, c, perm_padded, row_map, n_valid, pos, upstream, correct, softcap, de_acc, dc)
     _ev_end("bwd", ev)
-    groups = -(-(-(-v // BLOCK_VOCAB)) // gv)
-    LAUNCHES["count"] += 2 + groups * (4 if perm is not None else 3)
     LAST_COUNTERS["counters"] = counters
     de = de_acc if fp32_de else f32_to_bf16(de_acc)
     return de, dc, counters, perm
@@ -461,7 +449,6 @@ def gather_rows(src: torch.Tensor, index: torch.Tensor, rows: int) -> torch.Tens
     if rows:
         _lib.check(lib.cce_gather_rows(_p(src), _p(index), rows, src.shape[1], _p(dst),
                                        _stream(src.device)), "cce_gather_rows")
-        LAUNCHES["count"] += 1
     return dst
 
 
@@ -492,7 +479,6 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
                                 _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
-    LAUNCHES["count"] += 2 if perm is not None else 1
     c_t = gather_rows(c, perm, v) if perm is not None else c
     tile_max = torch.empty(lib.cce_tile_max_bytes(n, v) // 4, dtype=torch.float32, device=dev)
     lse_local = torch.empty(n, dtype=torch.float32, device=dev)
@@ -532,7 +518,6 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
                                  _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), stream),
                "cce_fwd_tiles")
     _ev_end("fwd", ev)
-    LAUNCHES["count"] += 3
     return lse_local, correct, state
 
 
@@ -599,8 +584,6 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
                                 _p(stats),
                                 ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
                                                 else 0), stream), "cce_bwd_kept")
-    passes = 1 + (0 if cap >= nt * mt else -(-nt // max(1, cap // mt)))
-    LAUNCHES["count"] += 3 + (1 if lab_cap else 0) + 6 + (passes - 1) * 4
     del ws
     if label_split:
         label_terms(e, state.c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream,
@@ -677,7 +660,6 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
     pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
                                 _p(perm_padded), _p(inv_perm), _p(pos), stream), "cce_bwd_prep")
-    LAUNCHES["count"] += 2 if perm is not None else 1
     del inv_perm
     nt = -(-n // BLOCK_TOKENS)
     mt = -(-v // BLOCK_VOCAB)
@@ -704,7 +686,6 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
                                      float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]),
                                      _p(corr_parts[g]), _p(tm_g), _p(None), 0, _p(None), _p(None), _p(None),
                                      stream), "cce_fwd_tiles")
-        LAUNCHES["count"] += 3 + (1 if perm is not None else 0)
     # the groups are vocabulary shards of this call: log-add-exp of their partials; the target
     # logit sits in exactly one group (0 elsewhere)
     lse_local, loss = merge_shards(lse_parts, corr_parts, targets, ignore_index)
@@ -767,7 +748,6 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
                                     _p(None), _p(None), cap, _p(ws), ws_bytes, _p(de), 1, int(g > 0),
                                     _p(dc_g), _p(counters), _p(overflow), _p(None), ctypes.c_void_p(done),
                                     stream), "cce_bwd_kept")
-        LAUNCHES["count"] += 3 + 6 + (1 if state.perm is not None else 0)
     del ws, shat
     if state.key:
         _remember_count(state.key, counters, 0)  # kept tiles of all groups: sizes the next call
@@ -879,7 +859,6 @@ def reduce_loss(loss: torch.Tensor, targets: torch.Tensor, ignore_index: int, re
     out = torch.empty((), dtype=torch.float32, device=loss.device)
     _lib.check(lib.cce_reduce_loss(_p(loss), _p(targets), int(ignore_index), loss.shape[0],
                                    REDUCTIONS[reduction], _p(out), _stream(loss.device)), "cce_reduce_loss")
-    LAUNCHES["count"] += 1
     return out
 
 
@@ -890,7 +869,6 @@ def upstream(grad: torch.Tensor, targets: torch.Tensor, ignore_index: int, reduc
     up = torch.empty(targets.shape[0], dtype=torch.float32, device=targets.device)
     _lib.check(lib.cce_upstream(_p(g), _p(targets), int(ignore_index), targets.shape[0],
                                 REDUCTIONS[reduction], _p(up), _stream(targets.device)), "cce_upstream")
-    LAUNCHES["count"] += 1
     return up
 
 
