@@ -36,7 +36,7 @@ def _inputs(n, d, v, seed=3):
     return e, c, x
 
 
-def _worker(rank, world, port, q, n, d, v, filt, cap, split=False, low=False):
+def _worker(rank, world, port, q, n, d, v, filt, cap, split=False, low=False, frozen_c=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -49,14 +49,15 @@ def _worker(rank, world, port, q, n, d, v, filt, cap, split=False, low=False):
         e_np, c_np, x_np = _inputs(n, d, v)
         v0, v1 = shard_range(v, rank, world)
         e = torch.from_numpy(e_np).cuda().bfloat16().requires_grad_(True)
-        c = torch.from_numpy(c_np[v0:v1]).cuda().bfloat16().requires_grad_(True)
+        c = torch.from_numpy(c_np[v0:v1]).cuda().bfloat16().requires_grad_(not frozen_c)
         t = torch.from_numpy(x_np).cuda()
         loss = linear_cross_entropy(e, c, t, filter_eps="auto" if filt else None, softcap=cap or None,
                                     process_group=dist.group.WORLD, vocab_start=v0,
                                     exempt_label_tiles=not split, low_memory=low)
         loss.backward()
         torch.cuda.synchronize()
-        q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy()))
+        dc = c.grad.float().cpu().numpy() if c.grad is not None else np.zeros((v1 - v0, d), np.float32)
+        q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), dc, c.grad is None))
     finally:
         dist.destroy_process_group()
 
@@ -86,12 +87,37 @@ def test_vocab_parallel_linear_cross_entropy_two_ranks(cuda_device, filt, cap, s
     up = O.default_upstream(xo, "mean-over-valid")
     fde, fdc = O.naive_backward(e_np, c_np, xo, up, softcap=cap)
     tol = 2e-2 if filt else 1e-2  # filtered: per-shard vocab orders, SURVEY B.2 filtering error
-    for rank, loss, de, _ in res:
+    for rank, loss, de, _, _ in res:
         assert abs(loss - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (rank, loss, ref_loss)
         assert O.rel_err(de, fde) < tol, rank
     assert np.array_equal(res[0][2], res[1][2])  # every rank holds the same all-reduced dE
     dc = np.concatenate([r[3] for r in res])
     assert O.rel_err(dc, fdc) < tol
+
+
+def test_vocab_parallel_frozen_classifier(cuda_device):
+    """A frozen classifier shard under vocab parallelism: no dC pass on any rank, the all-reduced
+    dE still equals the oracle's."""
+    import torch.multiprocessing as mp
+
+    world, n, d, v = 2, 600, 128, 5001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n, d, v, True, 0.0, False, False, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    e_np, c_np, x_np = _inputs(n, d, v)
+    xo = np.where(x_np == -100, -1, x_np)
+    fde, _ = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"))
+    for rank, loss, de, _, no_dc in res:
+        assert no_dc and O.rel_err(de, fde) < 2e-2, rank
+    assert np.array_equal(res[0][2], res[1][2])
 
 
 @pytest.mark.parametrize("low", [False, True])
