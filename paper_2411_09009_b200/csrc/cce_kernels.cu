@@ -369,8 +369,9 @@ KeptWs kept_layout(void* base, int64_t n, int64_t v, int64_t capacity, int64_t l
   w.keep_bytes = up((size_t)nt * mt);
   w.keep = b + o; o += w.keep_bytes;
   w.alist = reinterpret_cast<int2*>(b + o); o += up((size_t)(capacity + lab_capacity) * sizeof(int2));
-  w.rlist = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
-  w.pairs = reinterpret_cast<int2*>(b + o); o += up((size_t)capacity * sizeof(int2));
+  // recompute list / pairs: the fallback passes use the whole S-hat buffer (both regions)
+  w.rlist = reinterpret_cast<int2*>(b + o); o += up((size_t)(capacity + lab_capacity) * sizeof(int2));
+  w.pairs = reinterpret_cast<int2*>(b + o); o += up((size_t)(capacity + lab_capacity) * sizeof(int2));
   w.slot_bytes = up((size_t)nt * mt * 4);
   w.slot_of = reinterpret_cast<int32_t*>(b + o); o += w.slot_bytes;
   w.block_zero = b + o; o += up((size_t)nt);
@@ -912,8 +913,11 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
                              (const int*)w.ok, w.pairs, w.pair_count))
           return e;
     } else {
+      // fallback: the whole S-hat buffer as recompute slots (stored label tiles recomputed too),
+      // so each group covers more token tiles and the gated chain is shorter
       if (int e = launch_k(cce::list_single_kernel, dim3(1), dim3(1024), 0, stream, 1, w.keep, nt, mt, g0, g,
-                           (int)capacity_tiles, (int)lab_capacity, lab_slot, run_if, w.cnt_m, w.rcnt_m, w.off_m,
+                           (int)(capacity_tiles + lab_capacity), 0, (const int32_t*)nullptr, run_if, w.cnt_m,
+                           w.rcnt_m, w.off_m,
                            w.roff_m, w.alist, w.rlist, w.slot_of, w.cnt_n, w.list_count, w.rlist_count,
                            w.list_count + 3, w.pairs, w.pair_count))
         return e;
@@ -939,8 +943,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     p.row_map = row_map;
     p.eps = eps;
     p.label_split = label_split;
-    p.shat = shat_rec;
-    p.capacity = (int)capacity_tiles;
+    p.shat = primary ? shat_rec : shat_all;
+    p.capacity = (int)(primary ? capacity_tiles : capacity_tiles + lab_capacity);
     p.counters = counters;
     p.list = w.rlist;
     p.list_count = w.rlist_count;
@@ -1002,7 +1006,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     CCE_CUDA(cudaMemcpyAsync(stats + 1, w.rlist_count, sizeof(int), cudaMemcpyDeviceToDevice, stream));
   }
   if (grouped && !getenv("CCE_MEASURE_NO_FALLBACK")) {  // the env switch is for A/B timing only
-    const int g = (int)std::max<int64_t>(1, capacity_tiles / mt);
+    const int g = (int)std::max<int64_t>(1, (capacity_tiles + lab_capacity) / mt);
     for (int g0 = 0; g0 < nt; g0 += g)
       if (int e = run_pass(g0, std::min(g, nt - g0), false, overflow, g0 + g >= nt)) return e;
   }
