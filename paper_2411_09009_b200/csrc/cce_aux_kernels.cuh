@@ -779,25 +779,49 @@ __global__ void label_keys_kernel(const int32_t* __restrict__ row_map, const int
   val[k] = vv;
 }
 
-// dC: one block per sorted entry; the first entry of each label run sums the run in sort order
-// (deterministic) and adds it to that classifier row (fp32 sum, one bf16 rounding).
-__global__ void label_dc_kernel(const int32_t* __restrict__ key, const int32_t* __restrict__ val, int n,
-                                const __nv_bfloat16* __restrict__ E, const float* __restrict__ up,
-                                const float* __restrict__ correct, float softcap,
-                                const int32_t* __restrict__ perm, int d, __nv_bfloat16* __restrict__ dc) {
+// dC: blocks stride over the sorted entries (blockIdx.y = a 256-column chunk of D); the first
+// entry of each label run sums the run in sort order (deterministic, one fp32 sum per column,
+// one bf16 rounding into that classifier row).  The run's rows and coefficients are staged in
+// shared memory 512 at a time, so the E loads of a column are independent and pipeline: with
+// Zipf-distributed labels one run can hold hundreds of tokens.
+constexpr int LABEL_DC_CHUNK = 512;
+__global__ void __launch_bounds__(256) label_dc_kernel(
+    const int32_t* __restrict__ key, const int32_t* __restrict__ val, int n, const __nv_bfloat16* __restrict__ E,
+    const float* __restrict__ up, const float* __restrict__ correct, float softcap,
+    const int32_t* __restrict__ perm, int d, __nv_bfloat16* __restrict__ dc) {
   griddep_wait();
-  const int k = blockIdx.x;
-  const int32_t p = key[k];
-  if (p == INT_MAX || (k > 0 && key[k - 1] == p)) return;
-  const int crow = perm ? perm[p] : p;
-  for (int col = threadIdx.x; col < d; col += blockDim.x) {
+  __shared__ int s_row[LABEL_DC_CHUNK];
+  __shared__ float s_coef[LABEL_DC_CHUNK];
+  const int col = blockIdx.y * blockDim.x + threadIdx.x;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int32_t p = key[k];
+    if (p == INT_MAX || (k > 0 && key[k - 1] == p)) continue;  // not the head of a label run
     float acc = 0.f;
-    for (int j = k; j < n && key[j] == p; ++j) {
-      const int orow = val[j];
-      acc += label_coef(up, correct, softcap, orow) * __bfloat162float(E[(size_t)orow * d + col]);
+    for (int j0 = k;; j0 += LABEL_DC_CHUNK) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < LABEL_DC_CHUNK; t += blockDim.x) {
+        const int j = j0 + t;
+        const bool in = j < n && key[j] == p;  // a run is contiguous: valid entries form a prefix
+        const int orow = in ? val[j] : -1;
+        s_row[t] = orow;
+        s_coef[t] = in ? label_coef(up, correct, softcap, orow) : 0.f;
+      }
+      __syncthreads();
+      if (col < d) {
+#pragma unroll 4
+        for (int t = 0; t < LABEL_DC_CHUNK; ++t) {
+          const int orow = s_row[t];
+          if (orow < 0) break;
+          acc += s_coef[t] * __bfloat162float(E[(size_t)orow * d + col]);
+        }
+      }
+      if (s_row[LABEL_DC_CHUNK - 1] < 0) break;  // the run ended inside this chunk (uniform)
     }
-    __nv_bfloat16* dst = dc + (size_t)crow * d + col;
-    *dst = __float2bfloat16(__bfloat162float(*dst) + acc);
+    if (col < d) {
+      const int crow = perm ? perm[p] : p;
+      __nv_bfloat16* dst = dc + (size_t)crow * d + col;
+      *dst = __float2bfloat16(__bfloat162float(*dst) + acc);
+    }
   }
 }
 

@@ -1183,7 +1183,8 @@ int cce_label_terms(const void* E, const void* C, const int32_t* perm_padded, co
     PDL_LAUNCH(cce::label_keys_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, row_map, n_valid,
                pos, (int)n, key, val);
     CCE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, val, val_s, (int)n, 0, 32, stream));
-    PDL_LAUNCH(cce::label_dc_kernel, dim3((unsigned)n), dim3(256), 0, stream, key_s, val_s, (int)n,
+    PDL_LAUNCH(cce::label_dc_kernel, dim3((unsigned)std::min<int64_t>(n, 4 * num_sms()), (unsigned)((d + 255) / 256)),
+               dim3(256), 0, stream, key_s, val_s, (int)n,
                static_cast<const __nv_bfloat16*>(E), upstream, correct, softcap, perm_padded, (int)d,
                static_cast<__nv_bfloat16*>(dc));
   }

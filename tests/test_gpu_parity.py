@@ -1021,3 +1021,41 @@ def test_grouped_learned_plan_overflows_safely(cuda_device, monkeypatch):
                                           O.default_upstream(x, "mean-over-valid"), perm=perm)
         assert O.rel_err(de, rde) < GRAD_TOL and O.rel_err(dc, rdc) < GRAD_TOL
     assert flags == [0, 0, 1]  # only the dense call overflowed the learned slots
+
+
+@pytest.mark.parametrize("path", ["tiles", "lowmem"])
+def test_paper_ordering_long_label_runs(cuda_device, path):
+    """Paper ordering with many tokens sharing one label (Zipf-like targets): the exact label term
+    sums a run of 1200 tokens (three 512-token chunks of label_dc_kernel) in sort order."""
+    from paper_2411_09009_b200 import ops
+
+    rng = np.random.default_rng(123)
+    n, d, v = 1500, 96, 9000
+    e = O.round_to_bf16(rng.standard_normal((n, d)).astype(np.float32))
+    c = O.round_to_bf16((rng.standard_normal((v, d)) * 0.7 / math.sqrt(d)).astype(np.float32))
+    x = rng.integers(0, v, n)
+    x[rng.permutation(n)[:1200]] = 7
+    x[::31] = -1
+    ed, cd, td = _dev(e, torch.bfloat16), _dev(c, torch.bfloat16), _dev(x.astype(np.int64))
+    if path == "tiles":
+        lse_l, corr, st = ops.forward_tiles(ed, cd, td, -1, 0, 0.0, vocab_sorting=True, label_split=True)
+    else:
+        lse_l, corr = ops.forward_local(ed, cd, td, -1, 0, 0.0)
+    lse, loss = ops.merge_shards(lse_l[None], corr[None], td, -1)
+    up_np = O.default_upstream(x, "mean-over-valid")
+    up = _dev(up_np.astype(np.float32))
+    if path == "tiles":
+        de, dc, _ = ops.backward_tiles(st, td, lse, up, ignore_index=-1, label_split=True, correct=corr)
+        perm = st.perm.cpu().numpy()
+    else:
+        de, dc, _, pm = ops.backward_lowmem(ed, cd, td, lse, up, ignore_index=-1, label_split=True, correct=corr)
+        perm = pm.cpu().numpy()
+    torch.cuda.synchronize()
+    nl, nlse, _ = O.naive_forward(e, c, x)
+    ce, cl, idx = O.filter_ignored(e, x)
+    rde_c, rdc = O.lse_backward_blocked(ce, c, cl, nlse[idx].astype(np.float32), up_np[idx], perm=perm,
+                                        exempt_labels=False)
+    rde = np.zeros_like(e)
+    rde[idx] = rde_c
+    assert O.rel_err(de.float().cpu().numpy(), rde) < GRAD_TOL
+    assert O.rel_err(dc.float().cpu().numpy(), rdc) < GRAD_TOL
