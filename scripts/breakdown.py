@@ -25,7 +25,8 @@ if os.environ.get("BREAKDOWN_DIST", "iid") == "zipf":  # SURVEY D3 (bench.zipf_h
 
 def step():
     e.grad = c.grad = None
-    linear_cross_entropy(e, c, t, softcap=CAP or None, low_memory=LOW).backward()
+    linear_cross_entropy(e, c, t, softcap=CAP or None, low_memory=LOW,
+                         exempt_label_tiles=os.environ.get("BREAKDOWN_PAPER", "0") != "1").backward()
 
 
 for _ in range(4):
