@@ -144,7 +144,9 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
  * de_accumulate (fp32 dE only) the call adds its dE into de_out instead of writing it, so the
  * groups of one backward accumulate in a fixed order.
  * de_out or dc may be NULL (not both): that pass is skipped (an input that needs no gradient,
- * e.g. a frozen classifier). */
+ * e.g. a frozen classifier).  kept_per_vtile (optional, ceil(v/256) ints) receives the number of
+ * kept tiles of each vocab tile (sizing hints: low_memory groups follow the vocabulary's
+ * kept density). */
 size_t cce_tile_max_bytes(int64_t n, int64_t v);
 int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
@@ -158,7 +160,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
                  const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
                  void* de_out, int de_fp32, int de_accumulate, void* dc, unsigned long long* counters,
-                 int* overflow, int* stats, void* de_done_event, void* stream);
+                 int* overflow, int* stats, int* kept_per_vtile, void* de_done_event, void* stream);
 
 /* ---- low-memory backward: vocabulary groups (low_memory=True) ----
  * lse_backward over groups of `group_vtiles` vocab tiles in tile order: per group, the group's

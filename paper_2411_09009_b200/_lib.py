@@ -53,7 +53,7 @@ SIGNATURES = {
     "cce_bwd_kept": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64,
                              c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int, c_void_p,
                              c_i64, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_size, c_void_p,
-                             c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                             c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_bwd_lowmem_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_lowmem": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int, c_i64, c_void_p,

@@ -509,12 +509,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         return p.cnt_m[mm];
       };
       int cnt = start < units ? unit_cnt(start) : 0;
-      for (int u = start; u < units; u += stride, ++t) {
+      for (int u = start; u < units; u += stride) {
         const int un = u + stride;
         const int cnt_next = un < units ? unit_cnt(un) : 0;
-        const int buf = t & 1;
         const int ksteps = 2 * cnt;
         cnt = cnt_next;
+        // a vocab tile no token tile keeps: no accumulator hand-off (the epilogue skips it too;
+        // `t` counts only the units that use a buffer)
+        if (ksteps == 0) continue;
+        const int buf = t & 1;
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * DCH;
@@ -542,6 +545,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mma_commit_pair(&acc_full[buf]);
         else
           mma_commit(&acc_full[buf]);
+        ++t;
       }
     }
   } else {
@@ -554,17 +558,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     uint8_t* wstg = stg + quarter * 32 * DC_STG_PITCH;
     int t = 0;
-    for (int u = start; u < units; u += stride, ++t) {
+    for (int u = start; u < units; u += stride) {
       int vh, dc, m;
       dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
+      const bool has = p.cnt_m[m] > 0;
+      if (!has && p.accumulate) continue;  // nothing kept and nothing to write
       const int buf = t & 1;
       // per-unit loads issued before the wait so their latency hides behind it
-      const bool has = p.cnt_m[m] > 0;
       const int vpos = m * BN + vh * 128 + row;
       const int my_vrow = vpos < p.v ? (p.perm_store ? p.perm_store[vpos] : vpos) : -1;
-      mbar_wait(&acc_full[buf], (t >> 1) & 1);
-      tc_fence_after();
-      if (has || !p.accumulate) {
+      if (has) {  // empty units use no accumulator: their zero rows are written right away
+        mbar_wait(&acc_full[buf], (t >> 1) & 1);
+        tc_fence_after();
+      }
+      {
 #pragma unroll 1
         for (int c = 0; c < DCH / 64; ++c) {
           // 1) this thread's 64 columns -> bf16 -> staging row `lane`
@@ -615,6 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
         }
       }
+      if (!has) continue;
       tc_fence_before();
       if (CG == 2) {
         named_bar_sync(2, 128);
@@ -627,6 +635,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
         mbar_arrive(&acc_free[buf]);
       }
+      ++t;
     }
   }
   tc_fence_before();

@@ -821,7 +821,7 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
                  int label_split, void* shat, int64_t lab_capacity, const int32_t* lab_slot,
                  const void* lab_list, const int* lab_count, int64_t capacity_tiles, void* ws, size_t ws_bytes,
                  void* de_out, int de_fp32, int de_accumulate, void* dc, unsigned long long* counters,
-                 int* overflow, int* stats, void* de_done_event, void* stream_ptr) {
+                 int* overflow, int* stats, int* kept_per_vtile, void* de_done_event, void* stream_ptr) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_kept: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_kept: needs filtering (eps > 0); use cce_bwd without it");
@@ -1005,6 +1005,8 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
       CCE_CUDA(cudaMemsetAsync(stats, 0, sizeof(int), stream));
     CCE_CUDA(cudaMemcpyAsync(stats + 1, w.rlist_count, sizeof(int), cudaMemcpyDeviceToDevice, stream));
   }
+  if (kept_per_vtile)  // kept tiles per vocab tile of the whole batch (list_count_kernel)
+    CCE_CUDA(cudaMemcpyAsync(kept_per_vtile, w.cnt_m, (size_t)mt * sizeof(int), cudaMemcpyDeviceToDevice, stream));
   if (grouped && !getenv("CCE_MEASURE_NO_FALLBACK")) {  // the env switch is for A/B timing only
     const int g = (int)std::max<int64_t>(1, (capacity_tiles + lab_capacity) / mt);
     for (int g0 = 0; g0 < nt; g0 += g)

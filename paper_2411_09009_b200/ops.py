@@ -320,31 +320,45 @@ def lowmem_group_vtiles(n: int, d: int, v: int, default_mb: int = LOWMEM_SHAT_MB
 GROUP_MARGIN = 1.3  # headroom of the learned kept density when sizing vocabulary groups
 
 
-def grouped_plan(n: int, d: int, v: int, key) -> tuple[int, int]:
-    """(vocab tiles per group, S-hat slots per group) for low_memory=True.  Until a kept count of
-    this shape has been observed: the worst case (every tile of a group kept, lowmem_group_vtiles).
-    Afterwards the same memory -- CCE_LOWMEM_SHAT_MB of slots plus the group's rows of the
-    worst-case plan -- is split by the learned kept density, so groups grow (fewer passes over the
-    fp32 dE, fewer launches); a group that keeps more than its slots takes the on-device overflow
-    path of cce_bwd_kept."""
+def grouped_plan(n: int, d: int, v: int, key) -> tuple[list, int]:
+    """(vocab-tile ranges of the groups, S-hat slots per group) for low_memory=True.
+
+    Until kept counts of this shape have been observed: the worst case, equal groups with every
+    tile of a group kept (lowmem_group_vtiles).  Afterwards the same memory -- the worst-case
+    plan's S-hat slots plus one group's classifier rows -- is split in halves between slots and
+    rows, and vocab tiles are packed greedily by the previous call's kept tiles per vocab tile
+    (1.3x margin): dense tiles (the head of the sorted vocabulary under Zipf-like logits) form
+    small groups, sparse ones large groups.  A group that keeps more than its slots takes the
+    on-device overflow path of cce_bwd_kept."""
     nt = max(1, -(-n // BLOCK_TOKENS))
     mt = -(-v // BLOCK_VOCAB)
     # 128 MB measured best for this mode: 13.3 ms / 275 MiB vs 13.0 ms / 443 MiB at 256 MB
     # (Gemma-2-2B, profiles/r1/ab/ab_lowmem_budget.txt)
     gv0 = lowmem_group_vtiles(n, d, v, GROUPED_SHAT_MB)
-    worst = (gv0, nt * gv0)
-    hint = _KEPT_HINT.get(key)
-    if hint is None or os.environ.get("CCE_LOWMEM_WORST", "0") == "1":
+    worst = ([(m0, min(mt, m0 + gv0)) for m0 in range(0, mt, gv0)], nt * gv0)
+    if os.environ.get("CCE_LOWMEM_WORST", "0") == "1":
+        return worst
+    hint = _KEPT_HINT.get(key + ("per-vtile",))
+    if hint is None:
         return worst
     _harvest(hint)
-    if hint[2] is None:
+    cnt = hint[2]
+    if cnt is None or len(cnt) != mt:
         return worst
     rows_bytes = BLOCK_VOCAB * d * 2
     budget = nt * gv0 * SHAT_TILE_BYTES + gv0 * rows_bytes  # the worst-case plan's memory
-    per_vtile = GROUP_MARGIN * (hint[2] / mt) * SHAT_TILE_BYTES + rows_bytes
-    gv = int(max(gv0, min(mt, budget // max(per_vtile, 1))))
-    slots = min(nt * gv, max(gv, int(GROUP_MARGIN * hint[2] * gv / mt) + gv))
-    return gv, slots
+    slots = max(1, budget // 2 // SHAT_TILE_BYTES)
+    # cce_bwd_kept needs at least one token tile's vocab tiles of slots: groups stay <= slots
+    gmax = int(max(1, min(mt, budget // 2 // rows_bytes, slots)))
+    bounds, m0, acc = [], 0, 0.0
+    for m in range(mt):
+        need = GROUP_MARGIN * cnt[m]
+        if m > m0 and (m - m0 >= gmax or acc + need + (m + 1 - m0) > slots):
+            bounds.append((m0, m))
+            m0, acc = m, 0.0
+        acc += need
+    bounds.append((m0, mt))
+    return bounds, int(slots)
 
 
 def backward_lowmem(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
@@ -581,7 +595,7 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
                                 n, d, v, state.softcap, float(eps), int(bool(label_split)), _p(state.shat),
                                 lab_cap, _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), cap,
                                 _p(ws), ws_bytes, _p(de), int(fp32_de), 0, _p(dc), _p(counters), _p(overflow),
-                                _p(stats),
+                                _p(stats), _p(None),
                                 ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
                                                 else 0), stream), "cce_bwd_kept")
     del ws
@@ -665,8 +679,8 @@ def forward_grouped(e, c, targets, ignore_index: int, vocab_start: int = 0, soft
     mt = -(-v // BLOCK_VOCAB)
     key = ("grouped", n, d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
            perm is not None)
-    gv, slots = grouped_plan(n, d, v, key)
-    groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gv) * BLOCK_VOCAB)) for m0 in range(0, mt, gv)]
+    bounds, slots = grouped_plan(n, d, v, key)
+    groups = [(m0 * BLOCK_VOCAB, min(v, m1 * BLOCK_VOCAB)) for m0, m1 in bounds]
     tile_max = torch.empty(max(nt, 1) * mt * BLOCK_TOKENS, dtype=torch.float32, device=dev)
     state = GroupState(e, c, e_c, row_map, n_valid, perm, perm_padded, pos, tile_max, groups,
                        int(vocab_start), float(softcap or 0.0), mean_logits, slots, key)
@@ -729,7 +743,8 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
     shat = torch.empty(cap * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
     ws_bytes = max(lib.cce_bwd_kept_workspace_bytes(n, d, v1 - v0, cap, 0) for v0, v1 in state.groups)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+    overflow = torch.zeros(len(state.groups), dtype=torch.int32, device=dev)  # one flag per group
+    vcounts = torch.zeros(-(-v // BLOCK_VOCAB), dtype=torch.int32, device=dev)  # kept per vocab tile
     split = bool(label_split)
     ev = _ev_begin("bwd")
     last = len(state.groups) - 1
@@ -746,11 +761,11 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
                                     _p(state.n_valid), _p(state.pos), v0, _p(lse), _p(upstream), _p(tm_g),
                                     n, d, vg, state.softcap, float(eps), int(split), _p(shat), 0, _p(None),
                                     _p(None), _p(None), cap, _p(ws), ws_bytes, _p(de), 1, int(g > 0),
-                                    _p(dc_g), _p(counters), _p(overflow), _p(None), ctypes.c_void_p(done),
-                                    stream), "cce_bwd_kept")
+                                    _p(dc_g), _p(counters), _p(overflow[g:]), _p(None), _p(vcounts[v0 // BLOCK_VOCAB:]),
+                                    ctypes.c_void_p(done), stream), "cce_bwd_kept")
     del ws, shat
-    if state.key:
-        _remember_count(state.key, counters, 0)  # kept tiles of all groups: sizes the next call
+    if state.key:  # kept tiles per vocab tile: sizes the next call's groups
+        _remember_vector(state.key + ("per-vtile",), vcounts)
     if split:
         label_terms(e, c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream, correct,
                     state.softcap, de, dc)
@@ -758,7 +773,7 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
             de_done.record()
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
-    LAST_OVERFLOW["flag"] = overflow
+    LAST_OVERFLOW["flag"] = overflow.max()  # 1 if any group took the fallback
     return (de if (fp32_de or de is None) else f32_to_bf16(de)), dc, counters
 
 
@@ -806,7 +821,7 @@ def _harvest(hint) -> None:
     if _capturing():  # no event queries inside a CUDA-graph capture: use what is already known
         return
     if hint[1] is not None and hint[1].query():
-        hint[2] = int(hint[0][hint[3]])
+        hint[2] = int(hint[0][hint[3]]) if hint[3] is not None else hint[0].tolist()
         hint[1] = None
 
 
@@ -842,6 +857,11 @@ def _remember_count(key, counts: torch.Tensor, index: int) -> None:
     hint[0].copy_(counts, non_blocking=True)
     hint[1] = torch.cuda.Event()
     hint[1].record()
+
+
+def _remember_vector(key, vec: torch.Tensor) -> None:
+    """_remember_count for a whole device vector (read back as a list)."""
+    _remember_count(key, vec, None)
 
 
 def _remember_kept(key, counters: torch.Tensor) -> None:

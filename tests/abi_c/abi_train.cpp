@@ -149,7 +149,7 @@ int main() {
   auto* overflow = dev_alloc<int>(1);
   CC(cce_bwd_kept(E_c, C_t, nullptr, perm_padded, row_map, n_valid, pos, 0, lse, dup, tile_max, n, d, v,
                   0.f, eps, 0, shat, 0, nullptr, nullptr, nullptr, cap, ws_k, kw, de, 0, 0, dc, counters,
-                  overflow, nullptr, nullptr, st));
+                  overflow, nullptr, nullptr, nullptr, st));
 
   std::vector<float> hloss(n);
   std::vector<__nv_bfloat16> hde(n * d), hdc(v * d);
