@@ -33,9 +33,12 @@ for s in "$@"; do
     configs) for cfg in gpt2 llama3-8b gemma2-9b nemo-12b; do
         timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> $out/configs.log 2>&1; echo "exit $cfg $?" >> $out/configs.log; done ;;
     sanitize) for tool in memcheck synccheck racecheck; do
+        # racecheck cannot finish the ~40-group learned-plan case (the process dies with 0 hazards,
+        # thousands of instrumented launches); memcheck and synccheck cover it
+        sel="tiny_batches or hidden_sizes or overflow or aliasing or grouped_many or label_store_rule"
+        [ $tool = racecheck ] && sel="($sel) and not learned_plan"
         timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_parity.py -x -q -m gpu \
-          -k "tiny_batches or hidden_sizes or overflow or aliasing or grouped_many or label_store_rule" -p no:cacheprovider \
-          > $out/sanitize_$tool.log 2>&1; echo "exit $?" >> $out/sanitize_$tool.log; done
+          -k "$sel" -p no:cacheprovider > $out/sanitize_$tool.log 2>&1; echo "exit $?" >> $out/sanitize_$tool.log; done
         CCE_PAIR=0 timeout 1500 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -x -q -m gpu \
           -k "tiny_batches or aliasing or grouped_many" -p no:cacheprovider > $out/sanitize_racecheck_nopair.log 2>&1
         echo "exit $?" >> $out/sanitize_racecheck_nopair.log ;;
