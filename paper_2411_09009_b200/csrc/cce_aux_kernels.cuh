@@ -87,7 +87,10 @@ __global__ void ebar_reduce_kernel(const float* __restrict__ part, int nblk, int
 
 // key[v] = C[v] . ebar_sum / n_valid (fp32): the reference's mean_logits (kernels.py:305-308,
 // :317-318), a mean of logits over the valid tokens.  HBM-bound GEMV: ebar in smem, one warp per
-// row, 4 independent 16-byte loads in flight per lane.
+// row, 8 independent 16-byte loads in flight per lane.
+#ifndef CCE_SORTKEY_UNROLL
+#define CCE_SORTKEY_UNROLL 8  // independent 16-byte loads per lane per batch (profiles/r1/ab/sort_key_unroll.txt)
+#endif
 __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float* __restrict__ ebar_sum,
                                 const int* __restrict__ n_valid, int v, int d, float* __restrict__ key) {
   griddep_wait();
@@ -100,14 +103,17 @@ __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float
   const int n16 = d / 8;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < v; row += gridDim.x * warps) {
     const uint4* c = reinterpret_cast<const uint4*>(C + (size_t)row * d);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int U = CCE_SORTKEY_UNROLL;
+    float acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = 0.f;
     int j = lane;
-    for (; j + 96 < n16; j += 128) {
-      uint4 raw[4];
+    for (; j + 32 * (U - 1) < n16; j += 32 * U) {
+      uint4 raw[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) raw[u] = __ldg(c + j + 32 * u);
+      for (int u = 0; u < U; ++u) raw[u] = __ldg(c + j + 32 * u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[u]);
         const float* eb = s_ebar + (j + 32 * u) * 8;
 #pragma unroll
@@ -120,6 +126,8 @@ __global__ void sort_key_kernel(const __nv_bfloat16* __restrict__ C, const float
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[0] += __bfloat162float(h[q]) * s_ebar[j * 8 + q];
     }
+#pragma unroll
+    for (int u = 4; u < U; ++u) acc[u & 3] += acc[u];
     float a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);

@@ -216,6 +216,9 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 }
 
 // kernel<<<grid, block, smem, stream>>>(args) with the launch attributes of launch_k
+#ifndef CCE_SORTKEY_BPS
+#define CCE_SORTKEY_BPS 8  // sort-key GEMV blocks per SM (profiles/r1/ab/sort_key_unroll.txt)
+#endif
 #define PDL_LAUNCH(kernel, grid, block, smem, stream, ...)                                      \
   do {                                                                                         \
     if (int e_ = launch_k(kernel, grid, block, (size_t)(smem), stream, 1, __VA_ARGS__)) return e_; \
@@ -592,7 +595,7 @@ int cce_vocab_order(const void* C, const float* ebar_sum, const int* n_valid, in
   size_t tmp_bytes = need - 3 * (size_t)v * 4 - 1024;
   CCE_CUDA(cudaFuncSetAttribute(cce::sort_key_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(d * sizeof(float))));
-  PDL_LAUNCH(cce::sort_key_kernel, dim3((unsigned)std::min<int64_t>((v + 7) / 8, 4 * num_sms())), dim3(256), d * sizeof(float), stream, static_cast<const __nv_bfloat16*>(C), ebar_sum, n_valid, (int)v, (int)d, key);
+  PDL_LAUNCH(cce::sort_key_kernel, dim3((unsigned)std::min<int64_t>((v + 7) / 8, CCE_SORTKEY_BPS * num_sms())), dim3(256), d * sizeof(float), stream, static_cast<const __nv_bfloat16*>(C), ebar_sum, n_valid, (int)v, (int)d, key);
   CCE_CUDA(cudaGetLastError());
   PDL_LAUNCH(cce::iota_kernel, dim3((unsigned)((v + 255) / 256)), dim3(256), 0, stream, idx, (int)v);
   CCE_CUDA(cudaGetLastError());
