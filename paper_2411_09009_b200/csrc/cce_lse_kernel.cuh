@@ -359,6 +359,9 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
 #ifndef CCE_FWD_LDW
 #define CCE_FWD_LDW 32
 #endif
+#ifndef CCE_FWD_FAST
+#define CCE_FWD_FAST 1  // unmasked path for interior chunks (0: A/B against the masked loop)
+#endif
         constexpr int LW = CCE_FWD_LDW;  // TMEM columns per load-wait step (32 or 64)
 #pragma unroll 1
         for (int c = 0; c < BN / LW; ++c) {
@@ -369,19 +372,36 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
           tmem_ld_wait();
           float y[LW];
           float cm = -INFINITY;
+          const int cbase = col0 + c * LW;
+          // common chunk (inside V, no softcap, not this row's label): no per-column masks, and
+          // max(z * log2e) = round(max(z) * log2e) exactly (rounding is monotone) -- bit-identical
+          if (CCE_FWD_FAST && !use_softcap && cbase + LW <= p.v &&
+              !(tile_has_t && tpos >= cbase && tpos < cbase + LW)) {
+            float czm = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < LW; ++j) {
-            float z = __uint_as_float(r[j]);
-            const int col = col0 + c * LW + j;
-            const bool in_v = col < p.v;
-            if (in_v) zmax = fmaxf(zmax, z);
-            if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
-            if (tile_has_t && col == tpos) {
-              corr = z;
-              have_corr = true;
+            for (int j = 0; j < LW; ++j) {
+              y[j] = __uint_as_float(r[j]);
+              czm = fmaxf(czm, y[j]);
             }
-            y[j] = in_v ? z * LOG2E : -INFINITY;
-            cm = fmaxf(cm, y[j]);
+            zmax = fmaxf(zmax, czm);
+            cm = czm * LOG2E;
+#pragma unroll
+            for (int j = 0; j < LW; ++j) y[j] *= LOG2E;
+          } else {
+#pragma unroll
+            for (int j = 0; j < LW; ++j) {
+              float z = __uint_as_float(r[j]);
+              const int col = col0 + c * LW + j;
+              const bool in_v = col < p.v;
+              if (in_v) zmax = fmaxf(zmax, z);
+              if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
+              if (tile_has_t && col == tpos) {
+                corr = z;
+                have_corr = true;
+              }
+              y[j] = in_v ? z * LOG2E : -INFINITY;
+              cm = fmaxf(cm, y[j]);
+            }
           }
           const float nm = fmaxf(run_m, cm);
           if (nm != -INFINITY) {
