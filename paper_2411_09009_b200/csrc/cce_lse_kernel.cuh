@@ -438,17 +438,26 @@ tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
               tmem_ld32(tacc + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
               tmem_ld_wait();
               uint32_t pk[32];
+              if (CCE_FWD_FAST && !use_softcap && col0 + c * 64 + 64 <= p.v) {
 #pragma unroll
-              for (int j = 0; j < 64; j += 2) {
-                float dd[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  float z = __uint_as_float(r[j + h]);
-                  if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
-                  dd[h] = (col0 + c * 64 + j + h < p.v) ? z - zcmax : -INFINITY;
+                for (int j = 0; j < 64; j += 2) {
+                  const __half2 h2 = __floats2half2_rn(__uint_as_float(r[j]) - zcmax,
+                                                       __uint_as_float(r[j + 1]) - zcmax);
+                  pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
-                const __half2 h2 = __floats2half2_rn(dd[0], dd[1]);
-                pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 64; j += 2) {
+                  float dd[2];
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    float z = __uint_as_float(r[j + h]);
+                    if (use_softcap) z = p.softcap * softcap_tanh(z, inv_cap);
+                    dd[h] = (col0 + c * 64 + j + h < p.v) ? z - zcmax : -INFINITY;
+                  }
+                  const __half2 h2 = __floats2half2_rn(dd[0], dd[1]);
+                  pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
               }
 #pragma unroll
               for (int q = 0; q < 8; ++q)
