@@ -232,6 +232,25 @@ def reference_arm(args):
 # ------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    print(f"bench: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return rc
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -258,6 +277,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one per GPU,
+        # rendezvous on 127.0.0.1), exactly as the driver's torchrun command does
+        return relaunch_under_torchrun(args.gpus)
 
     import torch
     import torch.distributed as dist
@@ -275,6 +298,8 @@ def main():
     dev = torch.device("cuda", 0 if same_dev else local)
     torch.cuda.set_device(dev)
     group = None
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     # --force-dist: the distributed (vocab-parallel) path even for one rank -- exercises the NCCL
     # collectives on a single GPU (functional check)
     if world > 1 or args.force_dist:
@@ -283,6 +308,13 @@ def main():
         else:
             dist.init_process_group(backend)
         group = dist.group.WORLD
+        # communicator check: every rank joined, one device per rank (NCCL) -- logged for the run
+        probe = torch.ones(1, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(probe, group=group)
+        print(f"bench: rank {rank}/{world} backend={dist.get_backend(group)} device={dev} "
+              f"comm_nranks={int(probe.item())}", file=sys.stderr, flush=True)
+        if int(probe.item()) != world:
+            raise SystemExit(f"bench: communicator has {int(probe.item())} ranks, expected {world}")
 
     n, d, v, cap, pad_frac, sigma = CONFIGS[args.config]
     if args.sigma is not None:

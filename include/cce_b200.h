@@ -47,6 +47,13 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
 int cce_merge_shards(int num_shards, const float* lse_parts, const float* correct_parts,
                      const int64_t* targets, int64_t ignore_index, int64_t n, float* lse_out,
                      float* loss_out, void* stream);
+/* The same, plus the reference's label-range check (check_vocab, core.py:110-114) without a
+ * host read: with v_total > 0 a row whose target is neither ignore_index nor in [0, v_total) gets
+ * a NaN loss and *label_error is set to 1 (sticky; the caller reads it asynchronously and raises
+ * the reference's ValueError at its next call).  label_error may be NULL. */
+int cce_merge_shards_checked(int num_shards, const float* lse_parts, const float* correct_parts,
+                             const int64_t* targets, int64_t ignore_index, int64_t n, int64_t v_total,
+                             int* label_error, float* lse_out, float* loss_out, void* stream);
 
 /* ---- vocabulary order (compute_vocab_order, kernels.py:145-160) ----
  * cce_ebar: column sums of the rows of E whose target != ignore_index (targets may be NULL =

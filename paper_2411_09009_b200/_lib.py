@@ -32,6 +32,8 @@ SIGNATURES = {
                         c_void_p, c_size, c_void_p, c_void_p, c_void_p]),
     "cce_merge_shards": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_void_p,
                                  c_void_p, c_void_p]),
+    "cce_merge_shards_checked": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_ebar_workspace_bytes": (c_size, [c_i64, c_i64]),
     "cce_ebar": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p, c_size, c_void_p]),
     "cce_sort_workspace_bytes": (c_size, [c_i64]),

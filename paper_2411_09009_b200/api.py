@@ -323,9 +323,11 @@ def lse_forward(e, c, blocks: BlockSpec | None = None, options: CceOptions | Non
 def lse_backward(e, c, x, lse, upstream, blocks: BlockSpec | None = None,
                  options: CceOptions | None = None, order: VocabOrder | None = None,
                  stats: BackwardStats | None = None) -> Gradients:
-    """Filtered backward (kernels.py:327-486).  Compacts ignored rows first, as cce_loss does
-    (so filter decisions are taken on valid-row token tiles).  `order` (if given) is the vocab
-    order; otherwise the natural order is used, like the reference."""
+    """Filtered backward (kernels.py:327-486).  Like the reference, every row stays in place
+    (ignored rows carry zero upstream; their token blocks count as zero-upstream skips when the
+    whole block is ignored), so `stats` follows the reference's tile grid.  `order` (if given) is
+    the vocab order; otherwise the natural order is used, like the reference.  The GPU tile is
+    128 x 256 (BlockSpec.m_b other than 256 is rejected by BlockSpec itself)."""
     blocks = blocks or BlockSpec()
     options = options or CceOptions()
     E, C, X = _pair(e, c, x)
@@ -345,9 +347,10 @@ def lse_backward(e, c, x, lse, upstream, blocks: BlockSpec | None = None,
             raise ValueError(f"vocab order has {perm.shape[0]} entries, expected {C.shape[0]}")
     de, dc, counters, _ = ops.backward(E, C, X, lse_t, up, ignore_index=IGNORE_INDEX,
                                        eps=options.epsilon if options.filtering else None,
-                                       vocab_sorting=perm is not None, perm=perm, fp32_de=True)
+                                       vocab_sorting=perm is not None, perm=perm, fp32_de=True,
+                                       compact=False)
     if stats is not None:
-        s = ops.stats_from_counters(counters, int((X != IGNORE_INDEX).sum()), C.shape[0])
+        s = ops.stats_from_counters(counters, n, C.shape[0])
         stats.total_tiles, stats.skipped_epsilon, stats.skipped_zero_upstream = (
             s.total_tiles, s.skipped_epsilon, s.skipped_zero_upstream)
     d = _hidden(e)

@@ -30,10 +30,14 @@ __global__ void combine_splits_kernel(const float2* __restrict__ part, int split
 
 // Vocab-parallel / single-shard finish: lse = logaddexp over shards, correct = sum over shards.
 // Mirrors cce_loss's scatter (kernels.py:539-547): loss and lse are 0 at ignored rows.
+// Label range (check_vocab, core.py:110-114) without a host read: with v_total > 0, a row whose
+// label is neither ignore_index nor in [0, v_total) gets a NaN loss and sets *bad = 1 (sticky,
+// read by the host later, asynchronously).
 __global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
                                     const float* __restrict__ correct_parts,
                                     const int64_t* __restrict__ targets, int64_t ignore_index,
-                                    int n, float* __restrict__ lse_out, float* __restrict__ loss_out) {
+                                    int n, float* __restrict__ lse_out, float* __restrict__ loss_out,
+                                    int64_t v_total, int* __restrict__ bad) {
   griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -46,9 +50,12 @@ __global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
     corr += correct_parts[(size_t)q * n + i];
   }
   const float lse = (m == -INFINITY) ? -INFINITY : m + logf(acc);
-  const bool valid = targets[i] != ignore_index;
+  const int64_t tg = targets[i];
+  const bool valid = tg != ignore_index;
+  const bool out_of_range = valid && v_total > 0 && (tg < 0 || tg >= v_total);
+  if (out_of_range && bad != nullptr) *bad = 1;
   lse_out[i] = valid ? lse : 0.f;
-  loss_out[i] = valid ? lse - corr : 0.f;
+  loss_out[i] = out_of_range ? __int_as_float(0x7fc00000) : (valid ? lse - corr : 0.f);
 }
 
 // zero a float buffer (used for `correct` so rows whose label lives in another shard read 0)

@@ -531,14 +531,22 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   return 0;
 }
 
+int cce_merge_shards_checked(int num_shards, const float* lse_parts, const float* correct_parts,
+                             const int64_t* targets, int64_t ignore_index, int64_t n, int64_t v_total,
+                             int* label_error, float* lse_out, float* loss_out, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (n == 0) return 0;
+  PDL_LAUNCH(cce::merge_shards_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, num_shards,
+             lse_parts, correct_parts, targets, ignore_index, (int)n, lse_out, loss_out, v_total, label_error);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int cce_merge_shards(int num_shards, const float* lse_parts, const float* correct_parts,
                      const int64_t* targets, int64_t ignore_index, int64_t n, float* lse_out,
                      float* loss_out, void* stream_ptr) {
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  if (n == 0) return 0;
-  PDL_LAUNCH(cce::merge_shards_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, num_shards, lse_parts, correct_parts, targets, ignore_index, (int)n, lse_out, loss_out);
-  CCE_CUDA(cudaGetLastError());
-  return 0;
+  return cce_merge_shards_checked(num_shards, lse_parts, correct_parts, targets, ignore_index, n, 0, nullptr,
+                                  lse_out, loss_out, stream_ptr);
 }
 
 size_t cce_sort_workspace_bytes(int64_t v) {

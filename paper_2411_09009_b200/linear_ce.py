@@ -42,16 +42,35 @@ def _resolve_eps(filter_eps):
     return eps
 
 
+_GLOBAL_V: dict = {}
+
+
+def _global_vocab(v_local: int, group) -> int:
+    """Vocabulary size over all shards of `group` (one scalar all-reduce per group and shard size,
+    then cached)."""
+    import torch.distributed as dist
+
+    key = (id(group), v_local)
+    if key not in _GLOBAL_V:
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        x = torch.tensor([v_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(x, group=group)
+        _GLOBAL_V[key] = int(x.item())
+    return _GLOBAL_V[key]
+
+
 class _LinearCrossEntropy(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
-                vocab_start, low_memory, exempt_label_tiles):
+                vocab_start, low_memory, exempt_label_tiles, training, v_total):
         # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
         # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
         # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
         # backward, which then runs over vocabulary groups (ops.backward_lowmem).
+        # `training` is decided by the caller (grad mode on and an input requires grad): inside
+        # forward grad mode is always off, and needs_input_grad follows requires_grad even under
+        # torch.no_grad(), so an eval call would otherwise pay for the training forward.
         ctx.state = None
-        training = ctx.needs_input_grad[0] or ctx.needs_input_grad[1]
         if eps > 0 and not low_memory and training:
             lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
                                                               softcap, vocab_sorting, eps=eps,
@@ -64,17 +83,20 @@ class _LinearCrossEntropy(torch.autograd.Function):
         else:
             lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
         if group is None:
-            lse, loss = ops.merge_shards(lse_local[None], correct[None], targets, ignore_index)
+            lse, loss = ops.merge_shards(lse_local[None], correct[None], targets, ignore_index, v_total)
         else:
             from .vocab_parallel import gather_and_merge
 
-            lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group)
+            lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group, v_total)
         ctx.save_for_backward(e, c, targets, lse)
         ctx.cfg = (ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start)
         # paper ordering: the label term is applied apart from the filtered tiles and needs the
-        # forward's (softcapped) target logit of the rows whose label this shard owns
+        # forward's (softcapped) target logit of the rows whose label this shard owns (O(N): kept
+        # for a second backward under retain_graph)
         ctx.split = not exempt_label_tiles and eps > 0
         ctx.correct = correct if ctx.split else None
+        ctx.backwards = 0
+        ctx.had_state = ctx.state is not None
         if reduction == "none":
             return loss
         return ops.reduce_loss(loss, targets, ignore_index, reduction)  # mean: 0 if nothing valid
@@ -84,12 +106,17 @@ class _LinearCrossEntropy(torch.autograd.Function):
         e, c, targets, lse = ctx.saved_tensors
         ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start = ctx.cfg
         up = ops.upstream(grad_out, targets, ignore_index, reduction)  # default_upstream, core.py:181-200
+        ctx.backwards += 1
         state, ctx.state = ctx.state, None
-        split, correct, ctx.correct = ctx.split, ctx.correct, None
+        if ctx.had_state and ctx.backwards > 1:
+            raise RuntimeError("linear_cross_entropy: this forward's tile state was spent by the first backward "
+                               "(a second backward under retain_graph=True needs low_memory=True or "
+                               "filter_eps=None)")
+        split, correct = ctx.split, ctx.correct
         # a pass whose input needs no gradient is skipped (e.g. a frozen classifier: no dC pass)
         want = dict(want_de=ctx.needs_input_grad[0], want_dc=ctx.needs_input_grad[1])
         if isinstance(state, ops.GroupState):
-            done = torch.cuda.Event() if group is not None else None
+            done = ops.recorded_event() if group is not None else None
             de, dc, _ = ops.backward_grouped(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
                                              fp32_de=group is not None, de_done=done, label_split=split,
                                              correct=correct, **want)
@@ -106,7 +133,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 from .vocab_parallel import all_reduce_de_overlapped
 
                 # dE is complete before the dC pass: its all-reduce runs on a side stream meanwhile
-                done = torch.cuda.Event()
+                done = ops.recorded_event()
                 de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
                                                fp32_de=True, de_done=done, label_split=split, correct=correct,
                                                **want)
@@ -122,7 +149,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 from .vocab_parallel import all_reduce_de
 
                 de = all_reduce_de(de, group)
-        return de, dc, None, None, None, None, None, None, None, None, None, None
+        return de, dc, None, None, None, None, None, None, None, None, None, None, None, None
 
 
 def linear_cross_entropy(
@@ -166,10 +193,13 @@ def linear_cross_entropy(
     e2, c = ops.adapt_operands(e2, c)  # bf16, contiguous, hidden size padded to a multiple of 8
     ops.check_operands(e2, c, t2.to(torch.int64) if t2.dtype != torch.int64 else t2)
     t2 = t2.to(torch.int64).contiguous()
+    v_total = c.shape[0] if process_group is None else _global_vocab(c.shape[0], process_group)
+    # the reference's check_vocab (core.py:110-114): on the device, without a host read -- a label
+    # outside [0, V) gives a NaN loss at its row and a sticky device flag, reported here by the
+    # next call (ValueError) once its asynchronous copy has landed
+    ops.raise_label_error(e2.device, v_total)
     if process_group is None and (os.environ.get("CCE_CHECK_LABELS") == "1" or torch.is_anomaly_enabled()):
-        # the reference's check_vocab (core.py:110-114) needs a host read, so it runs only in debug
-        # mode; otherwise a label outside [0, V) counts as a row whose target logit is absent
-        # (loss = LSE), exactly as a label owned by another vocabulary shard
+        # debug mode: the same check on the host, raised by this call
         bad = (t2 != ignore_index) & ((t2 < 0) | (t2 >= c.shape[0]))
         if bool(bad.any()):
             raise ValueError(f"label out of range for vocab size {c.shape[0]}")
@@ -180,9 +210,10 @@ def linear_cross_entropy(
     if cap < 0:
         raise ValueError("softcap must be positive")
     eps = _resolve_eps(filter_eps)
+    training = torch.is_grad_enabled() and (e2.requires_grad or c.requires_grad)
     out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
                                     bool(vocab_sorting), process_group, int(vocab_start),
-                                    bool(low_memory), bool(exempt_label_tiles))
+                                    bool(low_memory), bool(exempt_label_tiles), training, int(v_total))
     if reduction == "none":
         return out.reshape(lead)
     return out

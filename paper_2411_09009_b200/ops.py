@@ -45,6 +45,23 @@ def _ev_end(name: str, a) -> None:
     KERNEL_EVENTS.setdefault(name, []).append((a, b))
 
 
+def recorded_event() -> torch.cuda.Event:
+    """A CUDA event that already exists (recorded once on the current stream), so its handle can
+    go to the C ABI: a torch Event is created lazily and its handle is 0 until first recorded, and
+    the library re-records it (cudaEventRecord) only when the handle is nonzero."""
+    ev = torch.cuda.Event()
+    ev.record()
+    return ev
+
+
+def _event_handle(ev) -> ctypes.c_void_p:
+    if ev is None:
+        return ctypes.c_void_p(0)
+    if ev.cuda_event == 0:
+        ev.record()
+    return ctypes.c_void_p(ev.cuda_event)
+
+
 def _p(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -120,17 +137,72 @@ def forward_local(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     return lse_local, correct
 
 
-def merge_shards(lse_parts, correct_parts, targets, ignore_index: int):
-    """log_add_exp merge over shards (kernels.py:121-137) + the cce_loss scatter (:539-547)."""
+def merge_shards(lse_parts, correct_parts, targets, ignore_index: int, v_total: int = 0):
+    """log_add_exp merge over shards (kernels.py:121-137) + the cce_loss scatter (:539-547).
+
+    v_total > 0 adds the reference's label-range check (check_vocab, core.py:110-114) on the
+    device: a label outside [0, v_total) that is not ignore_index gives a NaN loss and raises
+    the sticky device flag that `raise_label_error` reports (no host synchronisation here)."""
     lib = _lib.load()
     p, n = lse_parts.shape
-    lse = torch.empty(n, dtype=torch.float32, device=lse_parts.device)
-    loss = torch.empty(n, dtype=torch.float32, device=lse_parts.device)
+    dev = lse_parts.device
+    lse = torch.empty(n, dtype=torch.float32, device=dev)
+    loss = torch.empty(n, dtype=torch.float32, device=dev)
     if n:
-        _lib.check(lib.cce_merge_shards(p, _p(lse_parts.contiguous()), _p(correct_parts.contiguous()),
-                                        _p(targets), int(ignore_index), n, _p(lse), _p(loss),
-                                        _stream(lse_parts.device)), "cce_merge_shards")
+        flag = _label_state(dev)[0] if v_total > 0 else None
+        _lib.check(lib.cce_merge_shards_checked(p, _p(lse_parts.contiguous()), _p(correct_parts.contiguous()),
+                                                _p(targets), int(ignore_index), n, int(v_total), _p(flag),
+                                                _p(lse), _p(loss), _stream(dev)), "cce_merge_shards_checked")
+        if flag is not None:
+            _queue_label_flag(dev)
     return lse, loss
+
+
+# Label-range errors found on the device: per device [flag (device int32, sticky), pinned copy,
+# event of the copy in flight].  The flag is copied back asynchronously after each checked merge
+# and read (never waited for) by the next call, which raises the reference's ValueError.
+_LABEL_STATE: dict = {}
+
+
+def _label_state(dev: torch.device):
+    key = (dev.type, dev.index if dev.index is not None else torch.cuda.current_device())
+    st = _LABEL_STATE.get(key)
+    if st is None:
+        st = _LABEL_STATE[key] = [torch.zeros(1, dtype=torch.int32, device=dev),
+                                  torch.zeros(1, dtype=torch.int32).pin_memory(), None]
+    return st
+
+
+def _queue_label_flag(dev: torch.device) -> None:
+    if _capturing():
+        return
+    st = _label_state(dev)
+    if st[2] is not None:
+        return  # previous copy still in flight; it is read first
+    st[1].copy_(st[0], non_blocking=True)
+    st[2] = torch.cuda.Event()
+    st[2].record()
+
+
+def raise_label_error(dev: torch.device, v_total: int, wait: bool = False) -> None:
+    """Raise ValueError if an earlier call on `dev` saw a label outside [0, v_total) (the device
+    flag of merge_shards).  Without `wait`, only a copy that has already landed is read (no host
+    synchronisation); the flag is cleared once reported."""
+    if _capturing():
+        return
+    st = _label_state(dev)
+    if wait:
+        if st[2] is None:
+            _queue_label_flag(dev)
+        st[2].synchronize()
+    if st[2] is None or not st[2].query():
+        return
+    st[2] = None
+    if int(st[1][0]) != 0:
+        st[0].zero_()
+        st[1].zero_()
+        raise ValueError(f"label out of range for vocab size {v_total} (found on the device by an earlier "
+                         "call, whose loss is NaN at those rows)")
 
 
 def indexed_dot(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0):
@@ -209,9 +281,12 @@ def compact_rows(targets, ignore_index: int):
     return row_map, n_valid
 
 
+NO_COMPACTION = -(2 ** 62)  # an ignore value no label can take: compact_rows keeps every row
+
+
 def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: int = 0,
              softcap: float = 0.0, eps: float | None = EPSILON_DEFAULT, vocab_sorting: bool = True,
-             perm: torch.Tensor | None = None, fp32_de: bool = False):
+             perm: torch.Tensor | None = None, fp32_de: bool = False, compact: bool = True):
     """Filtered, vocab-sorted CCE backward (lse_backward, kernels.py:327-486).
 
     Ignored rows are compacted on the device first (filter_ignored, kernels.py:494-510), so
@@ -219,6 +294,8 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     `lse` / `upstream` are per original row; `upstream` must be 0 at ignored rows.  Returns
     (dE, dC, counters[3] tensor, perm); with fp32_de, dE stays fp32 (vocab-parallel all-reduces
     it before the cast).  The whole call is asynchronous: no value is read back to the host.
+    compact=False keeps every row in place, as the reference's lse_backward does (ignored rows
+    then only carry zero upstream), so tile counts follow its uncompacted grid.
     """
     lib = _lib.load()
     n, d = e.shape
@@ -227,7 +304,7 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     stream = _stream(dev)
     lse = lse.to(torch.float32).contiguous()
     upstream = upstream.to(torch.float32).contiguous()
-    row_map, n_valid = compact_rows(targets, ignore_index)
+    row_map, n_valid = compact_rows(targets, ignore_index if compact else NO_COMPACTION)
     if vocab_sorting and perm is None:
         perm, _ = vocab_order(e, c, targets, ignore_index, n_valid)
     vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
@@ -255,7 +332,7 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
     # S-hat slots: every token tile in one group with compact slots up to the budget; if more
     # tiles are kept than that, a fallback pass over budget-sized groups (worst case fits) runs,
     # gated on the device overflow flag -- no host read either way.
-    key = ("filter_pass", n, d, v, int(vocab_start), filt_eps, float(softcap or 0.0))
+    key = ("filter_pass", d, v, int(vocab_start), filt_eps, float(softcap or 0.0))
     cap0 = shat_capacity(key, nt, mt)
     plans = [(nt, cap0, None)]
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -276,7 +353,7 @@ def backward(e, c, targets, lse, upstream, *, ignore_index: int, vocab_start: in
         _ev_end("bwd", ev)
         all_counters.append(counters)
     counters = all_counters[0] if len(plans) == 1 else torch.where(overflow.bool(), all_counters[1], all_counters[0])
-    _remember_kept(key, counters)
+    _remember_kept(key, counters, nt)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
     return de, dc, counters, perm
@@ -512,9 +589,11 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     # recompute (profiles/r1/ab/ab_store_labels_by_d.txt).  CCE_STORE_LABELS=0 / 1 forces it.
     env = os.environ.get("CCE_STORE_LABELS")
     store_labels = store_labels and (env == "1" if env in ("0", "1") else d >= LABEL_STORE_MIN_D)
-    rkey = ("recompute", n, d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
+    # capacity hints are keyed by the head, not the batch: a count observed at another N is
+    # rescaled by the token-tile ratio (kept tiles grow linearly with the token tiles)
+    rkey = ("recompute", d, v, int(vocab_start), float(eps), float(softcap or 0.0), bool(label_split),
             bool(store_labels))
-    lkey = ("labels", n, d, v, int(vocab_start))
+    lkey = ("labels", d, v, int(vocab_start))
     state.rcap = shat_capacity(rkey, nt, mt)
     state.lab_cap = label_capacity(lkey, nt, mt) if store_labels else 0
     state.keys = (rkey, lkey)
@@ -581,7 +660,7 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     # if they fit; otherwise the library falls back (device flag, no host read) to token-tile
     # groups sized for the worst case
     if state.shat is None:
-        state.rcap = shat_capacity(("recompute-", n, d, v, state.vocab_start, float(eps), state.softcap), nt, mt)
+        state.rcap = shat_capacity(("recompute-", d, v, state.vocab_start, float(eps), state.softcap), nt, mt)
         state.shat = torch.empty(state.rcap * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
     cap, lab_cap = state.rcap, state.lab_cap
     overflow = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -596,8 +675,7 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
                                 lab_cap, _p(state.lab_slot), _p(state.lab_list), _p(state.lab_count), cap,
                                 _p(ws), ws_bytes, _p(de), int(fp32_de), 0, _p(dc), _p(counters), _p(overflow),
                                 _p(stats), _p(None),
-                                ctypes.c_void_p(de_done.cuda_event if de_done is not None and not label_split
-                                                else 0), stream), "cce_bwd_kept")
+                                _event_handle(None if label_split else de_done), stream), "cce_bwd_kept")
     del ws
     if label_split:
         label_terms(e, state.c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream,
@@ -606,9 +684,9 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
             de_done.record()
     LAST_STATS["stats"] = stats  # [label tiles stored by the forward, tiles recomputed]
     if state.keys:
-        _remember_count(state.keys[0], stats, 1)
+        _remember_count(state.keys[0], stats, 1, nt)
         if lab_cap:
-            _remember_count(state.keys[1], stats, 0)
+            _remember_count(state.keys[1], stats, 0, nt)
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
@@ -756,13 +834,13 @@ def backward_grouped(state: GroupState, targets, lse, upstream, *, ignore_index:
         tm_g = state.tile_max[nt * (v0 // BLOCK_VOCAB) * BLOCK_TOKENS:]
         perm_g = state.perm_padded[v0:] if state.perm_padded is not None else None
         dc_g = None if dc is None else (dc if state.perm_padded is not None else dc[v0:v1])
-        done = de_done.cuda_event if (de_done is not None and g == last and not split) else 0
+        done = _event_handle(de_done if (g == last and not split) else None)
         _lib.check(lib.cce_bwd_kept(_p(state.e_c), _p(c_g), _p(None), _p(perm_g), _p(state.row_map),
                                     _p(state.n_valid), _p(state.pos), v0, _p(lse), _p(upstream), _p(tm_g),
                                     n, d, vg, state.softcap, float(eps), int(split), _p(shat), 0, _p(None),
                                     _p(None), _p(None), cap, _p(ws), ws_bytes, _p(de), 1, int(g > 0),
                                     _p(dc_g), _p(counters), _p(overflow[g:]), _p(None), _p(vcounts[v0 // BLOCK_VOCAB:]),
-                                    ctypes.c_void_p(done), stream), "cce_bwd_kept")
+                                    done, stream), "cce_bwd_kept")
     del ws, shat
     if state.key:  # kept tiles per vocab tile: sizes the next call's groups
         _remember_vector(state.key + ("per-vtile",), vcounts)
@@ -809,7 +887,7 @@ def shat_capacity(key, nt: int, mt: int) -> int:
         if hint is not None:
             _harvest(hint)
             if hint[2] is not None:
-                cap = min(ceiling, max(int(hint[2] * KEPT_MARGIN), mt))  # floor: one token tile's tiles
+                cap = min(ceiling, max(int(_rescaled(hint, nt) * KEPT_MARGIN), mt))  # floor: one token tile's tiles
     return min(max(cap, mt), nt * mt)
 
 
@@ -823,6 +901,8 @@ def _harvest(hint) -> None:
     if hint[1] is not None and hint[1].query():
         hint[2] = int(hint[0][hint[3]]) if hint[3] is not None else hint[0].tolist()
         hint[1] = None
+        if len(hint) > 5:
+            hint[4] = hint[5]
 
 
 LABEL_MARGIN = 1.1
@@ -837,17 +917,26 @@ def label_capacity(key, nt: int, mt: int) -> int:
     if hint is not None:
         _harvest(hint)
         if hint[2] is not None:
-            return min(worst, int(hint[2] * LABEL_MARGIN) + nt)
+            return min(worst, int(_rescaled(hint, nt) * LABEL_MARGIN) + nt)
     return worst
 
 
-def _remember_count(key, counts: torch.Tensor, index: int) -> None:
-    """Queue an asynchronous copy of a device count (read by a later call once it has landed)."""
+def _rescaled(hint, nt: int) -> float:
+    """The hint's count at `nt` token tiles (counts of the tile path grow with the token tiles)."""
+    scale = hint[4] if len(hint) > 4 else None
+    return hint[2] * nt / scale if scale else hint[2]
+
+
+def _remember_count(key, counts: torch.Tensor, index: int, nt: int | None = None) -> None:
+    """Queue an asynchronous copy of a device count (read by a later call once it has landed);
+    `nt` records the token tiles it was observed at, so calls at another N can rescale it."""
     if _capturing():
         return
     hint = _KEPT_HINT.pop(key, None)
     if hint is None:
-        hint = [torch.zeros(counts.shape, dtype=counts.dtype).pin_memory(), None, None, index]
+        # [pinned copy, event of the copy in flight, harvested value, index, token tiles of the
+        #  harvested value, token tiles of the copy in flight]
+        hint = [torch.zeros(counts.shape, dtype=counts.dtype).pin_memory(), None, None, index, nt, nt]
         while len(_KEPT_HINT) >= KEPT_HINT_MAX:  # shapes that vary every step: drop the oldest
             _KEPT_HINT.pop(next(iter(_KEPT_HINT)))
     _KEPT_HINT[key] = hint  # (re)inserted last: the dict's order is least recently used first
@@ -857,6 +946,8 @@ def _remember_count(key, counts: torch.Tensor, index: int) -> None:
     hint[0].copy_(counts, non_blocking=True)
     hint[1] = torch.cuda.Event()
     hint[1].record()
+    if len(hint) > 5:
+        hint[5] = nt
 
 
 def _remember_vector(key, vec: torch.Tensor) -> None:
@@ -864,10 +955,10 @@ def _remember_vector(key, vec: torch.Tensor) -> None:
     _remember_count(key, vec, None)
 
 
-def _remember_kept(key, counters: torch.Tensor) -> None:
+def _remember_kept(key, counters: torch.Tensor, nt: int | None = None) -> None:
     """Queue an asynchronous copy of this call's kept-tile count (read by a later call once it
     has landed; the CPU usually runs ahead of the GPU, so the value may be a few calls old)."""
-    _remember_count(key, counters, 0)
+    _remember_count(key, counters, 0, nt)
 
 
 REDUCTIONS = {"none": 0, "sum": 1, "mean": 2}

@@ -28,14 +28,14 @@ def shard_range(vocab: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < rem else 0)
 
 
-def gather_and_merge(lse_local, correct, targets, ignore_index, group):
+def gather_and_merge(lse_local, correct, targets, ignore_index, group, v_total: int = 0):
     world = dist.get_world_size(group)
     n = lse_local.shape[0]
     mine = torch.stack([lse_local, correct]).contiguous()          # [2, N]
     flat = torch.empty((world * 2, n), dtype=mine.dtype, device=mine.device)
     dist.all_gather_into_tensor(flat, mine, group=group)
     allp = flat.view(world, 2, n)
-    return ops.merge_shards(allp[:, 0].contiguous(), allp[:, 1].contiguous(), targets, ignore_index)
+    return ops.merge_shards(allp[:, 0].contiguous(), allp[:, 1].contiguous(), targets, ignore_index, v_total)
 
 
 def all_reduce_de(de_acc, group):

@@ -37,7 +37,7 @@ def _install_doubles(ops):
         corr = np.where(own, z[np.arange(len(tt)), np.clip(loc, 0, c.shape[0] - 1)], 0.0)
         return torch.from_numpy(lse), torch.from_numpy(corr)
 
-    def merge_shards(lse_parts, correct_parts, t, ignore_index):
+    def merge_shards(lse_parts, correct_parts, t, ignore_index, v_total=0):
         lse = torch.logsumexp(lse_parts, dim=0)
         valid = t != ignore_index
         loss = torch.where(valid, lse - correct_parts.sum(0), torch.zeros_like(lse))
