@@ -159,6 +159,15 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
                   const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
                   size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
                   int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream);
+/* cce_fwd_gather: cce_fwd_tiles without copies -- E is the caller's [n][d] embeddings (rows read
+ * through row_map unless it is the identity) and C the caller's classifier in its own row order,
+ * read through perm_padded (cce_bwd_prep) with cp.async row gathers, so neither the compacted E
+ * nor the sorted classifier exists.  No label-tile store.  Results are bit-identical to
+ * cce_fwd_tiles on the copies. */
+int cce_fwd_gather(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                   const int* n_valid, const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v,
+                   float softcap, void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
+                   void* stream);
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
                                     int64_t lab_capacity);
 int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t* perm_padded, const int32_t* row_map,

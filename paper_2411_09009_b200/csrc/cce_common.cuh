@@ -24,6 +24,8 @@ constexpr int LSE_STAGES = 4;
 constexpr int LSE_STAGES_PAIR = CCE_LSE_STAGES_PAIR;
 constexpr int PAIR_STAGE_BYTES = A_BYTES + (BN / 2) * BK * 2;  // 128 E rows + 128 of 256 C rows
 constexpr int TMEM_COLS = 512;
+constexpr int LSE_CTRL_BYTES = 256;       // barriers / TMEM slot / votes of the logit-tile kernel
+constexpr int LSE_IDX_BYTES = (BM + BN) * 4;  // its row-gather index tables
 constexpr int DCH = 256;                  // D columns per gradient chunk (MMA N of dE / dC)
 constexpr int SHAT_TILE_BYTES = BM * BN * 2;  // one stored S-hat tile, bf16 row-major [128][256]
 
@@ -45,6 +47,7 @@ struct Params {
   int mt;            // vocab tiles
   int splits;        // vocab splits per token tile (units = nt * splits)
   int band;          // token tiles per raster band (bounds the E working set of concurrent CTAs)
+  int grid_cap;      // FWD / BWD: CTAs (pairs) per round of the static schedule, 0 = whole grid
   int num_kb;        // ceil(d / BK)
   float softcap;     // 0 => off
   // forward
@@ -71,7 +74,10 @@ struct Params {
                            //    label term is applied separately, cce_label_terms)
   const int32_t* perm;     // [mt*BN] tile-order position -> C row for gathers (nullptr = plain)
   const int32_t* row_map;  // compact row -> original row (padded); identity when no compaction
-  int e_gather;            // 1: load E rows through row_map with gather4 (else E is compacted)
+  int e_gather;            // 1: load E rows through row_map (cp.async gather unless the map is
+                           //    the identity; else E is compacted)
+  const __nv_bfloat16* e_rows;  // E base (row gathers), [n_total][d]
+  const __nv_bfloat16* c_rows;  // C base (row gathers through perm), [v][d]
   const uint8_t* block_zero;  // [token tiles] 1 if every upstream in the compact tile is zero
   float eps;               // filter threshold (0 = filtering off)
   __nv_bfloat16* shat;     // [capacity][BM][BN] S-hat of kept tiles, compact slots
@@ -200,6 +206,33 @@ __device__ __forceinline__ void load_rows_warp(const CUtensorMap* tm_tile, const
   } else {
     rg.issue(tm_gather, bar, dst, c0);
   }
+}
+
+// Row gather into a 128B-swizzled smem box by one warp with cp.async (16 B per lane): the box is
+// ROWS logical rows x 64 bf16 columns [col0, col0 + 64) of a row-major [*, d] matrix, logical
+// row r reading source row idx[r] (an smem table filled once per tile).  Lanes 8k..8k+7 take the
+// eight 16-B chunks of one row, so each warp instruction reads four whole 128-B row segments;
+// chunk j of row r lands at chunk (j ^ (r & 7)) of the row's 128 B -- the layout a 128B-swizzled
+// TMA box has, which the UMMA descriptors expect.  Columns >= d are zero-filled (d % 8 == 0).
+// Completion: cp.async groups (the caller commits, waits and relays to the stage's mbarrier after
+// a fence.proxy.async, because the tensor core reads smem through the async proxy).
+template <int ROWS>
+__device__ __forceinline__ void gather_box_async(uint8_t* dst, const __nv_bfloat16* src, int d,
+                                                 const int32_t* idx, int col0) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane & 7;
+  const uint32_t d0 = smem_u32(dst);
+  const uint32_t nbytes = (col0 + j * 8 < d) ? 16u : 0u;
+  const char* s0 = reinterpret_cast<const char*>(src) + (size_t)(nbytes ? col0 + j * 8 : 0) * 2;
+#pragma unroll 8
+  for (int r = lane >> 3; r < ROWS; r += 4)
+    cp_async16(d0 + r * 128 + ((j ^ (r & 7)) << 4), s0 + (int64_t)idx[r] * d * 2, nbytes);
+}
+
+// Fill a warp's smem index table: tab[r] = index[row0 + r] for r < rows (index == nullptr:
+// row0 + r).  The caller __syncwarp()s before use.
+__device__ __forceinline__ void load_index_table(int32_t* tab, const int32_t* index, int row0, int rows) {
+  for (int r = threadIdx.x & 31; r < rows; r += 32) tab[r] = index ? index[row0 + r] : row0 + r;
 }
 
 // softcap: z' = cap * tanh(z / cap), tanh(x) = 1 - 2 / (exp(2x) + 1) (exact limits at +-inf)

@@ -155,8 +155,10 @@ SideStream* side_stream() {
 }
 
 constexpr size_t kCtrlBytes = 256;
-constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes;
-constexpr size_t kLsePairSmem = 1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes;
+static_assert(kCtrlBytes == cce::LSE_CTRL_BYTES, "logit-tile kernel control block");
+constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes + cce::LSE_IDX_BYTES;
+constexpr size_t kLsePairSmem =
+    1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes + cce::LSE_IDX_BYTES;
 template <int CH, int KV>
 constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH, KV>::SMEM + kCtrlBytes; }
 constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
@@ -314,13 +316,52 @@ bool use_pairs() {
   return v != 0 && num_sms() >= 2;
 }
 
-// Vocabulary splits of the logit-tile kernel for `nt` token tiles (pairs: nt/2 token-tile pairs
-// on grid/2 CTA pairs).
+// Raster of the full-sweep logit-tile kernel (FWD / BWD): units (token tile or pair, vocab split)
+// in bands of `band` token tiles, split-major inside a band.
+//   * E fits the L2 budget (<= 40 MB of E tiles: Gemma-2-2B, GPT-2): one band, splits chosen so
+//     the units balance over the whole grid.
+//   * Larger heads: the grid shrinks to exactly band x splits CTAs (pairs), so every round of the
+//     static schedule is one whole band -- the CTAs running together then read `band` E tiles and
+//     `splits` C tiles, all L2-resident.  With a full grid, rounds drift across band boundaries
+//     and the working set doubles: at Mistral-NeMo the forward read 281 GB from DRAM (210x C) at
+//     1.0 GHz under the power cap (profiles/r2/ncu_fwd_large_heads.md).
+struct Raster {
+  int band;    // token tiles per band
+  int splits;  // vocab splits
+  int cap;     // CTAs (pairs) per round; 0 = the whole grid
+};
+
+Raster lse_raster(int nt, int mt, int64_t d, bool pair, bool prefer_fine) {
+  const int cg = pair ? 2 : 1;
+  const int grid = num_sms() / cg;
+  const int units_n = (nt + cg - 1) / cg;
+  const int64_t e_unit = (int64_t)cce::BM * d * 2 * cg;  // E bytes of one unit's token rows
+  const int bmax = (int)std::max<int64_t>(1, (40ll << 20) / e_unit);
+  if (units_n <= bmax || units_n < grid) {
+    const int band = std::min(units_n, bmax);
+    return Raster{band * cg, clamp_splits(choose_splits(units_n, mt, grid, prefer_fine), units_n, mt, band, grid), 0};
+  }
+  int bb = 1, bs = std::min(mt, grid);
+  for (int b = 1; b <= bmax; ++b) {
+    const int sp = std::min(mt, grid / b);
+    if (sp < 1) break;
+    if (b * sp > bb * bs || (b * sp == bb * bs && b > bb)) {
+      bb = b;
+      bs = sp;
+    }
+  }
+  return Raster{bb * cg, bs, bb * bs};
+}
+
 int lse_splits(int nt, int mt, int64_t d, bool pair, bool prefer_fine) {
-  const int grid = pair ? num_sms() / 2 : num_sms();
-  const int units_n = pair ? (nt + 1) / 2 : nt;
-  const int band = pair ? (choose_band(d) + 1) / 2 : choose_band(d);
-  return clamp_splits(choose_splits(units_n, mt, grid, prefer_fine), units_n, mt, band, grid);
+  return lse_raster(nt, mt, d, pair, prefer_fine).splits;
+}
+
+void set_raster(cce::Params& p, int nt, int mt, int64_t d, bool pair, bool prefer_fine) {
+  const Raster r = lse_raster(nt, mt, d, pair, prefer_fine);
+  p.band = r.band;
+  p.splits = r.splits;
+  p.grid_cap = r.cap;
 }
 
 // Launch cce_lse_kernel<MODE> on single CTAs or on CTA pairs (cluster of 2).
@@ -328,15 +369,16 @@ template <int MODE>
 int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CUtensorMap& tmEg,
                const CUtensorMap& tmC256, const CUtensorMap& tmCg, const CUtensorMap& tmC128,
                cudaStream_t stream) {
+  const int cap = (MODE != cce::KEPT && p.grid_cap > 0) ? p.grid_cap : (1 << 30);
   if (!pair) {
     if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 1>, kLseSmem)) return e;
     const int units = p.nt * p.splits;
-    return launch_k(cce::cce_lse_kernel<MODE, 1>, dim3(std::max(1, std::min(num_sms(), units))),
+    return launch_k(cce::cce_lse_kernel<MODE, 1>, dim3(std::max(1, std::min({num_sms(), units, cap}))),
                     dim3(cce::NUM_THREADS), kLseSmem, stream, 1, tmE, tmEg, tmC256, tmCg, p);
   }
   if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 2>, kLsePairSmem)) return e;
   const int pair_units = ((p.nt + 1) / 2) * p.splits;
-  const int grid = 2 * std::max(1, std::min(num_sms() / 2, pair_units));
+  const int grid = 2 * std::max(1, std::min({num_sms() / 2, pair_units, cap}));
   return launch_k(cce::cce_lse_kernel<MODE, 2>, dim3(grid), dim3(cce::NUM_THREADS), kLsePairSmem, stream, 2,
                   tmE, tmEg, tmC128, tmCg, p);
 }
@@ -498,7 +540,6 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const int grid = num_sms();
   const bool pair = use_pairs();
-  const int band = choose_band(d);
   const int splits = lse_splits(nt, mt, d, pair, false);
   if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd: workspace too small");
   CUtensorMap tmE, tmC, tmC128;
@@ -513,8 +554,7 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   p.nt = nt;
   p.n_base = 0;
   p.mt = mt;
-  p.splits = splits;
-  p.band = band;
+  set_raster(p, nt, mt, d, pair, false);
   p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
   p.softcap = softcap;
   p.targets = targets;
@@ -704,9 +744,8 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     p.nt = g;
     p.n_base = g0;
     p.mt = mt;
-    const bool pair = use_pairs() && !e_gather && (c_sorted || perm_padded == nullptr);
-    p.band = choose_band(d);
-    p.splits = lse_splits(g, mt, d, pair, true);
+    const bool pair = use_pairs();
+    set_raster(p, g, mt, d, pair, true);
     p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
     p.softcap = softcap;
     p.lse = lse;
@@ -715,6 +754,8 @@ int cce_bwd(const void* E, const void* C, const int32_t* perm_padded, int c_sort
     p.perm = c_sorted ? nullptr : perm_padded;
     p.row_map = row_map;
     p.e_gather = e_gather;
+    p.e_rows = static_cast<const __nv_bfloat16*>(E);
+    p.c_rows = static_cast<const __nv_bfloat16*>(C);
     p.block_zero = w.block_zero;
     p.eps = eps;
     p.shat = w.shat;
@@ -766,25 +807,32 @@ size_t cce_tile_max_bytes(int64_t n, int64_t v) {
   return (size_t)(nt * mt * cce::BM) * sizeof(float);
 }
 
-int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
-                  const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
-                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
-                  int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream_ptr) {
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
-  if (n < 0 || d <= 0 || v <= 0) return fail("cce_fwd_tiles: bad sizes");
-  if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail("cce_fwd_tiles: label tiles need slot maps");
-  if (d % 8 != 0) return fail("cce_fwd_tiles: D must be a multiple of 8 (16-byte TMA row pitch)");
-  if (!row_map || !n_valid || !pos || !tile_max) return fail("cce_fwd_tiles: row_map, n_valid, pos, tile_max required");
+}  // extern "C"
+
+namespace {
+// Forward over the backward's tile order (see cce_fwd_tiles / cce_fwd_gather in the header):
+// E_rows / C_rows are either the compacted / sorted copies (perm_padded == NULL, gather_e = 0) or
+// the caller's E and C read through row_map / perm_padded with cp.async row gathers.
+int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, const int32_t* perm_padded,
+                   int gather_e, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                   int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes,
+                   float* lse_local, float* correct, float* tile_max, void* lab_buf, int64_t lab_capacity,
+                   int32_t* lab_slot, void* lab_list, int* lab_count, cudaStream_t stream) {
+  const std::string w(what);
+  if (n < 0 || d <= 0 || v <= 0) return fail(w + ": bad sizes");
+  if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail(w + ": label tiles need slot maps");
+  if (d % 8 != 0) return fail(w + ": D must be a multiple of 8 (16-byte TMA row pitch)");
+  if (!row_map || !n_valid || !pos || !tile_max) return fail(w + ": row_map, n_valid, pos, tile_max required");
   if (n == 0) return 0;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
   const int mt = (int)((v + cce::BN - 1) / cce::BN);
   const bool pair = use_pairs();
   const int splits = lse_splits(nt, mt, d, pair, false);
-  if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail("cce_fwd_tiles: workspace too small");
+  if (ws_bytes < (size_t)splits * n * sizeof(float2)) return fail(w + ": workspace too small");
   CUtensorMap tmE, tmC, tmC128;
-  if (!make_tmap(&tmE, E_c, n, d, cce::BM) || !make_tmap(&tmC, C_t, v, d, cce::BN) ||
-      !make_tmap(&tmC128, C_t, v, d, cce::BN / 2))
-    return fail("cce_fwd_tiles: cuTensorMapEncodeTiled failed");
+  if (!make_tmap(&tmE, E_rows, n, d, cce::BM) || !make_tmap(&tmC, C_rows, v, d, cce::BN) ||
+      !make_tmap(&tmC128, C_rows, v, d, cce::BN / 2))
+    return fail(w + ": cuTensorMapEncodeTiled failed");
   cce::Params p{};
   p.n_total = (int)n;
   p.n_valid = n_valid;
@@ -793,13 +841,16 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   p.nt = nt;
   p.n_base = 0;
   p.mt = mt;
-  p.splits = splits;
-  p.band = choose_band(d);
+  set_raster(p, nt, mt, d, pair, false);
   p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
   p.softcap = softcap;
   p.pos = pos;
   p.pos_offset = (int)pos_offset;
   p.row_map = row_map;
+  p.perm = perm_padded;
+  p.e_gather = gather_e;
+  p.e_rows = static_cast<const __nv_bfloat16*>(E_rows);
+  p.c_rows = static_cast<const __nv_bfloat16*>(C_rows);
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   p.tile_max = tile_max;
@@ -817,6 +868,27 @@ int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, cons
   PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local);
   CCE_CUDA(cudaGetLastError());
   return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int cce_fwd_tiles(const void* E_c, const void* C_t, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws,
+                  size_t ws_bytes, float* lse_local, float* correct, float* tile_max, void* lab_buf,
+                  int64_t lab_capacity, int32_t* lab_slot, void* lab_list, int* lab_count, void* stream_ptr) {
+  return fwd_tiles_impl("cce_fwd_tiles", E_c, C_t, nullptr, 0, row_map, n_valid, pos, pos_offset, n, d, v, softcap,
+                        ws, ws_bytes, lse_local, correct, tile_max, lab_buf, lab_capacity, lab_slot, lab_list,
+                        lab_count, static_cast<cudaStream_t>(stream_ptr));
+}
+
+int cce_fwd_gather(const void* E, const void* C, const int32_t* perm_padded, const int32_t* row_map,
+                   const int* n_valid, const int32_t* pos, int64_t pos_offset, int64_t n, int64_t d, int64_t v,
+                   float softcap, void* ws, size_t ws_bytes, float* lse_local, float* correct, float* tile_max,
+                   void* stream_ptr) {
+  return fwd_tiles_impl("cce_fwd_gather", E, C, perm_padded, 1, row_map, n_valid, pos, pos_offset, n, d, v,
+                        softcap, ws, ws_bytes, lse_local, correct, tile_max, nullptr, 0, nullptr, nullptr, nullptr,
+                        static_cast<cudaStream_t>(stream_ptr));
 }
 
 
@@ -962,9 +1034,10 @@ int cce_bwd_kept(const void* E_c, const void* C_t, const void* C, const int32_t*
     p.pairs = w.pairs;
     p.pair_count = w.pair_count;
     const bool gathered = aliased && !primary;  // C_t may already hold dC: gather from C
-    if (gathered) {
+    if (gathered) {  // C rows through the permutation (cp.async gathers)
       p.perm = perm_padded;
-      if (int e = launch_lse<cce::KEPT>(p, false, tmE, tmE, tmCo, tmCog, tmC128h, stream)) return e;
+      p.c_rows = static_cast<const __nv_bfloat16*>(C);
+      if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmCo, tmCog, tmC128h, stream)) return e;
     } else if (int e = launch_lse<cce::KEPT>(p, pair, tmE, tmE, tmC, tmC, tmC128h, stream)) {
       return e;
     }
@@ -1123,8 +1196,7 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
     p.nt = nt;
     p.n_base = 0;
     p.mt = gm;
-    p.band = choose_band(d);
-    p.splits = lse_splits(nt, gm, d, pair, true);
+    set_raster(p, nt, gm, d, pair, true);
     p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
     p.softcap = softcap;
     p.lse = lse;

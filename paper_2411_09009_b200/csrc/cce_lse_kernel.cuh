@@ -122,16 +122,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   uint32_t* s_vote = tmem_slot + 1;     // [2][4]
   int* s_slot = reinterpret_cast<int*>(s_vote + 8);  // [2]
+  int32_t* s_eidx = reinterpret_cast<int32_t*>(smem + STAGES * SBYTES + LSE_CTRL_BYTES);  // [BM]
+  int32_t* s_cidx = s_eidx + BM;                                                          // [BN / CG]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const Rows rows(p.n_valid, p.n_total, p.n_base, p.nt);
+  // Row gathers (cp.async): C rows through the vocabulary order (no sorted copy of C) and E rows
+  // through the compaction map unless it is the identity.  Each producer then arrives twice per
+  // stage: once for the TMA bytes, once (relayed) when its gathered bytes have landed.
+  const bool gather_c = p.perm != nullptr;
+  const bool gather_e = p.e_gather != 0 && !rows.ident;
+  const bool gmode = gather_c || gather_e;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmE);
     tma_prefetch_desc(&tmC);
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], CG);  // pairs: both producers arrive on the leader's barrier
+      mbar_init(&full[i], CG * (gmode ? 2 : 1));  // pairs: both producers arrive on the leader's barrier
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -151,50 +160,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const Rows rows(p.n_valid, p.n_total, p.n_base, p.nt);
   auto no_skip = [](int, int) {};
 
   if (warp == 0) {
-    // ================================ TMA producer (whole warp) ===========================
+    // ============================ producer (whole warp: TMA + gathers) =====================
+    constexpr int CROWS = BN / CG;    // C rows this CTA loads per tile
+    constexpr int GLAG = 2;           // gathered stages in flight before their relay
     int stage = 0;
     uint32_t phase = 0;
-    const bool gather_e = p.e_gather != 0;
-    const bool gather_c = p.perm != nullptr;
-    RowGather rge, rgc;
-    int cur_n = -1;
-    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& t) {
-      if (CG == 1) {
-        if (t.n != cur_n) {
-          rge.load(gather_e ? p.row_map : nullptr, t.n * BM, BM);
-          cur_n = t.n;
-        }
-        rgc.load(p.perm, t.m * BN, BN);
+    int cur_n = -1, cur_m = -1;
+    int issued = 0, rstage = 0;       // gathered stages issued; stage of the next relay
+    // this CTA's gathered bytes of stage s have landed: make them visible to the async proxy
+    // (the tensor core) and arrive on the stage's full barrier (pairs: the leader's)
+    auto relay = [&](int s) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2 && rank != 0)
+          mbar_arrive_cluster(&full[s], 0);
+        else
+          mbar_arrive(&full[s]);
       }
+      rstage = (s + 1 == STAGES) ? 0 : s + 1;
+    };
+    const uint32_t tx_cta = (gather_e ? 0u : (uint32_t)A_BYTES) + (gather_c ? 0u : (uint32_t)CROWS * BK * 2);
+    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& t) {
+      if (gather_e && t.n != cur_n) {
+        load_index_table(s_eidx, p.row_map, t.n * BM, BM);
+        cur_n = t.n;
+      }
+      if (gather_c && t.m != cur_m) {
+        load_index_table(s_cidx, p.perm, t.m * BN + rank * CROWS, CROWS);
+        cur_m = t.m;
+      }
+      __syncwarp();
       for (int kb = 0; kb < p.num_kb; ++kb) {
         uint8_t* sa = smem + stage * SBYTES;
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (CG == 2) {
-            // both CTAs' bytes complete on the leader's barrier; the follower only arrives
+            // both CTAs' TMA bytes complete on the leader's barrier; the follower only arrives
             if (rank == 0)
-              mbar_arrive_expect_tx(&full[stage], 2 * SBYTES);
+              mbar_arrive_expect_tx(&full[stage], 2 * tx_cta);
             else
               mbar_arrive_cluster(&full[stage], 0);
             const uint32_t lb = leader_addr(&full[stage]);
-tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
-            tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * (BN / 2));
+            if (!gather_e) tma_load_2d_pair(&tmE, lb, sa, kb * BK, t.n * BM);
+            if (!gather_c) tma_load_2d_pair(&tmC, lb, sa + A_BYTES, kb * BK, t.m * BN + rank * CROWS);
           } else {
-            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], tx_cta);
+            if (!gather_e) tma_load_2d(&tmE, &full[stage], sa, kb * BK, t.n * BM);
+            if (!gather_c) tma_load_2d(&tmC, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);
           }
         }
         __syncwarp();
-        if (CG == 1) {
-          load_rows_warp<BM>(&tmE, &tmEg, rge, gather_e, &full[stage], sa, kb * BK, t.n * BM);
-          load_rows_warp<BN>(&tmC, &tmCg, rgc, gather_c, &full[stage], sa + A_BYTES, kb * BK, t.m * BN);
+        if (gmode) {
+          if (gather_e) gather_box_async<BM>(sa, p.e_rows, p.d, s_eidx, kb * BK);
+          if (gather_c) gather_box_async<CROWS>(sa + A_BYTES, p.c_rows, p.d, s_cidx, kb * BK);
+          cp_async_commit();
+          if (++issued > GLAG) {
+            cp_async_wait<GLAG>();
+            relay(rstage);
+          }
         }
         advance_stage(stage, phase, STAGES);
       }
     }, no_skip);
+    if (gmode) {  // drain: relay the stages still in flight
+      cp_async_wait<0>();
+      for (int k = 0; k < min(issued, GLAG); ++k) relay(rstage);
+    }
   } else if (warp == 1) {
     // ===================================== MMA issuer ====================================
     if (lane == 0 && rank == 0) {  // pairs: the leader issues for both CTAs

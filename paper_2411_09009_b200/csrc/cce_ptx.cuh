@@ -130,6 +130,20 @@ __device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar,
 }
 
 // ----------------------------------------------------------------------------------------
+// cp.async (LDGSTS): 16-byte global -> shared copies, L2 only (.cg); row gathers through an index
+// ----------------------------------------------------------------------------------------
+// src_bytes = 0 zero-fills the 16 bytes without reading (columns past the hidden size)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ----------------------------------------------------------------------------------------
 // clusters / CTA pairs (cta_group::2)
 // ----------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {

@@ -614,6 +614,84 @@ def forward_tiles(e, c, targets, ignore_index: int, vocab_start: int = 0, softca
     return lse_local, correct, state
 
 
+@dataclass
+class GatherState:
+    """What the copy-free training forward hands to the backward: only O(N + V) maps plus the
+    per-row tile maxima -- no compacted E, no sorted classifier (rows are gathered through
+    row_map / perm inside the kernels)."""
+
+    e: torch.Tensor
+    c: torch.Tensor
+    row_map: torch.Tensor
+    n_valid: torch.Tensor
+    perm: torch.Tensor | None
+    perm_padded: torch.Tensor | None
+    pos: torch.Tensor
+    tile_max: torch.Tensor
+    vocab_start: int
+    softcap: float
+    mean_logits: torch.Tensor | None = None
+
+    def nbytes(self) -> int:
+        own = [self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded]
+        return sum(t.numel() * t.element_size() for t in own if t is not None)
+
+
+def prepare_order(e, c, targets, ignore_index: int, vocab_start: int = 0, vocab_sorting: bool = True,
+                  perm: torch.Tensor | None = None):
+    """Compaction (filter_ignored, kernels.py:494-510), the vocabulary order (compute_vocab_order,
+    kernels.py:145-160) and label positions in that order: (row_map, n_valid, perm, perm_padded,
+    pos, mean_logits).  All on the device, O(N + V)."""
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    row_map, n_valid = compact_rows(targets, ignore_index)
+    mean_logits = None
+    if vocab_sorting and perm is None:
+        perm, mean_logits = vocab_order(e, c, targets, ignore_index, n_valid)
+    vpad = -(-v // BLOCK_VOCAB) * BLOCK_VOCAB
+    if perm is None:  # natural order: gathers through the identity keep one code path
+        perm = torch.arange(v, dtype=torch.int32, device=dev)
+    perm_padded = torch.empty(vpad, dtype=torch.int32, device=dev)
+    inv_perm = torch.empty(v, dtype=torch.int32, device=dev)
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
+                                _p(perm_padded), _p(inv_perm), _p(pos), _stream(dev)), "cce_bwd_prep")
+    return row_map, n_valid, perm, perm_padded, pos, mean_logits
+
+
+def forward_gather(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
+                   vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+    """Copy-free forward of the training path: (lse_local, correct, GatherState).
+
+    The same sweep as forward_tiles (compacted rows, vocabulary order, per-row tile maxima;
+    indexed_matmul + lse_forward, kernels.py:204-319), but the kernels read E through row_map and C
+    through the vocabulary order with row gathers, so the transients are O(N + V) plus the tile
+    maxima."""
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    row_map, n_valid, perm, perm_padded, pos, mean_logits = prepare_order(e, c, targets, ignore_index,
+                                                                          vocab_start, vocab_sorting, perm)
+    tile_max = torch.empty(lib.cce_tile_max_bytes(n, v) // 4, dtype=torch.float32, device=dev)
+    lse_local = torch.empty(n, dtype=torch.float32, device=dev)
+    correct = torch.empty(n, dtype=torch.float32, device=dev)
+    state = GatherState(e, c, row_map, n_valid, perm if vocab_sorting else None, perm_padded, pos, tile_max,
+                        int(vocab_start), float(softcap or 0.0), mean_logits)
+    if n == 0:
+        return lse_local, correct, state
+    ws_bytes = lib.cce_fwd_workspace_bytes(n, d, v)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    ev = _ev_begin("fwd")
+    _lib.check(lib.cce_fwd_gather(_p(e), _p(c), _p(perm_padded), _p(row_map), _p(n_valid), _p(pos), 0, n, d, v,
+                                  float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_local), _p(correct),
+                                  _p(tile_max), _stream(dev)), "cce_fwd_gather")
+    _ev_end("fwd", ev)
+    return lse_local, correct, state
+
+
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
                    eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
                    de_done: torch.cuda.Event | None = None, label_split: bool = False,

@@ -21,6 +21,20 @@ def golden_cases():
     return sorted(p.stem for p in GOLDEN.glob("*.npz"))
 
 
+@pytest.fixture(autouse=True)
+def _fresh_library_state():
+    """Every test starts without learned S-hat capacities (they are keyed by the head, so another
+    test's data could size this one's slots) and without a pending label-range error."""
+    try:
+        from paper_2411_09009_b200 import ops
+    except Exception:  # noqa: BLE001 - CPU-only collection without the package importable
+        yield
+        return
+    ops._KEPT_HINT.clear()
+    ops._LABEL_STATE.clear()
+    yield
+
+
 @pytest.fixture(scope="session")
 def cuda_device():
     import torch
