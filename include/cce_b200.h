@@ -194,6 +194,43 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
                    int64_t group_vtiles, void* ws, size_t ws_bytes, float* de_f32, void* dc,
                    unsigned long long* counters, void* stream);
 
+/* cce_fwd_group: cce_fwd_tiles over one vocabulary group of the sorted order (the bounded-memory
+ * training forward).  C_g holds the group's sorted rows [v0, v0 + v_group) (v0 a multiple of 256),
+ * label positions pos are global (pos - v0 is group-local); lse_part / correct_part are the group's
+ * partials (merge with cce_merge_shards); tile_max is the GLOBAL [ceil(n/128)][ceil(v_total/256)]
+ * [128] array, the group writing its own vocab tiles.  E is the caller's E with e_gather = 1 (rows
+ * read through row_map unless the compaction is the identity) or a compacted copy (e_gather = 0). */
+int cce_fwd_group(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total, float softcap,
+                  void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max, void* stream);
+
+/* ---- streamed backward: transient memory independent of the kept-tile count ----
+ * cce_bwd_stream replaces lse_backward (kernels.py:327-486) on the training path.  The decision
+ * comes from the forward's tile maxima (tile_max [ceil(n/128)][ceil(v/256)][128], the layout of
+ * cce_fwd_tiles / cce_fwd_group), exactly as in cce_bwd_kept.  The kept tiles are then
+ * recomputed twice, once in token-tile order for dE and once in vocabulary-tile order for dC, and
+ * streamed from the recomputing CTAs to the contracting CTAs through `ring` ([ring_slots][128][256]
+ * bf16; 256 slots = 16 MiB); no S-hat buffer grows with the kept count.
+ *   E          rows of the token tiles: the caller's E with e_gather = 1 (rows are read through
+ *              row_map unless the compaction is the identity) or a compacted copy with e_gather = 0
+ *   C          the caller's classifier; with a vocabulary order (perm_padded / inv_perm from
+ *              cce_bwd_prep) its rows are gathered into c_sorted ([v][d] bf16).  c_sorted may be dc:
+ *              dC is then written in the sorted order over the sorted copy and moved back to
+ *              vocabulary order in place (no second V x D buffer)
+ *   de_out     [n][d] bf16 (or fp32 with de_fp32), rows of ignored tokens left untouched (zero them)
+ *   counters   [3] u64 += {kept, eps-skipped, zero-upstream-skipped} (BackwardStats)
+ * de_done_event (optional) is recorded once every dE write is enqueued.  ring_slots >= 64. */
+size_t cce_bwd_stream_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t ring_slots);
+/* diagnostics: byte offsets of the stream lists inside the workspace (13 values; see
+ * scripts/stream_lists_check.py), returns the window size in items */
+int cce_bwd_stream_debug_layout(int64_t n, int64_t d, int64_t v, int64_t ring_slots, int64_t* offsets);
+int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
+                   const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                   const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d, int64_t v,
+                   float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
+                   size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+                   void* de_done_event, void* stream);
+
 /* ---- paper ordering (label_split = 1 in cce_bwd_kept / cce_bwd_lowmem) ----
  * PAPER.md Alg. 3 filters tiles on S alone, before the one-hot subtraction;
  * the reference instead never skips a tile holding a label (kernels.py:447-455).

@@ -59,6 +59,14 @@ __global__ void merge_shards_kernel(int P, const float* __restrict__ lse_parts,
 }
 
 // zero a float buffer (used for `correct` so rows whose label lives in another shard read 0)
+// Zero n 32-bit words.  A kernel rather than cudaMemsetAsync: inside a chain of programmatic
+// dependent launches a memset node is not ordered against the kernels around it.
+__global__ void zero_words_kernel(int* __restrict__ x, int64_t n) {
+  griddep_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = 0;
+}
+
 __global__ void fill_kernel(float* __restrict__ x, float v, int64_t n) {
   griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -31,6 +31,20 @@ constexpr int SHAT_TILE_BYTES = BM * BN * 2;  // one stored S-hat tile, bf16 row
 
 enum Mode { FWD = 0, BWD = 1, KEPT = 2 };
 
+// Streamed backward (cce_bwd_stream): S-hat tiles pass from producer CTAs (KEPT recompute) to
+// consumer CTAs (dE or dC) of the same grid through a ring of `ring` 64 KiB slots in HBM.  Item i
+// (its position in the pass's kept list) occupies slot i % ring; the producer waits until the
+// slot's previous item has been read by all its consumers, writes S-hat, then publishes
+// ready[slot] = lap + 1 (lap = i / ring); each consumer waits for that, loads the tile with TMA
+// and adds 1 to used[slot] once the bytes have landed.
+struct Stream {
+  int ring;          // slots (0: not streaming)
+  int* ready;        // [ring]
+  int* used;         // [ring]
+  int consumers;     // consumptions per item
+  int producers;     // the first `producers` CTAs of the grid recompute, the rest consume
+};
+
 // Forward (FWD) and backward filter pass (BWD, "B1") of the fused logit-tile kernel.
 //
 // Token rows: the forward runs on all n_total rows of E.  The backward runs on the compacted
@@ -93,6 +107,8 @@ struct Params {
   const int* list_count;   // kept tiles (slots used = min(count, capacity))
   const int2* pairs;       // CTA pairs: (first slot, 1 or 2 tiles) of one vocab tile
   const int* pair_count;
+  Stream st;               // KEPT streamed into a ring (TileRef.s is then the item index)
+  int tm_stride, tm_m0;    // FWD: tile_max row stride in vocab tiles (0: mt) and first vocab tile
 };
 
 // dE pass ("B2") and dC pass ("B3").
@@ -108,6 +124,7 @@ struct GradParams {
   const int32_t* perm_store;  // tile-order position -> dC row (padded), or nullptr
   const int32_t* row_map;  // compact row -> original row (padded)
   int e_gather;            // 1: gather E rows through row_map (else E is compacted)
+  const __nv_bfloat16* e_rows;  // E base of the row gathers (pairs: cp.async), [n_total][d]
   int atoms3d;             // 1: d % 64 == 0, operand tiles load as one 3-D TMA box (all atoms)
   __nv_bfloat16* de_bf16;  // [n_total][d]   (one of de_bf16 / de_f32)
   float* de_f32;
@@ -121,6 +138,27 @@ struct GradParams {
   int dc_block;            // dC: 0 vocab-tile-major units, B > 0 blocks of B vocab tiles, chunk-major
   int prefetch;            // dE: L2-prefetch C slices of the kept tiles this many vocab tiles ahead (0 = off)
   int debug;               // diagnostics only (CCE_DEBUG_GRAD): bit0 skip S-hat loads, bit1 skip E/C loads
+  // streamed backward: units are (segment, D chunk[, vocab half]); a segment is a run of at most B
+  // consecutive items of one owner (token tile for dE, vocab tile for dC).  An owner split over
+  // several segments sums them in segment order through an fp32 accumulator region (chain[] counts
+  // the segments folded in; acc_gen[] hands the region from one owner to the next).
+  Stream st;
+  const int4* seg;         // [*seg_count] (owner, first item, items, split index)
+  const int2* seg_aux;     // [*seg_count] (splits of the owner, accumulator id if splits > 1)
+  const int* seg_count;
+  const int2* items;       // the pass's kept list: (token tile, vocab tile) in stream order
+  const int* sidx;         // segment item k is items[sidx[k]] (nullptr: items[k]; dE segments
+                           // gather one token tile's items of a stream window)
+  int* chain;              // [owners * ndc * 2]
+  float* acc;              // [nacc][ndc][2][128][256]
+  int nacc;
+  int* acc_gen;            // [nacc * ndc * 2]
+  // dC over the storage of the sorted classifier: before a vocab tile's dC is written, every item
+  // of the tile (own_off[m] .. + own_cnt[m]) must have been read by all its consumers (the dE
+  // consumers read those C rows)
+  const int* own_off;
+  const int* own_cnt;
+  unsigned long long* prof;  // diagnostics (CCE_STREAM_PROF builds): per-unit timestamps
 };
 
 // Device-side view of the compaction: valid row count, token tiles of this launch.

@@ -47,6 +47,7 @@ constexpr int DC_B_BYTES = 64 * DCH * 2;        // E [64 tok][256 d]        = 32
 constexpr int DC_STAGE_BYTES = DC_A_BYTES + DC_B_BYTES;
 constexpr int DC_STG_PITCH = 144;                 // bytes per staged row (128 B + 16 B pad)
 constexpr int DC_STG_BYTES = 4 * 32 * DC_STG_PITCH;  // epilogue row-transpose staging, 4 warps
+constexpr int DC_IDX_BYTES = BM * 4;                 // E row-gather index table (pairs)
 
 // Visit, in index order, the stored tiles slot_of[i * stride] >= 0 for i < count; the warp reads
 // 32 entries per step and every lane calls f(i, slot) for each stored tile.
@@ -124,10 +125,9 @@ __device__ __forceinline__ void store_row32(float* dst_f32, __nv_bfloat16* dst_b
 // Units are ordered pair-major (the CTAs running at once share C[:, pair]) and handed out by an
 // atomic counter (p.sched): units differ in length (kept tiles per token tile, a lone last chunk).
 template <int CH, int KV>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    cce_de_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmC,
-                  const __grid_constant__ CUtensorMap tmC3, const __grid_constant__ CUtensorMap tmCg,
-                  const GradParams p) {
+__device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMap& tmC, const CUtensorMap& tmC3,
+                                        const CUtensorMap& tmCg, const GradParams& p, uint8_t* smem, int bid,
+                                        int nblk) {
   using Cfg = DeCfg<CH, KV>;
   constexpr int DE_STAGES = Cfg::STAGES;
   constexpr int DE_STAGE_BYTES = Cfg::STAGE_BYTES;
@@ -137,9 +137,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int DE_KV = KV;
   constexpr int ACC = Cfg::ACC;
   if (skip_launch(p.run_if)) return;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DE_STAGES * DE_STAGE_BYTES);
   uint64_t* empty = full + DE_STAGES;
   uint64_t* acc_full = empty + DE_STAGES;  // [ACC]
@@ -148,6 +145,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* unit_empty = unit_full + DE_QUEUE;
   int* s_unit = reinterpret_cast<int*>(unit_empty + DE_QUEUE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_unit + DE_QUEUE);
+  // streamed: per stage, the ring slot whose last bytes it carries (-1: none), set by the loader
+  // before the stage's arrival; the MMA thread counts the slot consumed once the stage has landed
+  int* s_sig = reinterpret_cast<int*>(smem + DE_STAGES * DE_STAGE_BYTES + 256);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -175,12 +175,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
   const int G = rows.g;
   const int npair = (p.ndc + DE_CH - 1) / DE_CH;
-  const int units = G * npair;
+  // streamed: units are (segment, chunk group), segment-major; otherwise (token tile, chunk group)
+  const bool stream = p.st.ring > 0;
+  const int units = (stream ? *p.seg_count : G) * npair;
+  constexpr int SPI = BN / DE_KV;  // stages per S-hat tile
   const bool plain = p.atoms3d && p.perm == nullptr;
   // unit u -> (chunk group j, token tile ln): chunk-major (concurrent CTAs share C[:, j]) or
   // token-tile-major (concurrent CTAs share S-hat[n])
   auto decode = [&](int u, int& j, int& ln) {
-    if (p.de_order == 0) {
+    if (stream) {  // ln = segment index
+      ln = u / npair;
+      j = u - ln * npair;
+    } else if (p.de_order == 0) {
       j = u / G;
       ln = u % G;
     } else if (p.de_order >= 2) {
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int u = 0;
       if (lane == 0) {
         mbar_wait(&unit_empty[k], ph ^ 1);
-        u = p.sched ? atomicAdd(p.sched, 1) : (int)blockIdx.x + q * (int)gridDim.x;
+        u = p.sched ? atomicAdd(p.sched, 1) : bid + q * nblk;
         if (u >= units) u = -1;
         s_unit[k] = u;
         mbar_arrive(&unit_full[k]);
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode(u, j, ln);
       const int nch = min(DE_CH, p.ndc - DE_CH * j);
       const uint32_t bytes = DE_A_BYTES + nch * DE_CHUNK_BYTES;
-      const int32_t* srow = p.slot_of + (size_t)ln * p.mt;
+      const int32_t* srow = stream ? nullptr : p.slot_of + (size_t)ln * p.mt;
       // L2 prefetch of the C slices of kept tiles [m + prefetch, ...): lane l covers vocab tile
       // pf_next + l, issued one batch of 32 ahead of use
       int pf_next = 0;
@@ -242,9 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           pf_next = min(pf_next + 32, m_hi);
         }
       };
-      prefetch_upto(p.prefetch);
-      for_each_kept(srow, p.mt, 1, [&](int m, int slot) {
-        prefetch_upto(m + p.prefetch);
+      auto load_tile = [&](int m, int slot, int sig) {
         for (int h = 0; h < BN / DE_KV; ++h) {
           RowGather rgc;
           rgc.load(p.perm, m * BN + DE_KV * h, DE_KV);
@@ -252,6 +256,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sb = sa + DE_A_BYTES;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
+            if (stream) s_sig[stage] = h == BN / DE_KV - 1 ? sig : -1;
             mbar_arrive_expect_tx(&full[stage], bytes);
             // S-hat [128 tok][KV voc]: swizzle atom h of the stored tile
 #if CCE_DE_HINT > 0
@@ -284,7 +289,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           advance_stage(stage, phase, DE_STAGES);
         }
-      });
+      };
+      if (stream) {
+        // the segment's items in stream order; each waits until its producer published it
+        const int4 sg = p.seg[ln];
+#ifdef CCE_STREAM_PROF
+        if (lane == 0 && p.prof) {
+          p.prof[(size_t)u * 8 + 0] = global_timer_ns();
+          p.prof[(size_t)u * 8 + 6] = bid;
+          p.prof[(size_t)u * 8 + 7] = ((unsigned long long)sg.x << 32) | (unsigned)sg.y;
+        }
+#endif
+#ifdef CCE_STREAM_TRACE
+        if (lane == 0 && bid < 4) printf("de cta %d unit %d seg %d (n %d start %d cnt %d split %d) chunk %d\n", bid, u, ln, sg.x, sg.y, sg.z, sg.w, j);
+#endif
+        for (int k = sg.y; k < sg.y + sg.z; ++k) {
+          const int i = p.sidx ? p.sidx[k] : k;
+          const int slot = i % p.st.ring;
+          if (lane == 0) {
+            spin_until_geq(&p.st.ready[slot], i / p.st.ring + 1);
+            fence_proxy_async_global();
+          }
+          __syncwarp();
+          load_tile(p.items[i].y, slot, slot);
+        }
+#ifdef CCE_STREAM_PROF
+        if (lane == 0 && p.prof) p.prof[(size_t)u * 8 + 1] = global_timer_ns();
+#endif
+      } else {
+        prefetch_upto(p.prefetch);
+        for_each_kept(srow, p.mt, 1, [&](int m, int slot) {
+          prefetch_upto(m + p.prefetch);
+          load_tile(m, slot, -1);
+        });
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -299,7 +337,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int j, ln;
         decode(u, j, ln);
         const int nch = min(DE_CH, p.ndc - DE_CH * j);
-        const int ksteps = (BN / DE_KV) * p.cnt_n[ln];
+        const int4 sg = stream ? p.seg[ln] : make_int4(0, 0, 0, 0);
+        const int ksteps = SPI * (stream ? sg.z : p.cnt_n[ln]);
         const int buf = q % ACC;
         mbar_wait(&acc_free[buf], ((q / ACC) & 1) ^ 1);
         tc_fence_after();
@@ -315,6 +354,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mma_bf16_ss(d_tmem + c * DCH, make_sdesc(a0 + ks * 32, 0, Cfg::A_SBO, Cfg::A_LAYOUT),
                           make_sdesc(b0 + c * DE_CHUNK_BYTES + ks * 2048, DE_KV * 128, 1024), IDESC,
                           (s | ks) != 0);
+          // streamed: the item's last S-hat stage has landed in smem -- its ring slot may be reused
+          if (stream) {
+            const int sig = s_sig[stage];
+            if (sig >= 0) red_relaxed_add_gpu(&p.st.used[sig], 1);
+          }
           mma_commit(&empty[stage]);
           advance_stage(stage, phase, DE_STAGES);
         }
@@ -324,6 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
+    const int epi_tid = threadIdx.x - 64;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     for (int q = 0;; ++q) {
       const int k = q % DE_QUEUE;
@@ -335,46 +380,142 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode(u, j, ln);
       const int nch = min(DE_CH, p.ndc - DE_CH * j);
       const int buf = q % ACC;
+#ifdef CCE_STREAM_PROF
+      const int u_prof = u;
+      if (epi_tid == 0 && p.prof && stream) p.prof[(size_t)u * 8 + 2] = global_timer_ns();
+#endif
       mbar_wait(&acc_full[buf], (q / ACC) & 1);
       tc_fence_after();
-      const bool has = p.cnt_n[ln] > 0;
+#ifdef CCE_STREAM_PROF
+      if (epi_tid == 0 && p.prof && stream) p.prof[(size_t)u * 8 + 3] = global_timer_ns();
+#endif
+      // streamed: the segment's owner (token tile) and its place in the owner's split chain
+      int nsplit = 1, split = 0, chain_key = 0, gen_key = 0;
+      const float* racc = nullptr;
+      float* wacc = nullptr;
+      bool has;
+      if (stream) {
+        const int4 sg = p.seg[ln];
+        const int2 sx = p.seg_aux[ln];
+        ln = sg.x;
+        has = sg.z > 0;
+        nsplit = sx.x;
+        split = sg.w;
+        if (nsplit > 1) {
+          // CH = 1: one 256-column chunk per unit, region (acc slot, chunk j)
+          gen_key = (sx.y % p.nacc) * p.ndc + j;
+          chain_key = ln * p.ndc + j;
+          // region [64 column quads][128 rows] of float4: a warp's 32 rows read 512 contiguous bytes
+          float* region = p.acc + (size_t)gen_key * BM * DCH + row * 4;
+          racc = split > 0 ? region : nullptr;
+          wacc = split < nsplit - 1 ? region : nullptr;
+          if (epi_tid == 0) {
+            if (split == 0)
+              spin_until_geq(&p.acc_gen[gen_key], sx.y / p.nacc);  // previous owner done with the region
+            else
+              spin_until_geq(&p.chain[chain_key], split);          // segments before this one folded in
+          }
+          named_bar_sync(1, 128);
+        }
+#ifdef CCE_STREAM_PROF
+        if (epi_tid == 0 && p.prof) p.prof[(size_t)u_prof * 8 + 4] = global_timer_ns();
+#endif
+      } else {
+        has = p.cnt_n[ln] > 0;
+      }
       const int grow = (p.n_base + ln) * BM + row;
       const bool valid = grow < rows.n && (has || !p.de_accumulate);  // accumulate: nothing to add
       const int drow = valid ? p.row_map[grow] : 0;
+      if (racc || wacc) {
+        // split owner (streamed): fold in the earlier segments and pass the sum on, 64 columns per
+        // step with every load of the step in flight at once (the region sits in L2)
 #pragma unroll 1
-      for (int c = 0; c < nch * (DCH / 32); ++c) {
-        const int col = DE_CH * j * DCH + c * 32;
-        float x[32];
-        if (has) {
-          uint32_t r[32];
-          tmem_ld32(tmem_base + lane_off + buf * (DE_CH * DCH) + c * 32, r);
-          tmem_ld_wait();
+        for (int c = 0; c < nch * (DCH / 64); ++c) {
+          const int col = DE_CH * j * DCH + c * 64;
+          float x[64];
+          {
+            uint32_t r[64];
+            tmem_ld32(tmem_base + lane_off + buf * (DE_CH * DCH) + c * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+            tmem_ld32(tmem_base + lane_off + buf * (DE_CH * DCH) + c * 64 + 32,
+                      *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = 0.f;
-        }
-        if (valid && col < p.d) {
-          const size_t off = (size_t)drow * p.d + col;
-          if (p.de_accumulate) {  // fp32 read-modify-write, fixed group order (deterministic)
-            const float* old = p.de_f32 + off;
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              if (i < p.d - col) {
-                const float4 o = *reinterpret_cast<const float4*>(old + i);
-                x[i] += o.x;
-                x[i + 1] += o.y;
-                x[i + 2] += o.z;
-                x[i + 3] += o.w;
-              }
+            for (int i = 0; i < 64; ++i) x[i] = __uint_as_float(r[i]);
           }
-          store_row32(p.de_f32 ? p.de_f32 + off : nullptr, p.de_bf16 ? p.de_bf16 + off : nullptr, x,
-                      p.d - col);
+          if (racc) {
+            float4 o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __ldcg(reinterpret_cast<const float4*>(racc) + (c * 16 + i) * BM);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              x[4 * i] += o[i].x;
+              x[4 * i + 1] += o[i].y;
+              x[4 * i + 2] += o[i].z;
+              x[4 * i + 3] += o[i].w;
+            }
+          }
+          if (wacc) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              __stcg(reinterpret_cast<float4*>(wacc) + (c * 16 + i) * BM,
+                     make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]));
+          } else if (valid) {
+            const size_t off = (size_t)drow * p.d + col;
+            store_row32(p.de_f32 ? p.de_f32 + off : nullptr, p.de_bf16 ? p.de_bf16 + off : nullptr, x, p.d - col);
+            if (col + 32 < p.d)
+              store_row32(p.de_f32 ? p.de_f32 + off + 32 : nullptr, p.de_bf16 ? p.de_bf16 + off + 32 : nullptr, x + 32,
+                          p.d - col - 32);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < nch * (DCH / 32); ++c) {
+          const int col = DE_CH * j * DCH + c * 32;
+          float x[32];
+          if (has) {
+            uint32_t r[32];
+            tmem_ld32(tmem_base + lane_off + buf * (DE_CH * DCH) + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = 0.f;
+          }
+          if (valid && col < p.d) {
+            const size_t off = (size_t)drow * p.d + col;
+            if (p.de_accumulate) {  // fp32 read-modify-write, fixed group order (deterministic)
+              const float* old = p.de_f32 + off;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                if (i < p.d - col) {
+                  const float4 o = *reinterpret_cast<const float4*>(old + i);
+                  x[i] += o.x;
+                  x[i + 1] += o.y;
+                  x[i + 2] += o.z;
+                  x[i + 3] += o.w;
+                }
+            }
+            store_row32(p.de_f32 ? p.de_f32 + off : nullptr, p.de_bf16 ? p.de_bf16 + off : nullptr, x,
+                        p.d - col);
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_free[buf]);
+#ifdef CCE_STREAM_PROF
+      if (epi_tid == 0 && p.prof && stream) p.prof[(size_t)u_prof * 8 + 5] = global_timer_ns();
+#endif
+      if (nsplit > 1) {  // hand the running sum / the region on
+        named_bar_sync(1, 128);
+        if (epi_tid == 0) {
+          __threadfence();
+          if (split < nsplit - 1)
+            st_release_gpu(&p.chain[chain_key], split + 1);
+          else
+            red_release_add_gpu(&p.acc_gen[gen_key], 1);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -385,6 +526,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+template <int CH, int KV>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cce_de_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmC,
+                  const __grid_constant__ CUtensorMap tmC3, const __grid_constant__ CUtensorMap tmCg,
+                  const GradParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  de_body<CH, KV>(tmS, tmC, tmC3, tmCg, p, smem, (int)blockIdx.x, (int)gridDim.x);
+}
+
 // ------------------------------------------------------------------------------------------
 // B3: dC
 // ------------------------------------------------------------------------------------------
@@ -393,10 +545,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // half (A) and half of the shared E[64 tok][256 d] operand (B, 128 d-columns), so per-SM operand
 // traffic per flop drops by a third; each CTA's TMEM holds its 128 vocab rows.
 template <int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    cce_dc_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmE,
-                  const __grid_constant__ CUtensorMap tmE3, const __grid_constant__ CUtensorMap tmEg,
-                  const GradParams p) {
+__device__ __forceinline__ void dc_body(const CUtensorMap& tmS, const CUtensorMap& tmE, const CUtensorMap& tmE3,
+                                        const CUtensorMap& tmEg, const GradParams& p, uint8_t* smem, int bid,
+                                        int nblk) {
   constexpr int B_BYTES = DC_B_BYTES / CG;  // this CTA's part of E[64 tok][256 d]
   constexpr int SBYTES = DC_A_BYTES + B_BYTES;
   // same smem footprint for both forms: pairs (32 KB stages) get 6 stages instead of 4
@@ -404,23 +555,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int DC_STAGES = STAGES;
   constexpr int DC_STAGE_BYTES = SBYTES;
   if (skip_launch(p.run_if)) return;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* stg = smem + cce::DC_STAGES * cce::DC_STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + DC_STG_BYTES);
   uint64_t* empty = full + DC_STAGES;
   uint64_t* acc_full = empty + DC_STAGES;
   uint64_t* acc_free = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+  int32_t* s_eidx = reinterpret_cast<int32_t*>(stg + DC_STG_BYTES + 256);  // [BM] (after the barriers)
+  int* s_sig = reinterpret_cast<int*>(stg + DC_STG_BYTES + 256 + DC_IDX_BYTES);  // [stages], see de_body
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
+  // pairs reading E through a compaction that is not the identity: cp.async row gathers, relayed
+  // to the leader's full barrier once landed (as in the logit-tile kernel)
+  const bool gather_pair = CG == 2 && p.e_gather != 0 && !rows.ident;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmS);
     tma_prefetch_desc(&tmE);
     for (int i = 0; i < DC_STAGES; ++i) {
-      mbar_init(&full[i], CG);  // pairs: both producers arrive on the leader's barrier
+      mbar_init(&full[i], CG * (gather_pair ? 2 : 1));  // pairs: both producers arrive on the leader's barrier
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -440,22 +594,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const Rows rows(p.n_valid, p.n_total, p.n_base, p.g);
   const int G = rows.g;
   // unit u = ((m * ndc) + dc) * 2 + vh: the two vocab halves of one (m, dchunk) run side by side
   // (CG = 1: adjacent units sharing their E / S-hat loads through L2; CG = 2: one CTA pair)
-  const int units = p.mt * p.ndc * 2;
-  const int start = CG == 2 ? (int)(blockIdx.x & ~1u) + rank : (int)blockIdx.x;
-  const int stride = (int)gridDim.x;
+  // streamed: units are (segment, D chunk, vocab half), segment-major; the segment's owner is
+  // the vocab tile
+  const bool stream = p.st.ring > 0;
+  const int units = (stream ? *p.seg_count : p.mt) * p.ndc * 2;
+  const int start = CG == 2 ? (bid & ~1) + rank : bid;
+  const int stride = nblk;
+  // unit -> (vocab tile or segment m, chunk, half)
+  auto decode = [&](int u, int& m, int& dc, int& vh) {
+    if (stream) {
+      vh = u & 1;
+      const int w = u >> 1;
+      m = w / p.ndc;
+      dc = w - m * p.ndc;
+    } else {
+      dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
+    }
+  };
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
+    constexpr int GLAG = 2;  // gathered stages in flight before their relay
+    int issued = 0, rstage = 0;
+    auto relay = [&](int st) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank != 0)
+          mbar_arrive_cluster(&full[st], 0);
+        else
+          mbar_arrive(&full[st]);
+      }
+      rstage = (st + 1 == DC_STAGES) ? 0 : st + 1;
+    };
     for (int u = start; u < units; u += stride) {
       int vh, dc, m;
-      dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
-      auto tile = [&](int ln, int slot) {
+      decode(u, m, dc, vh);
+      auto tile = [&](int ln, int slot, int sig = -1) {
         const int n = p.n_base + ln;
+        if (gather_pair) {
+          load_index_table(s_eidx, p.row_map, n * BM, BM);
+          __syncwarp();
+        }
         for (int h = 0; h < 2; ++h) {
           RowGather rge;
           rge.load(p.e_gather ? p.row_map : nullptr, n * BM + 64 * h, 64);
@@ -464,15 +648,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool e3 = p.atoms3d && !p.e_gather;
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
+            if (stream && rank == 0) s_sig[stage] = h == 1 ? sig : -1;
             if (CG == 2) {
               if (rank == 0)
-                mbar_arrive_expect_tx(&full[stage], 2 * SBYTES);
+                mbar_arrive_expect_tx(&full[stage], 2 * (gather_pair ? (uint32_t)DC_A_BYTES : (uint32_t)SBYTES));
               else
                 mbar_arrive_cluster(&full[stage], 0);
               const uint32_t lb = leader_addr(&full[stage]);
               // S-hat^T half vh: tokens [64h, +64) x vocab atoms 2vh, 2vh+1; E: this CTA's 2 atoms
               tma_load_3d_pair(&tmS, lb, sa, 0, slot * BM + 64 * h, 2 * vh);
-              tma_load_3d_pair(&tmE3, lb, sb, 0, n * BM + 64 * h, dc * (DCH / 64) + 2 * rank);
+              if (!gather_pair) tma_load_3d_pair(&tmE3, lb, sb, 0, n * BM + 64 * h, dc * (DCH / 64) + 2 * rank);
             } else {
               mbar_arrive_expect_tx(&full[stage], ((p.debug & 1) ? 0 : DC_A_BYTES) + ((p.debug & 2) ? 0 : DC_B_BYTES));
               // S-hat^T half: tokens [64h, +64) x vocab atoms 2vh, 2vh+1 in one box
@@ -482,6 +667,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           __syncwarp();
+          if (gather_pair) {  // this CTA's two 64-column atoms of E[64 tok] through row_map
+#pragma unroll 1
+            for (int a = 0; a < 2; ++a)
+              gather_box_async<64>(sb + a * (64 * 128), p.e_rows, p.d, s_eidx + 64 * h,
+                                   dc * DCH + 128 * rank + 64 * a);
+            cp_async_commit();
+            if (++issued > GLAG) {
+              cp_async_wait<GLAG>();
+              relay(rstage);
+            }
+          }
           if (CG == 1 && !e3) {
 #pragma unroll 1
             for (int a = 0; a < DCH / 64; ++a)
@@ -491,10 +687,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           advance_stage(stage, phase, DC_STAGES);
         }
       };
-      if (p.off_m != nullptr)  // contiguous slots of this vocab tile from the kept list
+      if (stream) {
+        const int4 sg = p.seg[m];
+        for (int i = sg.y; i < sg.y + sg.z; ++i) {
+          const int slot = i % p.st.ring;
+          if (lane == 0) {
+            spin_until_geq(&p.st.ready[slot], i / p.st.ring + 1);
+            fence_proxy_async_global();
+          }
+          __syncwarp();
+          tile(p.items[i].x - p.n_base, slot, slot);
+        }
+      } else if (p.off_m != nullptr) {  // contiguous slots of this vocab tile from the kept list
         for_each_listed(p.list, p.off_m[m], p.cnt_m[m], p.n_base, tile);
-      else
+      } else {
         for_each_kept(p.slot_of + m, G, p.mt, tile);
+      }
+    }
+    if (gather_pair) {  // drain: relay the stages still in flight
+      cp_async_wait<0>();
+      for (int k = 0; k < min(issued, GLAG); ++k) relay(rstage);
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // pairs: the leader issues for both CTAs
@@ -505,8 +717,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // the next unit's kept count is loaded one unit ahead (units are short: ~8 us at Gemma-2B)
       auto unit_cnt = [&](int uu) {
         int mm, dd, hh;
-        dc_unit(uu, p.mt, p.ndc, p.dc_block, mm, dd, hh);
-        return p.cnt_m[mm];
+        decode(uu, mm, dd, hh);
+        return stream ? p.seg[mm].z : p.cnt_m[mm];
       };
       int cnt = start < units ? unit_cnt(start) : 0;
       for (int u = start; u < units; u += stride) {
@@ -535,6 +747,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else
               mma_bf16_ss(d_tmem, ad, bd, IDESC, (s | ks) != 0);
           }
+          // streamed: both 64-token halves of the item's S-hat (both CTAs' halves, pairs) have
+          // landed -- the ring slot may be reused (one count per unit: both CTAs load per stage)
+          if (stream) {
+            const int sig = s_sig[stage];
+            if (sig >= 0) red_relaxed_add_gpu(&p.st.used[sig], 1);
+          }
           if (CG == 2)
             mma_commit_pair(&empty[stage]);
           else
@@ -560,9 +778,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int t = 0;
     for (int u = start; u < units; u += stride) {
       int vh, dc, m;
-      dc_unit(u, p.mt, p.ndc, p.dc_block, m, dc, vh);
-      const bool has = p.cnt_m[m] > 0;
+      decode(u, m, dc, vh);
+      // streamed: the segment's owner (vocab tile) and its place in the owner's split chain
+      int nsplit = 1, split = 0, chain_key = 0, gen_key = 0;
+      const float* racc = nullptr;
+      float* wacc = nullptr;
+      bool has;
+      if (stream) {
+        const int4 sg = p.seg[m];
+        const int2 sx = p.seg_aux[m];
+        m = sg.x;
+        has = sg.z > 0;
+        nsplit = sx.x;
+        split = sg.w;
+        if (nsplit > 1) {
+          gen_key = ((sx.y % p.nacc) * p.ndc + dc) * 2 + vh;
+          chain_key = (m * p.ndc + dc) * 2 + vh;
+          float* region = p.acc + (size_t)gen_key * BM * DCH + row * 4;  // column-quad-major (see dE)
+          racc = split > 0 ? region : nullptr;
+          wacc = split < nsplit - 1 ? region : nullptr;
+          if (epi_tid == 0) {
+            if (split == 0)
+              spin_until_geq(&p.acc_gen[gen_key], sx.y / p.nacc);
+            else
+              spin_until_geq(&p.chain[chain_key], split);
+          }
+          named_bar_sync(1, 128);
+        }
+      } else {
+        has = p.cnt_m[m] > 0;
+      }
       if (!has && p.accumulate) continue;  // nothing kept and nothing to write
+      if (stream && p.own_off && !wacc) {
+        // the final write lands on C rows of this tile in the sorted copy: wait until every item of
+        // the tile has been read by every consumer (counts only grow, so later laps satisfy it too)
+        if (epi_tid == 0) {
+          const int i0 = p.own_off[m], i1 = i0 + p.own_cnt[m];
+          for (int i = i0; i < i1; ++i)
+            spin_until_geq(&p.st.used[i % p.st.ring], (i / p.st.ring + 1) * p.st.consumers);
+        }
+        named_bar_sync(1, 128);
+      }
       const int buf = t & 1;
       // per-unit loads issued before the wait so their latency hides behind it
       const int vpos = m * BN + vh * 128 + row;
@@ -576,7 +832,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int c = 0; c < DCH / 64; ++c) {
           // 1) this thread's 64 columns -> bf16 -> staging row `lane`
           uint32_t pk[32];
-          if (has) {
+          if (has && nsplit > 1) {
+            // split owner: fold in the earlier segments, pass the sum on (or write it: last one)
+            uint32_t r0[32], r1[32];
+            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64, r0);
+            tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64 + 32, r1);
+            tmem_ld_wait();
+            float x[64];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              x[j] = __uint_as_float(r0[j]);
+              x[32 + j] = __uint_as_float(r1[j]);
+            }
+            if (racc) {
+#pragma unroll
+              for (int j = 0; j < 64; j += 4) {
+                const float4 o = __ldcg(reinterpret_cast<const float4*>(racc) + (c * 16 + j / 4) * BM);
+                x[j] += o.x;
+                x[j + 1] += o.y;
+                x[j + 2] += o.z;
+                x[j + 3] += o.w;
+              }
+            }
+            if (wacc) {
+#pragma unroll
+              for (int j = 0; j < 64; j += 4)
+                __stcg(reinterpret_cast<float4*>(wacc) + (c * 16 + j / 4) * BM,
+                       make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+              continue;  // warp-uniform: every thread of the unit takes this branch
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) pk[j] = pack_bf16x2(x[2 * j], x[2 * j + 1]);
+          } else if (has) {
             uint32_t r0[32], r1[32];
             tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64, r0);
             tmem_ld32(tmem_base + lane_off + buf * DCH + c * 64 + 32, r1);
@@ -636,6 +923,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_arrive(&acc_free[buf]);
       }
       ++t;
+      if (nsplit > 1) {  // hand the running sum / the region on
+        if (CG != 2) named_bar_sync(2, 128);  // (pairs: the barrier above already joined the epilogue)
+        if (epi_tid == 0) {
+          __threadfence();
+          if (split < nsplit - 1)
+            st_release_gpu(&p.chain[chain_key], split + 1);
+          else
+            red_release_add_gpu(&p.acc_gen[gen_key], 1);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -648,6 +945,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     else
       tmem_dealloc(tmem_base, TMEM_COLS);
   }
+}
+
+template <int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cce_dc_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmE,
+                  const __grid_constant__ CUtensorMap tmE3, const __grid_constant__ CUtensorMap tmEg,
+                  const GradParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  dc_body<CG>(tmS, tmE, tmE3, tmEg, p, smem, (int)blockIdx.x, (int)gridDim.x);
 }
 
 }  // namespace cce

@@ -26,6 +26,7 @@
 #include "cce_aux_kernels.cuh"
 #include "cce_grad_kernels.cuh"
 #include "cce_lse_kernel.cuh"
+#include "cce_stream.cuh"
 
 // =========================================================================================
 // Host side: C ABI
@@ -160,8 +161,9 @@ constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + 
 constexpr size_t kLsePairSmem =
     1024 + (size_t)cce::LSE_STAGES_PAIR * cce::PAIR_STAGE_BYTES + kCtrlBytes + cce::LSE_IDX_BYTES;
 template <int CH, int KV>
-constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH, KV>::SMEM + kCtrlBytes; }
-constexpr size_t kDcSmem = 1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes;
+constexpr size_t de_smem() { return 1024 + (size_t)cce::DeCfg<CH, KV>::SMEM + kCtrlBytes + 64; }
+constexpr size_t kDcSmem =
+    1024 + (size_t)cce::DC_STAGES * cce::DC_STAGE_BYTES + cce::DC_STG_BYTES + kCtrlBytes + cce::DC_IDX_BYTES + 64;
 
 // Launches inside the kept backward's pass chain use programmatic dependent launch (every kernel
 // there begins with griddepcontrol.wait): the next kernel is scheduled while its predecessor
@@ -817,7 +819,8 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
                    int gather_e, const int32_t* row_map, const int* n_valid, const int32_t* pos,
                    int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes,
                    float* lse_local, float* correct, float* tile_max, void* lab_buf, int64_t lab_capacity,
-                   int32_t* lab_slot, void* lab_list, int* lab_count, cudaStream_t stream) {
+                   int32_t* lab_slot, void* lab_list, int* lab_count, cudaStream_t stream, int tm_stride = 0,
+                   int tm_m0 = 0) {
   const std::string w(what);
   if (n < 0 || d <= 0 || v <= 0) return fail(w + ": bad sizes");
   if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail(w + ": label tiles need slot maps");
@@ -854,6 +857,8 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
   p.part = static_cast<float2*>(ws);
   p.correct = correct;
   p.tile_max = tile_max;
+  p.tm_stride = tm_stride;
+  p.tm_m0 = tm_m0;
   if (lab_buf) {
     CCE_CUDA(cudaMemsetAsync(lab_slot, 0xFF, (size_t)nt * mt * sizeof(int32_t), stream));
     CCE_CUDA(cudaMemsetAsync(lab_count, 0, sizeof(int), stream));
@@ -891,6 +896,17 @@ int cce_fwd_gather(const void* E, const void* C, const int32_t* perm_padded, con
                         static_cast<cudaStream_t>(stream_ptr));
 }
 
+
+int cce_fwd_group(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                  const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total, float softcap,
+                  void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max, void* stream_ptr) {
+  if (v0 % cce::BN != 0) return fail("cce_fwd_group: v0 must be a multiple of 256");
+  if (v0 + v_group > v_total) return fail("cce_fwd_group: group past the vocabulary");
+  return fwd_tiles_impl("cce_fwd_group", E, C_g, nullptr, e_gather, row_map, n_valid, pos, v0, n, d, v_group, softcap,
+                        ws, ws_bytes, lse_part, correct_part, tile_max, nullptr, 0, nullptr, nullptr, nullptr,
+                        static_cast<cudaStream_t>(stream_ptr), (int)((v_total + cce::BN - 1) / cce::BN),
+                        (int)(v0 / cce::BN));
+}
 
 size_t cce_bwd_kept_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t capacity_tiles,
                                     int64_t lab_capacity) {
@@ -1327,6 +1343,312 @@ int cce_f32_to_bf16(const float* x, void* y, int64_t count, void* stream_ptr) {
   const int64_t n4 = count / 4;
   if (n4 == 0) return 0;
   PDL_LAUNCH(cce::f32_to_bf16_kernel, dim3((unsigned)((n4 + 255) / 256)), dim3(256), 0, stream, x, static_cast<__nv_bfloat16*>(y), n4);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"
+
+// ---- streamed backward (cce_stream.cuh): bounded transients, any kept-tile count ----
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && atoi(e) > 0) ? atoi(e) : dflt;
+}
+int stream_seg_voc() { return env_int("CCE_STREAM_SEG_VOC", 64); }
+int stream_nacc() { return env_int("CCE_STREAM_NACC", 4); }
+int stream_window(int64_t ring) { return (int)std::min<int64_t>(ring - 1, env_int("CCE_STREAM_WINDOW", (int)(ring / 2))); }
+
+struct StreamWs {
+  uint8_t* block_zero;
+  uint8_t* keep;
+  int* voc_cnt;
+  int* voc_rcnt;
+  int* voc_off;
+  int2* items;      // vocab-tile-major kept list (the stream)
+  int4* cseg;       // dC segments (vocab tile owners)
+  int2* caux;
+  int2* pairs;      // producer CTA-pair entries
+  int* wcnt;        // [max windows][nt]
+  int* wsplit;
+  int* wstart;
+  int* nsplit;      // [nt]
+  int* sidx;        // [items] stream positions grouped by (window, token tile)
+  int4* eseg;       // dE segments (window, token tile)
+  int2* eaux;
+  int* ctrl;        // [0] items [1] dC segments [2] pairs [3] dE segments [4] permutation breaks
+  int* ready;
+  int* used;
+  int* chain_e;
+  int* chain_c;
+  int* gen_e;
+  int* gen_c;
+  size_t ctrl_bytes;  // zeroed per call (ctrl .. gen_c)
+  float* acc_e;       // [nt][ndc][128][256] fp32 dE partial sums across windows
+  float* acc_c;       // [nacc][ndc][2][128][256] fp32 partial sums of vocab tiles split over segments;
+                      // afterwards the row-permutation scratch (with acc_e)
+  uint8_t* perm_cls;
+  int32_t* perm_bidx;
+  int perm_cap;
+  int max_windows;
+  size_t total;
+};
+
+StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring) {
+  const int64_t nt = std::max<int64_t>(1, (n + cce::BM - 1) / cce::BM);
+  const int64_t mt = (v + cce::BN - 1) / cce::BN;
+  const int64_t ndc = (d + cce::DCH - 1) / cce::DCH;
+  const int64_t items = nt * mt;
+  const int64_t W = stream_window(ring);
+  const int64_t maxw = (items + W - 1) / W;
+  const int64_t seg_c = mt + items / stream_seg_voc() + 1;
+  const int64_t nacc = stream_nacc();
+  auto up = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  uint8_t* b = static_cast<uint8_t*>(base);
+  StreamWs w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* ptr = b ? b + o : nullptr;
+    o += up(bytes);
+    return ptr;
+  };
+  w.block_zero = take(nt);
+  w.keep = take(nt * mt);
+  w.voc_cnt = reinterpret_cast<int*>(take(mt * 4));
+  w.voc_rcnt = reinterpret_cast<int*>(take(mt * 4));
+  w.voc_off = reinterpret_cast<int*>(take(mt * 4));
+  w.items = reinterpret_cast<int2*>(take(items * 8));
+  w.cseg = reinterpret_cast<int4*>(take(seg_c * 16));
+  w.caux = reinterpret_cast<int2*>(take(seg_c * 8));
+  w.pairs = reinterpret_cast<int2*>(take((items / 2 + mt + 1) * 8));
+  w.wcnt = reinterpret_cast<int*>(take(maxw * nt * 4));
+  w.wsplit = reinterpret_cast<int*>(take(maxw * nt * 4));
+  w.wstart = reinterpret_cast<int*>(take(maxw * nt * 4));
+  w.nsplit = reinterpret_cast<int*>(take(nt * 4));
+  w.sidx = reinterpret_cast<int*>(take(items * 4));
+  w.eseg = reinterpret_cast<int4*>(take(items * 16));
+  w.eaux = reinterpret_cast<int2*>(take(items * 8));
+  const size_t c0 = o;
+  w.ctrl = reinterpret_cast<int*>(take(64));
+  w.ready = reinterpret_cast<int*>(take(ring * 4));
+  w.used = reinterpret_cast<int*>(take(ring * 4));
+  w.chain_e = reinterpret_cast<int*>(take(nt * ndc * 4));
+  w.chain_c = reinterpret_cast<int*>(take(mt * ndc * 2 * 4));
+  w.gen_e = reinterpret_cast<int*>(take(nt * ndc * 4));
+  w.gen_c = reinterpret_cast<int*>(take(nacc * ndc * 2 * 4));
+  w.ctrl_bytes = o - c0;
+  w.perm_cap = (int)(v / cce::PERM_K * 3 / 2 + 1024);
+  const size_t acc_e = (size_t)nt * ndc * cce::BM * cce::DCH * 4;
+  const size_t acc_c = (size_t)nacc * ndc * 2 * cce::BM * cce::DCH * 4;
+  const size_t perm_bytes = (size_t)w.perm_cap * d * 2;
+  uint8_t* accs = take(std::max(acc_e + acc_c, perm_bytes));
+  w.acc_e = reinterpret_cast<float*>(accs);
+  w.acc_c = reinterpret_cast<float*>(accs ? accs + acc_e : nullptr);
+  w.perm_cls = take(v);
+  w.perm_bidx = reinterpret_cast<int32_t*>(take(v * 4));
+  w.max_windows = (int)maxw;
+  w.total = o;
+  return w;
+}
+
+// In-place: rows X[p] -> X[perm[p]] (p < v); scratch from the stream workspace (after the pass).
+int unpermute_rows(__nv_bfloat16* X, const int32_t* perm, const int32_t* inv, int64_t v, int64_t d, const StreamWs& w,
+                   cudaStream_t stream) {
+  __nv_bfloat16* tmp = reinterpret_cast<__nv_bfloat16*>(w.acc_e);
+  PDL_LAUNCH(cce::unpermute_classify_kernel, dim3((unsigned)((v + 255) / 256)), dim3(256), 0, stream, perm, (int)v,
+             w.perm_cls, w.perm_bidx, w.ctrl + 4, w.perm_cap);
+  PDL_LAUNCH(cce::unpermute_save_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
+             static_cast<const __nv_bfloat16*>(X), (int)v, (int)d, (const uint8_t*)w.perm_cls,
+             (const int32_t*)w.perm_bidx, tmp);
+  PDL_LAUNCH(cce::unpermute_walk_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream, X, (int)v, (int)d, inv,
+             (const uint8_t*)w.perm_cls, (const int32_t*)w.perm_bidx, (const __nv_bfloat16*)tmp);
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+size_t cce_bwd_stream_workspace_bytes(int64_t n, int64_t d, int64_t v, int64_t ring_slots) {
+  return stream_layout(nullptr, n, d, v, ring_slots).total;
+}
+
+// Diagnostics: byte offsets in the workspace of {keep, items, wcnt, wstart, sidx, eseg, eaux, ctrl,
+// voc_cnt, voc_off, cseg, caux, pairs} (13 values), and the window size.
+int cce_bwd_stream_debug_layout(int64_t n, int64_t d, int64_t v, int64_t ring_slots, int64_t* out) {
+  const StreamWs w = stream_layout(reinterpret_cast<void*>(uintptr_t(1) << 20), n, d, v, ring_slots);
+  const void* ptrs[13] = {w.keep, w.items, w.wcnt, w.wstart, w.sidx, w.eseg, w.eaux, w.ctrl,
+                          w.voc_cnt, w.voc_off, w.cseg, w.caux, w.pairs};
+  for (int i = 0; i < 13; ++i) out[i] = (int64_t)(reinterpret_cast<uintptr_t>(ptrs[i])) - (int64_t(1) << 20);
+  return stream_window(ring_slots);
+}
+
+int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
+                   const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                   const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d, int64_t v,
+                   float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
+                   size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+                   void* de_done_event, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (d % 8 != 0) return fail("cce_bwd_stream: D must be a multiple of 8");
+  if (!(eps > 0.f)) return fail("cce_bwd_stream: needs filtering (eps > 0)");
+  if (!ring || ring_slots < 2 * stream_seg_voc()) return fail("cce_bwd_stream: ring_slots too small");
+  if (de_out == nullptr && dc == nullptr) return fail("cce_bwd_stream: neither dE nor dC requested");
+  if (perm_padded && (!c_sorted || !inv_perm)) return fail("cce_bwd_stream: vocabulary order needs c_sorted, inv_perm");
+  if (d % 64 != 0) return fail("cce_bwd_stream: D must be a multiple of 64 (CTA-pair operand boxes)");
+  if (n <= 0) return 0;
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
+  const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  const int ndc = (int)((d + cce::DCH - 1) / cce::DCH);
+  if (nt > 2048) return fail("cce_bwd_stream: at most 2048 token tiles (262144 rows) per call");
+  const StreamWs w = stream_layout(ws, n, d, v, ring_slots);
+  if (ws_bytes < w.total) return fail("cce_bwd_stream: workspace too small");
+  const int R = (int)ring_slots;
+  const int W = stream_window(ring_slots);
+  const int sms = num_sms();
+  if (sms < 6) return fail("cce_bwd_stream: needs at least 6 SMs");
+  PdlScope pdl_scope(true);
+
+  // sorted classifier: C[perm] into c_sorted (dC's own storage when dc == c_sorted)
+  const void* C_t = C;
+  if (perm_padded) {
+    PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
+               static_cast<const __nv_bfloat16*>(C), (const int32_t*)perm_padded, (int)v, (int)d,
+               static_cast<__nv_bfloat16*>(c_sorted));
+    C_t = c_sorted;
+  }
+  // decision (kernels.py:434-455), the stream (vocab-tile-major kept list), its segments
+  PDL_LAUNCH(cce::zero_words_kernel, dim3(64), dim3(256), 0, stream, w.ctrl, (int64_t)(w.ctrl_bytes / 4));
+  PDL_LAUNCH(cce::block_zero_kernel, dim3(nt), dim3(cce::BM), 0, stream, upstream, row_map, n_valid, w.block_zero);
+  PDL_LAUNCH(cce::decide_tiles_kernel, dim3((unsigned)((mt + cce::DECIDE_VT - 1) / cce::DECIDE_VT), (unsigned)nt),
+             dim3(256), 0, stream, tile_max, lse, pos, 0, row_map, n_valid, (const uint8_t*)w.block_zero, nt, mt,
+             softcap, eps, label_split, w.keep, counters);
+  PDL_LAUNCH(cce::list_count_kernel, dim3(mt), dim3(128), 0, stream, (const uint8_t*)w.keep, nt, mt, 0, nt,
+             (const int*)nullptr, (const int32_t*)nullptr, w.voc_cnt, w.voc_rcnt);
+  PDL_LAUNCH(cce::segments_kernel, dim3(1), dim3(1024), 0, stream, (const int*)w.voc_cnt, mt, stream_seg_voc(),
+             w.voc_off, w.ctrl + 0, w.cseg, w.caux, w.ctrl + 1, counters);
+  PDL_LAUNCH(cce::fill_items_kernel<false>, dim3(mt), dim3(256), 0, stream, (const uint8_t*)w.keep, nt, mt,
+             (const int*)w.voc_off, w.items);
+  PDL_LAUNCH(cce::build_pairs_kernel, dim3(1), dim3(1024), 0, stream, (const int*)w.voc_cnt, mt, (const int*)nullptr,
+             w.pairs, w.ctrl + 2);
+  // The window kernels run without programmatic dependent launch: under PDL they read the stream
+  // list before it is complete (measured: wrong dE segments on warm calls, CCE_STREAM_NOPDL=1 fixes
+  // it); three launch gaps of a few microseconds.  Diagnostics: CCE_STREAM_NOPDL bit1 also turns it
+  // off for the pass kernel.
+  const int pdl_mask = env_int("CCE_STREAM_NOPDL", 0) | 1;
+  if (de_out) {
+    PdlScope wpdl(!(pdl_mask & 1));
+    PDL_LAUNCH(cce::window_count_kernel, dim3(w.max_windows), dim3(256), (size_t)nt * 4, stream,
+               (const int2*)w.items, (const int*)(w.ctrl + 0), W, nt, w.wcnt);
+    PDL_LAUNCH(cce::window_segments_kernel, dim3(1), dim3(1024), 0, stream, (const int*)w.wcnt,
+               (const int*)(w.ctrl + 0), W, nt, w.wsplit, w.nsplit, w.wstart, w.eseg, w.eaux, w.ctrl + 3);
+    if (int e = ensure_attr(cce::window_fill_kernel, (size_t)9 * nt * 4)) return e;
+    PDL_LAUNCH(cce::window_fill_kernel, dim3(w.max_windows), dim3(256), (size_t)9 * nt * 4, stream,
+               (const int2*)w.items, (const int*)(w.ctrl + 0), W, nt, (const int*)w.wstart, w.sidx);
+  }
+
+  if (getenv("CCE_STREAM_LISTS_ONLY")) return 0;  // diagnostics: the lists alone
+  CUtensorMap tmE, tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h;
+  const bool ok = make_tmap(&tmE, E, n, d, cce::BM) && make_tmap(&tmC128, C_t, v, d, cce::BN / 2) &&
+                  make_tmap3d_inner(&tmSe, ring, (int64_t)R * cce::BM, cce::BN, 64, cce::BM, 1) &&
+                  make_tmap(&tmCk, C_t, v, d, cce::DE_KV) && make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) &&
+                  make_tmap3d(&tmSc, ring, (int64_t)R * cce::BM, cce::BN, 64, 2) && make_tmap(&tmE64, E, n, d, 64) &&
+                  make_tmap3d(&tmE3h, E, n, d, 64, cce::DCH / 128);
+  if (!ok) return fail("cce_bwd_stream: cuTensorMapEncodeTiled failed");
+
+  // roles: producers and dC consumers as CTA pairs, dE consumers single (about a third each)
+  const int grid = sms & ~1;
+  int P = env_int("CCE_STREAM_P", ((grid / 3) + 1) & ~1);
+  int Qc = dc ? env_int("CCE_STREAM_QC", ((grid / 3) + 1) & ~1) : 0;
+  P = std::max(2, P & ~1);
+  Qc = dc ? std::max(2, Qc & ~1) : 0;
+  if (!de_out) Qc = grid - P;
+  if (P + Qc > grid - (de_out ? 1 : 0)) return fail("cce_bwd_stream: CCE_STREAM_P + CCE_STREAM_QC leave no dE CTAs");
+  const int consumers = (dc ? ndc : 0) + (de_out ? ndc : 0);
+  const cce::Stream st{R, w.ready, w.used, consumers, P};
+
+  cce::Params p{};
+  p.n_total = (int)n;
+  p.n_valid = n_valid;
+  p.d = (int)d;
+  p.v = (int)v;
+  p.nt = nt;
+  p.mt = mt;
+  p.splits = 1;
+  p.band = choose_band(d);
+  p.num_kb = (int)((d + cce::BK - 1) / cce::BK);
+  p.softcap = softcap;
+  p.lse = lse;
+  p.upstream = upstream;
+  p.pos = pos;
+  p.row_map = row_map;
+  p.e_gather = e_gather;
+  p.e_rows = static_cast<const __nv_bfloat16*>(E);
+  p.eps = eps;
+  p.label_split = label_split;
+  p.shat = static_cast<__nv_bfloat16*>(ring);
+  p.counters = counters;
+  p.list = w.items;
+  p.list_count = w.ctrl + 0;
+  p.pairs = w.pairs;
+  p.pair_count = w.ctrl + 2;
+  p.st = st;
+  cce::GradParams q{};
+  q.n_total = (int)n;
+  q.d = (int)d;
+  q.v = (int)v;
+  q.mt = mt;
+  q.ndc = ndc;
+  q.n_valid = n_valid;
+  q.g = nt;
+  q.row_map = row_map;
+  q.e_gather = e_gather;
+  q.e_rows = static_cast<const __nv_bfloat16*>(E);
+  q.atoms3d = 1;
+  q.st = st;
+  q.items = w.items;
+  cce::GradParams qe = q;  // dE: segments (window, token tile) through sidx, accumulator id = token tile
+  qe.seg = w.eseg;
+  qe.seg_aux = w.eaux;
+  qe.seg_count = w.ctrl + 3;
+  qe.sidx = w.sidx;
+  qe.chain = w.chain_e;
+  qe.acc = w.acc_e;
+  qe.nacc = nt;
+  qe.acc_gen = w.gen_e;
+  qe.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
+  qe.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
+  if (!de_out) qe.seg_count = w.ctrl + 5;  // zero segments
+  cce::GradParams qc = q;  // dC: segments of vocab tiles (contiguous items)
+  qc.seg = w.cseg;
+  qc.seg_aux = w.caux;
+  qc.seg_count = w.ctrl + 1;
+  qc.chain = w.chain_c;
+  qc.acc = w.acc_c;
+  qc.nacc = stream_nacc();
+  qc.acc_gen = w.gen_c;
+  if (const char* pf = getenv("CCE_STREAM_PROF_PTR")) qe.prof = reinterpret_cast<unsigned long long*>(strtoull(pf, nullptr, 0));
+  const bool sorted_out = perm_padded && dc == c_sorted;  // dC lands in the sorted order, then moves
+  qc.dc = static_cast<__nv_bfloat16*>(dc);
+  qc.perm_store = sorted_out ? nullptr : perm_padded;
+  if (sorted_out && de_out) {  // dE consumers read the rows dC overwrites
+    qc.own_off = w.voc_off;
+    qc.own_cnt = w.voc_cnt;
+  }
+
+  if (getenv("CCE_STREAM_DEBUG"))
+    fprintf(stderr, "cce_bwd_stream: grid %d P %d Qc %d ring %d window %d consumers %d | ready %p used %p "
+            "chain_e %p chain_c %p gen_e %p gen_c %p ctrl %p\n", grid, P, Qc, R, W, consumers, (void*)w.ready,
+            (void*)w.used, (void*)w.chain_e, (void*)w.chain_c, (void*)w.gen_e, (void*)w.gen_c, (void*)w.ctrl);
+  constexpr size_t smem = std::max({kLsePairSmem, kDcSmem, de_smem<1, 64>()});
+  if (int e = ensure_attr(cce::cce_stream3_kernel, smem)) return e;
+  PdlScope spdl(!(pdl_mask & 2));
+  if (int e = launch_k(cce::cce_stream3_kernel, dim3(grid), dim3(cce::NUM_THREADS), smem, stream, 2, tmE, tmC128,
+                       tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h, p, qe, qc, Qc))
+    return e;
+  if (de_done_event) CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
+  if (sorted_out)
+    if (int e = unpermute_rows(static_cast<__nv_bfloat16*>(dc), perm_padded, inv_perm, v, d, w, stream)) return e;
   CCE_CUDA(cudaGetLastError());
   return 0;
 }

@@ -48,14 +48,14 @@ struct TileRef {
 // KEPT: grid-stride over the kept list (vocab-tile-major, so concurrent CTAs share C tiles).
 // `skip(n, count)` is called for BWD units whose upstream is all zero (kernels.py:434-438).
 template <int MODE, int CG, typename F, typename S>
-__device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, int rank, F&& f,
-                                              S&& skip) {
+__device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows, int rank, int bid, int nblk,
+                                              F&& f, S&& skip) {
   if (MODE == KEPT) {
     if (CG == 2) {
       // pair entry = up to two kept tiles of one vocab tile (consecutive slots); a lone tile's
       // partner CTA recomputes the same rows and discards them
       const int total = *p.pair_count;
-      for (int i = blockIdx.x >> 1; i < total; i += gridDim.x >> 1) {
+      for (int i = bid >> 1; i < total; i += nblk >> 1) {
         const int2 pe = p.pairs[i];
         const bool ok = rank < pe.y;
         const int slot = pe.x + (ok ? rank : 0);
@@ -64,8 +64,8 @@ __device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows,
       }
       return;
     }
-    const int total = min(*p.list_count, p.capacity);
-    for (int i = blockIdx.x; i < total; i += gridDim.x) {
+    const int total = p.st.ring ? *p.list_count : min(*p.list_count, p.capacity);
+    for (int i = bid; i < total; i += nblk) {
       const int2 t = p.list[i];
       f(TileRef{t.x, t.y, i, true, true, true, false});
     }
@@ -74,8 +74,8 @@ __device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows,
   const int gp = (rows.g + CG - 1) / CG;  // token tiles (CG = 2: token-tile pairs) of this launch
   const int units = gp * p.splits;
   const int band = max(1, min((p.band + CG - 1) / CG, gp));
-  const int start = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int stride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int start = CG == 2 ? bid >> 1 : bid;
+  const int stride = CG == 2 ? nblk >> 1 : nblk;
   for (int u = start; u < units; u += stride) {
     const int b = u / (band * p.splits);
     const int r = u - b * band * p.splits;
@@ -104,17 +104,15 @@ __device__ __forceinline__ void for_each_tile(const Params& p, const Rows& rows,
   }
 }
 
+// The kernel body, on CTA `bid` of `nblk` (the whole grid, or the producer role of the streamed
+// backward's kernel, cce_stream.cuh); `smem` is the 1024-aligned dynamic shared memory.
 template <int MODE, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    cce_lse_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
-                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
-                   const Params p) {
+__device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorMap& tmEg, const CUtensorMap& tmC,
+                                         const CUtensorMap& tmCg, const Params& p, uint8_t* smem, int bid,
+                                         int nblk) {
   constexpr int STAGES = CG == 2 ? LSE_STAGES_PAIR : LSE_STAGES;
   constexpr int SBYTES = CG == 2 ? PAIR_STAGE_BYTES : STAGE_BYTES;  // per-CTA bytes per stage
   if (skip_launch(p.run_if)) return;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SBYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: logits ready
@@ -165,7 +163,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ============================ producer (whole warp: TMA + gathers) =====================
     constexpr int CROWS = BN / CG;    // C rows this CTA loads per tile
-    constexpr int GLAG = 2;           // gathered stages in flight before their relay
+#ifndef CCE_GLAG
+#define CCE_GLAG 2
+#endif
+    constexpr int GLAG = CCE_GLAG < STAGES ? CCE_GLAG : STAGES - 1;  // gathered stages in flight before their relay
     int stage = 0;
     uint32_t phase = 0;
     int cur_n = -1, cur_m = -1;
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       rstage = (s + 1 == STAGES) ? 0 : s + 1;
     };
     const uint32_t tx_cta = (gather_e ? 0u : (uint32_t)A_BYTES) + (gather_c ? 0u : (uint32_t)CROWS * BK * 2);
-    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& t) {
+    for_each_tile<MODE, CG>(p, rows, rank, bid, nblk, [&](const TileRef& t) {
       if (gather_e && t.n != cur_n) {
         load_index_table(s_eidx, p.row_map, t.n * BM, BM);
         cur_n = t.n;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef&) {
+      for_each_tile<MODE, CG>(p, rows, rank, bid, nblk, [&](const TileRef&) {
         const int buf = t & 1;
         mbar_wait(&acc_free[buf], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     };
 
-    for_each_tile<MODE, CG>(p, rows, rank, [&](const TileRef& tr) {
+    for_each_tile<MODE, CG>(p, rows, rank, bid, nblk, [&](const TileRef& tr) {
       if (tr.n != cur_n || tr.ok != cur_ok) {  // KEPT pairs: a lone tile's partner visits it with ok = false
         load_row(tr.n, tr.ok);
         cur_n = tr.n;
@@ -501,13 +502,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         release_acc(buf);
-        if (p.tile_max && tr.ok) p.tile_max[((size_t)tr.n * p.mt + tr.m) * BM + row] = zmax;
+        if (p.tile_max && tr.ok)
+          p.tile_max[((size_t)tr.n * (p.tm_stride ? p.tm_stride : p.mt) + p.tm_m0 + tr.m) * BM + row] = zmax;
         if (tr.last && valid) {  // per ORIGINAL row (rows may be compacted, filter_ignored)
           p.part[(size_t)tr.s * p.n_total + orow] = make_float2(run_m, run_s);
           if (have_corr) p.correct[orow] = corr;
         }
       } else if (MODE == KEPT) {
-        if (tr.ok) store_shat(tacc, col0, tr.s);
+        if (p.st.ring == 0) {
+          if (tr.ok) store_shat(tacc, col0, tr.s);
+        } else if (tr.ok) {
+          // streamed: wait until the slot's previous item has been read by all its consumers,
+          // write S-hat, make it visible to their TMA loads (async proxy) and publish it
+          const int slot = tr.s % p.st.ring, lap = tr.s / p.st.ring;
+          if (epi_tid == 0) spin_until_geq(&p.st.used[slot], lap * p.st.consumers);
+          named_bar_sync(1, 128);
+          store_shat(tacc, col0, slot);
+          fence_proxy_async_global();
+          named_bar_sync(1, 128);
+          if (epi_tid == 0) {
+            __threadfence();
+            st_release_gpu(&p.st.ready[slot], lap + 1);
+          }
+        }
         release_acc(buf);
       } else if (!tr.ok || tr.zero) {
         // pairs only: this CTA's tile is missing or has zero upstream while the peer's is live
@@ -575,6 +592,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     else
       tmem_dealloc(tmem_base, TMEM_COLS);
   }
+}
+
+template <int MODE, int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cce_lse_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
+                   const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  lse_body<MODE, CG>(tmE, tmEg, tmC, tmCg, p, smem, (int)blockIdx.x, (int)gridDim.x);
 }
 
 }  // namespace cce

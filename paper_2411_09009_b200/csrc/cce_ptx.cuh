@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cstdio>
 
 namespace cce {
 
@@ -319,6 +320,52 @@ __device__ __forceinline__ void red_add_v4_bf16x2(__nv_bfloat16* p, uint32_t a, 
   asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b),
                "r"(c), "r"(d)
                : "memory");
+}
+
+// ----------------------------------------------------------------------------------------
+// Cross-CTA flags (GPU scope) for the streamed backward: release / acquire on 32-bit counters,
+// and the generic <-> async proxy fence for global memory (S-hat written with st.global by one
+// CTA, read with TMA by another)
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Consumption count of a ring slot, from the MMA thread once the slot's bytes have landed in smem
+// (observed through the stage's full barrier): relaxed -- a release would fence the issuing thread.
+__device__ __forceinline__ void red_relaxed_add_gpu(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= target (acquire).  A wait longer than ~20 s means a broken schedule: trap (the
+// launch fails with an error) rather than hang the device.
+__device__ __forceinline__ void spin_until_geq(const int* p, int target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const uint64_t t0 = global_timer_ns();
+  uint32_t ns = 32;
+  while (ld_acquire_gpu(p) < target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (global_timer_ns() - t0 > 20000000000ull) {
+      printf("cce: wait timed out: block %d thread %d at %p: %d < %d\n", (int)blockIdx.x, (int)threadIdx.x,
+             (const void*)p, *(volatile const int*)p, target);
+      __trap();
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -62,7 +62,7 @@ def _global_vocab(v_local: int, group) -> int:
 class _LinearCrossEntropy(torch.autograd.Function):
     @staticmethod
     def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
-                vocab_start, low_memory, exempt_label_tiles, training, v_total):
+                vocab_start, memory, exempt_label_tiles, training, v_total):
         # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
         # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
         # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
@@ -71,11 +71,15 @@ class _LinearCrossEntropy(torch.autograd.Function):
         # forward grad mode is always off, and needs_input_grad follows requires_grad even under
         # torch.no_grad(), so an eval call would otherwise pay for the training forward.
         ctx.state = None
-        if eps > 0 and not low_memory and training:
+        if eps > 0 and memory == "bounded" and training:
+            # default: vocabulary-grouped forward into the per-row tile maxima, streamed backward
+            lse_local, correct, ctx.state = ops.forward_stream(e, c, targets, ignore_index, vocab_start, softcap,
+                                                               vocab_sorting)
+        elif eps > 0 and memory == "fast" and training:
             lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
                                                               softcap, vocab_sorting, eps=eps,
                                                               label_split=not exempt_label_tiles)
-        elif eps > 0 and low_memory and training and os.environ.get("CCE_LOWMEM_RECOMPUTE", "0") == "0":
+        elif eps > 0 and memory == "grouped" and training and os.environ.get("CCE_LOWMEM_RECOMPUTE", "0") == "0":
             # bounded memory: the same decision from the forward, over vocabulary groups
             lse_local, correct, ctx.state = ops.forward_grouped(e, c, targets, ignore_index, vocab_start,
                                                                 softcap, vocab_sorting, eps=eps,
@@ -115,7 +119,16 @@ class _LinearCrossEntropy(torch.autograd.Function):
         split, correct = ctx.split, ctx.correct
         # a pass whose input needs no gradient is skipped (e.g. a frozen classifier: no dC pass)
         want = dict(want_de=ctx.needs_input_grad[0], want_dc=ctx.needs_input_grad[1])
-        if isinstance(state, ops.GroupState):
+        if isinstance(state, ops.StreamState):
+            done = ops.recorded_event() if group is not None else None
+            de, dc, _ = ops.backward_from_stream_state(state, lse, up, eps=eps, fp32_de=group is not None,
+                                                       de_done=done, label_split=split, correct=correct, **want)
+            del state
+            if group is not None and de is not None:
+                from .vocab_parallel import all_reduce_de_overlapped
+
+                de = all_reduce_de_overlapped(de, done, group)
+        elif isinstance(state, ops.GroupState):
             done = ops.recorded_event() if group is not None else None
             de, dc, _ = ops.backward_grouped(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
                                              fp32_de=group is not None, de_done=done, label_split=split,
@@ -165,18 +178,27 @@ def linear_cross_entropy(
     vocab_start: int = 0,
     low_memory: bool = False,
     exempt_label_tiles: bool = True,
+    memory: str | None = None,
 ) -> torch.Tensor:
     """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
 
     e: [..., D] CUDA embeddings; c: [V, D] classifier (nn.Linear weight layout); targets: [...]
     integer labels.  The kernels compute in bf16: fp32/fp16 operands are cast (gradients come
     back in the operands' dtype) and any D is accepted (zero-padded to a multiple of 8).  Returns a scalar for "mean"/"sum", else per-token losses of shape
-    e.shape[:-1].  The default keeps the sorted classifier copy and per-tile row maxima from the
-    forward, so the backward recomputes only the tiles it keeps.  low_memory=True bounds the
-    transients: forward and backward run over vocabulary groups of the sorted order, only one
-    group's classifier rows and S-hat slots exist at a time, and dE accumulates in fp32 (the
-    per-tile row maxima and the compacted E are kept from the forward; with filter_eps=None,
-    or CCE_LOWMEM_RECOMPUTE=1, only O(N) state is kept and the backward recomputes every tile).
+    e.shape[:-1].
+
+    memory selects the training path (filtering on):
+      "bounded" (default)  the forward sweeps vocabulary groups of the sorted order (one group's
+                 classifier rows gathered at a time) and keeps per-row tile maxima; the backward
+                 streams the kept tiles through a fixed 32 MiB ring from recomputing CTAs to the dE /
+                 dC CTAs of one persistent kernel (ops.backward_stream).  No transient grows with the
+                 kept-tile count.  Needs D % 64 == 0; other shapes take "fast".
+      "fast"     the forward keeps a sorted classifier copy and stores label tiles; the backward
+                 keeps every kept tile's S-hat (memory grows with the kept count)
+      "grouped"  (= low_memory=True) forward and backward over vocabulary groups with S-hat slots
+                 sized from the learned kept density; with filter_eps=None, or
+                 CCE_LOWMEM_RECOMPUTE=1, only O(N) state is kept and the backward recomputes every tile
+    CCE_MEMORY overrides the default.
 
     exempt_label_tiles=True is the reference's filter (a tile holding a label is never skipped,
     kernels.py:447-455).  False is the paper's Alg. 3 ordering: tiles are filtered on the softmax
@@ -211,9 +233,14 @@ def linear_cross_entropy(
         raise ValueError("softcap must be positive")
     eps = _resolve_eps(filter_eps)
     training = torch.is_grad_enabled() and (e2.requires_grad or c.requires_grad)
+    mode = "grouped" if low_memory else (memory or os.environ.get("CCE_MEMORY") or "bounded")
+    if mode not in ("bounded", "fast", "grouped"):
+        raise ValueError(f"memory must be 'bounded', 'fast' or 'grouped', got {mode!r}")
+    if mode == "bounded" and not (ops.stream_supported(e2.shape[1]) and e2.shape[0] <= 2048 * ops.BLOCK_TOKENS):
+        mode = "fast"  # the streamed backward's CTA-pair boxes need D % 64 == 0
     out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
                                     bool(vocab_sorting), process_group, int(vocab_start),
-                                    bool(low_memory), bool(exempt_label_tiles), training, int(v_total))
+                                    mode, bool(exempt_label_tiles), training, int(v_total))
     if reduction == "none":
         return out.reshape(lead)
     return out

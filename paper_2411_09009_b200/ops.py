@@ -638,10 +638,10 @@ class GatherState:
 
 
 def prepare_order(e, c, targets, ignore_index: int, vocab_start: int = 0, vocab_sorting: bool = True,
-                  perm: torch.Tensor | None = None):
+                  perm: torch.Tensor | None = None, with_inverse: bool = False):
     """Compaction (filter_ignored, kernels.py:494-510), the vocabulary order (compute_vocab_order,
     kernels.py:145-160) and label positions in that order: (row_map, n_valid, perm, perm_padded,
-    pos, mean_logits).  All on the device, O(N + V)."""
+    pos, mean_logits[, inv_perm]).  All on the device, O(N + V)."""
     lib = _lib.load()
     n, d = e.shape
     v = c.shape[0]
@@ -658,6 +658,8 @@ def prepare_order(e, c, targets, ignore_index: int, vocab_start: int = 0, vocab_
     pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.cce_bwd_prep(_p(perm), v, _p(targets), int(ignore_index), int(vocab_start), n,
                                 _p(perm_padded), _p(inv_perm), _p(pos), _stream(dev)), "cce_bwd_prep")
+    if with_inverse:
+        return row_map, n_valid, perm, perm_padded, pos, mean_logits, inv_perm
     return row_map, n_valid, perm, perm_padded, pos, mean_logits
 
 
@@ -690,6 +692,101 @@ def forward_gather(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
                                   _p(tile_max), _stream(dev)), "cce_fwd_gather")
     _ev_end("fwd", ev)
     return lse_local, correct, state
+
+
+@dataclass
+class StreamState:
+    """What the bounded-memory training forward hands to the streamed backward: the caller's E and C
+    (rows read through the compaction map / gathered per vocabulary group, never copied whole),
+    O(N + V) maps and the per-row tile maxima [ceil(n/128)][ceil(v/256)][128]."""
+
+    e: torch.Tensor
+    c: torch.Tensor
+    row_map: torch.Tensor
+    n_valid: torch.Tensor
+    perm: torch.Tensor | None
+    perm_padded: torch.Tensor | None
+    inv_perm: torch.Tensor | None
+    pos: torch.Tensor
+    tile_max: torch.Tensor
+    vocab_start: int
+    softcap: float
+    mean_logits: torch.Tensor | None = None
+
+    def nbytes(self) -> int:
+        own = [self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded, self.inv_perm]
+        return sum(t.numel() * t.element_size() for t in own if t is not None)
+
+
+FWD_GROUP_MB = 24  # sorted classifier rows of one vocabulary group in the bounded forward
+
+
+def fwd_group_tiles(d: int, mt: int) -> int:
+    """Vocab tiles per group of the bounded forward: the group's sorted rows within
+    CCE_FWD_GROUP_MB (default 24 MB; 16 tiles at D = 2304)."""
+    budget = int(os.environ.get("CCE_FWD_GROUP_MB", FWD_GROUP_MB)) << 20
+    return max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
+
+
+def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
+                   vocab_sorting: bool = True, perm: torch.Tensor | None = None):
+    """Bounded-memory forward of the training path: (lse_local, correct, StreamState).
+
+    indexed_matmul + lse_forward (kernels.py:204-319) over the backward's tiles (compacted rows,
+    the reference's vocabulary order) with the per-row tile maxima the decision needs, run over
+    vocabulary groups: each group's classifier rows are gathered into one small buffer (24 MB) and
+    swept with plain TMA tiles; the groups' (lse, correct) partials merge with the log-add-exp of
+    the vocab-parallel path (kernels.py:121-137).  E is read in place (through the compaction map
+    when rows are ignored).  Transients: the group buffer, the tile maxima, O(N + V) maps."""
+    lib = _lib.load()
+    n, d = e.shape
+    v = c.shape[0]
+    dev = e.device
+    row_map, n_valid, perm, perm_padded, pos, mean_logits, inv_perm = prepare_order(
+        e, c, targets, ignore_index, vocab_start, vocab_sorting, perm, with_inverse=True)
+    sorted_ = vocab_sorting or perm is not None
+    nt = max(1, -(-n // BLOCK_TOKENS))
+    mt = -(-v // BLOCK_VOCAB)
+    tile_max = torch.empty(nt * mt * BLOCK_TOKENS, dtype=torch.float32, device=dev)
+    state = StreamState(e, c, row_map, n_valid, perm if sorted_ else None, perm_padded if sorted_ else None,
+                        inv_perm if sorted_ else None, pos, tile_max, int(vocab_start), float(softcap or 0.0),
+                        mean_logits)
+    if n == 0:
+        z = torch.zeros(0, dtype=torch.float32, device=dev)
+        return z, z.clone(), state
+    gt = fwd_group_tiles(d, mt)
+    groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gt) * BLOCK_VOCAB)) for m0 in range(0, mt, gt)]
+    lse_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
+    corr_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
+    ws_bytes = max(lib.cce_fwd_workspace_bytes(n, d, v1 - v0) for v0, v1 in groups)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    buf = torch.empty(min(v, gt * BLOCK_VOCAB), d, dtype=torch.bfloat16, device=dev) if sorted_ else None
+    stream = _stream(dev)
+    ev = _ev_begin("fwd")
+    for g, (v0, v1) in enumerate(groups):
+        if sorted_:
+            c_g = buf[: v1 - v0]
+            _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(c_g), stream), "cce_gather_rows")
+        else:
+            c_g = c[v0:v1]
+        _lib.check(lib.cce_fwd_group(_p(e), 1, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
+                                     float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]), _p(corr_parts[g]),
+                                     _p(tile_max), stream), "cce_fwd_group")
+    _ev_end("fwd", ev)
+    del ws, buf
+    # the groups are vocabulary shards of this call; the target logit sits in exactly one of them
+    lse_local, _ = merge_shards(lse_parts, corr_parts, targets, ignore_index)
+    return lse_local, corr_parts.sum(0), state
+
+
+def backward_from_stream_state(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
+                               fp32_de: bool = False, de_done=None, label_split: bool = False,
+                               correct=None, want_de: bool = True, want_dc: bool = True):
+    """The streamed backward on a forward_stream state (the caller's E read in place)."""
+    return backward_stream(state.e, True, state.c, state.perm_padded, state.inv_perm, state.row_map, state.n_valid,
+                           state.pos, state.tile_max, lse, upstream, softcap=state.softcap, eps=eps, fp32_de=fp32_de,
+                           de_done=de_done, label_split=label_split, correct=correct, want_de=want_de,
+                           want_dc=want_dc, e_caller=state.e)
 
 
 def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: int,
@@ -768,6 +865,69 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
     _ev_end("bwd", ev)
     LAST_COUNTERS["counters"] = counters
     LAST_OVERFLOW["flag"] = overflow
+    return de, dc, counters
+
+
+STREAM_RING_SLOTS = 512  # S-hat ring of the streamed backward (64 KiB slots: 32 MiB)
+
+
+def stream_ring_slots() -> int:
+    return max(128, int(os.environ.get("CCE_STREAM_RING", STREAM_RING_SLOTS)))
+
+
+def stream_supported(d: int) -> bool:
+    """The streamed backward's CTA-pair operand boxes need D % 64 == 0 (every LM head size)."""
+    return d % 64 == 0
+
+
+def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n_valid, pos, tile_max, lse,
+                    upstream, *, softcap: float = 0.0, eps: float = EPSILON_DEFAULT, fp32_de: bool = False,
+                    de_done: torch.cuda.Event | None = None, label_split: bool = False,
+                    correct: torch.Tensor | None = None, want_de: bool = True, want_dc: bool = True,
+                    e_caller: torch.Tensor | None = None):
+    """Streamed backward of the training path (lse_backward, kernels.py:327-486): the decision from
+    the forward's tile maxima, then the kept tiles recomputed in token-tile order (dE) and in
+    vocabulary-tile order (dC), streamed through a fixed ring of S-hat slots.  Transients: the ring
+    (16 MiB), O(N + V) lists and maps, a few MiB of split accumulators -- none grows with the kept
+    count.  With a vocabulary order the sorted classifier lives in dC's own storage.
+    `e_rows` is the caller's E (e_gather) or a compacted copy.  Returns (dE, dC, counters[3])."""
+    lib = _lib.load()
+    n, d = e_rows.shape
+    v = c.shape[0]
+    dev = e_rows.device
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev) if want_de else None
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev) if want_dc else None
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    if n == 0:
+        return de, (dc.zero_() if dc is not None else None), counters
+    if not eps:
+        raise ValueError("backward_stream needs filtering (eps > 0)")
+    c_sorted = None
+    if perm_padded is not None:
+        # the sorted copy lives in dC's storage (dC then lands sorted and moves back in place);
+        # CCE_STREAM_ALIAS=0 gives it its own buffer (A/B and diagnostics)
+        alias = dc is not None and os.environ.get("CCE_STREAM_ALIAS", "1") != "0"
+        c_sorted = dc if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
+    slots = stream_ring_slots()
+    ring = torch.empty(slots * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
+    ws_bytes = lib.cce_bwd_stream_workspace_bytes(n, d, v, slots)
+    ws = (torch.zeros if os.environ.get("CCE_STREAM_ZERO_WS") else torch.empty)(ws_bytes, dtype=torch.uint8, device=dev)
+    ev = _ev_begin("bwd")
+    _lib.check(lib.cce_bwd_stream(_p(e_rows), int(bool(e_gather)), _p(c), _p(c_sorted), _p(perm_padded),
+                                  _p(inv_perm), _p(row_map), _p(n_valid), _p(pos), _p(lse), _p(upstream),
+                                  _p(tile_max), n, d, v, float(softcap or 0.0), float(eps), int(bool(label_split)),
+                                  _p(ring), slots, _p(ws), ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters),
+                                  _event_handle(None if label_split else de_done), _stream(dev)), "cce_bwd_stream")
+    del ws, ring
+    if label_split:
+        label_terms(e_caller if e_caller is not None else e_rows, c, perm_padded, row_map, n_valid, pos, upstream, correct,
+                    softcap, de, dc)
+        if de_done is not None:
+            de_done.record()
+    _ev_end("bwd", ev)
+    LAST_COUNTERS["counters"] = counters
     return de, dc, counters
 
 

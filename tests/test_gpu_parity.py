@@ -31,7 +31,7 @@ def _dev(x, dtype=None):
 # backward: token-grouped filter pass (api.lse_backward) / decision from the forward (training
 # default) / vocabulary-grouped filter pass (filtering off, CCE_LOWMEM_RECOMPUTE=1) / decision from
 # a forward over vocabulary groups (low_memory=True)
-PATHS = ["filter", "tiles", "lowmem", "grouped"]
+PATHS = ["filter", "tiles", "lowmem", "grouped", "stream"]
 
 
 def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sorting=True,
@@ -42,11 +42,12 @@ def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sortin
     cd = _dev(c, torch.bfloat16)
     td = _dev(x.astype(np.int64))
     pd = None if perm is None else _dev(perm.astype(np.int32))
-    tiles = path == "tiles" and bool(eps)
+    stream = path == "stream" and bool(eps) and ops.stream_supported(e.shape[1])
+    tiles = (path == "tiles" or stream) and bool(eps)
     grouped = path == "grouped" and bool(eps)
     if tiles:
         lse_l, corr, st = ops.forward_tiles(ed, cd, td, ignore_index, 0, softcap, vocab_sorting=sorting,
-                                            perm=pd)
+                                            perm=pd, store_labels=not stream)
     elif grouped:
         lse_l, corr, st = ops.forward_grouped(ed, cd, td, ignore_index, 0, softcap, vocab_sorting=sorting,
                                               perm=pd)
@@ -57,7 +58,15 @@ def _run(e, c, x, *, ignore_index=-1, softcap=0.0, eps=O.EPSILON_DEFAULT, sortin
         xx = np.where(x == ignore_index, -1, x)
         upstream = O.default_upstream(xx, "mean-over-valid")
     up = _dev(upstream.astype(np.float32))
-    if tiles:
+    if stream:
+        inv = None
+        if st.perm is not None:
+            inv = torch.empty_like(st.perm)
+            inv[st.perm.long()] = torch.arange(st.perm.shape[0], dtype=torch.int32, device=inv.device)
+        de, dc, cnt = ops.backward_stream(st.e_c, False, cd, st.perm_padded, inv, st.row_map, st.n_valid, st.pos,
+                                          st.tile_max, lse, up, softcap=softcap, eps=eps, e_caller=ed)
+        perm_out = st.perm
+    elif tiles:
         de, dc, cnt = ops.backward_tiles(st, td, lse, up, ignore_index=ignore_index, eps=eps)
         perm_out = st.perm
     elif grouped:
