@@ -269,8 +269,12 @@ __device__ __forceinline__ void gather_box_async(uint8_t* dst, const __nv_bfloat
 
 // Fill a warp's smem index table: tab[r] = index[row0 + r] for r < rows (index == nullptr:
 // row0 + r).  The caller __syncwarp()s before use.
-__device__ __forceinline__ void load_index_table(int32_t* tab, const int32_t* index, int row0, int rows) {
-  for (int r = threadIdx.x & 31; r < rows; r += 32) tab[r] = index ? index[row0 + r] : row0 + r;
+// Rows at or past `limit` (a CTA pair's missing partner tile, rows past the compacted count) read
+// source row 0 instead: their results are discarded, and the index array may end there.
+__device__ __forceinline__ void load_index_table(int32_t* tab, const int32_t* index, int row0, int rows,
+                                                 int limit = 0x7fffffff) {
+  for (int r = threadIdx.x & 31; r < rows; r += 32)
+    tab[r] = row0 + r >= limit ? 0 : (index ? index[row0 + r] : row0 + r);
 }
 
 // softcap: z' = cap * tanh(z / cap), tanh(x) = 1 - 2 / (exp(2x) + 1) (exact limits at +-inf)

@@ -637,7 +637,7 @@ __device__ __forceinline__ void dc_body(const CUtensorMap& tmS, const CUtensorMa
       auto tile = [&](int ln, int slot, int sig = -1) {
         const int n = p.n_base + ln;
         if (gather_pair) {
-          load_index_table(s_eidx, p.row_map, n * BM, BM);
+          load_index_table(s_eidx, p.row_map, n * BM, BM, rows.n);
           __syncwarp();
         }
         for (int h = 0; h < 2; ++h) {
