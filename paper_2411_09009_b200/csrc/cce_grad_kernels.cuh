@@ -402,11 +402,11 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
         nsplit = sx.x;
         split = sg.w;
         if (nsplit > 1) {
-          // CH = 1: one 256-column chunk per unit, region (acc slot, chunk j)
-          gen_key = (sx.y % p.nacc) * p.ndc + j;
-          chain_key = ln * p.ndc + j;
-          // region [64 column quads][128 rows] of float4: a warp's 32 rows read 512 contiguous bytes
-          float* region = p.acc + (size_t)gen_key * BM * DCH + row * 4;
+          // region (acc slot, chunk group j) of DE_CH * 256 columns, laid out [column quads][128
+          // rows] of float4: a warp's 32 rows read 512 contiguous bytes
+          gen_key = (sx.y % p.nacc) * npair + j;
+          chain_key = ln * npair + j;
+          float* region = p.acc + (size_t)gen_key * BM * (DE_CH * DCH) + row * 4;
           racc = split > 0 ? region : nullptr;
           wacc = split < nsplit - 1 ? region : nullptr;
           if (epi_tid == 0) {

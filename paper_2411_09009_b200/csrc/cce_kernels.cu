@@ -1438,7 +1438,7 @@ StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring
   w.gen_c = reinterpret_cast<int*>(take(nacc * ndc * 2 * 4));
   w.ctrl_bytes = o - c0;
   w.perm_cap = (int)(v / cce::PERM_K * 3 / 2 + 1024);
-  const size_t acc_e = (size_t)nt * ndc * cce::BM * cce::DCH * 4;
+  const size_t acc_e = (size_t)nt * ((ndc + 1) & ~1) * cce::BM * cce::DCH * 4;  // 512-column units round up
   const size_t acc_c = (size_t)nacc * ndc * 2 * cce::BM * cce::DCH * 4;
   const size_t perm_bytes = (size_t)w.perm_cap * d * 2;
   uint8_t* accs = take(std::max(acc_e + acc_c, perm_bytes));
@@ -1548,23 +1548,30 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   }
 
   if (getenv("CCE_STREAM_LISTS_ONLY")) return 0;  // diagnostics: the lists alone
+  // dE consumers: two double-buffered 256-column accumulators fed by 64-row stages (default) or one
+  // 512-column accumulator fed by 32-row stages (CCE_STREAM_DE=2; measured 7.8 vs 7.3 ms backward at
+  // Gemma-2-2B)
+  const int de_ch = env_int("CCE_STREAM_DE", 1) == 2 ? 2 : 1;
+  const int de_kv = de_ch == 2 ? 32 : 64;
   CUtensorMap tmE, tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h;
   const bool ok = make_tmap(&tmE, E, n, d, cce::BM) && make_tmap(&tmC128, C_t, v, d, cce::BN / 2) &&
-                  make_tmap3d_inner(&tmSe, ring, (int64_t)R * cce::BM, cce::BN, 64, cce::BM, 1) &&
-                  make_tmap(&tmCk, C_t, v, d, cce::DE_KV) && make_tmap3d(&tmC3, C_t, v, d, cce::DE_KV, cce::DCH / 64) &&
+                  make_tmap3d_inner(&tmSe, ring, (int64_t)R * cce::BM, cce::BN, de_kv, cce::BM, 1) &&
+                  make_tmap(&tmCk, C_t, v, d, de_kv) && make_tmap3d(&tmC3, C_t, v, d, de_kv, cce::DCH / 64) &&
                   make_tmap3d(&tmSc, ring, (int64_t)R * cce::BM, cce::BN, 64, 2) && make_tmap(&tmE64, E, n, d, 64) &&
                   make_tmap3d(&tmE3h, E, n, d, 64, cce::DCH / 128);
   if (!ok) return fail("cce_bwd_stream: cuTensorMapEncodeTiled failed");
 
   // roles: producers and dC consumers as CTA pairs, dE consumers single (about a third each)
   const int grid = sms & ~1;
-  int P = env_int("CCE_STREAM_P", ((grid / 3) + 1) & ~1);
-  int Qc = dc ? env_int("CCE_STREAM_QC", ((grid / 3) + 1) & ~1) : 0;
+  // measured at Gemma-2-2B (148 SMs): 36 / 50 / 62 beats the even split (14.9 vs 15.6 ms per step)
+  int P = env_int("CCE_STREAM_P", (grid * 36 / 148 + 1) & ~1);
+  int Qc = dc ? env_int("CCE_STREAM_QC", (grid * 50 / 148 + 1) & ~1) : 0;
   P = std::max(2, P & ~1);
   Qc = dc ? std::max(2, Qc & ~1) : 0;
   if (!de_out) Qc = grid - P;
   if (P + Qc > grid - (de_out ? 1 : 0)) return fail("cce_bwd_stream: CCE_STREAM_P + CCE_STREAM_QC leave no dE CTAs");
-  const int consumers = (dc ? ndc : 0) + (de_out ? ndc : 0);
+  // consumptions per item: one per dC pair-unit (D chunk) and one per dE unit (group of de_ch chunks)
+  const int consumers = (dc ? ndc : 0) + (de_out ? (ndc + de_ch - 1) / de_ch : 0);
   const cce::Stream st{R, w.ready, w.used, consumers, P};
 
   cce::Params p{};
@@ -1640,12 +1647,20 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
     fprintf(stderr, "cce_bwd_stream: grid %d P %d Qc %d ring %d window %d consumers %d | ready %p used %p "
             "chain_e %p chain_c %p gen_e %p gen_c %p ctrl %p\n", grid, P, Qc, R, W, consumers, (void*)w.ready,
             (void*)w.used, (void*)w.chain_e, (void*)w.chain_c, (void*)w.gen_e, (void*)w.gen_c, (void*)w.ctrl);
-  constexpr size_t smem = std::max({kLsePairSmem, kDcSmem, de_smem<1, 64>()});
-  if (int e = ensure_attr(cce::cce_stream3_kernel, smem)) return e;
   PdlScope spdl(!(pdl_mask & 2));
-  if (int e = launch_k(cce::cce_stream3_kernel, dim3(grid), dim3(cce::NUM_THREADS), smem, stream, 2, tmE, tmC128,
-                       tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h, p, qe, qc, Qc))
-    return e;
+  if (de_ch == 2) {
+    constexpr size_t smem = std::max({kLsePairSmem, kDcSmem, de_smem<2, 32>()});
+    if (int e = ensure_attr(cce::cce_stream3_kernel<2, 32>, smem)) return e;
+    if (int e = launch_k(cce::cce_stream3_kernel<2, 32>, dim3(grid), dim3(cce::NUM_THREADS), smem, stream, 2, tmE,
+                         tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h, p, qe, qc, Qc))
+      return e;
+  } else {
+    constexpr size_t smem = std::max({kLsePairSmem, kDcSmem, de_smem<1, 64>()});
+    if (int e = ensure_attr(cce::cce_stream3_kernel<1, 64>, smem)) return e;
+    if (int e = launch_k(cce::cce_stream3_kernel<1, 64>, dim3(grid), dim3(cce::NUM_THREADS), smem, stream, 2, tmE,
+                         tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h, p, qe, qc, Qc))
+      return e;
+  }
   if (de_done_event) CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
   if (sorted_out)
     if (int e = unpermute_rows(static_cast<__nv_bfloat16*>(dc), perm_padded, inv_perm, v, d, w, stream)) return e;

@@ -282,7 +282,9 @@ __global__ void __launch_bounds__(256) window_fill_kernel(const int2* __restrict
 }
 
 // Single vocabulary-major pass: CTAs [0, P) recompute (CTA pairs), [P, P + Qc) contract dC (CTA
-// pairs), the rest contract dE (single CTAs) -- every kept tile is recomputed once and read by both.
+// pairs), the rest contract dE (single CTAs; DE_CH 256-column chunks per unit, KV vocab rows per
+// stage) -- every kept tile is recomputed once and read by both.
+template <int DE_CH, int KV>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cce_stream3_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
                        const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmCk,
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else if (b < P + qc_ctas)
     dc_body<2>(tmSc, tmE64, tmE3, tmE64, qc, smem, b - P, qc_ctas);
   else
-    de_body<1, 64>(tmSe, tmCk, tmC3, tmCk, qe, smem, b - P - qc_ctas, (int)gridDim.x - P - qc_ctas);
+    de_body<DE_CH, KV>(tmSe, tmCk, tmC3, tmCk, qe, smem, b - P - qc_ctas, (int)gridDim.x - P - qc_ctas);
 }
 
 // The pass kernel: producers (KEPT recompute into the ring) are CTAs [0, producers), consumers the

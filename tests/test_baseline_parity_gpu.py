@@ -47,13 +47,17 @@ def _gpu(e, c, t, cap, path):
     from paper_2411_09009_b200 import ops
 
     ed, cd, td = e.cuda(), c.cuda(), t.cuda()
-    fwd = {"tiles": ops.forward_tiles, "grouped": ops.forward_grouped}[path]
+    fwd = {"stream": ops.forward_stream, "tiles": ops.forward_tiles, "grouped": ops.forward_grouped}[path]
     lse_l, corr, st = fwd(ed, cd, td, -100, 0, cap)
     lse, loss = ops.merge_shards(lse_l[None], corr[None], td, -100)
     nv = int((t != -100).sum())
     up = torch.where(td != -100, 1.0 / nv, 0.0).float()
-    bwd = {"tiles": ops.backward_tiles, "grouped": ops.backward_grouped}[path]
-    de, dc, cnt = bwd(st, td, lse, up, ignore_index=-100)
+    if path == "stream":  # the training default (memory="bounded")
+        ops.LAST_OVERFLOW["flag"] = torch.zeros(1, dtype=torch.int32)
+        de, dc, cnt = ops.backward_from_stream_state(st, lse, up)
+    else:
+        bwd = {"tiles": ops.backward_tiles, "grouped": ops.backward_grouped}[path]
+        de, dc, cnt = bwd(st, td, lse, up, ignore_index=-100)
     torch.cuda.synchronize()
     return dict(loss=loss.cpu().numpy(), lse=lse.cpu().numpy(), de=de.float().cpu().numpy(),
                 dc=dc.float().cpu().numpy(), cnt=cnt.cpu().numpy(), perm=st.perm.cpu().numpy(),
@@ -86,8 +90,7 @@ def _check_backward(got, ref_de, ref_dc, st, label):
 def test_gemma2b_full_size_filtered_vs_oracle(cuda_device, monkeypatch):
     n, d, v = 8192, 2304, 256000
     e, c, t = _inputs(n, d, v, seed=0)
-    base = _gpu(e, c, t, 0.0, "tiles")
-    assert base["overflow"] == 0
+    base = _gpu(e, c, t, 0.0, "stream")  # the default training path
     # forward: loss / lse against an fp32 torch reference of the same bf16 inputs (f64 logits
     # would need 33 GB), and against the f64 oracle on a 256-row subset
     ed, cd = e.cuda().float(), c.cuda().float()
@@ -101,7 +104,10 @@ def test_gemma2b_full_size_filtered_vs_oracle(cuda_device, monkeypatch):
     assert np.max(np.abs(base["loss"][sub] - nl)) <= LOSS_TOL * max(1.0, np.max(np.abs(nl)))
     # backward: the oracle's lse_backward with the GPU's order, tile geometry and lse
     ref_de, ref_dc, st = _oracle_backward(e, c, t, base["lse"], base["perm"], 0.0)
-    _check_backward(base, ref_de, ref_dc, st, "gemma2-2b default")
+    _check_backward(base, ref_de, ref_dc, st, "gemma2-2b default (bounded)")
+    fast = _gpu(e, c, t, 0.0, "tiles")
+    assert fast["overflow"] == 0 and np.array_equal(fast["perm"], base["perm"])
+    _check_backward(fast, ref_de, ref_dc, st, "gemma2-2b memory=fast")
     # the S-hat overflow fallback at the same shape: a budget below the kept tiles' S-hat
     monkeypatch.setenv("CCE_SHAT_BUDGET_MB", "96")
     small = _gpu(e, c, t, 0.0, "tiles")
@@ -129,7 +135,7 @@ def test_token_subset_at_baseline_shape(cuda_device, name):
     nl, nlse, _ = O.naive_forward(e.float().numpy(), c.float().numpy(), x, softcap=cap)
     valid = x != -1
     ref = None
-    for path in ("tiles", "grouped"):
+    for path in ("stream", "tiles", "grouped"):
         got = _gpu(e, c, t, cap, path)
         assert np.max(np.abs(got["loss"] - nl)) <= LOSS_TOL * max(1.0, np.max(np.abs(nl))), (name, path)
         assert np.max(np.abs(got["lse"][valid] - nlse[valid])) <= LOSS_TOL * np.max(np.abs(nlse[valid]))
