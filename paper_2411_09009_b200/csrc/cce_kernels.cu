@@ -1357,6 +1357,10 @@ int env_int(const char* name, int dflt) {
 }
 int stream_seg_voc() { return env_int("CCE_STREAM_SEG_VOC", 64); }
 int stream_nacc() { return env_int("CCE_STREAM_NACC", 4); }
+// dE consumers: two double-buffered 256-column accumulators fed by 64-row stages (default) or one
+// 512-column accumulator fed by 32-row stages (CCE_STREAM_DE=2; measured 7.8 vs 7.3 ms backward at
+// Gemma-2-2B)
+int stream_de_ch() { return env_int("CCE_STREAM_DE", 1) == 2 ? 2 : 1; }
 int stream_window(int64_t ring) { return (int)std::min<int64_t>(ring - 1, env_int("CCE_STREAM_WINDOW", (int)(ring / 2))); }
 
 struct StreamWs {
@@ -1438,7 +1442,8 @@ StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring
   w.gen_c = reinterpret_cast<int*>(take(nacc * ndc * 2 * 4));
   w.ctrl_bytes = o - c0;
   w.perm_cap = (int)(v / cce::PERM_K * 3 / 2 + 1024);
-  const size_t acc_e = (size_t)nt * ((ndc + 1) & ~1) * cce::BM * cce::DCH * 4;  // 512-column units round up
+  const int64_t dch = stream_de_ch();
+  const size_t acc_e = (size_t)nt * ((ndc + dch - 1) / dch * dch) * cce::BM * cce::DCH * 4;
   const size_t acc_c = (size_t)nacc * ndc * 2 * cce::BM * cce::DCH * 4;
   const size_t perm_bytes = (size_t)w.perm_cap * d * 2;
   uint8_t* accs = take(std::max(acc_e + acc_c, perm_bytes));
@@ -1548,10 +1553,7 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   }
 
   if (getenv("CCE_STREAM_LISTS_ONLY")) return 0;  // diagnostics: the lists alone
-  // dE consumers: two double-buffered 256-column accumulators fed by 64-row stages (default) or one
-  // 512-column accumulator fed by 32-row stages (CCE_STREAM_DE=2; measured 7.8 vs 7.3 ms backward at
-  // Gemma-2-2B)
-  const int de_ch = env_int("CCE_STREAM_DE", 1) == 2 ? 2 : 1;
+  const int de_ch = stream_de_ch();
   const int de_kv = de_ch == 2 ? 32 : 64;
   CUtensorMap tmE, tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h;
   const bool ok = make_tmap(&tmE, E, n, d, cce::BM) && make_tmap(&tmC128, C_t, v, d, cce::BN / 2) &&

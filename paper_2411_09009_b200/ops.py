@@ -769,9 +769,11 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
             _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(c_g), stream), "cce_gather_rows")
         else:
             c_g = c[v0:v1]
+        evk = _ev_begin("fwd_kernel")  # the logit-tile launches alone (bench roofline)
         _lib.check(lib.cce_fwd_group(_p(e), 1, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
                                      float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]), _p(corr_parts[g]),
                                      _p(tile_max), stream), "cce_fwd_group")
+        _ev_end("fwd_kernel", evk)
     _ev_end("fwd", ev)
     del ws, buf
     # the groups are vocabulary shards of this call; the target logit sits in exactly one of them

@@ -1,0 +1,85 @@
+"""Transient-memory regression bound of the training default (memory="bounded").
+
+The reference pins its loss-path transients (instrument.py:3-10: peak allocation minus inputs and
+outputs) with a recorded formula, 4 * (8 (N + V) + 8 threads (n_b m_b + d_b (n_b + m_b)))
+(/root/reference/pkg/tests/test_instrument.py:93-111).  The B200 path's transients are, per
+ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu):
+
+  forward   per-row tile maxima  ceil(N/128) * ceil(V/256) * 512 B
+            one vocabulary group of sorted classifier rows (CCE_FWD_GROUP_MB, 24 MiB)
+            O(N + V) maps and partials
+  backward  the S-hat ring (512 slots x 64 KiB = 32 MiB)
+            split-owner accumulators: ceil(N/128) * ceil(D/256) * 128 KiB (fp32 dE partial sums
+            across stream windows) + 4 * ceil(D/256) * 256 KiB (vocab tiles over several segments)
+            the tile maxima, O(N + V) maps and O(ceil(N/128) * ceil(V/256)) lists
+
+No term depends on how many tiles the filter keeps: the test runs each head at two logit scales
+whose kept-tile counts differ several-fold and requires the same peak.
+"""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MIB = 1 << 20
+
+
+def _budget(n, d, v):
+    nt, mt, ndc = -(-n // 128), -(-v // 256), -(-d // 256)
+    tile_max = nt * mt * 128 * 4
+    lists = nt * mt * 72 + (n + v) * 64  # keep flags, item lists, segments, windows; O(N + V) maps
+    fwd = tile_max + 24 * MIB + lists + 2 * MIB
+    acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
+    step = 512 * 64 * 1024 + acc + tile_max + lists + 4 * MIB
+    return fwd, step
+
+
+def _step(n, d, v, sigma, seed=0, pad=0.0):
+    from paper_2411_09009_b200 import linear_cross_entropy, ops
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    e = torch.randn(n, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    c = (torch.randn(v, d, device="cuda", generator=g) * sigma / math.sqrt(d)).bfloat16().requires_grad_(True)
+    t = torch.randint(0, v, (n,), device="cuda", generator=g)
+    if pad:
+        t[torch.rand(n, device="cuda", generator=g) < pad] = -100
+    linear_cross_entropy(e, c, t).backward()  # warm-up (tensor maps, allocator)
+    e.grad = c.grad = None
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    loss = linear_cross_entropy(e, c, t)
+    torch.cuda.synchronize()
+    fwd_peak = torch.cuda.max_memory_allocated() - base
+    loss.backward()
+    torch.cuda.synchronize()
+    grads = e.grad.numel() * e.grad.element_size() + c.grad.numel() * c.grad.element_size()
+    step_peak = torch.cuda.max_memory_allocated() - base - grads
+    kept = int(ops.LAST_COUNTERS["counters"][0])
+    return fwd_peak, step_peak, kept
+
+
+@pytest.mark.parametrize("n,d,v", [(8192, 2304, 256000), (4096, 768, 50257), (2048, 4096, 128256)])
+def test_training_transients_bounded_and_independent_of_kept_tiles(cuda_device, n, d, v):
+    fwd_budget, step_budget = _budget(n, d, v)
+    f1, s1, k1 = _step(n, d, v, sigma=1.0)
+    f3, s3, k3 = _step(n, d, v, sigma=4.0)
+    print(f"N={n} D={d} V={v}: kept {k1} / {k3} tiles, forward peak {f1 / MIB:.1f} / {f3 / MIB:.1f} MiB "
+          f"(budget {fwd_budget / MIB:.1f}), step peak {s1 / MIB:.1f} / {s3 / MIB:.1f} MiB "
+          f"(budget {step_budget / MIB:.1f})")
+    assert k3 > 1.5 * k1  # the two logit scales keep very different tile counts ...
+    for f, s in ((f1, s1), (f3, s3)):
+        assert f <= fwd_budget and s <= step_budget
+    assert abs(s3 - s1) <= 2 * MIB and abs(f3 - f1) <= 2 * MIB  # ... and the same transients
+
+
+def test_padded_batch_does_not_copy_e(cuda_device):
+    """Ignored rows are compacted by index (the kernels read E through the compaction map): a
+    25%-padded batch has the same transients as an unpadded one."""
+    n, d, v = 4096, 2304, 128256
+    _, s0, _ = _step(n, d, v, sigma=1.0)
+    _, s1, _ = _step(n, d, v, sigma=1.0, pad=0.25)
+    assert s1 <= s0 + 2 * MIB, (s0, s1)
