@@ -231,6 +231,12 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
                    size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
                    void* de_done_event, void* stream);
 
+/* diagnostics / tests: the in-place row unpermutation the streamed backward applies to dC when it
+ * lands in the sorted order: X[perm[p]] <- X[p] for p < v, X bf16 [v][d] (d % 8 == 0), inv the
+ * inverse permutation; ws of cce_bwd_stream_workspace_bytes(1, d, v, 512) bytes */
+int cce_unpermute_rows(void* X, const int32_t* perm, const int32_t* inv, int64_t v, int64_t d, void* ws,
+                       size_t ws_bytes, void* stream);
+
 /* ---- paper ordering (label_split = 1 in cce_bwd_kept / cce_bwd_lowmem) ----
  * PAPER.md Alg. 3 filters tiles on S alone, before the one-hot subtraction;
  * the reference instead never skips a tile holding a label (kernels.py:447-455).

@@ -1393,6 +1393,11 @@ struct StreamWs {
                       // afterwards the row-permutation scratch (with acc_e)
   uint8_t* perm_cls;
   int32_t* perm_bidx;
+  int32_t* perm_blist;
+  int32_t* perm_own;   // [v] member -> owner break position
+  int32_t* perm_seg;   // [cap][PERM_SEG] segment positions
+  int* perm_len;       // [cap]
+  int32_t* perm_rlist; // [v / 2 + 1] rotation owners
   int perm_cap;
   int max_windows;
   size_t total;
@@ -1441,7 +1446,8 @@ StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring
   w.gen_e = reinterpret_cast<int*>(take(nt * ndc * 4));
   w.gen_c = reinterpret_cast<int*>(take(nacc * ndc * 2 * 4));
   w.ctrl_bytes = o - c0;
-  w.perm_cap = (int)(v / cce::PERM_K * 3 / 2 + 1024);
+  // breaks: anchors (~v / PERM_K) + cut points (at most v / PERM_SEG), with headroom
+  w.perm_cap = (int)(v / cce::PERM_K * 5 / 4 + v / cce::PERM_SEG + 1024);
   const int64_t dch = stream_de_ch();
   const size_t acc_e = (size_t)nt * ((ndc + dch - 1) / dch * dch) * cce::BM * cce::DCH * 4;
   const size_t acc_c = (size_t)nacc * ndc * 2 * cce::BM * cce::DCH * 4;
@@ -1451,6 +1457,11 @@ StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring
   w.acc_c = reinterpret_cast<float*>(accs ? accs + acc_e : nullptr);
   w.perm_cls = take(v);
   w.perm_bidx = reinterpret_cast<int32_t*>(take(v * 4));
+  w.perm_blist = reinterpret_cast<int32_t*>(take((size_t)w.perm_cap * 4));
+  w.perm_own = reinterpret_cast<int32_t*>(take(v * 4));
+  w.perm_seg = reinterpret_cast<int32_t*>(take((size_t)w.perm_cap * cce::PERM_SEG * 4));
+  w.perm_len = reinterpret_cast<int*>(take((size_t)w.perm_cap * 4));
+  w.perm_rlist = reinterpret_cast<int32_t*>(take((size_t)(v / 2 + 1) * 4));
   w.max_windows = (int)maxw;
   w.total = o;
   return w;
@@ -1460,13 +1471,25 @@ StreamWs stream_layout(void* base, int64_t n, int64_t d, int64_t v, int64_t ring
 int unpermute_rows(__nv_bfloat16* X, const int32_t* perm, const int32_t* inv, int64_t v, int64_t d, const StreamWs& w,
                    cudaStream_t stream) {
   __nv_bfloat16* tmp = reinterpret_cast<__nv_bfloat16*>(w.acc_e);
+  // Without programmatic dependent launch: under PDL the walk saw stale chain tables (kernels two
+  // and more launches back; test_unpermute_rows_in_place fails with it, passes with CCE_PDL=0 or
+  // CUDA_LAUNCH_BLOCKING=1), as the window kernels of the pass did.  Six launch gaps.
+  PdlScope nopdl(false);
+  PDL_LAUNCH(cce::zero_words_kernel, dim3(32), dim3(256), 0, stream, w.perm_len, (int64_t)w.perm_cap);
   PDL_LAUNCH(cce::unpermute_classify_kernel, dim3((unsigned)((v + 255) / 256)), dim3(256), 0, stream, perm, (int)v,
-             w.perm_cls, w.perm_bidx, w.ctrl + 4, w.perm_cap);
-  PDL_LAUNCH(cce::unpermute_save_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
-             static_cast<const __nv_bfloat16*>(X), (int)v, (int)d, (const uint8_t*)w.perm_cls,
-             (const int32_t*)w.perm_bidx, tmp);
-  PDL_LAUNCH(cce::unpermute_walk_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream, X, (int)v, (int)d, inv,
-             (const uint8_t*)w.perm_cls, (const int32_t*)w.perm_bidx, (const __nv_bfloat16*)tmp);
+             w.perm_cls, w.perm_bidx, w.perm_own, w.perm_blist, w.ctrl + 4, w.perm_cap, w.perm_rlist, w.ctrl + 6);
+  PDL_LAUNCH(cce::unpermute_chains_kernel, dim3((unsigned)((v + 255) / 256)), dim3(256), 0, stream, (int)v,
+             (const uint8_t*)w.perm_cls, (const int32_t*)w.perm_bidx, (const int32_t*)w.perm_own, w.perm_seg,
+             w.perm_len);
+  // warps per (break, column block); the break count is on the device, the grid covers the cap
+  const dim3 grid((unsigned)((w.perm_cap + 7) / 8), (unsigned)((d + cce::PERM_COLS - 1) / cce::PERM_COLS));
+  PDL_LAUNCH(cce::unpermute_save_kernel, grid, dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(X), (int)d,
+             (const int32_t*)w.perm_blist, (const int*)(w.ctrl + 4), tmp);
+  PDL_LAUNCH(cce::unpermute_walk_kernel, grid, dim3(256), 0, stream, X, (int)d, inv, (const int32_t*)w.perm_bidx,
+             (const int32_t*)w.perm_blist, (const int32_t*)w.perm_seg, (const int*)w.perm_len,
+             (const int*)(w.ctrl + 4), (const __nv_bfloat16*)tmp);
+  PDL_LAUNCH(cce::unpermute_rotate_kernel, dim3((unsigned)num_sms(), grid.y), dim3(256), 0, stream, X, (int)d, inv,
+             (const int32_t*)w.perm_rlist, (const int*)(w.ctrl + 6));
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1488,6 +1511,19 @@ int cce_bwd_stream_debug_layout(int64_t n, int64_t d, int64_t v, int64_t ring_sl
   return stream_window(ring_slots);
 }
 
+// Diagnostics / tests: the streamed backward's in-place row unpermutation alone, X[perm[p]] <- X[p]
+// (bf16 [v, d]); ws from cce_bwd_stream_workspace_bytes(1, d, v, 512).
+int cce_unpermute_rows(void* X, const int32_t* perm, const int32_t* inv, int64_t v, int64_t d, void* ws,
+                       size_t ws_bytes, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (d % 8 != 0) return fail("cce_unpermute_rows: D must be a multiple of 8");
+  const StreamWs w = stream_layout(ws, 1, d, v, 512);
+  if (ws_bytes < w.total) return fail("cce_unpermute_rows: workspace too small");
+  PdlScope pdl_scope(true);
+  PDL_LAUNCH(cce::zero_words_kernel, dim3(64), dim3(256), 0, stream, w.ctrl, (int64_t)(w.ctrl_bytes / 4));
+  return unpermute_rows(static_cast<__nv_bfloat16*>(X), perm, inv, v, d, w, stream);
+}
+
 int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
                    const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
                    const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d, int64_t v,
@@ -1499,7 +1535,7 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   if (!(eps > 0.f)) return fail("cce_bwd_stream: needs filtering (eps > 0)");
   if (!ring || ring_slots < 2 * stream_seg_voc()) return fail("cce_bwd_stream: ring_slots too small");
   if (de_out == nullptr && dc == nullptr) return fail("cce_bwd_stream: neither dE nor dC requested");
-  if (perm_padded && (!c_sorted || !inv_perm)) return fail("cce_bwd_stream: vocabulary order needs c_sorted, inv_perm");
+  if (perm_padded && c_sorted && !inv_perm) return fail("cce_bwd_stream: a sorted copy needs inv_perm");
   if (d % 64 != 0) return fail("cce_bwd_stream: D must be a multiple of 64 (CTA-pair operand boxes)");
   if (n <= 0) return 0;
   const int nt = (int)((n + cce::BM - 1) / cce::BM);
@@ -1514,9 +1550,12 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   if (sms < 6) return fail("cce_bwd_stream: needs at least 6 SMs");
   PdlScope pdl_scope(true);
 
-  // sorted classifier: C[perm] into c_sorted (dC's own storage when dc == c_sorted)
+  // sorted classifier: C[perm] into c_sorted (dC's own storage when dc == c_sorted), or, with no
+  // c_sorted, C rows gathered through the order inside the pass (cp.async in the recompute CTAs,
+  // TMA gather4 in the dE CTAs) and dC scattered to vocabulary order by its epilogue
   const void* C_t = C;
-  if (perm_padded) {
+  const bool c_gather = perm_padded && !c_sorted;
+  if (perm_padded && c_sorted) {
     PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
                static_cast<const __nv_bfloat16*>(C), (const int32_t*)perm_padded, (int)v, (int)d,
                static_cast<__nv_bfloat16*>(c_sorted));
@@ -1553,12 +1592,13 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   }
 
   if (getenv("CCE_STREAM_LISTS_ONLY")) return 0;  // diagnostics: the lists alone
-  const int de_ch = stream_de_ch();
+  const int de_ch = c_gather ? 1 : stream_de_ch();  // row gathers need 64-row boxes
   const int de_kv = de_ch == 2 ? 32 : 64;
   CUtensorMap tmE, tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h;
   const bool ok = make_tmap(&tmE, E, n, d, cce::BM) && make_tmap(&tmC128, C_t, v, d, cce::BN / 2) &&
                   make_tmap3d_inner(&tmSe, ring, (int64_t)R * cce::BM, cce::BN, de_kv, cce::BM, 1) &&
-                  make_tmap(&tmCk, C_t, v, d, de_kv) && make_tmap3d(&tmC3, C_t, v, d, de_kv, cce::DCH / 64) &&
+                  (c_gather ? make_tmap(&tmCk, C, v, d, 1) : make_tmap(&tmCk, C_t, v, d, de_kv)) &&
+                  make_tmap3d(&tmC3, C_t, v, d, de_kv, cce::DCH / 64) &&
                   make_tmap3d(&tmSc, ring, (int64_t)R * cce::BM, cce::BN, 64, 2) && make_tmap(&tmE64, E, n, d, 64) &&
                   make_tmap3d(&tmE3h, E, n, d, 64, cce::DCH / 128);
   if (!ok) return fail("cce_bwd_stream: cuTensorMapEncodeTiled failed");
@@ -1596,6 +1636,10 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   p.eps = eps;
   p.label_split = label_split;
   p.shat = static_cast<__nv_bfloat16*>(ring);
+  if (c_gather) {
+    p.perm = perm_padded;
+    p.c_rows = static_cast<const __nv_bfloat16*>(C);
+  }
   p.counters = counters;
   p.list = w.items;
   p.list_count = w.ctrl + 0;
@@ -1616,7 +1660,8 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   q.atoms3d = 1;
   q.st = st;
   q.items = w.items;
-  cce::GradParams qe = q;  // dE: segments (window, token tile) through sidx, accumulator id = token tile
+  cce::GradParams qe = q;
+  if (c_gather) qe.perm = perm_padded;  // dE: C rows through the order (gather4 boxes)  // dE: segments (window, token tile) through sidx, accumulator id = token tile
   qe.seg = w.eseg;
   qe.seg_aux = w.eaux;
   qe.seg_count = w.ctrl + 3;
@@ -1637,7 +1682,7 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   qc.nacc = stream_nacc();
   qc.acc_gen = w.gen_c;
   if (const char* pf = getenv("CCE_STREAM_PROF_PTR")) qe.prof = reinterpret_cast<unsigned long long*>(strtoull(pf, nullptr, 0));
-  const bool sorted_out = perm_padded && dc == c_sorted;  // dC lands in the sorted order, then moves
+  const bool sorted_out = perm_padded && c_sorted && dc == c_sorted;  // dC lands in the sorted order, then moves
   qc.dc = static_cast<__nv_bfloat16*>(dc);
   qc.perm_store = sorted_out ? nullptr : perm_padded;
   if (sorted_out && de_out) {  // dE consumers read the rows dC overwrites

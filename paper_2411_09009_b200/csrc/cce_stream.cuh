@@ -331,144 +331,205 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // ---------------------------------------------------------------------------------------------
 // In-place row permutation: rows X[p] (sorted position p) move to row perm[p] (vocabulary order).
-// Position t receives X[inv[t]].  Cycles are cut at break points: anchors (a hash of the position
-// selects 1 in K) in a cycle of length >= 2, plus any position whose forward walk meets no anchor
-// within L steps.  Each break's row is saved to tmp first, then one warp per break walks its segment
-// backwards (X[t] = X[inv[t]]) until the predecessor is a break (X[t] = tmp[its index]).  Cycles
-// without an anchor (short ones) are rotated by the warp of their smallest position with the row
-// held in registers.  More breaks than tmp rows (cap) trap: it needs an adversarial permutation.
-// class: 0 fixed point / member of a cut or rotated cycle, 1 break, 2 rotation owner.
+// Position t receives X[inv[t]].
+//  * A cycle of length <= PERM_SEG without an anchor (a hash of the position selects 1 in PERM_K)
+//    is rotated by the warps of its smallest position (rotation list), the first row held in
+//    registers.
+//  * Every other cycle is cut into segments at break points: its anchors (or, with none, its
+//    smallest position) and every position whose distance along perm to the next of those is a
+//    multiple of PERM_SEG.  The segment of break b is dest_0 = b, dest_r = inv^r(b) for r < len;
+//    the last move's source is the next break, whose row was saved to tmp.
+// Kernels:
+//   classify  thread per position: walks perm forward to the next anchor (or around the cycle);
+//             a break takes a break-list entry k, a rotation owner a rotation entry, a member
+//             records its owner break and its distance r (1 <= r < PERM_SEG) to it
+//   chains    thread per member: seg[k][r - 1] = p, len[k] = max r -- the segment positions
+//             written out, so the row moves of a segment need no pointer chasing
+//   save      warp per (break, column block): tmp[k] = X[b]
+//   walk      warp per (break, column block): X[dest_r] = X[dest_r+1] (last: tmp of the next
+//             break), PERM_DEPTH moves per batch with every load of a batch before its stores
+//   rotate    warp per (rotation, column block), grid-stride over the rotation list
+// Segments, rotations and column blocks are independent, so every warp runs in parallel.  More
+// breaks than tmp rows (cap) trap; the cap covers every permutation (anchors + cuts).
 // ---------------------------------------------------------------------------------------------
 constexpr int PERM_K = 64;      // anchor density 1 / PERM_K
-constexpr int PERM_SEG = 96;    // longest segment (a walk of dependent row moves): a break every
-                                // PERM_SEG positions between anchors
-constexpr int PERM_L = 8192;
+constexpr int PERM_SEG = 96;    // longest segment: positions per break entry of the chain table
+constexpr int PERM_L = 8192;    // a walk this long without an anchor makes the position a break
+constexpr int PERM_VEC = 1;     // uint4 per lane of a column block: 256 columns per warp
+constexpr int PERM_COLS = 32 * 8 * PERM_VEC;
+constexpr int PERM_DEPTH = 8;   // row moves whose loads are in flight together
 __device__ __forceinline__ bool perm_anchor(int p) { return ((uint32_t)p * 2654435761u) >> 26 == 0; }  // 1 in 64
 
+// cls: 0 fixed point or rotation member / owner, 1 break, 2 + (r - 1) member at distance r of its owner (own[p] = owner
+// position); breaks: bidx[b] = k, blist[k] = b
 __global__ void unpermute_classify_kernel(const int32_t* __restrict__ perm, int v, uint8_t* __restrict__ cls,
-                                          int32_t* __restrict__ bidx, int* __restrict__ nbreak, int cap) {
+                                          int32_t* __restrict__ bidx, int32_t* __restrict__ own,
+                                          int32_t* __restrict__ blist, int* __restrict__ nbreak, int cap,
+                                          int32_t* __restrict__ rlist, int* __restrict__ nrot) {
   griddep_wait();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= v) return;
-  uint8_t c = 0;
-  if (perm[p] != p) {
+  int c = 0, dist = 0;  // c: 0 fixed, 1 break, 2 member at distance `dist` of the next cut point
+  int q = perm[p];
+  if (q != p) {
     if (perm_anchor(p)) {
       c = 1;
     } else {
-      int q = perm[p], mn = p, steps = 1;
+      int mn = p, steps = 1, smn = 0;
       bool found = false;
       while (q != p && steps < PERM_L) {
         if (perm_anchor(q)) {
           found = true;
           break;
         }
-        mn = min(mn, q);
+        if (q < mn) {
+          mn = q;
+          smn = steps;
+        }
         q = perm[q];
         ++steps;
       }
-      if (!found)
-        c = (q == p) ? (mn == p ? 2 : 0) : 1;  // short cycle: its owner rotates it
-      else if (steps % PERM_SEG == 0)
-        c = 1;  // bounds the walk between two anchors far apart
+      if (found) {
+        dist = steps;        // the next anchor
+      } else if (q == p && steps <= PERM_SEG) {
+        c = mn == p ? 3 : 4;  // a short anchorless cycle: rotated by its smallest position
+      } else {
+        dist = q == p ? smn : 0;  // a long anchorless cycle: cut at its smallest position;
+      }                           // no anchor within PERM_L: a break
+      if (c == 0) c = (dist % PERM_SEG == 0) ? 1 : 2;
     }
   }
-  cls[p] = c;
-  if (c == 1) {
-    const int k = atomicAdd(nbreak, 1);
-    if (k >= cap) __trap();
-    bidx[p] = k;
-  }
-}
-
-// Copy one row (d bf16) with a warp: every load of a 2048-column block is issued before any store,
-// so a chain of dependent row moves costs one memory round trip per row, not one per 16 bytes.
-__device__ __forceinline__ void warp_copy_row(__nv_bfloat16* dst, const __nv_bfloat16* src, int d) {
-  const int lane = threadIdx.x & 31;
-  for (int c0 = 0; c0 < d; c0 += 2048) {
-    uint4 r[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int col = c0 + (k * 32 + lane) * 8;
-      if (col < d) r[k] = __ldcg(reinterpret_cast<const uint4*>(src + col));
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int col = c0 + (k * 32 + lane) * 8;
-      if (col < d) *reinterpret_cast<uint4*>(dst + col) = r[k];
-    }
-  }
-}
-
-// warp per break: save its row
-__global__ void unpermute_save_kernel(const __nv_bfloat16* __restrict__ X, int v, int d,
-                                      const uint8_t* __restrict__ cls, const int32_t* __restrict__ bidx,
-                                      __nv_bfloat16* __restrict__ tmp) {
-  griddep_wait();
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p >= v || cls[p] != 1) return;
-  warp_copy_row(tmp + (size_t)bidx[p] * d, X + (size_t)p * d, d);
-}
-
-// warp per break (segment walk) or rotation owner (whole short cycle, row in registers)
-constexpr int PERM_REG_VEC = 4;  // uint4 per lane held in registers: rows up to 32*8*4 = 1024 columns per pass
-__global__ void unpermute_walk_kernel(__nv_bfloat16* __restrict__ X, int v, int d, const int32_t* __restrict__ inv,
-                                      const uint8_t* __restrict__ cls, const int32_t* __restrict__ bidx,
-                                      const __nv_bfloat16* __restrict__ tmp) {
-  griddep_wait();
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p >= v) return;
-  const uint8_t c = cls[p];
-  const int lane = threadIdx.x & 31;
-  if (c == 1) {
-    int t = p;
-    int s = inv[t];
-    bool brk = cls[s] == 1;
-    for (int steps = 0; steps <= v; ++steps) {
-      if (brk) {
-        warp_copy_row(X + (size_t)t * d, tmp + (size_t)bidx[s] * d, d);
-        return;
-      }
-      // the next hop's index loads are independent of this row's move: issue them first
-      const int s2 = inv[s];
-      const bool brk2 = cls[s2] == 1;
-      warp_copy_row(X + (size_t)t * d, X + (size_t)s * d, d);
-      __syncwarp();
-      t = s;
-      s = s2;
-      brk = brk2;
-    }
+  if (c >= 3) {
+    cls[p] = 0;  // members of a rotation need no chain entry
+    if (c == 3) rlist[atomicAdd(nrot, 1)] = p;
   } else if (c == 2) {
-    // rotate the cycle column block by column block: X[t] = X[inv[t]] around the cycle, the
-    // owner's own block held in registers
-    for (int c0 = 0; c0 < d; c0 += 32 * 8 * PERM_REG_VEC) {
-      uint4 keep[PERM_REG_VEC];
+    const int r = (dist - 1) % PERM_SEG + 1;  // the nearest cut point forward
+    int o = p;
+    for (int i = 0; i < r; ++i) o = perm[o];
+    own[p] = o;
+    cls[p] = (uint8_t)(1 + r);
+  } else {
+    cls[p] = (uint8_t)c;
+    if (c == 1) {
+      const int k = atomicAdd(nbreak, 1);
+      if (k >= cap) __trap();
+      bidx[p] = k;
+      blist[k] = p;
+    }
+  }
+}
+
+// thread per member: its place in the owner's chain (lens zeroed beforehand)
+__global__ void unpermute_chains_kernel(int v, const uint8_t* __restrict__ cls, const int32_t* __restrict__ bidx,
+                                        const int32_t* __restrict__ own, int32_t* __restrict__ seg,
+                                        int* __restrict__ lens) {
+  griddep_wait();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= v) return;
+  const int c = cls[p];
+  if (c < 2) return;
+  const int r = c - 1;
+  const int k = bidx[own[p]];
+  seg[(size_t)k * PERM_SEG + r - 1] = p;
+  atomicMax(&lens[k], r);
+}
+
+// warp per (break entry, column block): save the break's row block to tmp
+__global__ void unpermute_save_kernel(const __nv_bfloat16* __restrict__ X, int d, const int32_t* __restrict__ blist,
+                                      const int* __restrict__ nbreak, __nv_bfloat16* __restrict__ tmp) {
+  griddep_wait();
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= *nbreak) return;
+  const int lane = threadIdx.x & 31;
+  const int p = blist[k];
 #pragma unroll
-      for (int k = 0; k < PERM_REG_VEC; ++k) {
-        const int col = c0 + (k * 32 + lane) * 8;
-        if (col < d) keep[k] = __ldcg(reinterpret_cast<const uint4*>(X + (size_t)p * d + col));
-      }
-      int t = p;
-      while (true) {
-        const int s = inv[t];
-        if (s == p) {
+  for (int i = 0; i < PERM_VEC; ++i) {
+    const int col = blockIdx.y * PERM_COLS + (i * 32 + lane) * 8;
+    if (col < d)
+      *reinterpret_cast<uint4*>(tmp + (size_t)k * d + col) = __ldcg(reinterpret_cast<const uint4*>(X + (size_t)p * d + col));
+  }
+}
+
+// 16-byte global load ordered against the walker's stores (the compiler may not move either)
+__device__ __forceinline__ uint4 ld_cg_ordered(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr)
+               : "memory");
+  return r;
+}
+
+// warp per (break entry, column block): the moves of the break's segment
+__global__ void __launch_bounds__(256) unpermute_walk_kernel(__nv_bfloat16* X, int d, const int32_t* __restrict__ inv,
+                                                             const int32_t* __restrict__ bidx,
+                                                             const int32_t* __restrict__ blist,
+                                                             const int32_t* __restrict__ seg,
+                                                             const int* __restrict__ lens,
+                                                             const int* __restrict__ nbreak,
+                                                             const __nv_bfloat16* __restrict__ tmp) {
+  griddep_wait();
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= *nbreak) return;
+  const int lane = threadIdx.x & 31;
+  const int len = lens[k] + 1;  // moves: dest_0 = the break, dest_1 .. dest_{len-1} its members
+  // dest_r of r = lane + 32 j (PERM_SEG <= 96: three per lane)
+  int dst[3];
 #pragma unroll
-          for (int k = 0; k < PERM_REG_VEC; ++k) {
-            const int col = c0 + (k * 32 + lane) * 8;
-            if (col < d) *reinterpret_cast<uint4*>(X + (size_t)t * d + col) = keep[k];
-          }
-          break;
-        }
+  for (int j = 0; j < 3; ++j) {
+    const int r = lane + 32 * j;
+    dst[j] = r == 0 ? blist[k] : (r < len ? seg[(size_t)k * PERM_SEG + r - 1] : 0);
+  }
+  const int last = __shfl_sync(0xffffffffu, dst[(len - 1) >> 5], (len - 1) & 31);
+  const int tail = bidx[inv[last]];  // the last move's source: the next break's saved row
+  const int col = blockIdx.y * PERM_COLS + lane * 8;
+  const bool on = col < d;
+  for (int r0 = 0; r0 < len; r0 += PERM_DEPTH) {
+    uint4 val[PERM_DEPTH][PERM_VEC];
 #pragma unroll
-        for (int k = 0; k < PERM_REG_VEC; ++k) {
-          const int col = c0 + (k * 32 + lane) * 8;
-          if (col < d)
-            *reinterpret_cast<uint4*>(X + (size_t)t * d + col) =
-                __ldcg(reinterpret_cast<const uint4*>(X + (size_t)s * d + col));
-        }
-        __syncwarp();
-        t = s;
+    for (int j = 0; j < PERM_DEPTH; ++j) {
+      const int r = r0 + j;
+      const int s = r + 1;  // source of move r: dest_{r+1}
+      const int sp = __shfl_sync(0xffffffffu, s < 96 ? dst[s >> 5] : 0, s & 31);
+      if (r < len && on) {
+        const __nv_bfloat16* row = s < len ? X + (size_t)sp * d : tmp + (size_t)tail * d;
+#pragma unroll
+        for (int i = 0; i < PERM_VEC; ++i)
+          if (col + i * 256 < d) val[j][i] = ld_cg_ordered(row + col + i * 256);
       }
     }
+#pragma unroll
+    for (int j = 0; j < PERM_DEPTH; ++j) {
+      const int r = r0 + j;
+      const int dp = __shfl_sync(0xffffffffu, dst[(r >> 5) < 3 ? (r >> 5) : 2], r & 31);
+      if (r < len && on) {
+#pragma unroll
+        for (int i = 0; i < PERM_VEC; ++i)
+          if (col + i * 256 < d) *reinterpret_cast<uint4*>(X + (size_t)dp * d + col + i * 256) = val[j][i];
+      }
+    }
+  }
+}
+
+// warp per (rotation, column block), grid-stride over the rotation list: X[t] = X[inv[t]] around
+// a short cycle, the owner's own row block kept in registers
+__global__ void __launch_bounds__(256) unpermute_rotate_kernel(__nv_bfloat16* X, int d, const int32_t* __restrict__ inv,
+                                                               const int32_t* __restrict__ rlist,
+                                                               const int* __restrict__ nrot) {
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.y * PERM_COLS + lane * 8;
+  const bool on = col < d;
+  const int total = *nrot;
+  for (int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < total; k += gridDim.x * (blockDim.x >> 5)) {
+    const int p = rlist[k];
+    uint4 keep = on ? ld_cg_ordered(X + (size_t)p * d + col) : make_uint4(0, 0, 0, 0);
+    int t = p;
+    for (int s = inv[t]; s != p; s = inv[s]) {
+      if (on) *reinterpret_cast<uint4*>(X + (size_t)t * d + col) = ld_cg_ordered(X + (size_t)s * d + col);
+      t = s;
+    }
+    if (on) *reinterpret_cast<uint4*>(X + (size_t)t * d + col) = keep;
   }
 }
 

@@ -61,8 +61,11 @@ def _global_vocab(v_local: int, group) -> int:
 
 class _LinearCrossEntropy(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, e, c, targets, ignore_index, softcap, reduction, eps, vocab_sorting, group,
+    def forward(ctx, e, c, targets, t_shard, ignore_index, softcap, reduction, eps, vocab_sorting, group,
                 vocab_start, memory, exempt_label_tiles, training, v_total):
+        # targets: the caller's labels (ignore mask, label-range check, upstream); t_shard: the same
+        # labels in this shard's row coordinates (the kernels' targets; == targets unless the shard
+        # is block-cyclic, see vocab_parallel.cyclic_rows)
         # Training with filtering: the forward sweeps the backward's tiles (compacted rows, sorted
         # vocabulary) and records per-row tile maxima, so the backward recomputes kept tiles only.
         # low_memory / no filtering / inference: plain forward, only O(N) state survives to the
@@ -73,26 +76,26 @@ class _LinearCrossEntropy(torch.autograd.Function):
         ctx.state = None
         if eps > 0 and memory == "bounded" and training:
             # default: vocabulary-grouped forward into the per-row tile maxima, streamed backward
-            lse_local, correct, ctx.state = ops.forward_stream(e, c, targets, ignore_index, vocab_start, softcap,
+            lse_local, correct, ctx.state = ops.forward_stream(e, c, t_shard, ignore_index, vocab_start, softcap,
                                                                vocab_sorting)
         elif eps > 0 and memory == "fast" and training:
-            lse_local, correct, ctx.state = ops.forward_tiles(e, c, targets, ignore_index, vocab_start,
+            lse_local, correct, ctx.state = ops.forward_tiles(e, c, t_shard, ignore_index, vocab_start,
                                                               softcap, vocab_sorting, eps=eps,
                                                               label_split=not exempt_label_tiles)
         elif eps > 0 and memory == "grouped" and training and os.environ.get("CCE_LOWMEM_RECOMPUTE", "0") == "0":
             # bounded memory: the same decision from the forward, over vocabulary groups
-            lse_local, correct, ctx.state = ops.forward_grouped(e, c, targets, ignore_index, vocab_start,
+            lse_local, correct, ctx.state = ops.forward_grouped(e, c, t_shard, ignore_index, vocab_start,
                                                                 softcap, vocab_sorting, eps=eps,
                                                                 label_split=not exempt_label_tiles)
         else:
-            lse_local, correct = ops.forward_local(e, c, targets, ignore_index, vocab_start, softcap)
+            lse_local, correct = ops.forward_local(e, c, t_shard, ignore_index, vocab_start, softcap)
         if group is None:
             lse, loss = ops.merge_shards(lse_local[None], correct[None], targets, ignore_index, v_total)
         else:
             from .vocab_parallel import gather_and_merge
 
             lse, loss = gather_and_merge(lse_local, correct, targets, ignore_index, group, v_total)
-        ctx.save_for_backward(e, c, targets, lse)
+        ctx.save_for_backward(e, c, targets, t_shard, lse)
         ctx.cfg = (ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start)
         # paper ordering: the label term is applied apart from the filtered tiles and needs the
         # forward's (softcapped) target logit of the rows whose label this shard owns (O(N): kept
@@ -107,7 +110,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, grad_out):
-        e, c, targets, lse = ctx.saved_tensors
+        e, c, targets, t_shard, lse = ctx.saved_tensors
         ignore_index, softcap, reduction, eps, vocab_sorting, group, vocab_start = ctx.cfg
         up = ops.upstream(grad_out, targets, ignore_index, reduction)  # default_upstream, core.py:181-200
         ctx.backwards += 1
@@ -130,7 +133,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 de = all_reduce_de_overlapped(de, done, group)
         elif isinstance(state, ops.GroupState):
             done = ops.recorded_event() if group is not None else None
-            de, dc, _ = ops.backward_grouped(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+            de, dc, _ = ops.backward_grouped(state, t_shard, lse, up, ignore_index=ignore_index, eps=eps,
                                              fp32_de=group is not None, de_done=done, label_split=split,
                                              correct=correct, **want)
             del state
@@ -140,21 +143,21 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 de = all_reduce_de_overlapped(de, done, group)
         elif state is not None:
             if group is None:
-                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                de, dc, _ = ops.backward_tiles(state, t_shard, lse, up, ignore_index=ignore_index, eps=eps,
                                                label_split=split, correct=correct, **want)
             else:
                 from .vocab_parallel import all_reduce_de_overlapped
 
                 # dE is complete before the dC pass: its all-reduce runs on a side stream meanwhile
                 done = ops.recorded_event()
-                de, dc, _ = ops.backward_tiles(state, targets, lse, up, ignore_index=ignore_index, eps=eps,
+                de, dc, _ = ops.backward_tiles(state, t_shard, lse, up, ignore_index=ignore_index, eps=eps,
                                                fp32_de=True, de_done=done, label_split=split, correct=correct,
                                                **want)
                 if de is not None:
                     de = all_reduce_de_overlapped(de, done, group)
             del state
         else:  # low_memory=True or filtering off: vocabulary-grouped backward, bounded transients
-            de, dc, _, _ = ops.backward_lowmem(e, c, targets, lse, up, ignore_index=ignore_index,
+            de, dc, _, _ = ops.backward_lowmem(e, c, t_shard, lse, up, ignore_index=ignore_index,
                                                vocab_start=vocab_start, softcap=softcap, eps=eps,
                                                vocab_sorting=vocab_sorting, fp32_de=group is not None,
                                                label_split=split, correct=correct)
@@ -162,7 +165,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 from .vocab_parallel import all_reduce_de
 
                 de = all_reduce_de(de, group)
-        return de, dc, None, None, None, None, None, None, None, None, None, None, None, None
+        return de, dc, None, None, None, None, None, None, None, None, None, None, None, None, None
 
 
 def linear_cross_entropy(
@@ -179,6 +182,7 @@ def linear_cross_entropy(
     low_memory: bool = False,
     exempt_label_tiles: bool = True,
     memory: str | None = None,
+    vocab_rows: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Cross-entropy of softmax(e @ c.T) against targets without materialising the logits.
 
@@ -199,6 +203,11 @@ def linear_cross_entropy(
                  sized from the learned kept density; with filter_eps=None, or
                  CCE_LOWMEM_RECOMPUTE=1, only O(N) state is kept and the backward recomputes every tile
     CCE_MEMORY overrides the default.
+
+    vocab_rows (vocab-parallel, instead of vocab_start): the global vocabulary ids of `c`'s rows,
+    for shards that are not one contiguous range -- e.g. vocab_parallel.cyclic_rows, which deals
+    256-row blocks round-robin so that a frequency-ordered vocabulary (BPE ids) spreads its dense
+    head over every rank.  The labels are mapped to shard coordinates on the device.
 
     exempt_label_tiles=True is the reference's filter (a tile holding a label is never skipped,
     kernels.py:447-455).  False is the paper's Alg. 3 ordering: tiles are filtered on the softmax
@@ -228,6 +237,15 @@ def linear_cross_entropy(
         for name, x in (("embeddings", e2), ("classifier", c)):  # core.py:47
             if not bool(torch.isfinite(x).all()):
                 raise ValueError(f"{name} contains non-finite entries")
+    t_shard = t2
+    if vocab_rows is not None:
+        if vocab_start:
+            raise ValueError("pass vocab_rows or vocab_start, not both")
+        if vocab_rows.shape != (c.shape[0],):
+            raise ValueError(f"vocab_rows has shape {tuple(vocab_rows.shape)}, expected ({c.shape[0]},)")
+        if 0 <= ignore_index <= c.shape[0]:
+            raise ValueError("vocab_rows needs an ignore_index outside [0, shard rows]")
+        t_shard = ops.shard_targets(t2, vocab_rows.to(e2.device), v_total, int(ignore_index))
     cap = float(softcap) if softcap else 0.0
     if cap < 0:
         raise ValueError("softcap must be positive")
@@ -238,7 +256,7 @@ def linear_cross_entropy(
         raise ValueError(f"memory must be 'bounded', 'fast' or 'grouped', got {mode!r}")
     if mode == "bounded" and not (ops.stream_supported(e2.shape[1]) and e2.shape[0] <= 2048 * ops.BLOCK_TOKENS):
         mode = "fast"  # the streamed backward's CTA-pair boxes need D % 64 == 0
-    out = _LinearCrossEntropy.apply(e2, c, t2, int(ignore_index), cap, reduction, eps,
+    out = _LinearCrossEntropy.apply(e2, c, t2, t_shard, int(ignore_index), cap, reduction, eps,
                                     bool(vocab_sorting), process_group, int(vocab_start),
                                     mode, bool(exempt_label_tiles), training, int(v_total))
     if reduction == "none":

@@ -205,6 +205,19 @@ def raise_label_error(dev: torch.device, v_total: int, wait: bool = False) -> No
                          "call, whose loss is NaN at those rows)")
 
 
+def shard_targets(targets: torch.Tensor, vocab_rows: torch.Tensor, v_total: int, ignore_index: int) -> torch.Tensor:
+    """Labels in the coordinates of a shard holding global rows `vocab_rows` (local row k holds
+    global id vocab_rows[k]): an owned label becomes its local row, any other label the first row
+    past the shard (owned by another rank, as a label outside [vocab_start, vocab_start + V) is
+    for a contiguous shard), ignore_index stays.  On the device, O(N + V), no host read.  Labels
+    outside [0, v_total) are caught by merge_shards on the caller's targets."""
+    v_loc = vocab_rows.shape[0]
+    lut = torch.full((v_total + 1,), v_loc, dtype=torch.int64, device=targets.device)
+    lut[vocab_rows.to(torch.int64)] = torch.arange(v_loc, device=targets.device)
+    local = lut[targets.clamp(0, v_total)]
+    return torch.where(targets == ignore_index, targets, local).contiguous()
+
+
 def indexed_dot(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0):
     """out[i] = C[x_i] . E[i], 0 at ignored rows (indexed_matmul, kernels.py:204-251)."""
     lib = _lib.load()
@@ -907,9 +920,10 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
     if not eps:
         raise ValueError("backward_stream needs filtering (eps > 0)")
     c_sorted = None
-    if perm_padded is not None:
+    if perm_padded is not None and os.environ.get("CCE_STREAM_GATHER", "0") == "0":
         # the sorted copy lives in dC's storage (dC then lands sorted and moves back in place);
-        # CCE_STREAM_ALIAS=0 gives it its own buffer (A/B and diagnostics)
+        # CCE_STREAM_ALIAS=0 gives it its own buffer (A/B and diagnostics).  CCE_STREAM_GATHER=1:
+        # no sorted copy, the pass gathers C rows through the order and scatters dC rows
         alias = dc is not None and os.environ.get("CCE_STREAM_ALIAS", "1") != "0"
         c_sorted = dc if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
     slots = stream_ring_slots()

@@ -28,6 +28,18 @@ def shard_range(vocab: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < rem else 0)
 
 
+CYCLIC_BLOCK = 256  # rows per block of the block-cyclic layout: one vocabulary tile
+
+
+def cyclic_rows(vocab: int, rank: int, world: int, block: int = CYCLIC_BLOCK) -> torch.Tensor:
+    """Global vocabulary ids of `rank`'s rows in the block-cyclic layout: blocks
+    of `block` consecutive ids are dealt round-robin, block b to rank b % world.  A vocabulary
+    whose ids follow frequency (BPE merges) puts its dense head on every rank instead of rank 0;
+    pass the result as linear_cross_entropy(vocab_rows=...) with c = C[rows]."""
+    ids = torch.arange(vocab, dtype=torch.int64)
+    return ids[(ids // block) % world == rank]
+
+
 def gather_and_merge(lse_local, correct, targets, ignore_index, group, v_total: int = 0):
     world = dist.get_world_size(group)
     n = lse_local.shape[0]

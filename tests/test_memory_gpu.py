@@ -65,8 +65,8 @@ def _step(n, d, v, sigma, seed=0, pad=0.0):
 @pytest.mark.parametrize("n,d,v", [(8192, 2304, 256000), (4096, 768, 50257), (2048, 4096, 128256)])
 def test_training_transients_bounded_and_independent_of_kept_tiles(cuda_device, n, d, v):
     fwd_budget, step_budget = _budget(n, d, v)
-    f1, s1, k1 = _step(n, d, v, sigma=1.0)
-    f3, s3, k3 = _step(n, d, v, sigma=4.0)
+    f1, s1, k1 = _step(n, d, v, sigma=0.25)  # label tiles only
+    f3, s3, k3 = _step(n, d, v, sigma=4.0)   # most tiles kept
     print(f"N={n} D={d} V={v}: kept {k1} / {k3} tiles, forward peak {f1 / MIB:.1f} / {f3 / MIB:.1f} MiB "
           f"(budget {fwd_budget / MIB:.1f}), step peak {s1 / MIB:.1f} / {s3 / MIB:.1f} MiB "
           f"(budget {step_budget / MIB:.1f})")

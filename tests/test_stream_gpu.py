@@ -115,3 +115,54 @@ def test_stream_backward_paper_ordering(cuda_device):
     de, dc, cnt, rde, rdc, rcnt = _stream_run(e, c, t, label_split=True)
     assert torch.equal(cnt, rcnt)
     assert _rel(de, rde) < 8e-3 and _rel(dc, rdc) < 8e-3
+
+
+@pytest.mark.parametrize("n,d,v,ign,cap,sigma", [
+    (300, 64, 1000, 0.0, 0.0, 1.0),
+    (1000, 192, 5003, 0.3, 0.0, 2.0),
+    (777, 128, 20000, 0.1, 30.0, 3.0),
+    (4096, 768, 50257, 0.25, 0.0, 1.0),
+])
+def test_stream_gather_mode_bit_identical(cuda_device, monkeypatch, n, d, v, ign, cap, sigma):
+    """CCE_STREAM_GATHER=1: no sorted classifier copy -- the recompute CTAs gather C rows through the
+    order with cp.async, the dE CTAs with TMA gather4, and dC rows are scattered to vocabulary order
+    by the dC epilogue (no in-place unpermute).  Same operands, same order: bit-identical."""
+    e, c, t = _head(n, d, v, 3 * n + d, sigma=sigma, ign=ign)
+    base = _stream_run(e, c, t, softcap=cap)[:3]
+    monkeypatch.setenv("CCE_STREAM_GATHER", "1")
+    got = _stream_run(e, c, t, softcap=cap)[:3]
+    for a, b in zip(got, base):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("v,d,kind", [(1000, 64, "random"), (5003, 192, "random"), (256000, 2304, "random"),
+                                      (3000, 128, "identity"), (3000, 128, "shift"), (4096, 256, "swaps"),
+                                      (2000, 520, "random")])
+def test_unpermute_rows_in_place(cuda_device, v, d, kind):
+    """The in-place unpermutation of dC (cycle segments cut at anchors, chain tables, batched row
+    moves per column block) equals an out-of-place index copy, for random permutations (one giant
+    cycle plus small ones), the identity, one long anchor-free shift and many 2-cycles."""
+    from paper_2411_09009_b200 import _lib, ops
+
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(v + d)
+    if kind == "random":
+        perm = torch.randperm(v, device="cuda", generator=g)
+    elif kind == "identity":
+        perm = torch.arange(v, device="cuda")
+    elif kind == "shift":
+        perm = (torch.arange(v, device="cuda") + 1) % v
+    else:
+        perm = torch.arange(v, device="cuda").view(-1, 2).flip(1).reshape(-1)
+    perm = perm.to(torch.int32)
+    inv = torch.empty_like(perm)
+    inv[perm.long()] = torch.arange(v, dtype=torch.int32, device="cuda")
+    x = torch.randn(v, d, device="cuda", generator=g).bfloat16()
+    want = torch.empty_like(x)
+    want[perm.long()] = x
+    ws_bytes = lib.cce_bwd_stream_workspace_bytes(1, d, v, 512)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.cce_unpermute_rows(ops._p(x), ops._p(perm), ops._p(inv), v, d, ops._p(ws), ws_bytes,
+                                      ops._stream(x.device)), "cce_unpermute_rows")
+    torch.cuda.synchronize()
+    assert torch.equal(x, want)

@@ -122,3 +122,27 @@ def test_shard_range_partitions_vocab():
             assert spans[0][0] == 0 and spans[-1][1] == v
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def test_cyclic_rows_partition_and_shard_targets():
+    """Block-cyclic layout: the ranks' row sets partition the vocabulary; shard_targets maps an
+    owned label to its shard row, any other label past the shard, and keeps ignore_index."""
+    import torch
+
+    from paper_2411_09009_b200 import ops
+    from paper_2411_09009_b200.vocab_parallel import cyclic_rows
+
+    v, world = 5001, 3
+    rows = [cyclic_rows(v, r, world, block=256) for r in range(world)]
+    allr = torch.cat(rows).sort().values
+    assert torch.equal(allr, torch.arange(v))
+    t = torch.tensor([0, 255, 256, 767, 768, 5000, -100])
+    for r in range(world):
+        loc = ops.shard_targets(t, rows[r], v, -100)
+        for g, l in zip(t.tolist(), loc.tolist()):
+            if g == -100:
+                assert l == -100
+            elif (g // 256) % world == r:
+                assert rows[r][l] == g
+            else:
+                assert l == rows[r].shape[0]

@@ -202,3 +202,109 @@ def test_token_parallel_two_ranks(cuda_device):
     de = np.concatenate([r[2] for r in res])
     assert O.rel_err(de, fde) < 2e-2
     assert O.rel_err(res[0][3] + res[1][3], fdc) < 2e-2
+
+
+def _cyclic_worker(rank, world, port, q, n, d, v, layout, zipf):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_09009_b200 import linear_cross_entropy, ops
+        from paper_2411_09009_b200.vocab_parallel import cyclic_rows, shard_range
+
+        if zipf:
+            e_all, c_all, t = _zipf_by_id(n, d, v)
+        else:
+            e_np, c_np, x_np = _inputs(n, d, v)
+            e_all, c_all, t = torch.from_numpy(e_np).cuda().bfloat16(), torch.from_numpy(c_np).cuda().bfloat16(), \
+                torch.from_numpy(x_np).cuda()
+        if layout == "cyclic":
+            rows = cyclic_rows(v, rank, world)
+            kw = dict(vocab_rows=rows)
+        else:
+            v0, v1 = shard_range(v, rank, world)
+            rows = torch.arange(v0, v1)
+            kw = dict(vocab_start=v0)
+        e = e_all.clone().requires_grad_(True)
+        c = c_all[rows.cuda()].clone().requires_grad_(True)
+        loss = linear_cross_entropy(e, c, t, process_group=dist.group.WORLD, **kw)
+        loss.backward()
+        torch.cuda.synchronize()
+        kept = int(ops.LAST_COUNTERS["counters"][0])
+        q.put((rank, float(loss.item()), e.grad.float().cpu().numpy(), c.grad.float().cpu().numpy(),
+               rows.numpy(), kept))
+    finally:
+        dist.destroy_process_group()
+
+
+def _zipf_by_id(n, d, v, alpha=4.0):
+    """Token frequency falling with the id (a BPE vocabulary): a shared unit direction carries the
+    logit bias -log(id + 1); targets sampled from the softmax (Gumbel-max)."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    e = torch.randn(n, d, device="cuda", generator=g)
+    c = torch.randn(v, d, device="cuda", generator=g) / math.sqrt(d)
+    u = torch.randn(d, device="cuda", generator=g)
+    u = u / u.norm()
+    b = -torch.log(torch.arange(v, device="cuda", dtype=torch.float32) + 1.0)
+    b = b - b.mean()
+    e = (e + alpha * u).bfloat16()
+    c = (c + (b / alpha)[:, None] * u).bfloat16()
+    z = e.float() @ c.float().T
+    gum = -torch.log(-torch.log(torch.rand(z.shape, device="cuda", generator=g).clamp_min(1e-20)))
+    t = (z + gum).argmax(dim=1)
+    return e, c, t
+
+
+def _run_world(target, world, *args):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_block_cyclic_shards_match_oracle(cuda_device):
+    """Block-cyclic vocabulary shards (vocab_parallel.cyclic_rows, linear_cross_entropy(vocab_rows=))
+    give the single-device loss and gradients: labels mapped to shard rows on the device, dC rows
+    scattered back through the shard's row ids."""
+    world, n, d, v = 2, 600, 128, 5001
+    res = _run_world(_cyclic_worker, world, n, d, v, "cyclic", False)
+    e_np, c_np, x_np = _inputs(n, d, v)
+    xo = np.where(x_np == -100, -1, x_np)
+    nl, _, _ = O.naive_forward(e_np, c_np, xo)
+    ref_loss = float(nl[xo != -1].mean())
+    fde, fdc = O.naive_backward(e_np, c_np, xo, O.default_upstream(xo, "mean-over-valid"))
+    dc = np.zeros_like(fdc)
+    for rank, loss, de, dc_r, rows, _ in res:
+        assert abs(loss - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (rank, loss, ref_loss)
+        assert O.rel_err(de, fde) < 2e-2, rank
+        dc[rows] = dc_r
+    assert np.array_equal(res[0][2], res[1][2])
+    assert O.rel_err(dc, fdc) < 2e-2
+
+
+def test_block_cyclic_balances_a_frequency_ordered_vocabulary(cuda_device):
+    """with token frequency falling with the id, contiguous shards put the dense
+    head -- the kept tiles of the backward -- on rank 0; block-cyclic shards spread it (max / mean
+    kept tiles <= 1.2).  Both layouts give the same loss."""
+    world, n, d, v = 2, 4096, 256, 32768
+    out = {}
+    for layout in ("contiguous", "cyclic"):
+        res = _run_world(_cyclic_worker, world, n, d, v, layout, True)
+        kept = [r[5] for r in res]
+        out[layout] = (res[0][1], kept, max(kept) / (sum(kept) / world))
+    print(f"kept tiles per rank: contiguous {out['contiguous'][1]} (max/mean {out['contiguous'][2]:.2f}), "
+          f"cyclic {out['cyclic'][1]} (max/mean {out['cyclic'][2]:.2f})")
+    assert abs(out["contiguous"][0] - out["cyclic"][0]) <= 1e-3 * abs(out["cyclic"][0])
+    assert out["cyclic"][2] <= 1.2
+    assert out["contiguous"][2] > out["cyclic"][2]
