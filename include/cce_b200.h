@@ -231,6 +231,16 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
                    size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
                    void* de_done_event, void* stream);
 
+/* cce_bwd_stream with flags: bit 0 = c_sorted already holds C[perm] (no gather), bit 1 = add dC
+ * into dc (vocabulary order, bf16 accumulate; dc must not be c_sorted).  Token chunks of a large
+ * batch run one call each over a shared sorted copy (ops.backward_from_stream_state). */
+int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
+                      const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                      const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d,
+                      int64_t v, float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
+                      size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+                      void* de_done_event, int flags, void* stream);
+
 /* diagnostics / tests: the in-place row unpermutation the streamed backward applies to dC when it
  * lands in the sorted order: X[perm[p]] <- X[p] for p < v, X bf16 [v][d] (d % 8 == 0), inv the
  * inverse permutation; ws of cce_bwd_stream_workspace_bytes(1, d, v, 512) bytes */

@@ -61,6 +61,10 @@ SIGNATURES = {
                                c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int,
                                c_void_p, c_i64, c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p,
                                c_void_p, c_void_p]),
+    "cce_bwd_stream_ex": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64, c_f32, c_f32, c_int,
+                                  c_void_p, c_i64, c_void_p, c_size, c_void_p, c_int, c_void_p, c_void_p,
+                                  c_void_p, c_int, c_void_p]),
     "cce_unpermute_rows": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_size, c_void_p]),
     "cce_bwd_kept_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_kept": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64,

@@ -1524,12 +1524,32 @@ int cce_unpermute_rows(void* X, const int32_t* perm, const int32_t* inv, int64_t
   return unpermute_rows(static_cast<__nv_bfloat16*>(X), perm, inv, v, d, w, stream);
 }
 
+int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
+                      const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                      const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d,
+                      int64_t v, float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
+                      size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+                      void* de_done_event, int flags, void* stream_ptr);
+
 int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
                    const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
                    const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d, int64_t v,
                    float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
                    size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
                    void* de_done_event, void* stream_ptr) {
+  return cce_bwd_stream_ex(E, e_gather, C, c_sorted, perm_padded, inv_perm, row_map, n_valid, pos, lse, upstream,
+                           tile_max, n, d, v, softcap, eps, label_split, ring, ring_slots, ws, ws_bytes, de_out,
+                           de_fp32, dc, counters, de_done_event, 0, stream_ptr);
+}
+
+int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted, const int32_t* perm_padded,
+                      const int32_t* inv_perm, const int32_t* row_map, const int* n_valid, const int32_t* pos,
+                      const float* lse, const float* upstream, const float* tile_max, int64_t n, int64_t d,
+                      int64_t v, float softcap, float eps, int label_split, void* ring, int64_t ring_slots, void* ws,
+                      size_t ws_bytes, void* de_out, int de_fp32, void* dc, unsigned long long* counters,
+                      void* de_done_event, int flags, void* stream_ptr) {
+  const bool c_ready = (flags & 1) != 0;      // c_sorted already holds C[perm] (an earlier token chunk)
+  const bool dc_accumulate = (flags & 2) != 0;  // add into dc (vocabulary order) instead of writing it
   cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
   if (d % 8 != 0) return fail("cce_bwd_stream: D must be a multiple of 8");
   if (!(eps > 0.f)) return fail("cce_bwd_stream: needs filtering (eps > 0)");
@@ -1555,10 +1575,12 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   // TMA gather4 in the dE CTAs) and dC scattered to vocabulary order by its epilogue
   const void* C_t = C;
   const bool c_gather = perm_padded && !c_sorted;
+  if (dc_accumulate && (dc == c_sorted || !dc)) return fail("cce_bwd_stream: accumulating dC needs its own buffer");
   if (perm_padded && c_sorted) {
-    PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
-               static_cast<const __nv_bfloat16*>(C), (const int32_t*)perm_padded, (int)v, (int)d,
-               static_cast<__nv_bfloat16*>(c_sorted));
+    if (!c_ready)
+      PDL_LAUNCH(cce::gather_rows_kernel, dim3((unsigned)((v + 7) / 8)), dim3(256), 0, stream,
+                 static_cast<const __nv_bfloat16*>(C), (const int32_t*)perm_padded, (int)v, (int)d,
+                 static_cast<__nv_bfloat16*>(c_sorted));
     C_t = c_sorted;
   }
   // decision (kernels.py:434-455), the stream (vocab-tile-major kept list), its segments
@@ -1673,6 +1695,9 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   qe.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
   qe.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
   if (!de_out) qe.seg_count = w.ctrl + 5;  // zero segments
+  // dE units claimed in order from a counter (CCE_STREAM_DYN=0: static round-robin); same box:
+  // 6.31-6.39 vs 6.49 ms backward at Gemma-2-2B
+  if (getenv("CCE_STREAM_DYN") == nullptr || atoi(getenv("CCE_STREAM_DYN")) != 0) qe.sched = w.ctrl + 7;
   cce::GradParams qc = q;  // dC: segments of vocab tiles (contiguous items)
   qc.seg = w.cseg;
   qc.seg_aux = w.caux;
@@ -1685,6 +1710,7 @@ int cce_bwd_stream(const void* E, int e_gather, const void* C, void* c_sorted, c
   const bool sorted_out = perm_padded && c_sorted && dc == c_sorted;  // dC lands in the sorted order, then moves
   qc.dc = static_cast<__nv_bfloat16*>(dc);
   qc.perm_store = sorted_out ? nullptr : perm_padded;
+  qc.accumulate = dc_accumulate ? 1 : 0;
   if (sorted_out && de_out) {  // dE consumers read the rows dC overwrites
     qc.own_off = w.voc_off;
     qc.own_cnt = w.voc_cnt;

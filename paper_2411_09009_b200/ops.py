@@ -725,10 +725,42 @@ class StreamState:
     vocab_start: int
     softcap: float
     mean_logits: torch.Tensor | None = None
+    e_c: torch.Tensor | None = None  # compacted rows, when the batch is expected to ignore some
 
     def nbytes(self) -> int:
-        own = [self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded, self.inv_perm]
+        own = [self.row_map, self.n_valid, self.pos, self.tile_max, self.perm, self.perm_padded, self.inv_perm,
+               self.e_c]
         return sum(t.numel() * t.element_size() for t in own if t is not None)
+
+
+# Whether the last batch of a shape ignored rows: {(n, d): [pinned n_valid copy, event, n_valid]}.
+_IGNORED_HINT: dict = {}
+
+
+def compact_copy_wanted(n: int, d: int, n_valid: torch.Tensor) -> bool:
+    """The bounded forward reads E in place when no row is ignored, and through the compaction
+    map otherwise.  Row gathers (cp.async) make the forward's E loads request-bound (Llama-3-8B
+    with 25% padding: 30 vs 9 ms), so when rows are ignored the compacted rows are copied once
+    (N_valid x D, the size of E) and read with plain TMA boxes.  Whether they are is known only on
+    the device: the previous call of the same shape decides (its n_valid, read from a pinned copy
+    once its event has completed -- never a host synchronisation); unknown counts as ignored.  A
+    wrong guess only costs time: without the copy the kernels gather through the map."""
+    key = (n, d)
+    hint = _IGNORED_HINT.get(key)
+    wanted = True
+    if hint is not None:
+        if hint[1] is not None and not _capturing() and hint[1].query():
+            hint[2] = int(hint[0][0])
+            hint[1] = None
+        if hint[2] is not None:
+            wanted = hint[2] < n
+    if not _capturing() and (hint is None or hint[1] is None):
+        pinned = hint[0] if hint is not None else torch.empty(1, dtype=torch.int32).pin_memory()
+        pinned.copy_(n_valid, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        _IGNORED_HINT[key] = [pinned, ev, hint[2] if hint is not None else None]
+    return wanted
 
 
 FWD_GROUP_MB = 24  # sorted classifier rows of one vocabulary group in the bounded forward
@@ -761,9 +793,11 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
     nt = max(1, -(-n // BLOCK_TOKENS))
     mt = -(-v // BLOCK_VOCAB)
     tile_max = torch.empty(nt * mt * BLOCK_TOKENS, dtype=torch.float32, device=dev)
+    e_c = gather_rows(e, row_map, n) if n and compact_copy_wanted(n, d, n_valid) else None
     state = StreamState(e, c, row_map, n_valid, perm if sorted_ else None, perm_padded if sorted_ else None,
                         inv_perm if sorted_ else None, pos, tile_max, int(vocab_start), float(softcap or 0.0),
-                        mean_logits)
+                        mean_logits, e_c)
+    e_rows, e_gather = (e_c, 0) if e_c is not None else (e, 1)
     if n == 0:
         z = torch.zeros(0, dtype=torch.float32, device=dev)
         return z, z.clone(), state
@@ -783,7 +817,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
         else:
             c_g = c[v0:v1]
         evk = _ev_begin("fwd_kernel")  # the logit-tile launches alone (bench roofline)
-        _lib.check(lib.cce_fwd_group(_p(e), 1, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
+        _lib.check(lib.cce_fwd_group(_p(e_rows), e_gather, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
                                      float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]), _p(corr_parts[g]),
                                      _p(tile_max), stream), "cce_fwd_group")
         _ev_end("fwd_kernel", evk)
@@ -797,8 +831,15 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
 def backward_from_stream_state(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
                                fp32_de: bool = False, de_done=None, label_split: bool = False,
                                correct=None, want_de: bool = True, want_dc: bool = True):
-    """The streamed backward on a forward_stream state (the caller's E read in place)."""
-    return backward_stream(state.e, True, state.c, state.perm_padded, state.inv_perm, state.row_map, state.n_valid,
+    """The streamed backward on a forward_stream state (the caller's E read in place, or its
+    compacted copy when rows are ignored).  Batches of more than STREAM_CHUNK_TILES token tiles run
+    as token chunks (backward_stream_chunked)."""
+    n = state.e.shape[0]
+    if -(-n // BLOCK_TOKENS) > stream_chunk_tiles():
+        return backward_stream_chunked(state, lse, upstream, eps=eps, fp32_de=fp32_de, de_done=de_done,
+                                       label_split=label_split, correct=correct, want_de=want_de, want_dc=want_dc)
+    e_rows, e_gather = (state.e_c, False) if state.e_c is not None else (state.e, True)
+    return backward_stream(e_rows, e_gather, state.c, state.perm_padded, state.inv_perm, state.row_map, state.n_valid,
                            state.pos, state.tile_max, lse, upstream, softcap=state.softcap, eps=eps, fp32_de=fp32_de,
                            de_done=de_done, label_split=label_split, correct=correct, want_de=want_de,
                            want_dc=want_dc, e_caller=state.e)
@@ -940,6 +981,74 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
     if label_split:
         label_terms(e_caller if e_caller is not None else e_rows, c, perm_padded, row_map, n_valid, pos, upstream, correct,
                     softcap, de, dc)
+        if de_done is not None:
+            de_done.record()
+    _ev_end("bwd", ev)
+    LAST_COUNTERS["counters"] = counters
+    return de, dc, counters
+
+
+STREAM_CHUNK_TILES = 64  # token tiles per streamed pass (windows of 256 items: >= 4 items per dE segment)
+
+
+def stream_chunk_tiles() -> int:
+    return max(1, int(os.environ.get("CCE_STREAM_CHUNK_TILES", STREAM_CHUNK_TILES)))
+
+
+def backward_stream_chunked(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
+                            fp32_de: bool = False, de_done=None, label_split: bool = False, correct=None,
+                            want_de: bool = True, want_dc: bool = True):
+    """The streamed backward of a large batch as token chunks of STREAM_CHUNK_TILES tiles (8192 rows).
+
+    The pass's dE segments are a token tile's items inside one window of 256 stream items; with
+    more token tiles than a quarter window they shrink below a few items, and every segment costs
+    an fp32 read-modify-write of the tile's 128 x D partial sum.  Each chunk is therefore its own
+    pass over the same global decision inputs (tile maxima rows, lse, the vocabulary order): its
+    tile decisions equal the whole batch's, dE rows are written once by their chunk, and dC adds
+    over the chunks in bf16 (the fast path's group fallback does the same).  The sorted classifier
+    copy is built once in its own buffer (dC accumulates in vocabulary order, so it cannot hold it)
+    and E is read as a compacted copy.  Transients: O(V D) for the sorted copy and O(N D) for the
+    compacted rows, independent of the kept tiles."""
+    lib = _lib.load()
+    e = state.e
+    n, d = e.shape
+    v = state.c.shape[0]
+    dev = e.device
+    stream = _stream(dev)
+    lse = lse.to(torch.float32).contiguous()
+    upstream = upstream.to(torch.float32).contiguous()
+    if not eps:
+        raise ValueError("backward_stream needs filtering (eps > 0)")
+    de = torch.zeros(n, d, dtype=torch.float32 if fp32_de else torch.bfloat16, device=dev) if want_de else None
+    dc = torch.empty(v, d, dtype=torch.bfloat16, device=dev) if want_dc else None
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
+    e_c = state.e_c if state.e_c is not None else gather_rows(e, state.row_map, n)
+    c_sorted = gather_rows(state.c, state.perm, v) if state.perm_padded is not None and state.perm is not None else None
+    chunk = stream_chunk_tiles() * BLOCK_TOKENS
+    mt = -(-v // BLOCK_VOCAB)
+    slots = stream_ring_slots()
+    ring = torch.empty(slots * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
+    ws_bytes = lib.cce_bwd_stream_workspace_bytes(min(n, chunk), d, v, slots)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ev = _ev_begin("bwd")
+    for k, r0 in enumerate(range(0, n, chunk)):
+        r1 = min(n, r0 + chunk)
+        nv = (state.n_valid - r0).clamp(0, r1 - r0).to(torch.int32)  # compacted rows of this chunk
+        t0 = r0 // BLOCK_TOKENS
+        tm = state.tile_max[t0 * mt * BLOCK_TOKENS:]
+        last = r1 >= n
+        flags = 3 if k > 0 else 0  # later chunks: the sorted copy is built, dC adds
+        _lib.check(lib.cce_bwd_stream_ex(
+            _p(e_c[r0:r1]), 0, _p(state.c), _p(c_sorted), _p(state.perm_padded if c_sorted is not None else None),
+            _p(state.inv_perm), _p(state.row_map[r0:]), _p(nv), _p(state.pos), _p(lse), _p(upstream), _p(tm),
+            r1 - r0, d, v, float(state.softcap or 0.0), float(eps), int(bool(label_split)), _p(ring), slots, _p(ws),
+            ws_bytes, _p(de), int(fp32_de), _p(dc), _p(counters),
+            _event_handle(de_done if (last and not label_split) else None), flags if dc is not None else (flags & 1),
+            stream), "cce_bwd_stream_ex")
+    del ws, ring, c_sorted
+    if label_split:
+        label_terms(e, state.c, state.perm_padded, state.row_map, state.n_valid, state.pos, upstream, correct,
+                    state.softcap, de, dc)
         if de_done is not None:
             de_done.record()
     _ev_end("bwd", ev)
@@ -1165,8 +1274,12 @@ LABEL_MARGIN = 1.1
 def label_capacity(key, nt: int, mt: int) -> int:
     """Stored label-tile slots: the worst case (every valid row's label in its own vocab tile,
     ceil(n/128) * min(ceil(v/256), 128)) until a label count of this shape has been observed, then
-    that count plus a margin.  Too small is safe: tiles without a slot are recomputed."""
+    that count plus a margin.  Too small is safe: tiles without a slot are recomputed.  A fixed
+    CCE_SHAT_BUDGET_MB pins it to the worst case as well (the overflow fallback's group size
+    depends on it, and with it the bf16 summation order of dC across groups)."""
     worst = nt * min(mt, BLOCK_TOKENS)
+    if os.environ.get("CCE_SHAT_BUDGET_MB") is not None:
+        return worst
     hint = _KEPT_HINT.get(key)
     if hint is not None:
         _harvest(hint)

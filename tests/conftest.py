@@ -31,6 +31,7 @@ def _fresh_library_state():
         yield
         return
     ops._KEPT_HINT.clear()
+    ops._IGNORED_HINT.clear()
     ops._LABEL_STATE.clear()
     yield
 

@@ -166,3 +166,29 @@ def test_unpermute_rows_in_place(cuda_device, v, d, kind):
                                       ops._stream(x.device)), "cce_unpermute_rows")
     torch.cuda.synchronize()
     assert torch.equal(x, want)
+
+
+@pytest.mark.parametrize("n,d,v,ign,cap,sort", [(1000, 128, 5003, 0.2, 0.0, True), (1500, 256, 30000, 0.0, 30.0, True),
+                                                (700, 192, 4000, 0.1, 0.0, False)])
+def test_stream_token_chunks_match_whole_batch(cuda_device, monkeypatch, n, d, v, ign, cap, sort):
+    """Large batches run the streamed backward as token chunks over a shared sorted copy (dC added
+    over the chunks in bf16): the same tile decisions as the whole-batch pass, gradients within
+    the bf16 rounding of the chunk sums."""
+    from paper_2411_09009_b200 import ops
+
+    e, c, t = _head(n, d, v, 5 * n + d, sigma=2.0, ign=ign)
+
+    def run():
+        lse_l, corr, st = ops.forward_stream(e, c, t, -100, 0, cap, vocab_sorting=sort)
+        lse, _ = ops.merge_shards(lse_l[None], corr[None], t, -100)
+        up = ops.upstream(torch.ones((), device=e.device), t, -100, "mean")
+        out = ops.backward_from_stream_state(st, lse, up)
+        torch.cuda.synchronize()
+        return out
+
+    de0, dc0, cnt0 = run()
+    monkeypatch.setenv("CCE_STREAM_CHUNK_TILES", "2")
+    de1, dc1, cnt1 = run()
+    assert torch.equal(cnt0, cnt1), (cnt0.tolist(), cnt1.tolist())
+    assert _rel(de1, de0) < 8e-3 and _rel(dc1, dc0) < 1e-2, (_rel(de1, de0), _rel(dc1, dc0))
+    assert torch.all(de1[t == -100] == 0)
