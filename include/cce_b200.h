@@ -203,6 +203,17 @@ int cce_bwd_lowmem(const void* E, const void* C, const int32_t* perm_padded, con
 int cce_fwd_group(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total, float softcap,
                   void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max, void* stream);
+/* cce_fwd_group for the groups of one sweep: flags bit 0 = correct_part already zeroed (a label lands
+ * in exactly one group, so every group may write one shared array), bit 1 = leave the group's
+ * (max, sum-exp) partials ([cce_fwd_splits(n, d, v_group)][n] float2, log2 units) in ws and skip
+ * lse_part; cce_combine_parts then finishes lse over the groups' partials ([count][n] float2) at
+ * once, or, with lse_out == NULL, folds them into parts[0] (a running partial). */
+int cce_fwd_group_ex(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                     const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total,
+                     float softcap, void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max,
+                     int flags, void* stream);
+int cce_fwd_splits(int64_t n, int64_t d, int64_t v);
+int cce_combine_parts(const void* parts, int count, int64_t n, float* lse_out, void* stream);
 
 /* ---- streamed backward: transient memory independent of the kept-tile count ----
  * cce_bwd_stream replaces lse_backward (kernels.py:327-486) on the training path.  The decision

@@ -55,6 +55,11 @@ SIGNATURES = {
                                c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
     "cce_fwd_group": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
                               c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "cce_fwd_group_ex": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
+                                 c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_int,
+                                 c_void_p]),
+    "cce_fwd_splits": (c_int, [c_i64, c_i64, c_i64]),
+    "cce_combine_parts": (c_int, [c_void_p, c_int, c_i64, c_void_p, c_void_p]),
     "cce_bwd_stream_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),
     "cce_bwd_stream_debug_layout": (c_int, [c_i64, c_i64, c_i64, c_i64, c_void_p]),
     "cce_bwd_stream": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

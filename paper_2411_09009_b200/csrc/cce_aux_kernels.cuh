@@ -12,8 +12,10 @@ namespace cce {
 // ---------------------------------------------------------------------------------------
 
 // Merge the per-split (max2, sum2) partials of each row into this shard's natural-log LSE.
-__global__ void combine_splits_kernel(const float2* __restrict__ part, int splits, int n,
-                                      float* __restrict__ lse_local) {
+// out_part != nullptr: fold the partials into one (max, sum-exp) pair instead (it may alias part:
+// each thread reads its row of every partial before writing)
+__global__ void combine_splits_kernel(const float2* part, int splits, int n, float* __restrict__ lse_local,
+                                      float2* out_part) {
   griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -25,7 +27,10 @@ __global__ void combine_splits_kernel(const float2* __restrict__ part, int split
       const float2 v = part[(size_t)s * n + i];
       acc += v.y * exp2f(v.x - m);
     }
-  lse_local[i] = (m == -INFINITY) ? -INFINITY : (m + log2f(acc)) * 0.6931471805599453f;
+  if (out_part)
+    out_part[i] = make_float2(m, acc);
+  else
+    lse_local[i] = (m == -INFINITY) ? -INFINITY : (m + log2f(acc)) * 0.6931471805599453f;
 }
 
 // Vocab-parallel / single-shard finish: lse = logaddexp over shards, correct = sum over shards.

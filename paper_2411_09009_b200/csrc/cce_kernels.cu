@@ -568,7 +568,8 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   (void)units;
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
-  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local);
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local,
+             (float2*)nullptr);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -820,7 +821,7 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
                    int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes,
                    float* lse_local, float* correct, float* tile_max, void* lab_buf, int64_t lab_capacity,
                    int32_t* lab_slot, void* lab_list, int* lab_count, cudaStream_t stream, int tm_stride = 0,
-                   int tm_m0 = 0) {
+                   int tm_m0 = 0, int flags = 0) {
   const std::string w(what);
   if (n < 0 || d <= 0 || v <= 0) return fail(w + ": bad sizes");
   if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail(w + ": label tiles need slot maps");
@@ -868,9 +869,16 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
     p.lab_slot = lab_slot;
     p.lab_list = static_cast<int2*>(lab_list);
   }
-  PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
+  // flags (vocabulary groups of one sweep): bit 0 = `correct` already zeroed by the caller (the
+  // target logit lands in exactly one group), bit 1 = leave the (max, sum-exp) partials in ws for
+  // one combine over every group (cce_combine_parts) instead of finishing lse_local here
+  if (!(flags & 1))
+    PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
-  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local);
+  if (!(flags & 2))
+    PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream,
+               static_cast<const float2*>(ws), splits, (int)n, lse_local,
+             (float2*)nullptr);
   CCE_CUDA(cudaGetLastError());
   return 0;
 }
@@ -896,6 +904,39 @@ int cce_fwd_gather(const void* E, const void* C, const int32_t* perm_padded, con
                         static_cast<cudaStream_t>(stream_ptr));
 }
 
+
+int cce_fwd_splits(int64_t n, int64_t d, int64_t v) {
+  if (n <= 0 || v <= 0) return 1;
+  const int nt = (int)((n + cce::BM - 1) / cce::BM);
+  const int mt = (int)((v + cce::BN - 1) / cce::BN);
+  return lse_splits(nt, mt, d, use_pairs(), false);
+}
+
+int cce_combine_parts(const void* parts, int count, int64_t n, float* lse_out, void* stream_ptr) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_ptr);
+  if (n <= 0) return 0;
+  // reads partials written several launches back: without programmatic dependent launch (see
+  // unpermute_rows)
+  PdlScope pdl_scope(false);
+  // lse_out == nullptr: fold into the first partial (parts[0]) instead
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream,
+             static_cast<const float2*>(parts), count, (int)n, lse_out,
+             lse_out ? nullptr : static_cast<float2*>(const_cast<void*>(parts)));
+  CCE_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int cce_fwd_group_ex(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                     const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total,
+                     float softcap, void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max,
+                     int flags, void* stream_ptr) {
+  if (v0 % cce::BN != 0) return fail("cce_fwd_group: v0 must be a multiple of 256");
+  if (v0 + v_group > v_total) return fail("cce_fwd_group: group past the vocabulary");
+  return fwd_tiles_impl("cce_fwd_group", E, C_g, nullptr, e_gather, row_map, n_valid, pos, v0, n, d, v_group, softcap,
+                        ws, ws_bytes, lse_part, correct_part, tile_max, nullptr, 0, nullptr, nullptr, nullptr,
+                        static_cast<cudaStream_t>(stream_ptr), (int)((v_total + cce::BN - 1) / cce::BN),
+                        (int)(v0 / cce::BN), flags);
+}
 
 int cce_fwd_group(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
                   const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total, float softcap,

@@ -764,6 +764,7 @@ def compact_copy_wanted(n: int, d: int, n_valid: torch.Tensor) -> bool:
 
 
 FWD_GROUP_MB = 24  # sorted classifier rows of one vocabulary group in the bounded forward
+FWD_FOLD_GROUPS = 8  # groups whose (max, sum-exp) partials are folded by one combine launch
 
 
 def fwd_group_tiles(d: int, mt: int) -> int:
@@ -771,6 +772,17 @@ def fwd_group_tiles(d: int, mt: int) -> int:
     CCE_FWD_GROUP_MB (default 24 MB; 16 tiles at D = 2304)."""
     budget = int(os.environ.get("CCE_FWD_GROUP_MB", FWD_GROUP_MB)) << 20
     return max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(dev: torch.device) -> torch.cuda.Stream:
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    st = _SIDE.get(key)
+    if st is None:
+        st = _SIDE[key] = torch.cuda.Stream(dev)
+    return st
 
 
 def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softcap: float = 0.0,
@@ -803,29 +815,83 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
         return z, z.clone(), state
     gt = fwd_group_tiles(d, mt)
     groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gt) * BLOCK_VOCAB)) for m0 in range(0, mt, gt)]
-    lse_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
-    corr_parts = torch.empty(len(groups), n, dtype=torch.float32, device=dev)
-    ws_bytes = max(lib.cce_fwd_workspace_bytes(n, d, v1 - v0) for v0, v1 in groups)
-    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
-    buf = torch.empty(min(v, gt * BLOCK_VOCAB), d, dtype=torch.bfloat16, device=dev) if sorted_ else None
+    # the groups' (max, sum-exp) partials side by side after a running one (slot 0), folded into it
+    # every FWD_FOLD_GROUPS groups and finished by one combine; the target logit lands in exactly
+    # one group, so all groups write one zeroed array
+    splits = [lib.cce_fwd_splits(n, d, v1 - v0) for v0, v1 in groups]
+    fold = FWD_FOLD_GROUPS
+    slots = 1 + max(sum(splits[i:i + fold]) for i in range(0, len(groups), fold))
+    parts = torch.empty(slots, n, 2, dtype=torch.float32, device=dev)
+    parts[0, :, 0] = -float("inf")
+    parts[0, :, 1] = 0.0
+    correct = torch.zeros(n, dtype=torch.float32, device=dev)
+    lse_local = torch.empty(n, dtype=torch.float32, device=dev)
+    # two group buffers: group g + 1's rows are gathered on a side stream while group g is swept
+    # (CCE_FWD_OVERLAP=0: gathers in line)
+    overlap = sorted_ and len(groups) > 1 and os.environ.get("CCE_FWD_OVERLAP", "1") != "0" and not _capturing()
+    rows_g = min(v, gt * BLOCK_VOCAB)
+    bufs = [torch.empty(rows_g, d, dtype=torch.bfloat16, device=dev) for _ in range(2 if overlap else 1)] \
+        if sorted_ else []
     stream = _stream(dev)
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev) if overlap else None
+    gathered = [None, None]  # event: the buffer's gather is done
+    released = [None, None]  # event: the sweep reading the buffer is done
+
+    def gather(g):
+        v0, v1 = groups[g]
+        b = g % len(bufs)
+        if side is None:
+            _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(bufs[b]), stream),
+                       "cce_gather_rows")
+            return
+        if released[b] is not None:
+            side.wait_event(released[b])
+        with torch.cuda.stream(side):
+            _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(bufs[b]),
+                                           ctypes.c_void_p(side.cuda_stream)), "cce_gather_rows")
+            gathered[b] = torch.cuda.Event()
+            gathered[b].record(side)
+
     ev = _ev_begin("fwd")
-    for g, (v0, v1) in enumerate(groups):
+    if side is not None:
+        side.wait_stream(main)  # the order (perm) and the caller's C are ready
+    off = 1
+    if sorted_:
+        gather(0)
+    for g, ((v0, v1), sp) in enumerate(zip(groups, splits)):
         if sorted_:
-            c_g = buf[: v1 - v0]
-            _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(c_g), stream), "cce_gather_rows")
+            b = g % len(bufs)
+            if side is not None:
+                main.wait_event(gathered[b])
+                if g + 1 < len(groups):
+                    gather(g + 1)
+            c_g = bufs[b][: v1 - v0]
         else:
             c_g = c[v0:v1]
+        ws = parts[off:off + sp]
         evk = _ev_begin("fwd_kernel")  # the logit-tile launches alone (bench roofline)
-        _lib.check(lib.cce_fwd_group(_p(e_rows), e_gather, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
-                                     float(softcap or 0.0), _p(ws), ws_bytes, _p(lse_parts[g]), _p(corr_parts[g]),
-                                     _p(tile_max), stream), "cce_fwd_group")
+        _lib.check(lib.cce_fwd_group_ex(_p(e_rows), e_gather, _p(c_g), _p(row_map), _p(n_valid), _p(pos), v0, n, d,
+                                        v1 - v0, v, float(softcap or 0.0), _p(ws), sp * n * 8, _p(None),
+                                        _p(correct), _p(tile_max), 3, stream), "cce_fwd_group_ex")
         _ev_end("fwd_kernel", evk)
+        if sorted_:
+            if side is not None:
+                released[b] = torch.cuda.Event()
+                released[b].record(main)
+            elif g + 1 < len(groups):
+                gather(g + 1)
+        off += sp
+        if (g + 1) % fold == 0 and g + 1 < len(groups):
+            _lib.check(lib.cce_combine_parts(_p(parts), off, n, _p(None), stream), "cce_combine_parts")
+            off = 1
+    _lib.check(lib.cce_combine_parts(_p(parts), off, n, _p(lse_local), stream), "cce_combine_parts")
     _ev_end("fwd", ev)
-    del ws, buf
-    # the groups are vocabulary shards of this call; the target logit sits in exactly one of them
-    lse_local, _ = merge_shards(lse_parts, corr_parts, targets, ignore_index)
-    return lse_local, corr_parts.sum(0), state
+    if side is not None:
+        for b in bufs:
+            b.record_stream(side)
+    del parts, bufs
+    return lse_local, correct, state
 
 
 def backward_from_stream_state(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
