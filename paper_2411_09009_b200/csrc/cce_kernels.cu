@@ -1752,7 +1752,8 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
   qc.dc = static_cast<__nv_bfloat16*>(dc);
   qc.perm_store = sorted_out ? nullptr : perm_padded;
   qc.accumulate = dc_accumulate ? 1 : 0;
-  if (sorted_out && de_out) {  // dE consumers read the rows dC overwrites
+  if (sorted_out && de_out && !getenv("CCE_STREAM_NOWAIT")) {  // dE consumers read the rows dC overwrites
+    // (CCE_STREAM_NOWAIT: timing experiment only -- wrong results)
     qc.own_off = w.voc_off;
     qc.own_cnt = w.voc_cnt;
   }

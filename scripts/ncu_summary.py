@@ -10,6 +10,11 @@ KEYS = {
     "dram_write_bytes": ("dram__bytes_write.sum", 1),
     "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "l2_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    "l2_read_bytes": ("lts__t_sectors_op_read.sum", 32),
+    "l2_write_bytes": ("lts__t_sectors_op_write.sum", 32),
+    "l2_bytes": ("lts__t_bytes.sum", 1),
+    "smem_pipe_pct": ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
+    "issue_active_pct": ("sm__inst_issued.avg.pct_of_peak_sustained_elapsed", 1),
     "l1tex_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1),
     "registers": ("launch__registers_per_thread", 1),
     "grid": ("launch__grid_size", 1),

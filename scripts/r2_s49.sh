@@ -1,0 +1,6 @@
+#!/bin/bash
+python -m paper_2411_09009_b200._build > /dev/null 2>&1 || exit 1
+for i in 1 2; do
+for cfg in "X=1" "CCE_STREAM_NOWAIT=1" "CCE_STREAM_RING=256" "CCE_STREAM_RING=1024"; do
+  echo "$cfg: $(env $cfg REPS=5 timeout 200 python scripts/stream_pass_probe.py gemma2-2b both:1 2>&1 | grep gemma | awk '{print $4, $5}')"
+done; done
