@@ -260,6 +260,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="vocab", choices=["vocab", "token"])
     ap.add_argument("--sigma", type=float, default=None, help="logit std of the synthetic head")
+    ap.add_argument("--pad", type=float, default=None,
+                    help="fraction of each 4096-token sequence set to ignore_index (default: the config's)")
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--dist", default="iid", choices=["iid", "zipf"],
                     help="iid: E, C Gaussian, uniform targets (D1); zipf: a shared direction carries a "
@@ -320,6 +322,8 @@ def main():
             raise SystemExit(f"bench: communicator has {int(probe.item())} ranks, expected {world}")
 
     n, d, v, cap, pad_frac, sigma = CONFIGS[args.config]
+    if args.pad is not None:
+        pad_frac = args.pad
     if args.sigma is not None:
         sigma = args.sigma
     eps = None if args.no_filter else "auto"

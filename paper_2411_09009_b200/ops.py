@@ -763,13 +763,13 @@ def compact_copy_wanted(n: int, d: int, n_valid: torch.Tensor) -> bool:
     return wanted
 
 
-FWD_GROUP_MB = 24  # sorted classifier rows of one vocabulary group in the bounded forward
+FWD_GROUP_MB = 48  # sorted classifier rows of one vocabulary group in the bounded forward (two buffers)
 FWD_FOLD_GROUPS = 8  # groups whose (max, sum-exp) partials are folded by one combine launch
 
 
 def fwd_group_tiles(d: int, mt: int) -> int:
     """Vocab tiles per group of the bounded forward: the group's sorted rows within
-    CCE_FWD_GROUP_MB (default 24 MB; 16 tiles at D = 2304)."""
+    CCE_FWD_GROUP_MB (default 48 MB; 40 tiles at D = 2304)."""
     budget = int(os.environ.get("CCE_FWD_GROUP_MB", FWD_GROUP_MB)) << 20
     return max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
 
@@ -791,7 +791,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
 
     indexed_matmul + lse_forward (kernels.py:204-319) over the backward's tiles (compacted rows,
     the reference's vocabulary order) with the per-row tile maxima the decision needs, run over
-    vocabulary groups: each group's classifier rows are gathered into one small buffer (24 MB) and
+    vocabulary groups: each group's classifier rows are gathered into one small buffer (48 MB) and
     swept with plain TMA tiles; the groups' (lse, correct) partials merge with the log-add-exp of
     the vocab-parallel path (kernels.py:121-137).  E is read in place (through the compaction map
     when rows are ignored).  Transients: the group buffer, the tile maxima, O(N + V) maps."""

@@ -6,7 +6,7 @@ outputs) with a recorded formula, 4 * (8 (N + V) + 8 threads (n_b m_b + d_b (n_b
 ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu):
 
   forward   per-row tile maxima  ceil(N/128) * ceil(V/256) * 512 B
-            two vocabulary groups of sorted classifier rows (CCE_FWD_GROUP_MB, 24 MiB each: the
+            two vocabulary groups of sorted classifier rows (CCE_FWD_GROUP_MB, 48 MiB each: the
             next group is gathered on a side stream while one is swept)
             O(N + V) maps and partials; a batch with ignored rows adds their compacted copy
   backward  the S-hat ring (512 slots x 64 KiB = 32 MiB)
@@ -32,7 +32,9 @@ def _budget(n, d, v):
     nt, mt, ndc = -(-n // 128), -(-v // 256), -(-d // 256)
     tile_max = nt * mt * 128 * 4
     lists = nt * mt * 72 + (n + v) * 64  # keep flags, item lists, segments, windows; O(N + V) maps
-    fwd = tile_max + 2 * 24 * MIB + lists + 2 * MIB  # two group buffers (gather overlapped with the sweep)
+    # two group buffers (gather overlapped with the sweep) and the (max, sum-exp) partials of up to
+    # 8 groups x 8 vocabulary splits between folds
+    fwd = tile_max + 2 * 48 * MIB + 64 * n * 8 + lists + 2 * MIB
     acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
     step = 512 * 64 * 1024 + acc + tile_max + lists + 4 * MIB
     return fwd, step
