@@ -1,7 +1,8 @@
-// The memory="fast" training path (the round-1 default) driven from plain C++ through include/cce_b200.h alone: the call
-// sequence of ops.forward_tiles + ops.backward_tiles -- compaction, vocabulary
-// order, sorted classifier copy, tile-recording forward, shard merge, decision-from-forward
-// backward -- checked against double-precision loss, dE and dC computed here.
+// The default (bounded-memory) training path driven from plain C++ through include/cce_b200.h
+// alone: the call sequence of ops.forward_stream + ops.backward_from_stream_state
+// -- compaction, vocabulary order, per-group gathered classifier rows and tile-recording forward,
+// one combine of the groups' partials, shard merge, then the streamed backward with the sorted
+// copy built in dC's storage and moved back in place -- against double-precision loss, dE, dC.
 // N = 300, V = 1000: every 128 x 256 tile holds a label, so the reference's label exemption
 // (kernels.py:447-455) keeps every tile and the filtered gradient equals the exact one.
 // Exit code 0 = pass.  Built and run by tests/test_abi_c_gpu.py.
@@ -11,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 #include "cce_b200.h"
@@ -105,7 +107,7 @@ int main() {
   CK(cudaMemcpy(dx, x.data(), n * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dup, up.data(), n * 4, cudaMemcpyHostToDevice));
 
-  // 1. compaction (filter_ignored) and the compacted rows E_c
+  // 1. compaction (filter_ignored); rows are ignored, so the kernels read a compacted copy
   auto* row_map = dev_alloc<int32_t>(nt * 128);
   auto* n_valid = dev_alloc<int>(1);
   auto* E_c = dev_alloc<__nv_bfloat16>(n * d);
@@ -120,36 +122,45 @@ int main() {
   auto* key = dev_alloc<float>(v);
   CC(cce_ebar(dE, dx, ig, n, d, ebar, ws_e, ebw, st));
   CC(cce_vocab_order(dC, ebar, n_valid, v, d, perm, key, ws_s, sow, st));
-  // 3. label positions in tile order, the sorted classifier copy C_t
+  // 3. label positions in tile order and the inverse order
   auto* perm_padded = dev_alloc<int32_t>(vpad);
   auto* inv_perm = dev_alloc<int32_t>(v);
   auto* pos = dev_alloc<int32_t>(n);
-  auto* C_t = dev_alloc<__nv_bfloat16>(v * d);
   CC(cce_bwd_prep(perm, v, dx, ig, 0, n, perm_padded, inv_perm, pos, st));
-  CC(cce_gather_rows(dC, perm, v, d, C_t, st));
-  // 4. forward over the backward's tiles, recording per-row tile maxima; merge (one shard)
-  const size_t fw = cce_fwd_workspace_bytes(n, d, v);
-  auto* ws_f = dev_alloc<uint8_t>(fw);
-  auto* lse_l = dev_alloc<float>(n);
-  auto* corr = dev_alloc<float>(n);
+  // 4. forward over vocabulary groups of 2 tiles (512 sorted rows): each group's rows gathered,
+  //    swept into its (max, sum-exp) partials and its block of the tile maxima; one combine
+  const int64_t gv = 512;
+  auto* C_g = dev_alloc<__nv_bfloat16>(gv * d);
   auto* tile_max = dev_alloc<float>(cce_tile_max_bytes(n, v) / 4);
+  auto* corr = dev_alloc<float>(n);  // zeroed: a label lands in exactly one group
+  int total_splits = 0;
+  for (int64_t v0 = 0; v0 < v; v0 += gv) total_splits += cce_fwd_splits(n, d, std::min(gv, v - v0));
+  auto* parts = dev_alloc<float>((size_t)total_splits * n * 2);
+  int off = 0;
+  for (int64_t v0 = 0; v0 < v; v0 += gv) {
+    const int64_t vg = std::min(gv, v - v0);
+    const int sp = cce_fwd_splits(n, d, vg);
+    CC(cce_gather_rows(dC, perm + v0, vg, d, C_g, st));
+    CC(cce_fwd_group_ex(E_c, 0, C_g, row_map, n_valid, pos, v0, n, d, vg, v, 0.f, parts + (size_t)off * n * 2,
+                        (size_t)sp * n * 8, nullptr, corr, tile_max, 3, st));
+    off += sp;
+  }
+  auto* lse_l = dev_alloc<float>(n);
   auto* lse = dev_alloc<float>(n);
   auto* loss = dev_alloc<float>(n);
-  CC(cce_fwd_tiles(E_c, C_t, row_map, n_valid, pos, 0, n, d, v, 0.f, ws_f, fw, lse_l, corr, tile_max,
-                   nullptr, 0, nullptr, nullptr, nullptr, st));
+  CC(cce_combine_parts(parts, off, n, lse_l, st));
   CC(cce_merge_shards(1, lse_l, corr, dx, ig, n, lse, loss, st));
-  // 5. backward from the tile maxima: kept tiles recomputed into S-hat slots, dE / dC passes
-  const int64_t cap = nt * mt;  // every tile: no overflow path at this size
-  const size_t kw = cce_bwd_kept_workspace_bytes(n, d, v, cap, 0);
-  auto* ws_k = dev_alloc<uint8_t>(kw);
-  auto* shat = dev_alloc<uint8_t>(cap * 128 * 256 * 2);
+  // 5. streamed backward: 512-slot S-hat ring, the sorted copy in dC's storage (c_sorted == dc)
+  const int64_t ring_slots = 512;
+  const size_t sw = cce_bwd_stream_workspace_bytes(n, d, v, ring_slots);
+  auto* ws_b = dev_alloc<uint8_t>(sw);
+  auto* ring = dev_alloc<uint8_t>(ring_slots * 128 * 256 * 2);
   auto* de = dev_alloc<__nv_bfloat16>(n * d);  // zeroed: ignored rows stay 0
   auto* dc = dev_alloc<__nv_bfloat16>(v * d);
   auto* counters = dev_alloc<unsigned long long>(3);
-  auto* overflow = dev_alloc<int>(1);
-  CC(cce_bwd_kept(E_c, C_t, nullptr, perm_padded, row_map, n_valid, pos, 0, lse, dup, tile_max, n, d, v,
-                  0.f, eps, 0, shat, 0, nullptr, nullptr, nullptr, cap, ws_k, kw, de, 0, 0, dc, counters,
-                  overflow, nullptr, nullptr, nullptr, st));
+  CC(cce_bwd_stream(E_c, 0, dC, dc, perm_padded, inv_perm, row_map, n_valid, pos, lse, dup, tile_max, n, d, v,
+                    0.f, eps, 0, ring, ring_slots, ws_b, sw, de, 0, dc, counters, nullptr, st));
+  auto* overflow = dev_alloc<int>(1);  // (no overflow path on the streamed backward)
 
   std::vector<float> hloss(n);
   std::vector<__nv_bfloat16> hde(n * d), hdc(v * d);
@@ -176,6 +187,6 @@ int main() {
   std::printf("loss rel %.2e  dE rel %.2e  dC rel %.2e  kept %llu of %lld  overflow %d\n", e_loss, e_de, e_dc,
               hk[0], (long long)(nt * mt), hov);
   if (!(e_loss < 1e-3 && e_de < 1e-2 && e_dc < 1e-2) || hov != 0 || hk[0] != (unsigned long long)(nt * mt)) return 4;
-  std::printf("abi training path ok\n");
+  std::printf("abi bounded training path ok\n");
   return 0;
 }

@@ -1,8 +1,9 @@
 """The C ABI from plain C++ (Option C): the programs in tests/abi_c/ include only
 include/cce_b200.h and link libcce_b200.so.  abi_caller: forward + merge against a
-double-precision log-sum-exp, and the error channel.  abi_train: the whole default training path
+double-precision log-sum-exp, and the error channel.  abi_train: the memory="fast" training path
 (compaction, vocabulary order, sorted copy, tile-recording forward, kept backward) against
-double-precision loss, dE and dC."""
+double-precision loss, dE and dC.  abi_train_stream: the default bounded path (per-group forward,
+streamed backward) against the same."""
 import os
 import subprocess
 from pathlib import Path
@@ -13,7 +14,8 @@ ROOT = Path(__file__).resolve().parent.parent
 PKG = ROOT / "paper_2411_09009_b200"
 
 
-PROGRAMS = {"abi_caller": "abi caller ok", "abi_train": "abi training path ok"}
+PROGRAMS = {"abi_caller": "abi caller ok", "abi_train": "abi training path ok",
+            "abi_train_stream": "abi bounded training path ok"}
 
 
 def _build(tmp_path, name):
