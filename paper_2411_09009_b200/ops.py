@@ -887,9 +887,9 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
             off = 1
     _lib.check(lib.cce_combine_parts(_p(parts), off, n, _p(lse_local), stream), "cce_combine_parts")
     _ev_end("fwd", ev)
-    if side is not None:
-        for b in bufs:
-            b.record_stream(side)
+    # every side-stream gather is followed by a wait of the caller's stream on its event, and the
+    # next call's gathers start after side.wait_stream(main): the buffers are the caller stream's
+    # to free (no record_stream, which would hold them back from the allocator)
     del parts, bufs
     return lse_local, correct, state
 
@@ -993,8 +993,15 @@ def backward_tiles(state: TileState, targets, lse, upstream, *, ignore_index: in
 STREAM_RING_SLOTS = 512  # S-hat ring of the streamed backward (64 KiB slots: 32 MiB)
 
 
-def stream_ring_slots() -> int:
-    return max(128, int(os.environ.get("CCE_STREAM_RING", STREAM_RING_SLOTS)))
+def stream_ring_slots(token_tiles: int = 0) -> int:
+    """S-hat ring slots of one streamed pass: 512, or 8 per token tile (dE windows of half the
+    ring then hold >= 4 items of every token tile), up to 2048 (128 MiB).  Measured at
+    Gemma-2-9B (256 token tiles): 84 ms per step with 2048 slots in one pass, against 104 ms
+    with four 64-tile chunks of 512 slots (scripts/r2_s57.sh)."""
+    env = os.environ.get("CCE_STREAM_RING")
+    if env is not None:
+        return max(128, int(env))
+    return max(STREAM_RING_SLOTS, min(4 * STREAM_RING_SLOTS, 8 * token_tiles))
 
 
 def stream_supported(d: int) -> bool:
@@ -1033,7 +1040,7 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
         # no sorted copy, the pass gathers C rows through the order and scatters dC rows
         alias = dc is not None and os.environ.get("CCE_STREAM_ALIAS", "1") != "0"
         c_sorted = dc if alias else torch.empty(v, d, dtype=torch.bfloat16, device=dev)
-    slots = stream_ring_slots()
+    slots = stream_ring_slots(-(-n // BLOCK_TOKENS))
     ring = torch.empty(slots * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
     ws_bytes = lib.cce_bwd_stream_workspace_bytes(n, d, v, slots)
     ws = (torch.zeros if os.environ.get("CCE_STREAM_ZERO_WS") else torch.empty)(ws_bytes, dtype=torch.uint8, device=dev)
@@ -1054,7 +1061,7 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
     return de, dc, counters
 
 
-STREAM_CHUNK_TILES = 64  # token tiles per streamed pass (windows of 256 items: >= 4 items per dE segment)
+STREAM_CHUNK_TILES = 256  # token tiles per streamed pass (32768 rows; ring sized by stream_ring_slots)
 
 
 def stream_chunk_tiles() -> int:
@@ -1064,11 +1071,12 @@ def stream_chunk_tiles() -> int:
 def backward_stream_chunked(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
                             fp32_de: bool = False, de_done=None, label_split: bool = False, correct=None,
                             want_de: bool = True, want_dc: bool = True):
-    """The streamed backward of a large batch as token chunks of STREAM_CHUNK_TILES tiles (8192 rows).
+    """The streamed backward of a large batch as token chunks of STREAM_CHUNK_TILES tiles (32768 rows).
 
-    The pass's dE segments are a token tile's items inside one window of 256 stream items; with
-    more token tiles than a quarter window they shrink below a few items, and every segment costs
-    an fp32 read-modify-write of the tile's 128 x D partial sum.  Each chunk is therefore its own
+    The pass's dE segments are a token tile's items inside one window of ring / 2 stream items;
+    with more token tiles than a quarter window they shrink below a few items, and every segment
+    costs an fp32 read-modify-write of the tile's 128 x D partial sum.  The ring grows with the
+    token tiles up to 2048 slots (stream_ring_slots); beyond that each chunk is its own
     pass over the same global decision inputs (tile maxima rows, lse, the vocabulary order): its
     tile decisions equal the whole batch's, dE rows are written once by their chunk, and dC adds
     over the chunks in bf16 (the fast path's group fallback does the same).  The sorted classifier
@@ -1092,7 +1100,7 @@ def backward_stream_chunked(state: StreamState, lse, upstream, *, eps: float = E
     c_sorted = gather_rows(state.c, state.perm, v) if state.perm_padded is not None and state.perm is not None else None
     chunk = stream_chunk_tiles() * BLOCK_TOKENS
     mt = -(-v // BLOCK_VOCAB)
-    slots = stream_ring_slots()
+    slots = stream_ring_slots(-(-min(n, chunk) // BLOCK_TOKENS))
     ring = torch.empty(slots * SHAT_TILE_BYTES, dtype=torch.uint8, device=dev)
     ws_bytes = lib.cce_bwd_stream_workspace_bytes(min(n, chunk), d, v, slots)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)

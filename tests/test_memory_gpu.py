@@ -9,7 +9,7 @@ ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu)
             two vocabulary groups of sorted classifier rows (CCE_FWD_GROUP_MB, 48 MiB each: the
             next group is gathered on a side stream while one is swept)
             O(N + V) maps and partials; a batch with ignored rows adds their compacted copy
-  backward  the S-hat ring (512 slots x 64 KiB = 32 MiB)
+  backward  the S-hat ring (512 slots x 64 KiB = 32 MiB; 8 slots per token tile above 64 tiles)
             split-owner accumulators: ceil(N/128) * ceil(D/256) * 128 KiB (fp32 dE partial sums
             across stream windows) + 4 * ceil(D/256) * 256 KiB (vocab tiles over several segments)
             the tile maxima, O(N + V) maps and O(ceil(N/128) * ceil(V/256)) lists
@@ -36,7 +36,8 @@ def _budget(n, d, v):
     # 8 groups x 8 vocabulary splits between folds
     fwd = tile_max + 2 * 48 * MIB + 64 * n * 8 + lists + 2 * MIB
     acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
-    step = 512 * 64 * 1024 + acc + tile_max + lists + 4 * MIB
+    ring = max(512, min(2048, 8 * nt)) * 64 * 1024  # ops.stream_ring_slots
+    step = ring + acc + tile_max + lists + 4 * MIB
     return fwd, step
 
 
