@@ -137,11 +137,12 @@ def test_stream_gather_mode_bit_identical(cuda_device, monkeypatch, n, d, v, ign
 
 @pytest.mark.parametrize("v,d,kind", [(1000, 64, "random"), (5003, 192, "random"), (256000, 2304, "random"),
                                       (3000, 128, "identity"), (3000, 128, "shift"), (4096, 256, "swaps"),
-                                      (2000, 520, "random")])
+                                      (2000, 520, "random"), (20000, 256, "freecycle")])
 def test_unpermute_rows_in_place(cuda_device, v, d, kind):
     """The in-place unpermutation of dC (cycle segments cut at anchors, chain tables, batched row
     moves per column block) equals an out-of-place index copy, for random permutations (one giant
-    cycle plus small ones), the identity, one long anchor-free shift and many 2-cycles."""
+    cycle plus small ones), the identity, one long shift, many 2-cycles (rotated) and a 500-long
+    cycle without anchors (cut from its smallest position)."""
     from paper_2411_09009_b200 import _lib, ops
 
     lib = _lib.load()
@@ -152,8 +153,13 @@ def test_unpermute_rows_in_place(cuda_device, v, d, kind):
         perm = torch.arange(v, device="cuda")
     elif kind == "shift":
         perm = (torch.arange(v, device="cuda") + 1) % v
-    else:
+    elif kind == "swaps":
         perm = torch.arange(v, device="cuda").view(-1, 2).flip(1).reshape(-1)
+    else:  # one 500-long cycle through positions that are not anchors (cut every 96 from its minimum)
+        idx = [p for p in range(v) if ((p * 2654435761) & 0xFFFFFFFF) >> 26 != 0][:500]
+        perm = torch.arange(v, device="cuda")
+        src = torch.tensor(idx, device="cuda")
+        perm[src] = torch.roll(src, 1)
     perm = perm.to(torch.int32)
     inv = torch.empty_like(perm)
     inv[perm.long()] = torch.arange(v, dtype=torch.int32, device="cuda")
@@ -168,9 +174,11 @@ def test_unpermute_rows_in_place(cuda_device, v, d, kind):
     assert torch.equal(x, want)
 
 
-@pytest.mark.parametrize("n,d,v,ign,cap,sort", [(1000, 128, 5003, 0.2, 0.0, True), (1500, 256, 30000, 0.0, 30.0, True),
-                                                (700, 192, 4000, 0.1, 0.0, False)])
-def test_stream_token_chunks_match_whole_batch(cuda_device, monkeypatch, n, d, v, ign, cap, sort):
+@pytest.mark.parametrize("n,d,v,ign,cap,sort,fp32", [(1000, 128, 5003, 0.2, 0.0, True, False),
+                                                     (1500, 256, 30000, 0.0, 30.0, True, False),
+                                                     (700, 192, 4000, 0.1, 0.0, False, False),
+                                                     (900, 128, 6000, 0.1, 0.0, True, True)])
+def test_stream_token_chunks_match_whole_batch(cuda_device, monkeypatch, n, d, v, ign, cap, sort, fp32):
     """Large batches run the streamed backward as token chunks over a shared sorted copy (dC added
     over the chunks in bf16): the same tile decisions as the whole-batch pass, gradients within
     the bf16 rounding of the chunk sums."""
@@ -182,7 +190,7 @@ def test_stream_token_chunks_match_whole_batch(cuda_device, monkeypatch, n, d, v
         lse_l, corr, st = ops.forward_stream(e, c, t, -100, 0, cap, vocab_sorting=sort)
         lse, _ = ops.merge_shards(lse_l[None], corr[None], t, -100)
         up = ops.upstream(torch.ones((), device=e.device), t, -100, "mean")
-        out = ops.backward_from_stream_state(st, lse, up)
+        out = ops.backward_from_stream_state(st, lse, up, fp32_de=fp32)  # fp32: the vocab-parallel dE
         torch.cuda.synchronize()
         return out
 
