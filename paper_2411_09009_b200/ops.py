@@ -759,6 +759,9 @@ def compact_copy_wanted(n: int, d: int, n_valid: torch.Tensor) -> bool:
         pinned.copy_(n_valid, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
+        _IGNORED_HINT.pop(key, None)
+        while len(_IGNORED_HINT) >= KEPT_HINT_MAX:  # shapes that vary every step: drop the oldest
+            _IGNORED_HINT.pop(next(iter(_IGNORED_HINT)))
         _IGNORED_HINT[key] = [pinned, ev, hint[2] if hint is not None else None]
     return wanted
 
@@ -997,7 +1000,7 @@ def stream_ring_slots(token_tiles: int = 0) -> int:
     """S-hat ring slots of one streamed pass: 512, or 8 per token tile (dE windows of half the
     ring then hold >= 4 items of every token tile), up to 2048 (128 MiB).  Measured at
     Gemma-2-9B (256 token tiles): 84 ms per step with 2048 slots in one pass, against 104 ms
-    with four 64-tile chunks of 512 slots (scripts/r2_s57.sh)."""
+    with four 64-tile chunks of 512 slots (scripts/ab_r2/r2_s57.sh)."""
     env = os.environ.get("CCE_STREAM_RING")
     if env is not None:
         return max(128, int(env))
