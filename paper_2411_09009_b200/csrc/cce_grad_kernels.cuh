@@ -442,7 +442,7 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
 #pragma unroll
             for (int i = 0; i < 64; ++i) x[i] = __uint_as_float(r[i]);
           }
-          if (racc) {
+          if (racc && !(p.debug & 4)) {  // debug bit 2: skip the fold-in loads (timing only)
             float4 o[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __ldcg(reinterpret_cast<const float4*>(racc) + (c * 16 + i) * BM);
@@ -454,7 +454,8 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
               x[4 * i + 3] += o[i].w;
             }
           }
-          if (wacc) {
+          if (p.debug & 8) {  // debug bit 3: no stores (timing only)
+          } else if (wacc) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               __stcg(reinterpret_cast<float4*>(wacc) + (c * 16 + i) * BM,
