@@ -254,7 +254,7 @@ def linear_cross_entropy(
     mode = "grouped" if low_memory else (memory or os.environ.get("CCE_MEMORY") or "bounded")
     if mode not in ("bounded", "fast", "grouped"):
         raise ValueError(f"memory must be 'bounded', 'fast' or 'grouped', got {mode!r}")
-    if mode == "bounded" and not (ops.stream_supported(e2.shape[1]) and e2.shape[0] <= 2048 * ops.BLOCK_TOKENS):
+    if mode == "bounded" and not ops.stream_supported(e2.shape[1]):  # any N: large batches run in token chunks
         mode = "fast"  # the streamed backward's CTA-pair boxes need D % 64 == 0
     out = _LinearCrossEntropy.apply(e2, c, t2, t_shard, int(ignore_index), cap, reduction, eps,
                                     bool(vocab_sorting), process_group, int(vocab_start),

@@ -200,3 +200,24 @@ def test_stream_token_chunks_match_whole_batch(cuda_device, monkeypatch, n, d, v
     assert torch.equal(cnt0, cnt1), (cnt0.tolist(), cnt1.tolist())
     assert _rel(de1, de0) < 8e-3 and _rel(dc1, dc0) < 1e-2, (_rel(de1, de0), _rel(dc1, dc0))
     assert torch.all(de1[t == -100] == 0)
+
+
+def test_bounded_default_beyond_2048_token_tiles(cuda_device):
+    """linear_cross_entropy's bounded default at N = 270000 (2110 token tiles, more than one
+    streamed pass can hold): token chunks of 256 tiles, against memory="fast" on the same batch."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    n, d, v = 270000, 64, 2000
+    e0, c0, t = _head(n, d, v, 17, sigma=2.0, ign=0.05)
+    out = {}
+    for mode in ("bounded", "fast"):
+        e = e0.clone().requires_grad_(True)
+        c = c0.clone().requires_grad_(True)
+        loss = linear_cross_entropy(e, c, t, memory=mode)
+        loss.backward()
+        torch.cuda.synchronize()
+        out[mode] = (loss.item(), e.grad, c.grad)
+    lb, lf = out["bounded"][0], out["fast"][0]
+    assert abs(lb - lf) <= 1e-4 * abs(lf), (lb, lf)
+    assert _rel(out["bounded"][1], out["fast"][1]) < 1e-2
+    assert _rel(out["bounded"][2], out["fast"][2]) < 1e-2
