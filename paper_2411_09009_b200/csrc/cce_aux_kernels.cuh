@@ -191,6 +191,10 @@ __global__ void compact_rows_kernel(const int64_t* __restrict__ targets, int64_t
     __syncthreads();
   }
   if (threadIdx.x == 0) *n_valid = s_base;
+  // entries past the compacted count (up to the 128-row padding): row 0, so a gather of all n rows
+  // (the compacted copy of E) reads only real rows
+  const int pad = (n + BM - 1) / BM * BM;
+  for (int j = s_base + threadIdx.x; j < pad; j += T) row_map[j] = 0;
 }
 
 // out[i] = C[x_i] . E[i] (indexed_matmul, kernels.py:204-251); one warp per token row.
