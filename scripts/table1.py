@@ -49,6 +49,7 @@ def liger(e, c, t):
 
 METHODS = {
     "CCE (ours)": lambda e, c, t: linear_cross_entropy(e, c, t),
+    "CCE memory=fast": lambda e, c, t: linear_cross_entropy(e, c, t, memory="fast"),
     "CCE low_memory": lambda e, c, t: linear_cross_entropy(e, c, t, low_memory=True),
     "CCE (no vocab sorting)": lambda e, c, t: linear_cross_entropy(e, c, t, vocab_sorting=False),
     "CCE (no grad filter)": lambda e, c, t: linear_cross_entropy(e, c, t, filter_eps=None),
