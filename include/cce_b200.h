@@ -218,10 +218,12 @@ int cce_combine_parts(const void* parts, int count, int64_t n, float* lse_out, v
 /* ---- streamed backward: transient memory independent of the kept-tile count ----
  * cce_bwd_stream replaces lse_backward (kernels.py:327-486) on the training path.  The decision
  * comes from the forward's tile maxima (tile_max [ceil(n/128)][ceil(v/256)][128], the layout of
- * cce_fwd_tiles / cce_fwd_group), exactly as in cce_bwd_kept.  The kept tiles are then
- * recomputed twice, once in token-tile order for dE and once in vocabulary-tile order for dC, and
- * streamed from the recomputing CTAs to the contracting CTAs through `ring` ([ring_slots][128][256]
- * bf16; 256 slots = 16 MiB); no S-hat buffer grows with the kept count.
+ * cce_fwd_tiles / cce_fwd_group), exactly as in cce_bwd_kept.  Every kept tile is then recomputed
+ * once, in vocabulary-tile-major order, by the recomputing CTAs of one persistent kernel and
+ * streamed to its dC and dE CTAs through `ring` ([ring_slots][128][256] bf16; 512 slots = 32 MiB;
+ * ops.stream_ring_slots uses 8 per token tile above 64 token tiles, up to 2048); no S-hat buffer
+ * grows with the kept count.  At most 2048 token tiles per call (larger batches: token chunks
+ * with cce_bwd_stream_ex).
  *   E          rows of the token tiles: the caller's E with e_gather = 1 (rows are read through
  *              row_map unless the compaction is the identity) or a compacted copy with e_gather = 0
  *   C          the caller's classifier; with a vocabulary order (perm_padded / inv_perm from

@@ -1,13 +1,13 @@
 // Streamed backward (cce_bwd_stream): lse_backward (kernels.py:327-486) with transient memory
 // bounded independently of the kept-tile count.
 //
-// The decision from the forward's tile maxima (decide_tiles_kernel) gives the kept tiles.  Two
-// passes then recompute them, each in one persistent kernel whose CTAs split into two roles:
+// The decision from the forward's tile maxima (decide_tiles_kernel) gives the kept tiles.  One
+// persistent kernel (cce_stream3_kernel) recomputes each of them once; its CTAs split into roles:
 //   producers  the KEPT logit-tile body (cce_lse_kernel.cuh) recomputing kept tiles in stream
-//              order and writing S-hat into a ring of R slots in HBM (L2-resident at R = 256);
-//   consumers  the dE body (token pass: items in token-tile-major order, units = (segment, D
-//              chunk)) or the dC body (vocab pass: vocab-tile-major, CTA pairs, units = (segment,
-//              D chunk, vocab half)) reading S-hat from the ring with TMA.
+//              order (vocabulary-tile-major) and writing S-hat into a ring of R slots in HBM;
+//   consumers  the dC body (CTA pairs, units = (vocab tile segment, D chunk)) and the dE body
+//              (units = (window segment of a token tile, D chunk)) reading S-hat from the ring
+//              with TMA.
 // Slot reuse and readiness are counted with GPU-scope release / acquire flags (Stream in
 // cce_common.cuh); a segment is a run of at most B items of one owner, an owner with several
 // segments sums them in segment order through an fp32 region (deterministic).  Progress is
@@ -15,8 +15,9 @@
 // increasing order, consumers take units in increasing order, and every wait is on an earlier item,
 // segment or owner.
 //
-// The vocab pass writes dC in the sorted order into the storage of the sorted classifier copy the
-// token pass read; unpermute_* put the rows back in vocabulary order in place (cycle segments).
+// The dC role writes dC in the sorted order over the sorted classifier copy the other roles read
+// (once every reader of a vocabulary tile is done); unpermute_* put the rows back in vocabulary
+// order in place (cycle segments).
 #pragma once
 #include "cce_grad_kernels.cuh"
 #include "cce_lse_kernel.cuh"
@@ -302,31 +303,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     dc_body<2>(tmSc, tmE64, tmE3, tmE64, qc, smem, b - P, qc_ctas);
   else
     de_body<DE_CH, KV>(tmSe, tmCk, tmC3, tmCk, qe, smem, b - P - qc_ctas, (int)gridDim.x - P - qc_ctas);
-}
-
-// The pass kernel: producers (KEPT recompute into the ring) are CTAs [0, producers), consumers the
-// rest.  PASS 0 = token pass (single CTAs, dE consumers), 1 = vocab pass (dC consumers; CG = 2: CTA
-// pairs for both roles).
-template <int PASS, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    cce_stream_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
-                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
-                      const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmX,
-                      const __grid_constant__ CUtensorMap tmX3, const __grid_constant__ CUtensorMap tmXg,
-                      const Params p, const GradParams q) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const int P = p.st.producers;
-  const int b = (int)blockIdx.x;
-  if (b < P) {
-    lse_body<KEPT, CG>(tmE, tmEg, tmC, tmCg, p, smem, b, P);
-  } else {
-    if constexpr (PASS == 0)
-      de_body<1, 64>(tmS, tmX, tmX3, tmXg, q, smem, b - P, (int)gridDim.x - P);
-    else
-      dc_body<CG>(tmS, tmX, tmX3, tmXg, q, smem, b - P, (int)gridDim.x - P);
-  }
 }
 
 // ---------------------------------------------------------------------------------------------
