@@ -794,10 +794,11 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
 
     indexed_matmul + lse_forward (kernels.py:204-319) over the backward's tiles (compacted rows,
     the reference's vocabulary order) with the per-row tile maxima the decision needs, run over
-    vocabulary groups: each group's classifier rows are gathered into one small buffer (48 MB) and
-    swept with plain TMA tiles; the groups' (lse, correct) partials merge with the log-add-exp of
-    the vocab-parallel path (kernels.py:121-137).  E is read in place (through the compaction map
-    when rows are ignored).  Transients: the group buffer, the tile maxima, O(N + V) maps."""
+    vocabulary groups: each group's classifier rows are gathered into one of two 48 MB buffers (on
+    a side stream, while the previous group is swept) and swept with plain TMA tiles; the groups'
+    (max, sum-exp) partials are folded by log-add-exp (kernels.py:121-137).  E is read in place
+    when no row is ignored and as a compacted copy otherwise (compact_copy_wanted).  Transients:
+    the group buffers, the tile maxima, O(N + V) maps (and the compacted rows of a padded batch)."""
     lib = _lib.load()
     n, d = e.shape
     v = c.shape[0]
