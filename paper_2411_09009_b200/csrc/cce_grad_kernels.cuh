@@ -442,7 +442,14 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
 #pragma unroll
             for (int i = 0; i < 64; ++i) x[i] = __uint_as_float(r[i]);
           }
-          if (racc && !(p.debug & 4)) {  // debug bit 2: skip the fold-in loads (timing only)
+#ifndef CCE_DE_RED
+#define CCE_DE_RED 1
+#endif
+          // a middle segment adds its partial with vector reductions in L2 (no read: the chain
+          // still orders the segments, so the fp32 sum keeps its order); the first stores it, the
+          // last folds the running sum in and writes dE
+          const bool mid = CCE_DE_RED && racc && wacc;
+          if (racc && !mid && !(p.debug & 4)) {  // debug bit 2: skip the fold-in loads (timing only)
             float4 o[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __ldcg(reinterpret_cast<const float4*>(racc) + (c * 16 + i) * BM);
@@ -455,6 +462,11 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
             }
           }
           if (p.debug & 8) {  // debug bit 3: no stores (timing only)
+          } else if (mid) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              red_add_v4_f32(reinterpret_cast<float*>(reinterpret_cast<float4*>(wacc) + (c * 16 + i) * BM), x[4 * i], x[4 * i + 1],
+                             x[4 * i + 2], x[4 * i + 3]);
           } else if (wacc) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
