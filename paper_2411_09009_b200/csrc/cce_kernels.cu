@@ -1668,9 +1668,10 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
 
   // roles: producers and dC consumers as CTA pairs, dE consumers single (about a third each)
   const int grid = sms & ~1;
-  // measured at Gemma-2-2B (148 SMs): 36 / 50 / 62 beats the even split (14.9 vs 15.6 ms per step)
-  int P = env_int("CCE_STREAM_P", (grid * 36 / 148 + 1) & ~1);
-  int Qc = dc ? env_int("CCE_STREAM_QC", (grid * 50 / 148 + 1) & ~1) : 0;
+  // measured at Gemma-2-2B (148 SMs): 32 / 54 / 62 (6.14 ms backward pass) beats 36 / 50 / 62
+  // (6.27 ms) and the even split (scripts/ab_r2/r2_split2.sh)
+  int P = env_int("CCE_STREAM_P", (grid * 32 / 148 + 1) & ~1);
+  int Qc = dc ? env_int("CCE_STREAM_QC", (grid * 54 / 148 + 1) & ~1) : 0;
   P = std::max(2, P & ~1);
   Qc = dc ? std::max(2, Qc & ~1) : 0;
   if (!de_out) Qc = grid - P;
