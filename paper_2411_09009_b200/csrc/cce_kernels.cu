@@ -1668,10 +1668,16 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
 
   // roles: producers and dC consumers as CTA pairs, dE consumers single (about a third each)
   const int grid = sms & ~1;
-  // measured at Gemma-2-2B (148 SMs): 32 / 54 / 62 (6.14 ms backward pass) beats 36 / 50 / 62
-  // (6.27 ms) and the even split (scripts/ab_r2/r2_split2.sh)
-  int P = env_int("CCE_STREAM_P", (grid * 32 / 148 + 1) & ~1);
-  int Qc = dc ? env_int("CCE_STREAM_QC", (grid * 54 / 148 + 1) & ~1) : 0;
+  // Recompute CTAs by hidden size: a kept tile's recompute has a fixed epilogue (S-hat of 128 x 256
+  // logits) and a mainloop growing with D, the contractions grow with D alone, so small heads need
+  // more recompute CTAs.  Measured best (148 SMs, scripts/ab_r2/r2_split2.sh, r2_splitd.sh): 56 at
+  // D = 768 (1.15 vs 1.57 ms with 32), 36 at 1536, 32 at 2304 (6.14 vs 6.27 ms with 36) and 4096;
+  // the rest split 54 : 62 between dC and dE.
+  const double pd = d <= 768 ? 56.0 : d <= 1536 ? 56.0 - (d - 768) * (20.0 / 768.0)
+                    : d <= 2304 ? 36.0 - (d - 1536) * (4.0 / 768.0) : 32.0;
+  const int p_def = ((int)(grid * pd / 148.0 + 0.5) + 1) & ~1;
+  int P = env_int("CCE_STREAM_P", p_def);
+  int Qc = dc ? env_int("CCE_STREAM_QC", ((int)((grid - p_def) * 54.0 / 116.0 + 0.5) + 1) & ~1) : 0;
   P = std::max(2, P & ~1);
   Qc = dc ? std::max(2, Qc & ~1) : 0;
   if (!de_out) Qc = grid - P;
