@@ -155,6 +155,17 @@ SideStream* side_stream() {
   return &x;
 }
 
+// The last streamed pass launched on a device (cce_bwd_stream_ex): passes are chained across streams.
+struct PassOrder {
+  std::mutex mu;
+  cudaEvent_t last = nullptr;
+  cudaStream_t stream = nullptr;
+};
+PassOrder& pass_order(int dev) {
+  static PassOrder po[64];
+  return po[dev & 63];
+}
+
 constexpr size_t kCtrlBytes = 256;
 static_assert(kCtrlBytes == cce::LSE_CTRL_BYTES, "logit-tile kernel control block");
 constexpr size_t kLseSmem = 1024 + (size_t)cce::LSE_STAGES * cce::STAGE_BYTES + kCtrlBytes + cce::LSE_IDX_BYTES;
@@ -1770,7 +1781,28 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
     fprintf(stderr, "cce_bwd_stream: grid %d P %d Qc %d ring %d window %d consumers %d | ready %p used %p "
             "chain_e %p chain_c %p gen_e %p gen_c %p ctrl %p\n", grid, P, Qc, R, W, consumers, (void*)w.ready,
             (void*)w.used, (void*)w.chain_e, (void*)w.chain_c, (void*)w.gen_e, (void*)w.gen_c, (void*)w.ctrl);
-  PdlScope spdl(!(pdl_mask & 2));
+  // Two streamed passes must never run at once: each needs every SM (one CTA per SM, CTAs waiting
+  // on each other), so two passes sharing the GPU could each hold half of it and wait forever.
+  // Passes of this process on one device are chained: a pass on another stream than the previous
+  // one waits for it first (same stream: already ordered).  Not under stream capture (a graph
+  // orders its own work).
+  int dev_id = 0;
+  CCE_CUDA(cudaGetDevice(&dev_id));
+  PassOrder& order = pass_order(dev_id);
+  std::lock_guard<std::mutex> order_lock(order.mu);
+  cudaStreamCaptureStatus capture = cudaStreamCaptureStatusNone;
+  CCE_CUDA(cudaStreamIsCapturing(stream, &capture));
+  const bool ordered = capture == cudaStreamCaptureStatusNone;
+  bool waited = false;
+  if (ordered) {
+    if (!order.last) {
+      CCE_CUDA(cudaEventCreateWithFlags(&order.last, cudaEventDisableTiming));
+    } else if (order.stream != stream) {
+      CCE_CUDA(cudaStreamWaitEvent(stream, order.last, 0));
+      waited = true;
+    }
+  }
+  PdlScope spdl(!(pdl_mask & 2) && !waited);
   if (de_ch == 2) {
     constexpr size_t smem = std::max({kLsePairSmem, kDcSmem, de_smem<2, 32>()});
     if (int e = ensure_attr(cce::cce_stream3_kernel<2, 32>, smem)) return e;
@@ -1783,6 +1815,10 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
     if (int e = launch_k(cce::cce_stream3_kernel<1, 64>, dim3(grid), dim3(cce::NUM_THREADS), smem, stream, 2, tmE,
                          tmC128, tmSe, tmCk, tmC3, tmSc, tmE64, tmE3h, p, qe, qc, Qc))
       return e;
+  }
+  if (ordered) {
+    CCE_CUDA(cudaEventRecord(order.last, stream));
+    order.stream = stream;
   }
   if (de_done_event) CCE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(de_done_event), stream));
   if (sorted_out)

@@ -10,7 +10,8 @@ sys.path.insert(0, ".")
 from paper_2411_09009_b200 import ops  # noqa: E402
 
 CFG = {"gemma2-2b": (8192, 2304, 256000, 0.0), "gpt2": (4096, 768, 50257, 0.0), "small": (2048, 512, 40000, 0.0),
-       "llama": (8192, 4096, 128256, 0.0), "d1536": (8192, 1536, 128000, 0.0)}
+       "llama": (8192, 4096, 128256, 0.0), "d1536": (8192, 1536, 128000, 0.0),
+       "gemma9b": (32768, 3584, 256000, 30.0), "gemma2b-cap": (8192, 2304, 256000, 30.0)}
 name = sys.argv[1] if len(sys.argv) > 1 else "gemma2-2b"
 n, d, v, cap = CFG[name]
 g = torch.Generator(device="cuda").manual_seed(0)
