@@ -221,3 +221,25 @@ def test_bounded_default_beyond_2048_token_tiles(cuda_device):
     assert abs(lb - lf) <= 1e-4 * abs(lf), (lb, lf)
     assert _rel(out["bounded"][1], out["fast"][1]) < 1e-2
     assert _rel(out["bounded"][2], out["fast"][2]) < 1e-2
+
+
+def test_bounded_default_across_changing_batches(cuda_device):
+    """A training loop whose batches change shape and padding from step to step (the learned
+    compaction choice and ring sizing follow the batch): every step equals memory="fast"."""
+    from paper_2411_09009_b200 import linear_cross_entropy
+
+    d, v = 256, 30000
+    for step, (n, ign) in enumerate([(3000, 0.0), (3000, 0.3), (5000, 0.3), (5000, 0.0), (700, 0.5), (3000, 0.0)]):
+        e0, c0, t = _head(n, d, v, 100 + step, sigma=2.0, ign=ign)
+        out = {}
+        for mode in ("bounded", "fast"):
+            e = e0.clone().requires_grad_(True)
+            c = c0.clone().requires_grad_(True)
+            loss = linear_cross_entropy(e, c, t, memory=mode)
+            loss.backward()
+            torch.cuda.synchronize()
+            out[mode] = (loss.item(), e.grad, c.grad)
+        assert abs(out["bounded"][0] - out["fast"][0]) <= 1e-4 * abs(out["fast"][0]), step
+        assert _rel(out["bounded"][1], out["fast"][1]) < 1e-2, step
+        assert _rel(out["bounded"][2], out["fast"][2]) < 1e-2, step
+        assert torch.all(out["bounded"][1][t == -100] == 0), step
