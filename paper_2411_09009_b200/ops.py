@@ -999,13 +999,15 @@ STREAM_RING_SLOTS = 512  # S-hat ring of the streamed backward (64 KiB slots: 32
 
 def stream_ring_slots(token_tiles: int = 0) -> int:
     """S-hat ring slots of one streamed pass: 512, or 8 per token tile (dE windows of half the
-    ring then hold >= 4 items of every token tile), up to 2048 (128 MiB).  Measured at
-    Gemma-2-9B (256 token tiles): 84 ms per step with 2048 slots in one pass, against 104 ms
-    with four 64-tile chunks of 512 slots (scripts/ab_r2/r2_s57.sh)."""
+    ring then hold >= 4 items of every token tile), up to 4096 (256 MiB, 512 token tiles).
+    Measured at Gemma-2-9B (256 token tiles): 84 ms per step with 2048 slots in one pass, against
+    104 ms with four 64-tile chunks of 512 slots (scripts/ab_r2/r2_s57.sh); at NeMo (512 token
+    tiles) one pass with 4096 slots takes 336 ms at a 1.70 GiB step peak, two 256-tile chunks
+    323 ms at 2.78 GiB (scripts/ab_r2/r2_nemo.sh)."""
     env = os.environ.get("CCE_STREAM_RING")
     if env is not None:
         return max(128, int(env))
-    return max(STREAM_RING_SLOTS, min(4 * STREAM_RING_SLOTS, 8 * token_tiles))
+    return max(STREAM_RING_SLOTS, min(8 * STREAM_RING_SLOTS, 8 * token_tiles))
 
 
 def stream_supported(d: int) -> bool:
@@ -1065,7 +1067,7 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
     return de, dc, counters
 
 
-STREAM_CHUNK_TILES = 256  # token tiles per streamed pass (32768 rows; ring sized by stream_ring_slots)
+STREAM_CHUNK_TILES = 512  # token tiles per streamed pass (65536 rows; ring sized by stream_ring_slots)
 
 
 def stream_chunk_tiles() -> int:
@@ -1075,12 +1077,12 @@ def stream_chunk_tiles() -> int:
 def backward_stream_chunked(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,
                             fp32_de: bool = False, de_done=None, label_split: bool = False, correct=None,
                             want_de: bool = True, want_dc: bool = True):
-    """The streamed backward of a large batch as token chunks of STREAM_CHUNK_TILES tiles (32768 rows).
+    """The streamed backward of a large batch as token chunks of STREAM_CHUNK_TILES tiles (65536 rows).
 
     The pass's dE segments are a token tile's items inside one window of ring / 2 stream items;
     with more token tiles than a quarter window they shrink below a few items, and every segment
     costs an fp32 read-modify-write of the tile's 128 x D partial sum.  The ring grows with the
-    token tiles up to 2048 slots (stream_ring_slots); beyond that each chunk is its own
+    token tiles up to 4096 slots (stream_ring_slots); beyond that each chunk is its own
     pass over the same global decision inputs (tile maxima rows, lse, the vocabulary order): its
     tile decisions equal the whole batch's, dE rows are written once by their chunk, and dC adds
     over the chunks in bf16 (the fast path's group fallback does the same).  The sorted classifier

@@ -36,7 +36,7 @@ def _budget(n, d, v):
     # 8 groups x 8 vocabulary splits between folds
     fwd = tile_max + 2 * 48 * MIB + 64 * n * 8 + lists + 2 * MIB
     acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
-    ring = max(512, min(2048, 8 * nt)) * 64 * 1024  # ops.stream_ring_slots
+    ring = max(512, min(4096, 8 * nt)) * 64 * 1024  # ops.stream_ring_slots
     step = ring + acc + tile_max + lists + 4 * MIB
     return fwd, step
 
