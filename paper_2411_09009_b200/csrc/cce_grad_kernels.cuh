@@ -857,7 +857,10 @@ __device__ __forceinline__ void dc_body(const CUtensorMap& tmS, const CUtensorMa
               x[j] = __uint_as_float(r0[j]);
               x[32 + j] = __uint_as_float(r1[j]);
             }
-            if (racc) {
+            // as in dE: a middle segment adds its partial with L2 vector reductions (no read; the
+            // chain orders the segments), the first stores, the last folds in and writes dC
+            const bool mid = CCE_DE_RED && racc && wacc;
+            if (racc && !mid) {
 #pragma unroll
               for (int j = 0; j < 64; j += 4) {
                 const float4 o = __ldcg(reinterpret_cast<const float4*>(racc) + (c * 16 + j / 4) * BM);
@@ -869,9 +872,13 @@ __device__ __forceinline__ void dc_body(const CUtensorMap& tmS, const CUtensorMa
             }
             if (wacc) {
 #pragma unroll
-              for (int j = 0; j < 64; j += 4)
-                __stcg(reinterpret_cast<float4*>(wacc) + (c * 16 + j / 4) * BM,
-                       make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+              for (int j = 0; j < 64; j += 4) {
+                float4* dst = reinterpret_cast<float4*>(wacc) + (c * 16 + j / 4) * BM;
+                if (mid)
+                  red_add_v4_f32(reinterpret_cast<float*>(dst), x[j], x[j + 1], x[j + 2], x[j + 3]);
+                else
+                  __stcg(dst, make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+              }
               continue;  // warp-uniform: every thread of the unit takes this branch
             }
 #pragma unroll
