@@ -650,6 +650,7 @@ __device__ __forceinline__ void dc_body(const CUtensorMap& tmS, const CUtensorMa
       auto tile = [&](int ln, int slot, int sig = -1) {
         const int n = p.n_base + ln;
         if (gather_pair) {
+          __syncwarp();  // every lane is done reading the previous item's table
           load_index_table(s_eidx, p.row_map, n * BM, BM, rows.n);
           __syncwarp();
         }

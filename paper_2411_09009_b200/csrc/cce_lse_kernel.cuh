@@ -186,6 +186,7 @@ __device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorM
     };
     const uint32_t tx_cta = (gather_e ? 0u : (uint32_t)A_BYTES) + (gather_c ? 0u : (uint32_t)CROWS * BK * 2);
     for_each_tile<MODE, CG>(p, rows, rank, bid, nblk, [&](const TileRef& t) {
+      if (gmode) __syncwarp();  // every lane is done reading the tables for the previous tile
       if (gather_e && t.n != cur_n) {
         load_index_table(s_eidx, p.row_map, t.n * BM, BM, rows.n);
         cur_n = t.n;
