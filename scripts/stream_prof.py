@@ -41,7 +41,7 @@ print(f"units {len(P)}, ctas {len(np.unique(bid))}, windows {win.max() + 1}, spa
 cols = ["prod_start", "loads_done", "epi_begin", "acc_full", "chain_ok", "epi_end"]
 for k in range(1, 6):
     dlt = T[:, k] - T[:, k - 1]
-    print(f"{cols[k-1]}->{cols[k]}: mean {np.nanmean(dlt):.1f} us, p50 {np.nanpercentile(dlt, 50):.1f}, p90 {np.nanpercentile(dlt, 90):.1f}, max {np.nanmax(dlt):.1f}")
+    print(f"{cols[k-1]}->{cols[k]}: mean {np.nanmean(dlt):.2f} us, p50 {np.nanpercentile(dlt, 50):.2f}, p90 {np.nanpercentile(dlt, 90):.2f}, max {np.nanmax(dlt):.1f}")
 for w in [0, 1, 2, 10, 20, int(win.max())]:
     m = win == w
     print(f"window {w}: units {m.sum()}, loads from {np.nanmin(T[m,0]):.0f} to {np.nanmax(T[m,1]):.0f} us, "
