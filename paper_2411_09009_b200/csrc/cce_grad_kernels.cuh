@@ -257,9 +257,18 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (stream) s_sig[stage] = h == BN / DE_KV - 1 ? sig : -1;
-            mbar_arrive_expect_tx(&full[stage], bytes);
+            // debug (timing only, wrong results): bit 0 skips the S-hat loads, bit 1 the C loads
+            mbar_arrive_expect_tx(&full[stage], bytes - ((p.debug & 1) ? DE_A_BYTES : 0) -
+                                                    ((p.debug & 2) ? nch * DE_CHUNK_BYTES : 0));
             // S-hat [128 tok][KV voc]: swizzle atom h of the stored tile
 #if CCE_DE_HINT > 0
+            if (p.debug & 3) {
+              if (!(p.debug & 1)) tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
+              if (plain && !(p.debug & 2))
+                for (int c = 0; c < nch; ++c)
+                  tma_load_3d(&tmC3, &full[stage], sb + c * DE_CHUNK_BYTES, 0, m * BN + DE_KV * h,
+                              (DE_CH * j + c) * (DCH / 64));
+            } else {
             // L2 priorities: 1 (default) = keep C slices (shared by the token tiles of a chunk,
             // which reach a vocab tile tens of us apart), stream S-hat; 2 = the reverse (slower)
             const uint64_t pol_s = CCE_DE_HINT == 1 ? l2_policy_evict_first() : l2_policy_evict_last();
@@ -269,6 +278,7 @@ __device__ __forceinline__ void de_body(const CUtensorMap& tmS, const CUtensorMa
               for (int c = 0; c < nch; ++c)
                 tma_load_3d_hint(&tmC3, &full[stage], sb + c * DE_CHUNK_BYTES, 0, m * BN + DE_KV * h,
                                  (DE_CH * j + c) * (DCH / 64), pol_c);
+            }
 #else
             tma_load_3d(&tmS, &full[stage], sa, 0, slot * BM, h);
             if (plain)  // C [64 voc][256 d] per chunk as 4 atoms

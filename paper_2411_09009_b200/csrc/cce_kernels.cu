@@ -1750,7 +1750,8 @@ int cce_bwd_stream_ex(const void* E, int e_gather, const void* C, void* c_sorted
   qe.chain = w.chain_e;
   qe.acc = w.acc_e;
   qe.nacc = nt;
-  qe.debug = env_int("CCE_STREAM_DEBUG_DE", 0);  // diagnostics only (wrong results): 4 skip fold-in loads, 8 no stores
+  // diagnostics only (wrong results): 1 / 2 skip the S-hat / C operand loads, 4 the fold-in loads, 8 the stores
+  qe.debug = env_int("CCE_STREAM_DEBUG_DE", 0);
   qe.acc_gen = w.gen_e;
   qe.de_bf16 = de_fp32 ? nullptr : static_cast<__nv_bfloat16*>(de_out);
   qe.de_f32 = de_fp32 ? static_cast<float*>(de_out) : nullptr;
