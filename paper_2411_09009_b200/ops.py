@@ -770,11 +770,43 @@ FWD_GROUP_MB = 48  # sorted classifier rows of one vocabulary group in the bound
 FWD_FOLD_GROUPS = 8  # groups whose (max, sum-exp) partials are folded by one combine launch
 
 
-def fwd_group_tiles(d: int, mt: int) -> int:
+def fwd_group_tiles(d: int, mt: int, n: int = 0, sms: int = 0) -> int:
     """Vocab tiles per group of the bounded forward: the group's sorted rows within
-    CCE_FWD_GROUP_MB (default 48 MB; 40 tiles at D = 2304)."""
+    CCE_FWD_GROUP_MB (default 48 MB; at most 40 tiles at D = 2304), sized so each launch's tiles
+    fill whole waves of the persistent grid.  Each group launch sweeps (token-tile pairs) x (group
+    tiles) logit tiles over sms/2 CTA pairs and ends when its last wave does, so a group whose tile
+    count is a multiple of the pair count wastes no tail: at Gemma-2B 37 tiles x 32 pairs = 16
+    waves of 74 pairs (27 groups + 1) instead of 40 x 32 = 17.3 waves (25 groups); ~0.14 ms per
+    forward (`scripts/ab_r2/r2_fgroup.sh`).  The estimate counts waves plus a small per-launch
+    cost over candidate sizes down to 3/4 of the budget; batches the kernel rasters in bands
+    (many token tiles) keep the budget's size."""
     budget = int(os.environ.get("CCE_FWD_GROUP_MB", FWD_GROUP_MB)) << 20
-    return max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
+    cap = max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
+    if n <= 0 or sms <= 0 or os.environ.get("CCE_FWD_GROUP_FIT", "1") == "0":
+        return cap
+    pairs = os.environ.get("CCE_PAIR", "1") != "0" and sms >= 2
+    units = -(-(-(-n // BLOCK_TOKENS)) // (2 if pairs else 1))  # token tiles (pairs) per launch
+    grid = sms // 2 if pairs else sms
+    if units > max(1, (40 << 20) // (BLOCK_TOKENS * d * 2 * (2 if pairs else 1))) and units >= grid:
+        return cap  # banded raster (cce_kernels.cu lse_raster): not whole-wave launches
+    launch_cost = 0.4  # waves: launch gap + pipeline fill of one group launch
+
+    def cost(g):
+        full, rest = divmod(mt, g)
+        waves = full * -(-(units * g) // grid) + (-(-(units * rest) // grid) if rest else 0)
+        return waves + launch_cost * (full + (1 if rest else 0))
+
+    return min(range(cap, max(1, (3 * cap) // 4) - 1, -1), key=cost)  # ties: the larger group
+
+
+_SMS: dict = {}
+
+
+def _sm_count(dev: torch.device) -> int:
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _SMS:
+        _SMS[key] = torch.cuda.get_device_properties(key).multi_processor_count
+    return _SMS[key]
 
 
 _SIDE: dict = {}
@@ -817,7 +849,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
     if n == 0:
         z = torch.zeros(0, dtype=torch.float32, device=dev)
         return z, z.clone(), state
-    gt = fwd_group_tiles(d, mt)
+    gt = fwd_group_tiles(d, mt, n, _sm_count(dev))
     groups = [(m0 * BLOCK_VOCAB, min(v, (m0 + gt) * BLOCK_VOCAB)) for m0 in range(0, mt, gt)]
     # the groups' (max, sum-exp) partials side by side after a running one (slot 0), folded into it
     # every FWD_FOLD_GROUPS groups and finished by one combine; the target logit lands in exactly

@@ -6,7 +6,7 @@ outputs) with a recorded formula, 4 * (8 (N + V) + 8 threads (n_b m_b + d_b (n_b
 ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu):
 
   forward   per-row tile maxima  ceil(N/128) * ceil(V/256) * 512 B
-            two vocabulary groups of sorted classifier rows (CCE_FWD_GROUP_MB, 48 MiB each: the
+            two vocabulary groups of sorted classifier rows (at most CCE_FWD_GROUP_MB, 48 MiB, each: the
             next group is gathered on a side stream while one is swept)
             O(N + V) maps and partials; a batch with ignored rows adds their compacted copy
   backward  the S-hat ring (512 slots x 64 KiB = 32 MiB; 8 slots per token tile above 64 tiles)
