@@ -9,6 +9,7 @@ anything on the host; if libcce_b200.so is missing, the first call raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 from dataclasses import dataclass
 
@@ -784,7 +785,12 @@ def fwd_group_tiles(d: int, mt: int, n: int = 0, sms: int = 0) -> int:
     cap = max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
     if n <= 0 or sms <= 0 or os.environ.get("CCE_FWD_GROUP_FIT", "1") == "0":
         return cap
-    pairs = os.environ.get("CCE_PAIR", "1") != "0" and sms >= 2
+    return _fitted_group_tiles(d, mt, n, sms, cap, os.environ.get("CCE_PAIR", "1") != "0")
+
+
+@functools.lru_cache(maxsize=256)
+def _fitted_group_tiles(d: int, mt: int, n: int, sms: int, cap: int, pair_env: bool) -> int:
+    pairs = pair_env and sms >= 2
     units = -(-(-(-n // BLOCK_TOKENS)) // (2 if pairs else 1))  # token tiles (pairs) per launch
     grid = sms // 2 if pairs else sms
     if units > max(1, (40 << 20) // (BLOCK_TOKENS * d * 2 * (2 if pairs else 1))) and units >= grid:
