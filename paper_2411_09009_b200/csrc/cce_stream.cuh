@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ---------------------------------------------------------------------------------------------
 // In-place row permutation: rows X[p] (sorted position p) move to row perm[p] (vocabulary order).
 // Position t receives X[inv[t]].
-//  * A cycle of length <= PERM_SEG without an anchor (a hash of the position selects 1 in PERM_K)
+//  * A cycle of length <= PERM_SEG without an anchor (a hash of the position selects 1 in PERM_K = 32)
 //    is rotated by the warps of its smallest position (rotation list), the first row held in
 //    registers.
 //  * Every other cycle is cut into segments at break points: its anchors (or, with none, its
@@ -328,13 +328,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // Segments, rotations and column blocks are independent, so every warp runs in parallel.  More
 // breaks than tmp rows (cap) trap; the cap covers every permutation (anchors + cuts).
 // ---------------------------------------------------------------------------------------------
-constexpr int PERM_K = 64;      // anchor density 1 / PERM_K
+#ifndef CCE_PERM_K_LOG2
+#define CCE_PERM_K_LOG2 5
+#endif
+constexpr int PERM_K = 1 << CCE_PERM_K_LOG2;  // anchor density 1 / PERM_K
 constexpr int PERM_SEG = 96;    // longest segment: positions per break entry of the chain table
 constexpr int PERM_L = 8192;    // a walk this long without an anchor makes the position a break
 constexpr int PERM_VEC = 1;     // uint4 per lane of a column block: 256 columns per warp
 constexpr int PERM_COLS = 32 * 8 * PERM_VEC;
 constexpr int PERM_DEPTH = 8;   // row moves whose loads are in flight together
-__device__ __forceinline__ bool perm_anchor(int p) { return ((uint32_t)p * 2654435761u) >> 26 == 0; }  // 1 in 64
+__device__ __forceinline__ bool perm_anchor(int p) { return ((uint32_t)p * 2654435761u) >> (32 - CCE_PERM_K_LOG2) == 0; }
 
 // cls: 0 fixed point or rotation member / owner, 1 break, 2 + (r - 1) member at distance r of its owner (own[p] = owner
 // position); breaks: bidx[b] = k, blist[k] = b
