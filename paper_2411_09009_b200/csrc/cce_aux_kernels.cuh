@@ -13,20 +13,42 @@ namespace cce {
 
 // Merge the per-split (max2, sum2) partials of each row into this shard's natural-log LSE.
 // out_part != nullptr: fold the partials into one (max, sum-exp) pair instead (it may alias part:
-// each thread reads its row of every partial before writing)
-__global__ void combine_splits_kernel(const float2* part, int splits, int n, float* __restrict__ lse_local,
-                                      float2* out_part) {
+// every read of a row precedes the block barrier before its write).  Block = 32 rows x
+// COMBINE_GROUPS slot groups: warp g reads slots g, g + 8, ... of 32 consecutive rows (coalesced
+// 256 B per slot), the groups' maxima and then their sums meet in shared memory in a fixed order
+// (deterministic).  Hundreds of partials per row (the bounded forward folds 8 groups of up to
+// ~40 splits) cost a few microseconds instead of a serial loop per thread.
+constexpr int COMBINE_ROWS = 32;
+constexpr int COMBINE_GROUPS = 8;
+__global__ void __launch_bounds__(COMBINE_ROWS * COMBINE_GROUPS)
+    combine_splits_kernel(const float2* part, int splits, int n, float* __restrict__ lse_local, float2* out_part) {
   griddep_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  __shared__ float s_red[COMBINE_GROUPS][COMBINE_ROWS];
+  const int r = threadIdx.x & (COMBINE_ROWS - 1);
+  const int g = threadIdx.x / COMBINE_ROWS;
+  const int i = blockIdx.x * COMBINE_ROWS + r;
+  const bool ok = i < n;
   float m = -INFINITY;
-  for (int s = 0; s < splits; ++s) m = fmaxf(m, part[(size_t)s * n + i].x);
+  if (ok)
+    for (int s = g; s < splits; s += COMBINE_GROUPS) m = fmaxf(m, part[(size_t)s * n + i].x);
+  s_red[g][r] = m;
+  __syncthreads();
+  m = s_red[0][r];
+#pragma unroll
+  for (int k = 1; k < COMBINE_GROUPS; ++k) m = fmaxf(m, s_red[k][r]);
   float acc = 0.f;
-  if (m != -INFINITY)
-    for (int s = 0; s < splits; ++s) {
+  if (ok && m != -INFINITY)
+    for (int s = g; s < splits; s += COMBINE_GROUPS) {
       const float2 v = part[(size_t)s * n + i];
       acc += v.y * exp2f(v.x - m);
     }
+  __syncthreads();  // every group has read the maxima
+  s_red[g][r] = acc;
+  __syncthreads();
+  if (g != 0 || !ok) return;
+  acc = s_red[0][r];
+#pragma unroll
+  for (int k = 1; k < COMBINE_GROUPS; ++k) acc += s_red[k][r];
   if (out_part)
     out_part[i] = make_float2(m, acc);
   else

@@ -579,7 +579,8 @@ int cce_fwd(const void* E, const void* C, const int64_t* targets, int64_t n, int
   PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   (void)units;
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
-  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local,
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + cce::COMBINE_ROWS - 1) / cce::COMBINE_ROWS)),
+             dim3(cce::COMBINE_ROWS * cce::COMBINE_GROUPS), 0, stream, static_cast<const float2*>(ws), splits, (int)n, lse_local,
              (float2*)nullptr);
   CCE_CUDA(cudaGetLastError());
   return 0;
@@ -887,7 +888,8 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
     PDL_LAUNCH(cce::fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream, correct, 0.f, n);
   if (int e = launch_lse<cce::FWD>(p, pair, tmE, tmE, tmC, tmC, tmC128, stream)) return e;
   if (!(flags & 2))
-    PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream,
+    PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + cce::COMBINE_ROWS - 1) / cce::COMBINE_ROWS)),
+             dim3(cce::COMBINE_ROWS * cce::COMBINE_GROUPS), 0, stream,
                static_cast<const float2*>(ws), splits, (int)n, lse_local,
              (float2*)nullptr);
   CCE_CUDA(cudaGetLastError());
@@ -930,7 +932,8 @@ int cce_combine_parts(const void* parts, int count, int64_t n, float* lse_out, v
   // unpermute_rows)
   PdlScope pdl_scope(false);
   // lse_out == nullptr: fold into the first partial (parts[0]) instead
-  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, stream,
+  PDL_LAUNCH(cce::combine_splits_kernel, dim3((unsigned)((n + cce::COMBINE_ROWS - 1) / cce::COMBINE_ROWS)),
+             dim3(cce::COMBINE_ROWS * cce::COMBINE_GROUPS), 0, stream,
              static_cast<const float2*>(parts), count, (int)n, lse_out,
              lse_out ? nullptr : static_cast<float2*>(const_cast<void*>(parts)));
   CCE_CUDA(cudaGetLastError());

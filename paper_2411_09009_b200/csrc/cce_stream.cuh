@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ---------------------------------------------------------------------------------------------
 // In-place row permutation: rows X[p] (sorted position p) move to row perm[p] (vocabulary order).
 // Position t receives X[inv[t]].
-//  * A cycle of length <= PERM_SEG without an anchor (a hash of the position selects 1 in PERM_K = 32)
+//  * A cycle of length <= PERM_SEG without an anchor (a hash of the position selects 1 in PERM_K = 64)
 //    is rotated by the warps of its smallest position (rotation list), the first row held in
 //    registers.
 //  * Every other cycle is cut into segments at break points: its anchors (or, with none, its
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // breaks than tmp rows (cap) trap; the cap covers every permutation (anchors + cuts).
 // ---------------------------------------------------------------------------------------------
 #ifndef CCE_PERM_K_LOG2
-#define CCE_PERM_K_LOG2 5
+#define CCE_PERM_K_LOG2 6
 #endif
 constexpr int PERM_K = 1 << CCE_PERM_K_LOG2;  // anchor density 1 / PERM_K
 constexpr int PERM_SEG = 96;    // longest segment: positions per break entry of the chain table

@@ -11,7 +11,8 @@ ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu)
             O(N + V) maps and partials; a batch with ignored rows adds their compacted copy
   backward  the S-hat ring (512 slots x 64 KiB = 32 MiB; 8 slots per token tile above 64 tiles)
             split-owner accumulators: ceil(N/128) * ceil(D/256) * 128 KiB (fp32 dE partial sums
-            across stream windows) + 4 * ceil(D/256) * 256 KiB (vocab tiles over several segments)
+            across stream windows) + 4 * ceil(D/256) * 256 KiB (vocab tiles over several segments),
+            or, if larger, the unpermutation's saved break rows (V/64 * 5/4 + V/96 + 1024 rows of D)
             the tile maxima, O(N + V) maps and O(ceil(N/128) * ceil(V/256)) lists
 
 No term depends on how many tiles the filter keeps: the test runs each head at two logit scales
@@ -36,6 +37,10 @@ def _budget(n, d, v):
     # 8 groups x 8 vocabulary splits between folds
     fwd = tile_max + 2 * 48 * MIB + 64 * n * 8 + lists + 2 * MIB
     acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
+    # the unpermutation's saved break rows reuse the accumulators' storage after the pass: one row
+    # per break (anchors 1 in 64 with headroom, cuts every 96 positions); larger at small N, large D
+    perm_cap = v // 64 * 5 // 4 + v // 96 + 1024
+    acc = max(acc, perm_cap * d * 2)
     ring = max(512, min(4096, 8 * nt)) * 64 * 1024  # ops.stream_ring_slots
     step = ring + acc + tile_max + lists + 4 * MIB
     return fwd, step

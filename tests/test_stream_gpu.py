@@ -156,7 +156,7 @@ def test_unpermute_rows_in_place(cuda_device, v, d, kind):
     elif kind == "swaps":
         perm = torch.arange(v, device="cuda").view(-1, 2).flip(1).reshape(-1)
     else:  # one 500-long cycle through positions that are not anchors (cut every 96 from its minimum)
-        idx = [p for p in range(v) if ((p * 2654435761) & 0xFFFFFFFF) >> 27 != 0][:500]
+        idx = [p for p in range(v) if ((p * 2654435761) & 0xFFFFFFFF) >> 26 != 0][:500]
         perm = torch.arange(v, device="cuda")
         src = torch.tensor(idx, device="cuda")
         perm[src] = torch.roll(src, 1)
