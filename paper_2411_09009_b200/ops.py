@@ -773,11 +773,11 @@ FWD_FOLD_GROUPS = 8  # groups whose (max, sum-exp) partials are folded by one co
 
 def fwd_group_tiles(d: int, mt: int, n: int = 0, sms: int = 0) -> int:
     """Vocab tiles per group of the bounded forward: the group's sorted rows within
-    CCE_FWD_GROUP_MB (default 48 MB; at most 40 tiles at D = 2304), sized so each launch's tiles
+    CCE_FWD_GROUP_MB (default 48 MB; at most 42 tiles at D = 2304), sized so each launch's tiles
     fill whole waves of the persistent grid.  Each group launch sweeps (token-tile pairs) x (group
     tiles) logit tiles over sms/2 CTA pairs and ends when its last wave does, so a group whose tile
     count is a multiple of the pair count wastes no tail: at Gemma-2B 37 tiles x 32 pairs = 16
-    waves of 74 pairs (27 groups + 1) instead of 40 x 32 = 17.3 waves (25 groups); ~0.14 ms per
+    waves of 74 pairs (27 groups + 1) instead of 42 x 32 = 18.2 waves (24 groups); ~0.14 ms per
     forward (`scripts/ab_r2/r2_fgroup.sh`).  The estimate counts waves plus a small per-launch
     cost over candidate sizes down to 3/4 of the budget; batches the kernel rasters in bands
     (many token tiles) keep the budget's size."""
@@ -832,7 +832,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
 
     indexed_matmul + lse_forward (kernels.py:204-319) over the backward's tiles (compacted rows,
     the reference's vocabulary order) with the per-row tile maxima the decision needs, run over
-    vocabulary groups: each group's classifier rows are gathered into one of two 48 MB buffers (on
+    vocabulary groups: each group's classifier rows are gathered into one of two <= 48 MB buffers (on
     a side stream, while the previous group is swept) and swept with plain TMA tiles; the groups'
     (max, sum-exp) partials are folded by log-add-exp (kernels.py:121-137).  E is read in place
     when no row is ignored and as a compacted copy otherwise (compact_copy_wanted).  Transients:
@@ -1061,7 +1061,8 @@ def backward_stream(e_rows, e_gather: bool, c, perm_padded, inv_perm, row_map, n
     """Streamed backward of the training path (lse_backward, kernels.py:327-486): the decision from
     the forward's tile maxima, then the kept tiles recomputed in token-tile order (dE) and in
     vocabulary-tile order (dC), streamed through a fixed ring of S-hat slots.  Transients: the ring
-    (16 MiB), O(N + V) lists and maps, a few MiB of split accumulators -- none grows with the kept
+    (32 MiB; 8 slots per token tile above 64 tiles), O(N + V) lists and maps, the split accumulators
+    (N x D fp32 for dE) -- none grows with the kept
     count.  With a vocabulary order the sorted classifier lives in dC's own storage.
     `e_rows` is the caller's E (e_gather) or a compacted copy.  Returns (dE, dC, counters[3])."""
     lib = _lib.load()
