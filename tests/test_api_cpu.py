@@ -124,3 +124,25 @@ def test_capacity_hint_cache_is_bounded(monkeypatch):
         ops._remember_count(("shape", i), torch.tensor([i, 2 * i]), 1)
     assert len(ops._KEPT_HINT) == 8
     assert ("shape", 49) in ops._KEPT_HINT and ("shape", 0) not in ops._KEPT_HINT
+
+
+def test_forward_groups_fill_whole_waves(monkeypatch):
+    """ops.fwd_group_tiles: the bounded forward's vocabulary groups stay within the byte budget
+    and, when a smaller group fills whole waves of the CTA-pair grid, take it (Gemma-2B on 148
+    SMs: 37 tiles x 32 token-tile pairs = 16 waves of 74 pairs; the budget alone gives 42)."""
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.delenv("CCE_FWD_GROUP_MB", raising=False)
+    monkeypatch.delenv("CCE_FWD_GROUP_FIT", raising=False)
+    mt = 1000
+    assert ops.fwd_group_tiles(2304, mt) == 42
+    g = ops.fwd_group_tiles(2304, mt, 8192, 148)
+    assert g == 37 and (32 * g) % 74 == 0
+    for n, d, v in [(4096, 768, 50257), (16384, 4096, 128256), (300, 64, 1000), (1, 64, 256),
+                    (32768, 3584, 256000), (65536, 5120, 131072)]:
+        m = -(-v // 256)
+        cap = ops.fwd_group_tiles(d, m)
+        g = ops.fwd_group_tiles(d, m, n, 148)
+        assert 1 <= g <= cap and g * 256 * d * 2 <= max(48 << 20, 256 * d * 2)
+    monkeypatch.setenv("CCE_FWD_GROUP_FIT", "0")
+    assert ops.fwd_group_tiles(2304, mt, 8192, 148) == 42
