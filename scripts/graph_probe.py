@@ -1,58 +1,64 @@
-"""Eager step vs the same step captured in a CUDA graph (same box, same inputs): the difference
-is what launch gaps and host work cost.  Also checks the graph replay's gradients."""
-import math, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-from paper_2411_09009_b200 import linear_cross_entropy
+"""Eager vs CUDA-graph replay of the default training step (linear_cross_entropy fwd+bwd) at a
+BASELINE head: per-step device time over REPS steps, and the replayed step's loss and gradients
+against the eager step on the same inputs (bitwise).  Usage: python scripts/graph_probe.py [config]"""
+import math
+import os
+import sys
 
-N, D, V = 8192, 2304, 256000
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2411_09009_b200 import linear_cross_entropy  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "gemma2-2b"
+reps = int(os.environ.get("REPS", 20))
+n, d, v, cap, pad, sigma = bench.CONFIGS[cfg]
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
-e = torch.randn(N, D, device=dev, generator=g).bfloat16().requires_grad_(True)
-c = (torch.randn(V, D, device=dev, generator=g) / math.sqrt(D)).bfloat16().requires_grad_(True)
-t = torch.randint(0, V, (N,), device=dev, generator=g)
+e = torch.randn(n, d, device=dev, generator=g).bfloat16().requires_grad_(True)
+c = (torch.randn(v, d, device=dev, generator=g) * sigma / math.sqrt(d)).bfloat16().requires_grad_(True)
+t = torch.randint(0, v, (n,), device=dev, generator=g)
 
 
 def step():
-    e.grad = None
-    c.grad = None
-    loss = linear_cross_entropy(e, c, t)
+    e.grad = c.grad = None
+    loss = linear_cross_entropy(e, c, t, softcap=cap or None)
     loss.backward()
     return loss
 
 
-def timed(fn, k=10):
-    for _ in range(3):
-        fn()
+def timed(fn):
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(k):
+    for _ in range(reps):
         fn()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / k
+    return a.elapsed_time(b) / reps
 
 
-eager = timed(step)
-ref = (step().item(), e.grad.clone(), c.grad.clone())
-s = torch.cuda.Stream()
-s.wait_stream(torch.cuda.current_stream())
-with torch.cuda.stream(s):
+side = torch.cuda.Stream()
+side.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(side):
     for _ in range(3):
         step()
-torch.cuda.current_stream().wait_stream(s)
+torch.cuda.current_stream().wait_stream(side)
+timed(step)  # settle
+ref_loss = step().detach().clone()
+ref_de, ref_dc = e.grad.clone(), c.grad.clone()
 graph = torch.cuda.CUDAGraph()
-try:
-    e.grad = None
-    c.grad = None
-    with torch.cuda.graph(graph):
-        loss = linear_cross_entropy(e, c, t)
-        loss.backward()
-    replay = timed(graph.replay)
-    graph.replay()
-    torch.cuda.synchronize()
-    same = torch.equal(e.grad, ref[1]) and torch.equal(c.grad, ref[2]) and loss.item() == ref[0]
-    print(f"eager {eager:.3f} ms/step, graph replay {replay:.3f} ms/step, identical results: {same}")
-except Exception as exc:
-    print(f"eager {eager:.3f} ms/step; capture failed: {type(exc).__name__}: {exc}")
+e.grad = c.grad = None
+with torch.cuda.graph(graph):
+    g_loss = linear_cross_entropy(e, c, t, softcap=cap or None)
+    g_loss.backward()
+g_de, g_dc = e.grad, c.grad
+graph.replay()
+torch.cuda.synchronize()
+same = torch.equal(g_loss, ref_loss) and torch.equal(g_de, ref_de) and torch.equal(g_dc, ref_dc)
+rounds = []
+for _ in range(3):  # interleaved: clocks drift under the power cap
+    rounds.append((timed(step), timed(graph.replay)))
+print(f"{cfg}: " + "  ".join(f"eager {a:.3f} / graph {b:.3f} ms" for a, b in rounds) +
+      f"  bitwise-equal {same}")
