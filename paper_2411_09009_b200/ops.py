@@ -767,35 +767,40 @@ def compact_copy_wanted(n: int, d: int, n_valid: torch.Tensor) -> bool:
     return wanted
 
 
-FWD_GROUP_MB = 48  # sorted classifier rows of one vocabulary group in the bounded forward (two buffers)
+FWD_GROUP_MB = 52  # sorted classifier rows of one vocabulary group in the bounded forward (two buffers)
 FWD_FOLD_GROUPS = 8  # groups whose (max, sum-exp) partials are folded by one combine launch
 
 
 def fwd_group_tiles(d: int, mt: int, n: int = 0, sms: int = 0) -> int:
     """Vocab tiles per group of the bounded forward: the group's sorted rows within
-    CCE_FWD_GROUP_MB (default 48 MB; at most 42 tiles at D = 2304), sized so each launch's tiles
-    fill whole waves of the persistent grid.  Each group launch sweeps (token-tile pairs) x (group
-    tiles) logit tiles over sms/2 CTA pairs and ends when its last wave does, so a group whose tile
-    count is a multiple of the pair count wastes no tail: at Gemma-2B 37 tiles x 32 pairs = 16
-    waves of 74 pairs (27 groups + 1) instead of 42 x 32 = 18.2 waves (24 groups); ~0.14 ms per
-    forward (`scripts/ab_r2/r2_fgroup.sh`).  The estimate counts waves plus a small per-launch
-    cost over candidate sizes down to 3/4 of the budget; batches the kernel rasters in bands
-    (many token tiles) keep the budget's size."""
+    CCE_FWD_GROUP_MB (default 52 MB: 46 tiles at D = 2304, which keeps the forward's peak, 150 MiB,
+    under the backward's 157 MiB), sized so each launch's tiles fill whole waves of the persistent
+    grid.  Each group launch sweeps (token-tile pairs) x (group tiles) logit tiles over sms/2 CTA
+    pairs and ends when its last wave does; every launch also costs its fill and drain
+    (CCE_FWD_LAUNCH_WAVES, 1.5 waves: `scripts/fwd_split_probe.py` measured ~26 us per launch).
+    At Gemma-2B: 46 tiles x 32 token-tile pairs = 19.9 waves of 74 pairs, 22 launches; 0.2-0.3 ms
+    per forward faster than 37-tile groups (27 launches) and ~0.4 ms faster than the unfitted
+    42-tile groups of the 48 MB budget (`scripts/ab_r2/r2_fgroup2.sh`, `r2_fgroup3.sh`).  The
+    estimate (waves plus launches) is minimised over sizes down to 3/4 of the budget; batches the
+    kernel rasters in bands (many token tiles) keep the budget's size."""
     budget = int(os.environ.get("CCE_FWD_GROUP_MB", FWD_GROUP_MB)) << 20
     cap = max(1, min(mt, budget // (BLOCK_VOCAB * d * 2)))
     if n <= 0 or sms <= 0 or os.environ.get("CCE_FWD_GROUP_FIT", "1") == "0":
         return cap
-    return _fitted_group_tiles(d, mt, n, sms, cap, os.environ.get("CCE_PAIR", "1") != "0")
+    return _fitted_group_tiles(d, mt, n, sms, cap, os.environ.get("CCE_PAIR", "1") != "0",
+                               float(os.environ.get("CCE_FWD_LAUNCH_WAVES", 1.5)))
 
 
 @functools.lru_cache(maxsize=256)
-def _fitted_group_tiles(d: int, mt: int, n: int, sms: int, cap: int, pair_env: bool) -> int:
+def _fitted_group_tiles(d: int, mt: int, n: int, sms: int, cap: int, pair_env: bool, launch_cost: float) -> int:
     pairs = pair_env and sms >= 2
     units = -(-(-(-n // BLOCK_TOKENS)) // (2 if pairs else 1))  # token tiles (pairs) per launch
     grid = sms // 2 if pairs else sms
     if units > max(1, (40 << 20) // (BLOCK_TOKENS * d * 2 * (2 if pairs else 1))) and units >= grid:
         return cap  # banded raster (cce_kernels.cu lse_raster): not whole-wave launches
-    launch_cost = 0.4  # waves: launch gap + pipeline fill of one group launch
+    # launch_cost (waves): launch gap, pipeline fill and drain of one group launch
+    # (scripts/fwd_split_probe.py: 27 launches instead of one cost ~0.67 ms at Gemma-2B, ~1.7 waves
+    # of ~15 us each)
 
     def cost(g):
         full, rest = divmod(mt, g)
@@ -832,7 +837,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
 
     indexed_matmul + lse_forward (kernels.py:204-319) over the backward's tiles (compacted rows,
     the reference's vocabulary order) with the per-row tile maxima the decision needs, run over
-    vocabulary groups: each group's classifier rows are gathered into one of two <= 48 MB buffers (on
+    vocabulary groups: each group's classifier rows are gathered into one of two <= 52 MB buffers (on
     a side stream, while the previous group is swept) and swept with plain TMA tiles; the groups'
     (max, sum-exp) partials are folded by log-add-exp (kernels.py:121-137).  E is read in place
     when no row is ignored and as a compacted copy otherwise (compact_copy_wanted).  Transients:
@@ -861,7 +866,7 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
     # every FWD_FOLD_GROUPS groups and finished by one combine; the target logit lands in exactly
     # one group, so all groups write one zeroed array
     splits = [lib.cce_fwd_splits(n, d, v1 - v0) for v0, v1 in groups]
-    fold = FWD_FOLD_GROUPS
+    fold = int(os.environ.get("CCE_FWD_FOLD", FWD_FOLD_GROUPS))
     slots = 1 + max(sum(splits[i:i + fold]) for i in range(0, len(groups), fold))
     parts = torch.empty(slots, n, 2, dtype=torch.float32, device=dev)
     parts[0, :, 0] = -float("inf")

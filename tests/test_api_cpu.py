@@ -128,21 +128,29 @@ def test_capacity_hint_cache_is_bounded(monkeypatch):
 
 def test_forward_groups_fill_whole_waves(monkeypatch):
     """ops.fwd_group_tiles: the bounded forward's vocabulary groups stay within the byte budget
-    and, when a smaller group fills whole waves of the CTA-pair grid, take it (Gemma-2B on 148
-    SMs: 37 tiles x 32 token-tile pairs = 16 waves of 74 pairs; the budget alone gives 42)."""
+    and trade whole waves of the CTA-pair grid against launch count.  Gemma-2B on 148 SMs: the
+    default 52 MB budget gives 46 tiles (19.9 waves, 22 launches); a 48 MB budget with cheap
+    launches takes 37 tiles (32 token-tile pairs x 37 = exactly 16 waves of 74 pairs) over its
+    budget's 42 (18.2 waves)."""
     from paper_2411_09009_b200 import ops
 
-    monkeypatch.delenv("CCE_FWD_GROUP_MB", raising=False)
-    monkeypatch.delenv("CCE_FWD_GROUP_FIT", raising=False)
+    for k in ("CCE_FWD_GROUP_MB", "CCE_FWD_GROUP_FIT", "CCE_FWD_LAUNCH_WAVES", "CCE_PAIR"):
+        monkeypatch.delenv(k, raising=False)
     mt = 1000
+    assert ops.fwd_group_tiles(2304, mt) == 46
+    assert ops.fwd_group_tiles(2304, mt, 8192, 148) == 46
+    monkeypatch.setenv("CCE_FWD_GROUP_MB", "48")
+    monkeypatch.setenv("CCE_FWD_LAUNCH_WAVES", "0.4")
     assert ops.fwd_group_tiles(2304, mt) == 42
     g = ops.fwd_group_tiles(2304, mt, 8192, 148)
     assert g == 37 and (32 * g) % 74 == 0
+    monkeypatch.delenv("CCE_FWD_GROUP_MB")
+    monkeypatch.delenv("CCE_FWD_LAUNCH_WAVES")
     for n, d, v in [(4096, 768, 50257), (16384, 4096, 128256), (300, 64, 1000), (1, 64, 256),
                     (32768, 3584, 256000), (65536, 5120, 131072)]:
         m = -(-v // 256)
         cap = ops.fwd_group_tiles(d, m)
         g = ops.fwd_group_tiles(d, m, n, 148)
-        assert 1 <= g <= cap and g * 256 * d * 2 <= max(48 << 20, 256 * d * 2)
+        assert 1 <= g <= cap and g * 256 * d * 2 <= max(52 << 20, 256 * d * 2)
     monkeypatch.setenv("CCE_FWD_GROUP_FIT", "0")
-    assert ops.fwd_group_tiles(2304, mt, 8192, 148) == 42
+    assert ops.fwd_group_tiles(2304, mt, 8192, 148) == 46

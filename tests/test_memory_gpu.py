@@ -6,7 +6,7 @@ outputs) with a recorded formula, 4 * (8 (N + V) + 8 threads (n_b m_b + d_b (n_b
 ops.forward_stream / ops.backward_stream and stream_layout (csrc/cce_kernels.cu):
 
   forward   per-row tile maxima  ceil(N/128) * ceil(V/256) * 512 B
-            two vocabulary groups of sorted classifier rows (at most CCE_FWD_GROUP_MB, 48 MiB, each: the
+            two vocabulary groups of sorted classifier rows (at most CCE_FWD_GROUP_MB, 52 MiB, each: the
             next group is gathered on a side stream while one is swept)
             O(N + V) maps and partials; a batch with ignored rows adds their compacted copy
   backward  the S-hat ring (512 slots x 64 KiB = 32 MiB; 8 slots per token tile above 64 tiles)
@@ -35,7 +35,7 @@ def _budget(n, d, v):
     lists = nt * mt * 72 + (n + v) * 64  # keep flags, item lists, segments, windows; O(N + V) maps
     # two group buffers (gather overlapped with the sweep) and the (max, sum-exp) partials of up to
     # 8 groups x 8 vocabulary splits between folds
-    fwd = tile_max + 2 * 48 * MIB + 64 * n * 8 + lists + 2 * MIB
+    fwd = tile_max + 2 * 52 * MIB + 64 * n * 8 + lists + 2 * MIB
     acc = nt * ndc * 128 * 256 * 4 + 4 * ndc * 2 * 128 * 256 * 4
     # the unpermutation's saved break rows reuse the accumulators' storage after the pass: one row
     # per break (anchors 1 in 64 with headroom, cuts every 96 positions); larger at small N, large D
