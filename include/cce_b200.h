@@ -212,6 +212,20 @@ int cce_fwd_group_ex(const void* E, int e_gather, const void* C_g, const int32_t
                      const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total,
                      float softcap, void* ws, size_t ws_bytes, float* lse_part, float* correct_part, float* tile_max,
                      int flags, void* stream);
+/* One launch of the bounded forward's group chain (ops.forward_stream; replaces the per-group
+ * gather launches and stream waits around cce_fwd_group_ex): sweeps group g from its buffer C_g
+ * once *ready >= 1 (nullptr: stream order), without waiting for the previous launch to finish
+ * (no_dep_wait); counts its exited CTAs in *exit_ctr, the last setting *released = 1; and, in the
+ * same launch, gathers the next group's rows C[next_perm[r]] (r < next_rows) into next_dst once
+ * *next_wait >= 1 (the launch before this one has exited; nullptr: at once), counting shares in
+ * *next_ctr, the last setting *next_done = 1 (the next launch's `ready`).  next_dst NULL: no
+ * gather.  Counters and flags start at zero. */
+int cce_fwd_group_sync(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                       const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total,
+                       float softcap, void* ws, size_t ws_bytes, float* correct_part, float* tile_max,
+                       const int* ready, int* exit_ctr, int* released, int no_dep_wait, const void* C,
+                       const int32_t* next_perm, int64_t next_rows, void* next_dst, const int* next_wait,
+                       int* next_ctr, int* next_done, void* stream);
 int cce_fwd_splits(int64_t n, int64_t d, int64_t v);
 int cce_combine_parts(const void* parts, int count, int64_t n, float* lse_out, void* stream);
 

@@ -58,6 +58,10 @@ SIGNATURES = {
     "cce_fwd_group_ex": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
                                  c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_int,
                                  c_void_p]),
+    "cce_fwd_group_sync": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
+                                   c_i64, c_i64, c_f32, c_void_p, c_size, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p]),
     "cce_fwd_splits": (c_int, [c_i64, c_i64, c_i64]),
     "cce_combine_parts": (c_int, [c_void_p, c_int, c_i64, c_void_p, c_void_p]),
     "cce_bwd_stream_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_i64]),

@@ -109,6 +109,22 @@ struct Params {
   const int* pair_count;
   Stream st;               // KEPT streamed into a ring (TileRef.s is then the item index)
   int tm_stride, tm_m0;    // FWD: tile_max row stride in vocab tiles (0: mt) and first vocab tile
+  // FWD over vocabulary groups as one chain of programmatic-dependent launches (ops.forward_stream,
+  // cce_fwd_group_sync): launch g sweeps group g from a buffer the previous launch's gather warps
+  // filled, and its own gather warp (warp 6 of a 224-thread launch) fills the other buffer with
+  // group g + 1 once launch g - 1 has exited (that buffer is the one launch g - 1 read).  No launch
+  // waits for the previous one to finish: each waits on flags for exactly what it reads.
+  const int* sync_ready;   // 1 once this launch's group is in its buffer (nullptr: stream order)
+  int* sync_exit;          // CTAs of this launch that exited; the last sets *sync_released = 1
+  int* sync_released;
+  int no_dep_wait;         // 1: no griddepcontrol.wait (the flags order every input)
+  const int32_t* g_perm;   // gather warp: row r of g_dst <- g_src[g_perm[r]], r < g_rows
+  const __nv_bfloat16* g_src;
+  __nv_bfloat16* g_dst;
+  int g_rows;
+  const int* g_wait;       // gather only once *g_wait >= 1 (nullptr: at once)
+  int* g_ctr;              // gather shares done; the last sets *g_done = 1
+  int* g_done;
 };
 
 // dE pass ("B2") and dC pass ("B3").
@@ -187,6 +203,12 @@ __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void griddep_trigger() {
+#if CCE_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 __device__ __forceinline__ bool skip_launch(const int* run_if) {

@@ -377,22 +377,37 @@ void set_raster(cce::Params& p, int nt, int mt, int64_t d, bool pair, bool prefe
   p.grid_cap = r.cap;
 }
 
+using LseKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, cce::Params);
+template <int MODE, int CG>
+LseKernel sync_kernel() {
+  if constexpr (MODE == cce::FWD)
+    return cce::cce_lse_sync_kernel<cce::FWD, CG>;
+  else
+    return nullptr;
+}
+
 // Launch cce_lse_kernel<MODE> on single CTAs or on CTA pairs (cluster of 2).
 template <int MODE>
 int launch_lse(const cce::Params& p, bool pair, const CUtensorMap& tmE, const CUtensorMap& tmEg,
                const CUtensorMap& tmC256, const CUtensorMap& tmCg, const CUtensorMap& tmC128,
                cudaStream_t stream) {
   const int cap = (MODE != cce::KEPT && p.grid_cap > 0) ? p.grid_cap : (1 << 30);
+  // a launch of the forward's group chain (Params::sync_*): the 224-thread kernel with a gather warp
+  const bool sync = MODE == cce::FWD && (p.sync_exit != nullptr || p.g_dst != nullptr);
+  // (the 224-thread kernel exists for FWD only)
+  constexpr int SMODE = MODE == cce::FWD ? cce::FWD : -1;
   if (!pair) {
-    if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 1>, kLseSmem)) return e;
+    auto k = sync ? sync_kernel<SMODE, 1>() : cce::cce_lse_kernel<MODE, 1>;
+    if (int e = ensure_attr(k, kLseSmem)) return e;
     const int units = p.nt * p.splits;
-    return launch_k(cce::cce_lse_kernel<MODE, 1>, dim3(std::max(1, std::min({num_sms(), units, cap}))),
-                    dim3(cce::NUM_THREADS), kLseSmem, stream, 1, tmE, tmEg, tmC256, tmCg, p);
+    return launch_k(k, dim3(std::max(1, std::min({num_sms(), units, cap}))),
+                    dim3(sync ? cce::SYNC_THREADS : cce::NUM_THREADS), kLseSmem, stream, 1, tmE, tmEg, tmC256, tmCg, p);
   }
-  if (int e = ensure_attr(cce::cce_lse_kernel<MODE, 2>, kLsePairSmem)) return e;
+  auto k = sync ? sync_kernel<SMODE, 2>() : cce::cce_lse_kernel<MODE, 2>;
+  if (int e = ensure_attr(k, kLsePairSmem)) return e;
   const int pair_units = ((p.nt + 1) / 2) * p.splits;
   const int grid = 2 * std::max(1, std::min({num_sms() / 2, pair_units, cap}));
-  return launch_k(cce::cce_lse_kernel<MODE, 2>, dim3(grid), dim3(cce::NUM_THREADS), kLsePairSmem, stream, 2,
+  return launch_k(k, dim3(grid), dim3(sync ? cce::SYNC_THREADS : cce::NUM_THREADS), kLsePairSmem, stream, 2,
                   tmE, tmEg, tmC128, tmCg, p);
 }
 
@@ -833,7 +848,7 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
                    int64_t pos_offset, int64_t n, int64_t d, int64_t v, float softcap, void* ws, size_t ws_bytes,
                    float* lse_local, float* correct, float* tile_max, void* lab_buf, int64_t lab_capacity,
                    int32_t* lab_slot, void* lab_list, int* lab_count, cudaStream_t stream, int tm_stride = 0,
-                   int tm_m0 = 0, int flags = 0) {
+                   int tm_m0 = 0, int flags = 0, const cce::Params* sync = nullptr) {
   const std::string w(what);
   if (n < 0 || d <= 0 || v <= 0) return fail(w + ": bad sizes");
   if (lab_buf && (!lab_slot || !lab_list || !lab_count)) return fail(w + ": label tiles need slot maps");
@@ -872,6 +887,19 @@ int fwd_tiles_impl(const char* what, const void* E_rows, const void* C_rows, con
   p.tile_max = tile_max;
   p.tm_stride = tm_stride;
   p.tm_m0 = tm_m0;
+  if (sync) {  // the forward's group chain (cce_fwd_group_sync)
+    p.sync_ready = sync->sync_ready;
+    p.sync_exit = sync->sync_exit;
+    p.sync_released = sync->sync_released;
+    p.no_dep_wait = sync->no_dep_wait;
+    p.g_perm = sync->g_perm;
+    p.g_src = sync->g_src;
+    p.g_dst = sync->g_dst;
+    p.g_rows = sync->g_rows;
+    p.g_wait = sync->g_wait;
+    p.g_ctr = sync->g_ctr;
+    p.g_done = sync->g_done;
+  }
   if (lab_buf) {
     CCE_CUDA(cudaMemsetAsync(lab_slot, 0xFF, (size_t)nt * mt * sizeof(int32_t), stream));
     CCE_CUDA(cudaMemsetAsync(lab_count, 0, sizeof(int), stream));
@@ -950,6 +978,42 @@ int cce_fwd_group_ex(const void* E, int e_gather, const void* C_g, const int32_t
                         ws, ws_bytes, lse_part, correct_part, tile_max, nullptr, 0, nullptr, nullptr, nullptr,
                         static_cast<cudaStream_t>(stream_ptr), (int)((v_total + cce::BN - 1) / cce::BN),
                         (int)(v0 / cce::BN), flags);
+}
+
+// One launch of the bounded forward's group chain: cce_fwd_group_ex over group g (C_g: its buffer)
+// with no wait on the previous launch (no_dep_wait) but on *ready (its rows gathered; nullptr: the
+// stream orders it), counting this launch's exited CTAs in *exit_ctr (the last sets *released = 1),
+// and, in the same launch, gathering the next group's rows C[next_perm[r]], r < next_rows, into
+// next_dst once *next_wait >= 1 (the launch before this one exited; nullptr: at once), counted
+// in *next_ctr (the last share sets *next_done = 1).  next_dst == nullptr: nothing to gather.
+int cce_fwd_group_sync(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,
+                       const int32_t* pos, int64_t v0, int64_t n, int64_t d, int64_t v_group, int64_t v_total,
+                       float softcap, void* ws, size_t ws_bytes, float* correct_part, float* tile_max,
+                       const int* ready, int* exit_ctr, int* released, int no_dep_wait, const void* C,
+                       const int32_t* next_perm, int64_t next_rows, void* next_dst, const int* next_wait,
+                       int* next_ctr, int* next_done, void* stream_ptr) {
+  if (v0 % cce::BN != 0) return fail("cce_fwd_group_sync: v0 must be a multiple of 256");
+  if (v0 + v_group > v_total) return fail("cce_fwd_group_sync: group past the vocabulary");
+  if (!exit_ctr || !released) return fail("cce_fwd_group_sync: exit counter and released flag required");
+  if (next_dst && (!C || !next_perm || !next_ctr || !next_done))
+    return fail("cce_fwd_group_sync: a gather needs C, next_perm, next_ctr and next_done");
+  cce::Params sp{};
+  sp.sync_ready = ready;
+  sp.sync_exit = exit_ctr;
+  sp.sync_released = released;
+  sp.no_dep_wait = no_dep_wait ? 1 : 0;
+  sp.g_perm = next_perm;
+  sp.g_src = static_cast<const __nv_bfloat16*>(C);
+  sp.g_dst = static_cast<__nv_bfloat16*>(next_dst);
+  sp.g_rows = next_dst ? (int)next_rows : 0;
+  sp.g_wait = next_wait;
+  sp.g_ctr = next_ctr;
+  sp.g_done = next_done;
+  PdlScope pdl(true);
+  return fwd_tiles_impl("cce_fwd_group_sync", E, C_g, nullptr, e_gather, row_map, n_valid, pos, v0, n, d, v_group,
+                        softcap, ws, ws_bytes, nullptr, correct_part, tile_max, nullptr, 0, nullptr, nullptr, nullptr,
+                        static_cast<cudaStream_t>(stream_ptr), (int)((v_total + cce::BN - 1) / cce::BN),
+                        (int)(v0 / cce::BN), 3, &sp);
 }
 
 int cce_fwd_group(const void* E, int e_gather, const void* C_g, const int32_t* row_map, const int* n_valid,

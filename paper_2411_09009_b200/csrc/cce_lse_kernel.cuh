@@ -112,7 +112,10 @@ __device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorM
                                          int nblk) {
   constexpr int STAGES = CG == 2 ? LSE_STAGES_PAIR : LSE_STAGES;
   constexpr int SBYTES = CG == 2 ? PAIR_STAGE_BYTES : STAGE_BYTES;  // per-CTA bytes per stage
-  if (skip_launch(p.run_if)) return;
+  if (p.no_dep_wait)
+    griddep_trigger();  // the flags below order every input of this launch
+  else if (skip_launch(p.run_if))
+    return;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SBYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: logits ready
@@ -162,6 +165,11 @@ __device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorM
 
   if (warp == 0) {
     // ============================ producer (whole warp: TMA + gathers) =====================
+    if (p.sync_ready) {  // this launch's group lands in its buffer (the previous launch's gathers)
+      if (lane == 0) spin_until_geq(p.sync_ready, 1);
+      __syncwarp();
+      fence_proxy_async_global();  // generic-proxy row copies, read here by TMA
+    }
     constexpr int CROWS = BN / CG;    // C rows this CTA loads per tile
 #ifndef CCE_GLAG
 #define CCE_GLAG 2
@@ -271,8 +279,60 @@ __device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorM
         ++t;
       }, no_skip);
     }
+  } else if (warp == NUM_THREADS / 32) {
+    // ============== gather warp (224-thread launches): the next group's rows ==============
+    if (p.g_dst) {
+      if (p.g_wait) {  // the buffer is free once the launch before this one has exited
+        if (lane == 0) spin_until_geq(p.g_wait, 1);
+        __syncwarp();
+        (void)ld_acquire_gpu(p.g_wait);  // every lane: its reads are ordered after the chain's inputs
+      }
+      // this CTA's share of the rows, two rows at a time: 16-byte copies, up to 16 loads in flight
+      // per lane (32-bit index arithmetic; the share is a few hundred KB per launch)
+      const int r0 = (int)((int64_t)p.g_rows * bid / nblk), r1 = (int)((int64_t)p.g_rows * (bid + 1) / nblk);
+      const int n16 = p.d / 8;
+      for (int r = r0; r < r1; r += 2) {
+        const bool two = r + 1 < r1;
+        const uint4* s0 = reinterpret_cast<const uint4*>(p.g_src + (size_t)p.g_perm[r] * p.d);
+        const uint4* s1 = reinterpret_cast<const uint4*>(p.g_src + (size_t)p.g_perm[two ? r + 1 : r] * p.d);
+        uint4* d0 = reinterpret_cast<uint4*>(p.g_dst + (size_t)r * p.d);
+        uint4* d1 = d0 + n16;
+        for (int j0 = 0; j0 < n16; j0 += 32 * 8) {
+          uint4 a[8], b[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = j0 + lane + 32 * u;
+            if (j < n16) {
+              a[u] = __ldg(s0 + j);
+              b[u] = __ldg(s1 + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = j0 + lane + 32 * u;
+            if (j < n16) {
+              d0[j] = a[u];
+              if (two) d1[j] = b[u];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(p.g_ctr, 1) == nblk - 1) {
+          __threadfence();
+          st_release_gpu(p.g_done, 1);
+        }
+      }
+    }
   } else {
     // ===================================== epilogue ======================================
+    if (p.sync_ready) {  // every lane: its reads (targets, positions) ordered after the chain's inputs
+      if (lane == 0) spin_until_geq(p.sync_ready, 1);
+      __syncwarp();
+      (void)ld_acquire_gpu(p.sync_ready);
+    }
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -593,6 +653,27 @@ __device__ __forceinline__ void lse_body(const CUtensorMap& tmE, const CUtensorM
     else
       tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  if (p.sync_exit && threadIdx.x == 0) {  // every TMA read of this CTA has landed
+    __threadfence();
+    if (atomicAdd(p.sync_exit, 1) == nblk - 1) {
+      __threadfence();
+      st_release_gpu(p.sync_released, 1);
+    }
+  }
+}
+
+// The forward over vocabulary groups as a chain of launches (Params::sync_*): one more warp, the
+// gather warp, copies the next group's rows while this launch sweeps its own.
+constexpr int SYNC_THREADS = NUM_THREADS + 32;
+template <int MODE, int CG>
+__global__ void __launch_bounds__(SYNC_THREADS, 1)
+    cce_lse_sync_kernel(const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmEg,
+                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCg,
+                        const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  lse_body<MODE, CG>(tmE, tmEg, tmC, tmCg, p, smem, (int)blockIdx.x, (int)gridDim.x);
 }
 
 template <int MODE, int CG>

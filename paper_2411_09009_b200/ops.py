@@ -873,13 +873,28 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
     parts[0, :, 1] = 0.0
     correct = torch.zeros(n, dtype=torch.float32, device=dev)
     lse_local = torch.empty(n, dtype=torch.float32, device=dev)
-    # two group buffers: group g + 1's rows are gathered on a side stream while group g is swept
-    # (CCE_FWD_OVERLAP=0: gathers in line)
-    overlap = sorted_ and len(groups) > 1 and os.environ.get("CCE_FWD_OVERLAP", "1") != "0" and not _capturing()
+    # two group buffers.  Default: group g + 1's rows are gathered on a side stream while group g
+    # is swept, each launch waiting for its gather's event (CCE_FWD_OVERLAP=0: gathers in line).
+    # CCE_FWD_CHAIN=1: the group launches form one chain of programmatic dependent launches
+    # (cce_fwd_group_sync) -- launch g sweeps group g while its gather warp fills the other buffer
+    # with group g + 1 -- synchronised by device flags, so a launch's CTAs start as the previous
+    # launch's CTAs exit.  Bit-identical; its forward is 0.2-0.3 ms faster at Gemma-2B, but under
+    # the power cap the backward after it runs ~0.15 ms slower (lower clocks), so the step gains
+    # ~0.1 ms (`scripts/ab_r2/r2_chain2.sh`): opt-in.
+    chain = sorted_ and len(groups) > 1 and os.environ.get("CCE_FWD_CHAIN", "0") == "1" and not _capturing()
+    overlap = sorted_ and len(groups) > 1 and os.environ.get("CCE_FWD_OVERLAP", "1") != "0" and not _capturing() \
+        and not chain
     rows_g = min(v, gt * BLOCK_VOCAB)
-    bufs = [torch.empty(rows_g, d, dtype=torch.bfloat16, device=dev) for _ in range(2 if overlap else 1)] \
+    bufs = [torch.empty(rows_g, d, dtype=torch.bfloat16, device=dev) for _ in range(2 if overlap or chain else 1)] \
         if sorted_ else []
     stream = _stream(dev)
+    if chain:
+        ev = _ev_begin("fwd")
+        forward_chain(lib, e_rows, e_gather, c, perm, row_map, n_valid, pos, n, d, v, softcap, groups, splits,
+                      fold, parts, correct, tile_max, lse_local, bufs, stream)
+        _ev_end("fwd", ev)
+        del parts, bufs
+        return lse_local, correct, state
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev) if overlap else None
     gathered = [None, None]  # event: the buffer's gather is done
@@ -939,6 +954,43 @@ def forward_stream(e, c, targets, ignore_index: int, vocab_start: int = 0, softc
     # to free (no record_stream, which would hold them back from the allocator)
     del parts, bufs
     return lse_local, correct, state
+
+
+def forward_chain(lib, e_rows, e_gather, c, perm, row_map, n_valid, pos, n, d, v, softcap, groups, splits, fold,
+                  parts, correct, tile_max, lse_local, bufs, stream):
+    """forward_stream's group launches as one chain (cce_fwd_group_sync): launch g waits for its
+    rows (ready[g], set by launch g - 1's gather warps) instead of for launch g - 1 to finish, and
+    gathers group g + 1 into the other buffer once launch g - 1 has exited (released[g - 1]).  A
+    launch after a fold (cce_combine_parts, which reads the partial slots the next launch writes)
+    waits for it as usual."""
+    dev = e_rows.device
+    ng = len(groups)
+    flags = torch.zeros(4, ng, dtype=torch.int32, device=dev)  # ready, exited CTAs, released, gather shares
+    ready, exits, released, shares = flags[0], flags[1], flags[2], flags[3]
+    v0, v1 = groups[0]
+    _lib.check(lib.cce_gather_rows(_p(c), _p(perm[v0:v1]), v1 - v0, d, _p(bufs[0]), stream), "cce_gather_rows")
+    evk = _ev_begin("fwd_kernel")  # the chain's launches (and its folds) as one interval: events
+    off = 1                        # between the launches would break the chain
+    after_launch = False
+    for g, ((v0, v1), sp) in enumerate(zip(groups, splits)):
+        nxt = g + 1 < ng
+        n0, n1 = groups[g + 1] if nxt else (0, 0)
+        _lib.check(lib.cce_fwd_group_sync(
+            _p(e_rows), e_gather, _p(bufs[g % 2][: v1 - v0]), _p(row_map), _p(n_valid), _p(pos), v0, n, d, v1 - v0, v,
+            float(softcap or 0.0), _p(parts[off:off + sp]), sp * n * 8, _p(correct), _p(tile_max),
+            _p(ready[g:]) if g else None, _p(exits[g:]), _p(released[g:]), int(after_launch), _p(c),
+            _p(perm[n0:]) if nxt else None, n1 - n0, _p(bufs[(g + 1) % 2]) if nxt else None,
+            _p(released[g - 1:]) if (nxt and g) else None, _p(shares[g + 1:]) if nxt else None,
+            _p(ready[g + 1:]) if nxt else None, stream), "cce_fwd_group_sync")
+        after_launch = True
+        off += sp
+        if (g + 1) % fold == 0 and g + 1 < ng:
+            _lib.check(lib.cce_combine_parts(_p(parts), off, n, _p(None), stream), "cce_combine_parts")
+            off = 1
+            after_launch = False
+    _ev_end("fwd_kernel", evk)
+    _lib.check(lib.cce_combine_parts(_p(parts), off, n, _p(lse_local), stream), "cce_combine_parts")
+    del flags
 
 
 def backward_from_stream_state(state: StreamState, lse, upstream, *, eps: float = EPSILON_DEFAULT,

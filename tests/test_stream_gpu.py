@@ -243,3 +243,30 @@ def test_bounded_default_across_changing_batches(cuda_device):
         assert _rel(out["bounded"][1], out["fast"][1]) < 1e-2, step
         assert _rel(out["bounded"][2], out["fast"][2]) < 1e-2, step
         assert torch.all(out["bounded"][1][t == -100] == 0), step
+
+
+@pytest.mark.parametrize("n,d,v,ign,cap,group_mb", [(4096, 768, 50257, 0.0, 0.0, 4), (1000, 256, 30000, 0.2, 30.0, 1),
+                                                      (8192, 2304, 256000, 0.0, 0.0, 52)])
+def test_forward_chain_bit_identical(cuda_device, monkeypatch, n, d, v, ign, cap, group_mb):
+    """The bounded forward's group launches as one flag-synchronised chain (CCE_FWD_CHAIN=1: each
+    launch gathers the next group in a warp of its own and no launch waits for the previous one to
+    finish) give the same lse, target logits and tile maxima, bit for bit, as the per-group stream
+    waits -- over many groups (small CCE_FWD_GROUP_MB), folds, ignored rows and softcap."""
+    from paper_2411_09009_b200 import ops
+
+    monkeypatch.setenv("CCE_FWD_GROUP_MB", str(group_mb))
+    e, c, t = _head(n, d, v, n + d + 7, ign=ign)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("CCE_FWD_CHAIN", mode)
+        for _ in range(2):  # the second call runs on the learned compaction hint
+            lse_l, corr, st = ops.forward_stream(e, c, t, -100, 0, cap)
+        torch.cuda.synchronize()
+        out[mode] = (lse_l, corr, st.tile_max)
+    valid = t != -100
+    nv = int(valid.sum())
+    tm0, tm1 = out["0"][2], out["1"][2]
+    mt = -(-v // 256)
+    rows = (torch.arange(tm0.numel() // (mt * 128) * 128, device=e.device).view(-1, 1, 128) < nv)
+    assert torch.equal(out["0"][0][valid], out["1"][0][valid]) and torch.equal(out["0"][1][valid], out["1"][1][valid])
+    assert torch.equal(torch.where(rows, tm0.view(-1, mt, 128), 0.0), torch.where(rows, tm1.view(-1, mt, 128), 0.0))
