@@ -10,6 +10,6 @@ for l in sys.stdin:
     elif 'rror' in l or 'timed out' in l: print(l.strip()[:300])
 "; }
 for i in 1 2 3; do
-  echo "chain:  $(run X=1)"
+  echo "chain:  $(run CCE_FWD_CHAIN=1)"
   echo "events: $(run CCE_FWD_CHAIN=0)"
 done

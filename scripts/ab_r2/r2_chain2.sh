@@ -8,6 +8,6 @@ for l in sys.stdin:
         d=json.loads(l); k=d['kernel_ms']; print(f\"{d['ms_per_step']:.3f} ms  fwd {k['fwd']:.3f} bwd {k['bwd']:.3f} clk {d['clocks']['sm_mhz']}\")
 "; }
 for i in 1 2 3 4 5; do
-  echo "chain:  $(run X=1)"
+  echo "chain:  $(run CCE_FWD_CHAIN=1)"
   echo "events: $(run CCE_FWD_CHAIN=0)"
 done
